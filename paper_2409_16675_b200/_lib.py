@@ -1,0 +1,81 @@
+"""ctypes binding of the C ABI in include/ctb200.h (libctb200.so, built in-tree).
+
+There is deliberately no fallback: if the library is missing or no CUDA
+device is visible, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libctb200.so"
+
+CTB_OK, CTB_ERR_ARG, CTB_ERR_CUDA, CTB_ERR_UNSUPPORTED = 0, -1, -2, -3
+BASE_Q, BASE_T, BASE_B = 0, 1, 2
+
+_c_void_p = ctypes.c_void_p
+_u64 = ctypes.c_uint64
+_u32 = ctypes.c_uint32
+_int = ctypes.c_int
+
+# name -> (restype, argtypes); every symbol declared in include/ctb200.h
+SIGNATURES: dict[str, tuple] = {
+    "ctb_last_error": (ctypes.c_char_p, []),
+    "ctb_version": (_int, []),
+    "ctb_ctx_create": (_int, [ctypes.POINTER(_c_void_p), _u32, ctypes.POINTER(_u64), _u32,
+                              ctypes.POINTER(_u64), _u32, _u32]),
+    "ctb_ctx_destroy": (_int, [_c_void_p]),
+    "ctb_ctx_word_bytes": (_int, [_c_void_p, _int]),
+    "ctb_ctx_base_size": (_int, [_c_void_p, _int]),
+    "ctb_ctx_base_primes": (_int, [_c_void_p, _int, ctypes.POINTER(_u64), _u32]),
+    "ctb_ntt_forward": (_int, [_c_void_p, _int, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_ntt_inverse": (_int, [_c_void_p, _int, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_pointwise_mul": (_int, [_c_void_p, _int, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_ring_mul": (_int, [_c_void_p, _int, _c_void_p, _u64, _c_void_p, _u64, _c_void_p, _u64, _c_void_p]),
+    "ctb_cpmul": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_pp_mul": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_probe_modmul": (_int, [_int, _u64, _c_void_p, ctypes.POINTER(_u64), _c_void_p]),
+}
+
+
+class CtbError(RuntimeError):
+    """A libctb200 call failed (argument, CUDA or unsupported-shape error)."""
+
+    def __init__(self, code: int, what: str, msg: str):
+        super().__init__(f"{what} failed ({code}): {msg}")
+        self.code = code
+
+
+_lock = threading.Lock()
+_lib: ctypes.CDLL | None = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libctb200.so once; raise loudly if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise CtbError(CTB_ERR_ARG, "load",
+                               f"{LIB_PATH} is missing; build it with `python -m paper_2409_16675_b200.build`")
+            lib = ctypes.CDLL(str(LIB_PATH))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != CTB_OK:
+        msg = load().ctb_last_error()
+        raise CtbError(rc, what, msg.decode() if msg else "")
+
+
+def u64_array(values) -> ctypes.Array:
+    vals = [int(v) for v in values]
+    return (_u64 * max(1, len(vals)))(*vals)

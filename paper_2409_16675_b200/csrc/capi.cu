@@ -1,0 +1,83 @@
+// Context lifetime and introspection entry points of the C ABI.
+#include <string>
+#include "bigint.hpp"
+#include "ctb200.h"
+#include "kernels.hpp"
+
+using namespace ctb;
+
+namespace ctb {
+Ctx::~Ctx() {
+  for (auto& b : base) free_base(b);
+}
+}  // namespace ctb
+
+extern "C" const char* ctb_last_error(void) { return get_error(); }
+extern "C" int ctb_version(void) { return 1; }
+
+extern "C" int ctb_ctx_create(ctb_ctx_t** out, uint32_t n, const uint64_t* q_primes, uint32_t n_q,
+                              const uint64_t* t_primes, uint32_t n_t, uint32_t relin_base_bits) {
+  if (!out) { set_error("ctb_ctx_create: null output"); return ERR_ARG; }
+  *out = nullptr;
+  if (n < 4 || (n & (n - 1))) { set_error("ring degree must be a power of two >= 4"); return ERR_ARG; }
+  if (!q_primes || n_q == 0) { set_error("ctb_ctx_create: no cipher primes"); return ERR_ARG; }
+  uint32_t logn = 0;
+  while ((1u << logn) < n) ++logn;
+  if (logn > 13) { set_error("ring degree above 8192 unsupported"); return ERR_UNSUPPORTED; }
+  Ctx* c = new Ctx();
+  c->n = n; c->logn = logn; c->relin_base_bits = relin_base_bits;
+  std::string err;
+  // plain modulus t = prod t_j (< 2^63, as the reference's uint64 plain ring, ring.py:151-152)
+  std::vector<uint64_t> tmod, delta;
+  if (n_t) {
+    BigU tb(1);
+    for (uint32_t j = 0; j < n_t; ++j) tb.mul_small(t_primes[j]);
+    if (tb.bit_length() > 63) { delete c; set_error("plain modulus must be below 2^63"); return ERR_UNSUPPORTED; }
+    c->t = tb.word64(0);
+    c->t_half = c->t / 2;
+    BigU q(1);
+    for (uint32_t i = 0; i < n_q; ++i) q.mul_small(q_primes[i]);
+    BigU dq = q;
+    dq.divmod_small(c->t);  // Delta = floor(q / t)  (he.py:88-90)
+    for (uint32_t i = 0; i < n_q; ++i) {
+      tmod.push_back(c->t % q_primes[i]);
+      delta.push_back(dq.mod_small(q_primes[i]));
+    }
+    int rc = build_base(c->base[BASE_T], t_primes, (int)n_t, logn, err);
+    if (rc) { delete c; set_error("plain base: " + err); return rc == -2 ? ERR_CUDA : ERR_ARG; }
+    if (n_t == 2) {
+      const uint64_t inv = invmod(t_primes[0] % t_primes[1], t_primes[1]);
+      c->crt_inv = (uint32_t)inv;
+      c->crt_inv_q = (uint32_t)(((unsigned __int128)inv << 32) / t_primes[1]);
+    }
+  }
+  int rc = build_base(c->base[BASE_Q], q_primes, (int)n_q, logn, err, n_t ? tmod.data() : nullptr,
+                      n_t ? delta.data() : nullptr);
+  if (rc) { delete c; set_error("cipher base: " + err); return rc == -2 ? ERR_CUDA : ERR_ARG; }
+  *out = reinterpret_cast<ctb_ctx_t*>(c);
+  return OK;
+}
+
+extern "C" int ctb_ctx_destroy(ctb_ctx_t* ctx) {
+  delete reinterpret_cast<Ctx*>(ctx);
+  return OK;
+}
+
+extern "C" int ctb_ctx_word_bytes(const ctb_ctx_t* ctx, int base) {
+  if (!ctx || base < 0 || base >= BASE_COUNT) return ERR_ARG;
+  const Base& b = reinterpret_cast<const Ctx*>(ctx)->base[base];
+  return b.size() ? b.word : ERR_ARG;
+}
+
+extern "C" int ctb_ctx_base_size(const ctb_ctx_t* ctx, int base) {
+  if (!ctx || base < 0 || base >= BASE_COUNT) return ERR_ARG;
+  return reinterpret_cast<const Ctx*>(ctx)->base[base].size();
+}
+
+extern "C" int ctb_ctx_base_primes(const ctb_ctx_t* ctx, int base, uint64_t* out, uint32_t cap) {
+  if (!ctx || base < 0 || base >= BASE_COUNT || !out) return ERR_ARG;
+  const Base& b = reinterpret_cast<const Ctx*>(ctx)->base[base];
+  uint32_t k = 0;
+  for (; k < cap && k < (uint32_t)b.size(); ++k) out[k] = b.primes[k];
+  return (int)k;
+}

@@ -1,0 +1,122 @@
+// Prime tables: twiddles, Shoup quotients, Montgomery constants.
+#include <cstring>
+#include "ctx.hpp"
+
+namespace ctb {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+const char* get_error() { return g_err.c_str(); }
+
+static uint32_t bitrev(uint32_t x, uint32_t bits) {
+  uint32_t y = 0;
+  for (uint32_t i = 0; i < bits; ++i) { y = (y << 1) | (x & 1); x >>= 1; }
+  return y;
+}
+
+// Smallest-witness primitive 2N-th root, exactly as ring._find_root_of_unity
+// (ring.py:93-102): first g >= 2 whose cofactor power psi has psi^N == -1.
+static bool find_psi(uint64_t p, uint32_t n, uint64_t& psi) {
+  const uint64_t order = 2ull * n;
+  if ((p - 1) % order != 0) return false;
+  const uint64_t cof = (p - 1) / order;
+  for (uint64_t g = 2; g < p && g < (1ull << 32); ++g) {
+    uint64_t c = powmod(g, cof, p);
+    if (powmod(c, n, p) == p - 1) { psi = c; return true; }
+  }
+  return false;
+}
+
+template <typename T>
+static T shoup_q(uint64_t w, uint64_t p) {
+  constexpr int W = 8 * sizeof(T);
+  return (T)(((unsigned __int128)w << W) / p);
+}
+
+template <typename T>
+static int build_typed(Base& b, uint32_t logn, std::string& err, const uint64_t* tmod,
+                       const uint64_t* delta) {
+  const int L = b.size();
+  const uint32_t n = 1u << logn;
+  constexpr int W = 8 * sizeof(T);
+  std::vector<PrimeTab<T>> tabs(L);
+  const int ent = shape_tw_entries((int)logn);  // pass-major pairs per direction
+  std::vector<T> tw((size_t)L * 2 * 2 * ent);
+  cudaError_t ce = cudaMalloc(&b.d_tw, tw.size() * sizeof(T));
+  if (ce != cudaSuccess) { err = std::string("cudaMalloc twiddles: ") + cudaGetErrorString(ce); return -2; }
+  ce = cudaMalloc(&b.d_tabs, sizeof(PrimeTab<T>) * (L ? L : 1));
+  if (ce != cudaSuccess) { err = std::string("cudaMalloc tables: ") + cudaGetErrorString(ce); return -2; }
+  T* d_tw = (T*)b.d_tw;
+  for (int l = 0; l < L; ++l) {
+    const uint64_t p = b.primes[l];
+    uint64_t psi;
+    if (!find_psi(p, n, psi)) { err = "no primitive 2N-th root of unity mod " + std::to_string(p); return -1; }
+    const uint64_t psi_inv = invmod(psi, p);
+    T* f = tw.data() + (size_t)l * 4 * ent;
+    T* iv = f + 2 * ent;
+    // powers in natural order, then scatter by bit reversal
+    std::vector<uint64_t> pw(n), pwi(n);
+    pw[0] = 1; pwi[0] = 1;
+    for (uint32_t i = 1; i < n; ++i) { pw[i] = mulmod(pw[i - 1], psi, p); pwi[i] = mulmod(pwi[i - 1], psi_inv, p); }
+    // pass k, group B, stage i, block jb  ->  table index m + b = 2^(s+i) + B*2^i + jb
+    for (int k = 0; k < shape_npass((int)logn); ++k) {
+      const int s = shape_pass_s((int)logn, k), r = shape_pass_r((int)logn, k);
+      for (int B = 0; B < (1 << s); ++B)
+        for (int i = 0; i < r; ++i)
+          for (int jb = 0; jb < (1 << i); ++jb) {
+            const uint32_t mb = (1u << (s + i)) + ((uint32_t)B << i) + jb;
+            const size_t e = (size_t)shape_tw_off((int)logn, k) + (size_t)B * (1u << r) + (1u << i) - 1 + jb;
+            const uint64_t w = pw[bitrev(mb, logn)], wi = pwi[bitrev(mb, logn)];
+            f[2 * e] = (T)w;  f[2 * e + 1] = shoup_q<T>(w, p);
+            iv[2 * e] = (T)wi; iv[2 * e + 1] = shoup_q<T>(wi, p);
+          }
+    }
+    PrimeTab<T>& t = tabs[l];
+    std::memset(&t, 0, sizeof(t));
+    t.p = (T)p; t.p2 = (T)(2 * p);
+    T x = 1;  // Newton: p^-1 mod 2^W
+    for (int it = 0; it < 7; ++it) x = (T)(x * (T)(2 - (T)p * x));
+    t.pinv = x;
+    const uint64_t ninv = invmod(n % p, p);
+    t.ninv = (T)ninv; t.ninv_q = shoup_q<T>(ninv, p);
+    const uint64_t R = (uint64_t)(((unsigned __int128)1 << W) % p);
+    const uint64_t ninvr = mulmod(ninv, R, p);
+    t.ninvr = (T)ninvr; t.ninvr_q = shoup_q<T>(ninvr, p);
+    t.one_q = shoup_q<T>(1, p);
+    t.r2 = (T)R; t.r2_q = shoup_q<T>(R, p);
+    t.rr = (T)mulmod(R, R, p);
+    if (tmod) t.tmod = (T)(tmod[l] % p);
+    if (delta) { t.delta = (T)(delta[l] % p); t.delta_q = shoup_q<T>(delta[l] % p, p); }
+    t.fwd = d_tw + (size_t)l * 4 * ent;
+    t.inv = t.fwd + 2 * ent;
+  }
+  ce = cudaMemcpy(b.d_tw, tw.data(), tw.size() * sizeof(T), cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess && L)
+    ce = cudaMemcpy(b.d_tabs, tabs.data(), sizeof(PrimeTab<T>) * L, cudaMemcpyHostToDevice);
+  if (ce != cudaSuccess) { err = std::string("cudaMemcpy tables: ") + cudaGetErrorString(ce); return -2; }
+  return 0;
+}
+
+int build_base(Base& b, const uint64_t* primes, int count, uint32_t logn, std::string& err,
+               const uint64_t* tmod, const uint64_t* delta) {
+  b.primes.assign(primes, primes + count);
+  const uint32_t n = 1u << logn;
+  bool small = true;
+  for (uint64_t p : b.primes) {
+    if (p < 3 || p % (2ull * n) != 1) { err = "prime " + std::to_string(p) + " is not 1 mod 2N"; return -1; }
+    if (p >= (1ull << 62)) { err = "prime " + std::to_string(p) + " exceeds 62 bits"; return -1; }
+    if (p >= (1ull << 30)) small = false;
+  }
+  b.word = small ? 4 : 8;
+  return small ? build_typed<uint32_t>(b, logn, err, tmod, delta)
+               : build_typed<uint64_t>(b, logn, err, tmod, delta);
+}
+
+void free_base(Base& b) {
+  if (b.d_tabs) cudaFree(b.d_tabs);
+  if (b.d_tw) cudaFree(b.d_tw);
+  b.d_tabs = b.d_tw = nullptr;
+  b.primes.clear();
+}
+
+}  // namespace ctb

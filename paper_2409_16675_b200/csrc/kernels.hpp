@@ -1,0 +1,65 @@
+// Shared launch plumbing for the ring kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "ctx.hpp"
+#include "ntt.cuh"
+
+namespace ctb {
+
+constexpr int OK = 0;
+constexpr int ERR_ARG = -1;
+constexpr int ERR_CUDA = -2;
+constexpr int ERR_UNSUPPORTED = -3;
+
+inline int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return OK;
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return ERR_CUDA;
+}
+
+// Launch a CTA-per-polynomial-limb kernel with the double-buffered exchange image.
+// EXTRA_POLYS: additional N-word thread-private strips after the image.
+template <typename T, int LOGN, int EXTRA_POLYS = 0, typename... KArgs, typename... Args>
+inline cudaError_t launch_ntt_kernel(void (*kern)(KArgs...), size_t nblocks, cudaStream_t s,
+                                     Args... args) {
+  using Sh = NttShape<LOGN>;
+  const size_t smem = (2 * (size_t)SmemImage<T, LOGN>::WORDS + (size_t)EXTRA_POLYS * Sh::N) * sizeof(T);
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  if (nblocks == 0) return cudaSuccess;
+  kern<<<(unsigned)nblocks, Sh::THREADS, smem, s>>>(args...);
+  return cudaGetLastError();
+}
+
+#define CTB_CASE_LOGN(L_, ...) \
+  case L_: {                   \
+    constexpr int LOGN = L_;   \
+    __VA_ARGS__;               \
+  } break;
+
+// Dispatch a body over the supported ring degrees N = 2^2 .. 2^13.
+#define CTB_DISPATCH_LOGN(logn, ...)                                  \
+  switch (logn) {                                                     \
+    CTB_CASE_LOGN(2, __VA_ARGS__)                                     \
+    CTB_CASE_LOGN(3, __VA_ARGS__)                                     \
+    CTB_CASE_LOGN(4, __VA_ARGS__)                                     \
+    CTB_CASE_LOGN(5, __VA_ARGS__)                                     \
+    CTB_CASE_LOGN(6, __VA_ARGS__)                                     \
+    CTB_CASE_LOGN(7, __VA_ARGS__)                                     \
+    CTB_CASE_LOGN(8, __VA_ARGS__)                                     \
+    CTB_CASE_LOGN(9, __VA_ARGS__)                                     \
+    CTB_CASE_LOGN(10, __VA_ARGS__)                                    \
+    CTB_CASE_LOGN(11, __VA_ARGS__)                                    \
+    CTB_CASE_LOGN(12, __VA_ARGS__)                                    \
+    CTB_CASE_LOGN(13, __VA_ARGS__)                                    \
+    default:                                                          \
+      set_error("ring degree 2^" + std::to_string(logn) + " unsupported"); \
+      return ERR_UNSUPPORTED;                                         \
+  }
+
+}  // namespace ctb

@@ -1,0 +1,321 @@
+// Batched NTT / INTT, ring products, fused CPMul and PPMul (sm_100a).
+//
+// Replaces, on device:
+//   ring._NttPlan.forward/inverse          ring.py:186-217  (ctb_ntt_forward/inverse)
+//   ring.ring_mul -> _crt_ntt_mul          ring.py:404-474  (ctb_ring_mul)
+//   He.cp_mul (lift + 2 ring_mul)          he.py:366-382    (ctb_cpmul, fused)
+//   He.pp_mul (plain-ring ring_mul + CRT)  he.py:441-445, ring.py:477-485 (ctb_pp_mul)
+// Layout: residues [poly][limb][N] (uint32 or uint64 words), plain [poly][N] uint64.
+#include <algorithm>
+#include "kernels.hpp"
+#include "ctb200.h"
+
+namespace ctb {
+
+template <typename T, int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
+k_ntt_fwd(const T* in, T* out, const PrimeTab<T>* __restrict__ tabs, int L) {
+  using Sh = NttShape<LOGN>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Exchanger<T, LOGN> ex{reinterpret_cast<T*>(smem_raw)};
+  const int limb = blockIdx.x % L;
+  const size_t off = (size_t)blockIdx.x * Sh::N;
+  PrimeRegs<T> pr(tabs + limb);
+  T x[Sh::E];
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) x[k] = in[off + coef_base<LOGN>() + coef_off<LOGN>(k)];
+  ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) out[off + eval_base<LOGN>() + eval_off<LOGN>(k)] = reduce4(x[k], pr.p);
+}
+
+template <typename T, int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
+k_ntt_inv(const T* in, T* out, const PrimeTab<T>* __restrict__ tabs, int L) {
+  using Sh = NttShape<LOGN>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Exchanger<T, LOGN> ex{reinterpret_cast<T*>(smem_raw)};
+  const int limb = blockIdx.x % L;
+  const size_t off = (size_t)blockIdx.x * Sh::N;
+  PrimeRegs<T> pr(tabs + limb);
+  T x[Sh::E];
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) x[k] = in[off + eval_base<LOGN>() + eval_off<LOGN>(k)];
+  ntt_inv_regs<T, LOGN>(x, ex, pr.inv, pr.p, pr.p2);
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k)
+    out[off + coef_base<LOGN>() + coef_off<LOGN>(k)] = csub(shoup_mul(x[k], pr.ninv, pr.ninv_q, pr.p), pr.p);
+}
+
+// out[i] = a[i * sa] * b[i * sb] in Z_q[x]/(x^N+1), per limb; sa/sb are poly strides (0 = broadcast).
+template <typename T, int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
+k_ring_mul(const T* a, uint64_t sa, const T* b, uint64_t sb, T* out,
+           const PrimeTab<T>* __restrict__ tabs, int L) {
+  using Sh = NttShape<LOGN>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Exchanger<T, LOGN> ex{reinterpret_cast<T*>(smem_raw)};
+  const int limb = blockIdx.x % L;
+  const size_t poly = blockIdx.x / L;
+  const size_t LN = (size_t)L * Sh::N;
+  PrimeRegs<T> pr(tabs + limb);
+  const T* pa = a + poly * sa * LN + (size_t)limb * Sh::N;
+  const T* pb = b + poly * sb * LN + (size_t)limb * Sh::N;
+  T y[Sh::E], x[Sh::E];
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) y[k] = pb[coef_base<LOGN>() + coef_off<LOGN>(k)];
+  ntt_fwd_regs<T, LOGN>(y, ex, pr.fwd, pr.p, pr.p2);
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) y[k] = shoup_mul(y[k], pr.ninvr, pr.ninvr_q, pr.p);
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) x[k] = pa[coef_base<LOGN>() + coef_off<LOGN>(k)];
+  ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) x[k] = mont_mul(x[k], y[k], pr.p, pr.pinv);
+  ntt_inv_regs<T, LOGN>(x, ex, pr.inv, pr.p, pr.p2);
+  T* po = out + poly * LN + (size_t)limb * Sh::N;
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) po[coef_base<LOGN>() + coef_off<LOGN>(k)] = csub(x[k], pr.p);
+}
+
+// Eval-domain slotwise product (ring.pointwise_mul, ring.py:572-584).
+template <typename T>
+__global__ void k_pointwise(const T* a, const T* b, T* out, const PrimeTab<T>* __restrict__ tabs,
+                            int L, uint32_t n, uint64_t total) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const int limb = (int)((i / n) % L);
+    const PrimeTab<T>* t = tabs + limb;
+    const T p = t->p, pinv = t->pinv;
+    T v = mont_mul(a[i], b[i], p, pinv);       // a b R^-1
+    v = mont_mul(v, t->rr, p, pinv);           // a b
+    out[i] = csub(v, p);
+  }
+}
+
+// Fused CPMul: ct [B][2][L][N] x pt [B][N] (uint64 in [0,t)) -> out [B][2][L][N].
+// One CTA per (ciphertext, limb): NTT of the centred lift of pt once (scaled
+// into the Montgomery domain with N^-1 folded), then per part: NTT, slotwise
+// Montgomery product, INTT, canonical store.  he.py:366-382 / he.py:325-327.
+template <typename T, int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
+k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>* __restrict__ tabs,
+        int L, uint64_t t_half) {
+  using Sh = NttShape<LOGN>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Exchanger<T, LOGN> ex{reinterpret_cast<T*>(smem_raw)};
+  // NTT(lift(pt)) parks in a thread-private shared-memory strip (slot k of
+  // thread t at k*THREADS + t: conflict-free, no barrier needed) so that only
+  // one transform's worth of residues is live in registers.
+  T* ysm = reinterpret_cast<T*>(smem_raw) + 2 * SmemImage<T, LOGN>::WORDS + threadIdx.x;
+  const int limb = blockIdx.x % L;
+  const size_t b = blockIdx.x / L;
+  PrimeRegs<T> pr(tabs + limb);
+  const T tmod = tabs[limb].tmod;
+  T x[Sh::E];
+  {
+    const uint64_t* ppt = pt + b * Sh::N + coef_base<LOGN>();
+#pragma unroll
+    for (int k = 0; k < Sh::E; ++k) {
+      const uint64_t v = __ldg(ppt + coef_off<LOGN>(k));
+      T r = csub(pr.reduce_u64_lazy(v), pr.p);         // v mod p
+      if (v > t_half) r = sub_mod(r, tmod, pr.p);       // centred lift: v - t (he.py:325-327)
+      x[k] = r;
+    }
+    ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
+#pragma unroll
+    for (int k = 0; k < Sh::E; ++k) ysm[k * Sh::THREADS] = shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p);
+  }
+#pragma unroll 1
+  for (int part = 0; part < 2; ++part) {
+    const size_t off = ((b * 2 + part) * L + limb) * (size_t)Sh::N + coef_base<LOGN>();
+#pragma unroll
+    for (int k = 0; k < Sh::E; ++k) x[k] = ct[off + coef_off<LOGN>(k)];
+    ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
+#pragma unroll
+    for (int k = 0; k < Sh::E; ++k) x[k] = mont_mul(x[k], ysm[k * Sh::THREADS], pr.p, pr.pinv);
+    ntt_inv_regs<T, LOGN>(x, ex, pr.inv, pr.p, pr.p2);
+#pragma unroll
+    for (int k = 0; k < Sh::E; ++k) out[off + coef_off<LOGN>(k)] = csub(x[k], pr.p);
+  }
+}
+
+// PPMul in the plain ring Z_t[x]/(x^N+1), t = t0 (* t1): per-prime NTT
+// product then the 2-prime CRT of ring._crt_combine (ring.py:478-485).
+template <int LOGN>
+__device__ __forceinline__ void plain_prime_product(const uint64_t* a, const uint64_t* b,
+                                                    const PrimeTab<uint32_t>* tab,
+                                                    Exchanger<uint32_t, LOGN>& ex,
+                                                    uint32_t (&x)[NttShape<LOGN>::E]) {
+  using Sh = NttShape<LOGN>;
+  PrimeRegs<uint32_t> pr(tab);
+  uint32_t y[Sh::E];
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) y[k] = csub(pr.reduce_u64_lazy(__ldg(b + coef_base<LOGN>() + coef_off<LOGN>(k))), pr.p);
+  ntt_fwd_regs<uint32_t, LOGN>(y, ex, pr.fwd, pr.p, pr.p2);
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) y[k] = shoup_mul(y[k], pr.ninvr, pr.ninvr_q, pr.p);
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) x[k] = csub(pr.reduce_u64_lazy(__ldg(a + coef_base<LOGN>() + coef_off<LOGN>(k))), pr.p);
+  ntt_fwd_regs<uint32_t, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) x[k] = mont_mul(x[k], y[k], pr.p, pr.pinv);
+  ntt_inv_regs<uint32_t, LOGN>(x, ex, pr.inv, pr.p, pr.p2);
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) x[k] = csub(x[k], pr.p);
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
+k_pp_mul(const uint64_t* a, const uint64_t* b, uint64_t* out, const PrimeTab<uint32_t>* __restrict__ tabs,
+         int LT, uint32_t c_inv, uint32_t c_inv_q) {
+  using Sh = NttShape<LOGN>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Exchanger<uint32_t, LOGN> ex{reinterpret_cast<uint32_t*>(smem_raw)};
+  const size_t off = (size_t)blockIdx.x * Sh::N;
+  uint32_t r0[Sh::E];
+  plain_prime_product<LOGN>(a + off, b + off, tabs, ex, r0);
+  if (LT == 1) {
+#pragma unroll
+    for (int k = 0; k < Sh::E; ++k) out[off + coef_base<LOGN>() + coef_off<LOGN>(k)] = r0[k];
+    return;
+  }
+  uint32_t r1[Sh::E];
+  plain_prime_product<LOGN>(a + off, b + off, tabs + 1, ex, r1);
+  const uint32_t p0 = tabs[0].p;
+  PrimeRegs<uint32_t> p1(tabs + 1);
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) {
+    const uint32_t r0m = csub(p1.reduce_u64_lazy(r0[k]), p1.p);
+    const uint32_t d = csub(shoup_mul(sub_mod(r1[k], r0m, p1.p), c_inv, c_inv_q, p1.p), p1.p);
+    out[off + coef_base<LOGN>() + coef_off<LOGN>(k)] = (uint64_t)r0[k] + (uint64_t)p0 * d;
+  }
+}
+
+}  // namespace ctb
+
+// ---------------------------------------------------------------------------
+// C-ABI entry points (declared in include/ctb200.h)
+// ---------------------------------------------------------------------------
+using namespace ctb;
+
+static inline const Base* base_of(const ctb_ctx_t* ctx, int base) {
+  if (!ctx || base < 0 || base >= BASE_COUNT) return nullptr;
+  const Base* b = &reinterpret_cast<const Ctx*>(ctx)->base[base];
+  return b->size() ? b : nullptr;
+}
+
+extern "C" int ctb_ntt_forward(const ctb_ctx_t* ctx, int base, const void* in, void* out,
+                               uint64_t n_polys, void* stream) {
+  const Base* b = base_of(ctx, base);
+  if (!b || !in || !out) { set_error("ctb_ntt_forward: bad context, base or buffer"); return ERR_ARG; }
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  const size_t nblk = n_polys * b->size();
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  if (b->word == 4) {
+    using T = uint32_t;
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_ntt_fwd<T, LOGN>, nblk, s, (const T*)in, (T*)out,
+                                                      (const PrimeTab<T>*)b->d_tabs, b->size())));
+  } else {
+    using T = uint64_t;
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_ntt_fwd<T, LOGN>, nblk, s, (const T*)in, (T*)out,
+                                                      (const PrimeTab<T>*)b->d_tabs, b->size())));
+  }
+  return cuda_status(e, "ctb_ntt_forward");
+}
+
+extern "C" int ctb_ntt_inverse(const ctb_ctx_t* ctx, int base, const void* in, void* out,
+                               uint64_t n_polys, void* stream) {
+  const Base* b = base_of(ctx, base);
+  if (!b || !in || !out) { set_error("ctb_ntt_inverse: bad context, base or buffer"); return ERR_ARG; }
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  const size_t nblk = n_polys * b->size();
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  if (b->word == 4) {
+    using T = uint32_t;
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_ntt_inv<T, LOGN>, nblk, s, (const T*)in, (T*)out,
+                                                      (const PrimeTab<T>*)b->d_tabs, b->size())));
+  } else {
+    using T = uint64_t;
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_ntt_inv<T, LOGN>, nblk, s, (const T*)in, (T*)out,
+                                                      (const PrimeTab<T>*)b->d_tabs, b->size())));
+  }
+  return cuda_status(e, "ctb_ntt_inverse");
+}
+
+extern "C" int ctb_pointwise_mul(const ctb_ctx_t* ctx, int base, const void* a, const void* bb, void* out,
+                                 uint64_t n_polys, void* stream) {
+  const Base* b = base_of(ctx, base);
+  if (!b || !a || !bb || !out) { set_error("ctb_pointwise_mul: bad context, base or buffer"); return ERR_ARG; }
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  const uint64_t total = n_polys * b->size() * (uint64_t)c->n;
+  if (!total) return OK;
+  const unsigned grid = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (b->word == 4)
+    k_pointwise<uint32_t><<<grid, 256, 0, s>>>((const uint32_t*)a, (const uint32_t*)bb, (uint32_t*)out,
+                                               (const PrimeTab<uint32_t>*)b->d_tabs, b->size(), c->n, total);
+  else
+    k_pointwise<uint64_t><<<grid, 256, 0, s>>>((const uint64_t*)a, (const uint64_t*)bb, (uint64_t*)out,
+                                               (const PrimeTab<uint64_t>*)b->d_tabs, b->size(), c->n, total);
+  return cuda_status(cudaGetLastError(), "ctb_pointwise_mul");
+}
+
+extern "C" int ctb_ring_mul(const ctb_ctx_t* ctx, int base, const void* a, uint64_t a_stride, const void* bb,
+                            uint64_t b_stride, void* out, uint64_t n_polys, void* stream) {
+  const Base* b = base_of(ctx, base);
+  if (!b || !a || !bb || !out) { set_error("ctb_ring_mul: bad context, base or buffer"); return ERR_ARG; }
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  const size_t nblk = n_polys * b->size();
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  if (b->word == 4) {
+    using T = uint32_t;
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_ring_mul<T, LOGN>, nblk, s, (const T*)a, a_stride,
+                                                      (const T*)bb, b_stride, (T*)out,
+                                                      (const PrimeTab<T>*)b->d_tabs, b->size())));
+  } else {
+    using T = uint64_t;
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_ring_mul<T, LOGN>, nblk, s, (const T*)a, a_stride,
+                                                      (const T*)bb, b_stride, (T*)out,
+                                                      (const PrimeTab<T>*)b->d_tabs, b->size())));
+  }
+  return cuda_status(e, "ctb_ring_mul");
+}
+
+extern "C" int ctb_cpmul(const ctb_ctx_t* ctx, const void* ct, const uint64_t* pt, void* out, uint64_t batch,
+                         void* stream) {
+  const Base* b = base_of(ctx, BASE_Q);
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (!b || !c->t || !ct || !pt || !out) { set_error("ctb_cpmul: bad context (needs cipher+plain ring) or buffer"); return ERR_ARG; }
+  const size_t nblk = batch * b->size();
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  if (b->word == 4) {
+    using T = uint32_t;
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN, 1>(k_cpmul<T, LOGN>, nblk, s, (const T*)ct, pt, (T*)out,
+                                                         (const PrimeTab<T>*)b->d_tabs, b->size(), c->t_half)));
+  } else {
+    using T = uint64_t;
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN, 1>(k_cpmul<T, LOGN>, nblk, s, (const T*)ct, pt, (T*)out,
+                                                         (const PrimeTab<T>*)b->d_tabs, b->size(), c->t_half)));
+  }
+  return cuda_status(e, "ctb_cpmul");
+}
+
+extern "C" int ctb_pp_mul(const ctb_ctx_t* ctx, const uint64_t* a, const uint64_t* bb, uint64_t* out,
+                          uint64_t n_polys, void* stream) {
+  const Base* b = base_of(ctx, BASE_T);
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (!b || !a || !bb || !out) { set_error("ctb_pp_mul: context has no plain ring or bad buffer"); return ERR_ARG; }
+  if (b->word != 4 || b->size() > 2) { set_error("ctb_pp_mul: plain ring must be 1-2 primes below 2^30"); return ERR_UNSUPPORTED; }
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<uint32_t, LOGN>(k_pp_mul<LOGN>, n_polys, s, a, bb, out,
+                                                           (const PrimeTab<uint32_t>*)b->d_tabs, b->size(),
+                                                           c->crt_inv, c->crt_inv_q)));
+  return cuda_status(e, "ctb_pp_mul");
+}
+

@@ -1,0 +1,301 @@
+// CTA-resident negacyclic NTT over one RNS limb of one polynomial.
+//
+// Mathematical contract (identical to the reference, ring.py:164-217):
+//   forward: out[k] = a(psi^(2*bitrev_logN(k)+1)) mod p, i.e. the in-place
+//            Cooley-Tukey pass over the twiddle table w[i] = psi^bitrev(i),
+//            natural order in, bit-reversed order out, canonical [0, p);
+//   inverse: the exact inverse map, canonical [0, p).
+// psi is chosen exactly as ring._find_root_of_unity (ring.py:93-102), so the
+// evaluation-domain layout is bit-identical to ring.ntt_forward.
+//
+// Execution model (B200, sm_100a): one CTA owns one (polynomial, limb).  Each
+// of THREADS threads keeps E = N/THREADS residues in registers; the logN
+// butterfly stages are grouped into passes of up to log2(E) stages that run
+// entirely in registers (radix-2^r butterfly networks), and consecutive passes
+// exchange data through an XOR-swizzled shared-memory image of the polynomial
+// (bank-conflict-free for every pass layout: tools/swizzle_check.py).  The
+// first pass reads coalesced from HBM (thread t owns t + j*THREADS) and the
+// last forward pass leaves each thread 2^r contiguous evaluation slots, which
+// is exactly the layout the first inverse pass needs, so a pointwise product
+// between a forward and an inverse transform costs no data movement.
+#pragma once
+#include <cstdint>
+#include "modarith.cuh"
+
+namespace ctb {
+
+// Per-prime constant block (device memory, read-only after ctx creation).
+template <typename T>
+struct PrimeTab {
+  T p, p2, pinv;        // p, 2p, p^-1 mod 2^W
+  T ninv, ninv_q;       // N^-1 mod p and its Shoup quotient
+  T ninvr, ninvr_q;     // N^-1 * 2^W mod p (enters the Montgomery domain, 1/N folded)
+  T one_q;              // floor(2^W / p): Shoup quotient of w = 1 (generic reduction)
+  T r2, r2_q;           // 2^W mod p (u32: splitting 64-bit inputs) and Shoup quotient
+  T rr;                 // 2^(2W) mod p (leaves the Montgomery domain)
+  T tmod;               // plain modulus t mod p (cipher base only: centred lift)
+  T delta, delta_q;     // floor(q/t) mod p and Shoup quotient (cipher base only)
+  const T* fwd;         // pass-major (w, w') pairs, w = psi^bitrev(m + b)   (shape_tw_off)
+  const T* inv;         // same layout, psi^-bitrev(m + b)
+};
+
+// Pass schedule of the CTA transform, as runtime-capable constexpr functions
+// so the host table builder (ctx.cu) and the device code agree exactly.
+__host__ __device__ constexpr int shape_loge(int logn) { return logn >= 9 ? 4 : (logn >= 6 ? logn - 5 : 1); }
+__host__ __device__ constexpr int shape_npass(int logn) { return (logn + shape_loge(logn) - 1) / shape_loge(logn); }
+__host__ __device__ constexpr int shape_first_r(int logn) { return logn - (shape_npass(logn) - 1) * shape_loge(logn); }
+__host__ __device__ constexpr int shape_pass_s(int logn, int k) { return k == 0 ? 0 : shape_first_r(logn) + (k - 1) * shape_loge(logn); }
+__host__ __device__ constexpr int shape_pass_r(int logn, int k) { return k == 0 ? shape_first_r(logn) : shape_loge(logn); }
+// Twiddles are stored pass-major: pass k, butterfly group B (2^s groups) owns
+// 2^r consecutive (w, w') entries, entry (2^i - 1) + jb serving stage s+i,
+// block jb -- one base pointer per pass and group, immediate offsets inside.
+__host__ __device__ constexpr int shape_tw_off(int logn, int k) {
+  int off = 0;
+  for (int q = 0; q < k; ++q) off += 1 << (shape_pass_s(logn, q) + shape_pass_r(logn, q));
+  return off;
+}
+__host__ __device__ constexpr int shape_tw_entries(int logn) { return shape_tw_off(logn, shape_npass(logn)); }
+
+template <int LOGN>
+struct NttShape {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int LOGE = shape_loge(LOGN);
+  static constexpr int E = 1 << LOGE;
+  static constexpr int THREADS = N / E;
+  // resident CTAs per SM the register allocation is capped for
+  static constexpr int MINB = THREADS >= 512 ? 1 : (THREADS >= 256 ? 2 : 4);
+  static constexpr int NPASS = shape_npass(LOGN);
+  static constexpr int FIRST_R = shape_first_r(LOGN);
+  __host__ __device__ static constexpr int pass_s(int k) { return shape_pass_s(LOGN, k); }
+  __host__ __device__ static constexpr int pass_r(int k) { return shape_pass_r(LOGN, k); }
+  __host__ __device__ static constexpr int tw_off(int k) { return shape_tw_off(LOGN, k); }
+};
+
+// Shared-memory image of a polynomial: element idx lives at word
+// phys(idx) = sum over set bits b of idx of WEIGHT[b].  The weights are
+// 2^b plus a little padding chosen so that, in every pass layout, the 32
+// lanes of a warp (16 for 64-bit words) hit distinct banks
+// (tools/swizzle_check.py proves it for every supported N >= 1024).  Because
+// phys is additive over disjoint bit sets and the thread part and slot part of
+// a pass index occupy disjoint bits, every access is [thread base + immediate].
+template <typename T>
+__host__ __device__ constexpr int smem_weight(int logn, int b) {
+  constexpr int W32[14] = {1, 2, 4, 8, 16, 33, 66, 132, 272, 552, 1088, 2176, 4352, 8704};
+  constexpr int W64[14] = {1, 2, 4, 8, 16, 33, 66, 132, 264, 528, 1056, 2112, 4224, 8448};
+  return logn < 9 ? (1 << b) : (sizeof(T) == 4 ? W32[b] : W64[b]);
+}
+
+template <typename T, int LOGN>
+__host__ __device__ constexpr int phys(int idx) {
+  int r = 0;
+  for (int b = 0; b < LOGN; ++b) r += ((idx >> b) & 1) * smem_weight<T>(LOGN, b);
+  return r;
+}
+
+template <typename T, int LOGN>
+struct SmemImage {
+  static constexpr int WORDS = phys<T, LOGN>((1 << LOGN) - 1) + 1;
+};
+
+// Thread -> group permutation of a pass: the last pass of N >= 1024 rotates the
+// low six thread bits so its lanes avoid the bank of the middle passes.
+template <int LOGN, bool LAST>
+__host__ __device__ constexpr int pass_thread(int t) {
+  if constexpr (LAST && LOGN >= 10) return ((t & 31) << 1) | ((t >> 5) & 1) | (t & ~63);
+  return t;
+}
+
+// Index of register slot k of thread t in the layout of pass (S0, R).  The
+// thread part (k = 0) and the slot part (t = 0) have disjoint bits, so
+// pass_index(t, k) == pass_index(t, 0) | pass_index(0, k).
+template <int LOGN, int S0, int R>
+__host__ __device__ constexpr int pass_index(int t, int k) {
+  using Sh = NttShape<LOGN>;
+  constexpr int G = 1 << R;
+  constexpr int S = Sh::N >> (S0 + R);
+  constexpr bool LAST = (S0 + R == LOGN);
+  const int gg = k / G, j = k % G;
+  const int g = gg * Sh::THREADS + (t == 0 ? 0 : pass_thread<LOGN, LAST>(t));
+  const int o = g & (S - 1);
+  const int B = g >> (LOGN - S0 - R);
+  return B * (Sh::N >> S0) + o + j * S;
+}
+
+// Twiddle pair (w, w') load through the read-only path.  volatile keeps the
+// compiler from CSE-ing the same table entries across the several transforms
+// of one kernel (that would pin ~180 registers and wreck occupancy); the
+// reloads hit L1.
+template <typename T>
+__device__ __forceinline__ void load_tw(const T* tab, int i, T& w, T& wq) {
+  if constexpr (sizeof(T) == 4) {
+    asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(w), "=r"(wq) : "l"(tab + 2 * i));
+  } else {
+    asm volatile("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(w), "=l"(wq) : "l"(tab + 2 * i));
+  }
+}
+
+// Harvey CT butterfly: X, Y in [0,4p) -> X+WY, X-WY in [0,4p).
+template <typename T>
+__device__ __forceinline__ void ct_bfly(T& X, T& Y, T w, T wq, T p, T p2) {
+  T x = csub(X, p2);
+  T t = shoup_mul(Y, w, wq, p);
+  X = x + t;
+  Y = x - t + p2;
+}
+
+// Harvey GS butterfly: X, Y in [0,2p) -> X+Y, (X-Y)W in [0,2p).
+template <typename T>
+__device__ __forceinline__ void gs_bfly(T& X, T& Y, T w, T wq, T p, T p2) {
+  T u = csub(X + Y, p2);
+  T v = X - Y + p2;
+  Y = shoup_mul(v, w, wq, p);
+  X = u;
+}
+
+template <typename T, int LOGN, int K>
+__device__ __forceinline__ void fwd_pass(T (&x)[NttShape<LOGN>::E], const T* tw, T p, T p2) {
+  using Sh = NttShape<LOGN>;
+  constexpr int S0 = Sh::pass_s(K), R = Sh::pass_r(K);
+  constexpr int G = 1 << R;
+#pragma unroll
+  for (int gg = 0; gg < Sh::E / G; ++gg) {
+    const int g = gg * Sh::THREADS + threadIdx.x;
+    const int B = g >> (LOGN - S0 - R);
+    const T* tg = tw + 2 * (Sh::tw_off(K) + B * G);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int h = 1 << (R - i - 1);
+#pragma unroll
+      for (int jb = 0; jb < (1 << i); ++jb) {
+        T w, wq;
+        load_tw(tg, (1 << i) - 1 + jb, w, wq);
+#pragma unroll
+        for (int jj = 0; jj < h; ++jj) {
+          const int a = gg * G + jb * 2 * h + jj;
+          ct_bfly(x[a], x[a + h], w, wq, p, p2);
+        }
+      }
+    }
+  }
+}
+
+template <typename T, int LOGN, int K>
+__device__ __forceinline__ void inv_pass(T (&x)[NttShape<LOGN>::E], const T* tw, T p, T p2) {
+  using Sh = NttShape<LOGN>;
+  constexpr int S0 = Sh::pass_s(K), R = Sh::pass_r(K);
+  constexpr int G = 1 << R;
+#pragma unroll
+  for (int gg = 0; gg < Sh::E / G; ++gg) {
+    const int g = gg * Sh::THREADS + threadIdx.x;
+    const int B = g >> (LOGN - S0 - R);
+    const T* tg = tw + 2 * (Sh::tw_off(K) + B * G);
+#pragma unroll
+    for (int i = R - 1; i >= 0; --i) {
+      const int h = 1 << (R - i - 1);
+#pragma unroll
+      for (int jb = 0; jb < (1 << i); ++jb) {
+        T w, wq;
+        load_tw(tg, (1 << i) - 1 + jb, w, wq);
+#pragma unroll
+        for (int jj = 0; jj < h; ++jj) {
+          const int a = gg * G + jb * 2 * h + jj;
+          gs_bfly(x[a], x[a + h], w, wq, p, p2);
+        }
+      }
+    }
+  }
+}
+
+// Double-buffered shared-memory exchange between two pass layouts.
+template <typename T, int LOGN>
+struct Exchanger {
+  T* buf;      // 2 * SmemImage::WORDS words
+  int cur = 0;
+  template <int SA, int RA, int SB, int RB>
+  __device__ __forceinline__ void run(T (&x)[NttShape<LOGN>::E]) {
+    using Sh = NttShape<LOGN>;
+    T* b = buf + cur * SmemImage<T, LOGN>::WORDS;
+    cur ^= 1;
+    T* wa = b + phys<T, LOGN>(pass_index<LOGN, SA, RA>(threadIdx.x, 0));
+    T* wb = b + phys<T, LOGN>(pass_index<LOGN, SB, RB>(threadIdx.x, 0));
+#pragma unroll
+    for (int k = 0; k < Sh::E; ++k) wa[phys<T, LOGN>(pass_index<LOGN, SA, RA>(0, k))] = x[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < Sh::E; ++k) x[k] = wb[phys<T, LOGN>(pass_index<LOGN, SB, RB>(0, k))];
+  }
+};
+
+template <typename T, int LOGN, int K = 0>
+__device__ __forceinline__ void ntt_fwd_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN>& ex,
+                                             const T* tw, T p, T p2) {
+  using Sh = NttShape<LOGN>;
+  constexpr int S = Sh::pass_s(K), R = Sh::pass_r(K);
+  fwd_pass<T, LOGN, K>(x, tw, p, p2);
+  if constexpr (K + 1 < Sh::NPASS) {
+    ex.template run<S, R, Sh::pass_s(K + 1), Sh::pass_r(K + 1)>(x);
+    ntt_fwd_regs<T, LOGN, K + 1>(x, ex, tw, p, p2);
+  }
+}
+
+template <typename T, int LOGN, int K = NttShape<LOGN>::NPASS - 1>
+__device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN>& ex,
+                                             const T* tw, T p, T p2) {
+  using Sh = NttShape<LOGN>;
+  constexpr int S = Sh::pass_s(K), R = Sh::pass_r(K);
+  inv_pass<T, LOGN, K>(x, tw, p, p2);
+  if constexpr (K > 0) {
+    ex.template run<S, R, Sh::pass_s(K - 1), Sh::pass_r(K - 1)>(x);
+    ntt_inv_regs<T, LOGN, K - 1>(x, ex, tw, p, p2);
+  }
+}
+
+// Coefficient-domain layout (first pass, coalesced: thread t owns t + j*THREADS):
+// element index = coef_base() + coef_off(k).
+template <int LOGN>
+__device__ __forceinline__ int coef_base() {
+  return pass_index<LOGN, 0, NttShape<LOGN>::FIRST_R>(threadIdx.x, 0);
+}
+template <int LOGN>
+__host__ __device__ constexpr int coef_off(int k) {
+  return pass_index<LOGN, 0, NttShape<LOGN>::FIRST_R>(0, k);
+}
+// Evaluation-domain layout (last pass; bit-reversed storage order).
+template <int LOGN>
+__device__ __forceinline__ int eval_base() {
+  using Sh = NttShape<LOGN>;
+  return pass_index<LOGN, Sh::pass_s(Sh::NPASS - 1), Sh::pass_r(Sh::NPASS - 1)>(threadIdx.x, 0);
+}
+template <int LOGN>
+__host__ __device__ constexpr int eval_off(int k) {
+  using Sh = NttShape<LOGN>;
+  return pass_index<LOGN, Sh::pass_s(Sh::NPASS - 1), Sh::pass_r(Sh::NPASS - 1)>(0, k);
+}
+
+// Load a PrimeTab into registers (uniform across the CTA).
+template <typename T>
+struct PrimeRegs {
+  T p, p2, pinv, ninv, ninv_q, ninvr, ninvr_q, one_q, r2, r2_q, rr;
+  const T* fwd;
+  const T* inv;
+  __device__ __forceinline__ explicit PrimeRegs(const PrimeTab<T>* tab) {
+    p = tab->p; p2 = tab->p2; pinv = tab->pinv;
+    ninv = tab->ninv; ninv_q = tab->ninv_q;
+    ninvr = tab->ninvr; ninvr_q = tab->ninvr_q;
+    one_q = tab->one_q; r2 = tab->r2; r2_q = tab->r2_q; rr = tab->rr;
+    fwd = tab->fwd; inv = tab->inv;
+  }
+  // Reduce an arbitrary 64-bit value mod p into [0, 2p).
+  __device__ __forceinline__ T reduce_u64_lazy(uint64_t v) const {
+    if constexpr (sizeof(T) == 4) {
+      uint32_t hi = (uint32_t)(v >> 32), lo = (uint32_t)v;
+      uint32_t a = shoup_mul<uint32_t>(hi, r2, r2_q, p);   // hi * 2^32 mod p, [0,2p)
+      uint32_t b = shoup_mul<uint32_t>(lo, 1u, one_q, p);  // lo mod p, [0,2p)
+      return csub(a + b, p2);                               // [0,2p)
+    } else {
+      return shoup_mul<uint64_t>(v, 1ull, one_q, p);       // [0,2p)
+    }
+  }
+};
+
+}  // namespace ctb

@@ -1,0 +1,157 @@
+"""Device-resident RNS contexts: the Python face of the C ABI.
+
+PyTorch supplies device memory and the current CUDA stream (plumbing only);
+every arithmetic step runs in libctb200.so.  Residue tensors are
+[poly][limb][N] with dtype int32 for bases whose primes are < 2^30 (the words
+are the unsigned residues, all < 2^30) and int64 otherwise; plain-ring
+polynomials are int64 [poly][N] with values in [0, t).
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import torch
+
+from . import _lib
+from ._lib import BASE_B, BASE_Q, BASE_T, check
+
+__all__ = ["RnsContext", "BASE_Q", "BASE_T", "BASE_B"]
+
+
+def _stream() -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: torch.Tensor) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class RnsContext:
+    """Tables for one (N, q primes, t primes) parameter set; read-only, thread-safe."""
+
+    _cache: dict = {}
+    _cache_lock = threading.Lock()
+
+    @classmethod
+    def get(cls, n: int, q_primes, t_primes=(), relin_base_bits: int = 16, device=None) -> "RnsContext":
+        dev = torch.cuda.current_device() if device is None else torch.device(device).index
+        key = (n, tuple(int(p) for p in q_primes), tuple(int(p) for p in t_primes), relin_base_bits, dev)
+        with cls._cache_lock:
+            ctx = cls._cache.get(key)
+            if ctx is None:
+                ctx = cls(n, key[1], key[2], relin_base_bits)
+                cls._cache[key] = ctx
+        return ctx
+
+    def __init__(self, n: int, q_primes, t_primes=(), relin_base_bits: int = 16):
+        if not torch.cuda.is_available():
+            raise _lib.CtbError(_lib.CTB_ERR_CUDA, "RnsContext", "no CUDA device visible (no CPU fallback exists)")
+        self._lib = _lib.load()
+        self.n = int(n)
+        self.q_primes = tuple(int(p) for p in q_primes)
+        self.t_primes = tuple(int(p) for p in t_primes)
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        h = ctypes.c_void_p()
+        q = _lib.u64_array(self.q_primes)
+        t = _lib.u64_array(self.t_primes)
+        check(self._lib.ctb_ctx_create(ctypes.byref(h), self.n, q, len(self.q_primes), t, len(self.t_primes),
+                                       relin_base_bits), "ctb_ctx_create")
+        self._h = h
+        self.t = 1
+        for p in self.t_primes:
+            self.t *= p
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                self._lib.ctb_ctx_destroy(h)
+            except Exception:
+                pass
+
+    # -- introspection ------------------------------------------------------
+    def word_bytes(self, base: int = BASE_Q) -> int:
+        return self._lib.ctb_ctx_word_bytes(self._h, base)
+
+    def base_size(self, base: int = BASE_Q) -> int:
+        return self._lib.ctb_ctx_base_size(self._h, base)
+
+    def dtype(self, base: int = BASE_Q) -> torch.dtype:
+        return torch.int32 if self.word_bytes(base) == 4 else torch.int64
+
+    @property
+    def L(self) -> int:
+        return len(self.q_primes)
+
+    # -- checks ---------------------------------------------------------------
+    def _check_res(self, x: torch.Tensor, base: int, name: str) -> int:
+        if not (x.is_cuda and x.is_contiguous()):
+            raise ValueError(f"{name}: expected a contiguous CUDA tensor")
+        if x.dtype != self.dtype(base):
+            raise ValueError(f"{name}: expected dtype {self.dtype(base)}, got {x.dtype}")
+        L = self.base_size(base)
+        if x.dim() < 2 or x.shape[-1] != self.n or x.shape[-2] != L:
+            raise ValueError(f"{name}: expected [..., {L}, {self.n}], got {tuple(x.shape)}")
+        return x.numel() // (L * self.n)
+
+    def _check_plain(self, x: torch.Tensor, name: str) -> int:
+        if not (x.is_cuda and x.is_contiguous()) or x.dtype != torch.int64 or x.shape[-1] != self.n:
+            raise ValueError(f"{name}: expected a contiguous CUDA int64 tensor [..., {self.n}]")
+        return x.numel() // self.n
+
+    # -- kernels ----------------------------------------------------------------
+    def ntt_forward(self, x: torch.Tensor, base: int = BASE_Q, out: torch.Tensor | None = None) -> torch.Tensor:
+        npoly = self._check_res(x, base, "ntt_forward")
+        out = torch.empty_like(x) if out is None else out
+        check(self._lib.ctb_ntt_forward(self._h, base, _ptr(x), _ptr(out), npoly, _stream()), "ctb_ntt_forward")
+        return out
+
+    def ntt_inverse(self, x: torch.Tensor, base: int = BASE_Q, out: torch.Tensor | None = None) -> torch.Tensor:
+        npoly = self._check_res(x, base, "ntt_inverse")
+        out = torch.empty_like(x) if out is None else out
+        check(self._lib.ctb_ntt_inverse(self._h, base, _ptr(x), _ptr(out), npoly, _stream()), "ctb_ntt_inverse")
+        return out
+
+    def pointwise_mul(self, a: torch.Tensor, b: torch.Tensor, base: int = BASE_Q) -> torch.Tensor:
+        npoly = self._check_res(a, base, "pointwise_mul")
+        if b.shape != a.shape:
+            raise ValueError("pointwise_mul: shape mismatch")
+        self._check_res(b, base, "pointwise_mul")
+        out = torch.empty_like(a)
+        check(self._lib.ctb_pointwise_mul(self._h, base, _ptr(a), _ptr(b), _ptr(out), npoly, _stream()),
+              "ctb_pointwise_mul")
+        return out
+
+    def ring_mul(self, a: torch.Tensor, b: torch.Tensor, base: int = BASE_Q) -> torch.Tensor:
+        """Negacyclic products a[i] * b[i]; a leading dim of 1 broadcasts."""
+        na = self._check_res(a, base, "ring_mul")
+        nb = self._check_res(b, base, "ring_mul")
+        n = max(na, nb)
+        if na not in (1, n) or nb not in (1, n):
+            raise ValueError("ring_mul: batch sizes do not broadcast")
+        shape = a.shape if na == n else b.shape
+        out = torch.empty(shape, dtype=a.dtype, device=a.device)
+        check(self._lib.ctb_ring_mul(self._h, base, _ptr(a), 0 if na == 1 else 1, _ptr(b), 0 if nb == 1 else 1,
+                                     _ptr(out), n, _stream()), "ctb_ring_mul")
+        return out
+
+    def cpmul(self, ct: torch.Tensor, pt: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """ct [B, 2, L, N] x pt [B, N] (int64 in [0, t)) -> [B, 2, L, N]."""
+        if ct.dim() != 4 or ct.shape[1] != 2:
+            raise ValueError("cpmul: ciphertexts must be [B, 2, L, N]")
+        self._check_res(ct, BASE_Q, "cpmul")
+        nb = self._check_plain(pt, "cpmul")
+        if nb != ct.shape[0]:
+            raise ValueError("cpmul: one plaintext per ciphertext")
+        out = torch.empty_like(ct) if out is None else out
+        check(self._lib.ctb_cpmul(self._h, _ptr(ct), _ptr(pt), _ptr(out), ct.shape[0], _stream()), "ctb_cpmul")
+        return out
+
+    def pp_mul(self, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+        na = self._check_plain(a, "pp_mul")
+        if b.shape != a.shape:
+            raise ValueError("pp_mul: shape mismatch")
+        out = torch.empty_like(a)
+        check(self._lib.ctb_pp_mul(self._h, _ptr(a), _ptr(b), _ptr(out), na, _stream()), "ctb_pp_mul")
+        return out
