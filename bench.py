@@ -106,8 +106,8 @@ def cpu_baseline(seconds: float):
     from oracle.cpu_baseline import CpuPool, usable_cores
     pool = CpuPool(usable_cores())
     try:
-        ops, wall = pool.run(1)
-        per_proc = max(1, int(seconds / max(wall, 1e-3)))
+        pool.run(1)
+        per_proc = max(1, int(seconds / max(pool.last_per_op, 1e-3)))
         ops, wall = pool.run(per_proc)
     finally:
         pool.close()

@@ -56,11 +56,17 @@ def _make_inputs(P, seed, count):
     return cts, pts
 
 
+_STATE: dict = {}
+
+
 def _worker(args):
     seed, n_ops, n = args
-    P = H.default_params(n)
-    cts, pts = _make_inputs(P, seed, 2)
-    reference_cp_mul(cts[0], pts[0], P)  # warm twiddle plans
+    if _STATE.get("n") != n:
+        P = H.default_params(n)
+        _STATE.update(n=n, P=P, inputs=_make_inputs(P, seed, 2))
+        reference_cp_mul(_STATE["inputs"][0][0], _STATE["inputs"][1][0], P)  # warm twiddle plans
+    P = _STATE["P"]
+    cts, pts = _STATE["inputs"]
     t0 = time.perf_counter()
     for k in range(n_ops):
         reference_cp_mul(cts[k % 2], pts[k % 2], P)
@@ -82,13 +88,14 @@ class CpuPool:
         self.n = n
         self._pool = mp.get_context("fork").Pool(self.procs)
         # warm every worker's plan cache
-        self._pool.map(_worker, [(s, 1, n) for s in range(self.procs)])
+        self._pool.map(_worker, [(s, 1, n) for s in range(self.procs)], chunksize=1)
 
     def run(self, ops_per_proc: int) -> tuple[int, float]:
         """Run ops_per_proc CPMuls in every process; return (ops, wall seconds)."""
         t0 = time.perf_counter()
-        res = self._pool.map(_worker, [(1000 + s, ops_per_proc, self.n) for s in range(self.procs)])
+        res = self._pool.map(_worker, [(1000 + s, ops_per_proc, self.n) for s in range(self.procs)], chunksize=1)
         wall = time.perf_counter() - t0
+        self.last_per_op = max(r[1] / max(r[0], 1) for r in res)
         return sum(r[0] for r in res), wall
 
     def close(self):

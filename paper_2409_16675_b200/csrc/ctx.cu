@@ -1,5 +1,7 @@
 // Prime tables: twiddles, Shoup quotients, Montgomery constants.
 #include <cstring>
+#include <mutex>
+#include <unordered_set>
 #include "ctx.hpp"
 
 namespace ctb {
@@ -7,6 +9,17 @@ namespace ctb {
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 const char* get_error() { return g_err.c_str(); }
+
+static std::mutex g_attr_mu;
+static std::unordered_set<const void*> g_attr_set;
+bool smem_attr_done(const void* kern) {
+  std::lock_guard<std::mutex> g(g_attr_mu);
+  return g_attr_set.count(kern) != 0;
+}
+void smem_attr_mark(const void* kern) {
+  std::lock_guard<std::mutex> g(g_attr_mu);
+  g_attr_set.insert(kern);
+}
 
 static uint32_t bitrev(uint32_t x, uint32_t bits) {
   uint32_t y = 0;

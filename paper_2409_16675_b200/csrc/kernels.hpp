@@ -19,17 +19,21 @@ inline int cuda_status(cudaError_t e, const char* what) {
 }
 
 // Launch a CTA-per-polynomial-limb kernel with the double-buffered exchange image.
+// Per-kernel record of the dynamic shared-memory opt-in (cudaFuncSetAttribute
+// is per function, so it is keyed by the kernel pointer).
+bool smem_attr_done(const void* kern);
+void smem_attr_mark(const void* kern);
+
 // EXTRA_POLYS: additional N-word thread-private strips after the image.
 template <typename T, int LOGN, int EXTRA_POLYS = 0, typename... KArgs, typename... Args>
 inline cudaError_t launch_ntt_kernel(void (*kern)(KArgs...), size_t nblocks, cudaStream_t s,
                                      Args... args) {
   using Sh = NttShape<LOGN>;
   const size_t smem = (2 * (size_t)SmemImage<T, LOGN>::WORDS + (size_t)EXTRA_POLYS * Sh::N) * sizeof(T);
-  static bool attr_done = false;
-  if (!attr_done) {
+  if (!smem_attr_done((const void*)kern)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_done = true;
+    smem_attr_mark((const void*)kern);
   }
   if (nblocks == 0) return cudaSuccess;
   kern<<<(unsigned)nblocks, Sh::THREADS, smem, s>>>(args...);

@@ -159,7 +159,7 @@ __device__ __forceinline__ void fwd_pass(T (&x)[NttShape<LOGN>::E], const T* tw,
   constexpr int G = 1 << R;
 #pragma unroll
   for (int gg = 0; gg < Sh::E / G; ++gg) {
-    const int g = gg * Sh::THREADS + threadIdx.x;
+    const int g = gg * Sh::THREADS + pass_thread<LOGN, S0 + R == LOGN>(threadIdx.x);
     const int B = g >> (LOGN - S0 - R);
     const T* tg = tw + 2 * (Sh::tw_off(K) + B * G);
 #pragma unroll
@@ -186,7 +186,7 @@ __device__ __forceinline__ void inv_pass(T (&x)[NttShape<LOGN>::E], const T* tw,
   constexpr int G = 1 << R;
 #pragma unroll
   for (int gg = 0; gg < Sh::E / G; ++gg) {
-    const int g = gg * Sh::THREADS + threadIdx.x;
+    const int g = gg * Sh::THREADS + pass_thread<LOGN, S0 + R == LOGN>(threadIdx.x);
     const int B = g >> (LOGN - S0 - R);
     const T* tg = tw + 2 * (Sh::tw_off(K) + B * G);
 #pragma unroll
