@@ -1,4 +1,5 @@
 // Context lifetime and introspection entry points of the C ABI.
+#include <cstdlib>
 #include <string>
 #include "bigint.hpp"
 #include "ctb200.h"
@@ -26,6 +27,15 @@ extern "C" int ctb_ctx_create(ctb_ctx_t** out, uint32_t n, const uint64_t* q_pri
   if (logn > 13) { set_error("ring degree above 8192 unsupported"); return ERR_UNSUPPORTED; }
   Ctx* c = new Ctx();
   c->n = n; c->logn = logn; c->relin_base_bits = relin_base_bits;
+  {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    c->wave_chunk = 2u * (uint32_t)(sms > 0 ? sms : 148);
+    if (const char* env = std::getenv("CTB_WAVE_CHUNK")) {  // tuning knob
+      const long v = std::strtol(env, nullptr, 10);
+      if (v > 0) c->wave_chunk = (uint32_t)v;
+    }
+  }
   std::string err;
   // plain modulus t = prod t_j (< 2^63, as the reference's uint64 plain ring, ring.py:151-152)
   std::vector<uint64_t> tmod, delta;

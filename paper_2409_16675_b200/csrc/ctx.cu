@@ -1,6 +1,7 @@
 // Prime tables: twiddles, Shoup quotients, Montgomery constants.
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <unordered_set>
 #include "ctx.hpp"
 
@@ -19,6 +20,29 @@ bool smem_attr_done(const void* kern) {
 void smem_attr_mark(const void* kern) {
   std::lock_guard<std::mutex> g(g_attr_mu);
   g_attr_set.insert(kern);
+}
+
+static std::mutex g_grid_mu;
+static std::unordered_map<const void*, uint32_t> g_grid;
+uint32_t persistent_grid(const void* kern, int threads, size_t smem) {
+  {
+    std::lock_guard<std::mutex> g(g_grid_mu);
+    auto it = g_grid.find(kern);
+    if (it != g_grid.end()) return it->second;
+  }
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (!smem_attr_done(kern)) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_attr_mark(kern);
+  }
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  const uint32_t grid = (uint32_t)(sms * per_sm);
+  std::lock_guard<std::mutex> g(g_grid_mu);
+  g_grid[kern] = grid;
+  return grid;
 }
 
 static uint32_t bitrev(uint32_t x, uint32_t bits) {
@@ -53,8 +77,8 @@ static int build_typed(Base& b, uint32_t logn, std::string& err, const uint64_t*
   const uint32_t n = 1u << logn;
   constexpr int W = 8 * sizeof(T);
   std::vector<PrimeTab<T>> tabs(L);
-  const int ent = shape_tw_entries((int)logn);  // pass-major pairs per direction
-  std::vector<T> tw((size_t)L * 2 * 2 * ent);
+  const int ent = shape_tw_entries((int)logn);  // pairs per prime (both directions)
+  std::vector<T> tw((size_t)L * 2 * ent);
   cudaError_t ce = cudaMalloc(&b.d_tw, tw.size() * sizeof(T));
   if (ce != cudaSuccess) { err = std::string("cudaMalloc twiddles: ") + cudaGetErrorString(ce); return -2; }
   ce = cudaMalloc(&b.d_tabs, sizeof(PrimeTab<T>) * (L ? L : 1));
@@ -64,24 +88,22 @@ static int build_typed(Base& b, uint32_t logn, std::string& err, const uint64_t*
     const uint64_t p = b.primes[l];
     uint64_t psi;
     if (!find_psi(p, n, psi)) { err = "no primitive 2N-th root of unity mod " + std::to_string(p); return -1; }
-    const uint64_t psi_inv = invmod(psi, p);
-    T* f = tw.data() + (size_t)l * 4 * ent;
-    T* iv = f + 2 * ent;
+    T* f = tw.data() + (size_t)l * 2 * ent;
     // powers in natural order, then scatter by bit reversal
-    std::vector<uint64_t> pw(n), pwi(n);
-    pw[0] = 1; pwi[0] = 1;
-    for (uint32_t i = 1; i < n; ++i) { pw[i] = mulmod(pw[i - 1], psi, p); pwi[i] = mulmod(pwi[i - 1], psi_inv, p); }
-    // pass k, group B, stage i, block jb  ->  table index m + b = 2^(s+i) + B*2^i + jb
+    std::vector<uint64_t> pw(n);
+    pw[0] = 1;
+    for (uint32_t i = 1; i < n; ++i) pw[i] = mulmod(pw[i - 1], psi, p);
+    // pass k, group B, stage i, block jb -> psi^bitrev(2^(s+i) + B*2^i + jb) at pair
+    // tw_off(k) + e * 2^s + B with e = 2^i - 1 + jb (entry-major, see ntt.cuh TwSrc)
     for (int k = 0; k < shape_npass((int)logn); ++k) {
       const int s = shape_pass_s((int)logn, k), r = shape_pass_r((int)logn, k);
       for (int B = 0; B < (1 << s); ++B)
         for (int i = 0; i < r; ++i)
           for (int jb = 0; jb < (1 << i); ++jb) {
             const uint32_t mb = (1u << (s + i)) + ((uint32_t)B << i) + jb;
-            const size_t e = (size_t)shape_tw_off((int)logn, k) + (size_t)B * (1u << r) + (1u << i) - 1 + jb;
-            const uint64_t w = pw[bitrev(mb, logn)], wi = pwi[bitrev(mb, logn)];
+            const size_t e = (size_t)shape_tw_off((int)logn, k) + ((size_t)((1u << i) - 1 + jb) << s) + B;
+            const uint64_t w = pw[bitrev(mb, logn)];
             f[2 * e] = (T)w;  f[2 * e + 1] = shoup_q<T>(w, p);
-            iv[2 * e] = (T)wi; iv[2 * e + 1] = shoup_q<T>(wi, p);
           }
     }
     PrimeTab<T>& t = tabs[l];
@@ -100,8 +122,8 @@ static int build_typed(Base& b, uint32_t logn, std::string& err, const uint64_t*
     t.rr = (T)mulmod(R, R, p);
     if (tmod) t.tmod = (T)(tmod[l] % p);
     if (delta) { t.delta = (T)(delta[l] % p); t.delta_q = shoup_q<T>(delta[l] % p, p); }
-    t.fwd = d_tw + (size_t)l * 4 * ent;
-    t.inv = t.fwd + 2 * ent;
+    t.fwd = d_tw + (size_t)l * 2 * ent;
+    t.inv = t.fwd;
   }
   ce = cudaMemcpy(b.d_tw, tw.data(), tw.size() * sizeof(T), cudaMemcpyHostToDevice);
   if (ce == cudaSuccess && L)

@@ -40,6 +40,23 @@ inline cudaError_t launch_ntt_kernel(void (*kern)(KArgs...), size_t nblocks, cud
   return cudaGetLastError();
 }
 
+// Resident CTAs per SM x SM count for a persistent kernel (cached per kernel).
+uint32_t persistent_grid(const void* kern, int threads, size_t smem);
+
+// Launch with an explicit grid and dynamic shared memory (opt-in handled).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_kernel_grid(void (*kern)(KArgs...), uint32_t grid, int threads, size_t smem,
+                                      cudaStream_t s, Args... args) {
+  if (!smem_attr_done((const void*)kern)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    smem_attr_mark((const void*)kern);
+  }
+  if (grid == 0) return cudaSuccess;
+  kern<<<grid, threads, smem, s>>>(args...);
+  return cudaGetLastError();
+}
+
 #define CTB_CASE_LOGN(L_, ...) \
   case L_: {                   \
     constexpr int LOGN = L_;   \

@@ -94,49 +94,71 @@ __global__ void k_pointwise(const T* a, const T* b, T* out, const PrimeTab<T>* _
 }
 
 // Fused CPMul: ct [B][2][L][N] x pt [B][N] (uint64 in [0,t)) -> out [B][2][L][N].
-// One CTA per (ciphertext, limb): NTT of the centred lift of pt once (scaled
-// into the Montgomery domain with N^-1 folded), then per part: NTT, slotwise
-// Montgomery product, INTT, canonical store.  he.py:366-382 / he.py:325-327.
-template <typename T, int LOGN>
+// he.py:366-382 with the centred lift of he.py:325-327.
+//
+// Persistent and limb-stationary: CTA k serves limb k % L for ciphertexts
+// k / L, k / L + n_l, ... (n_l = CTAs on that limb).  With SMEM_TW it first
+// stages its prime's twiddle table (35 KB at N=4096) in shared memory, so every
+// butterfly's twiddle is a conflict-free LDS instead of an L1/L2 round trip.
+// Per ciphertext: NTT(lift(pt)) once -- scaled by N^-1 * 2^32 into the
+// Montgomery domain and parked in a thread-private shared strip -- then per
+// part: NTT, slotwise Montgomery product, INTT, canonical store.  The 7 limb
+// groups advance through the batch together, so a plaintext read by all 7
+// limbs is an L2 hit after the first.
+template <typename T, int LOGN, bool SMEM_TW>
 __global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
 k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>* __restrict__ tabs,
-        int L, uint64_t t_half) {
+        int L, uint64_t t_half, uint32_t batch) {
   using Sh = NttShape<LOGN>;
+  constexpr int TW_WORDS = SMEM_TW ? 2 * shape_tw_entries(LOGN) : 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Exchanger<T, LOGN> ex{reinterpret_cast<T*>(smem_raw)};
-  // NTT(lift(pt)) parks in a thread-private shared-memory strip (slot k of
-  // thread t at k*THREADS + t: conflict-free, no barrier needed) so that only
-  // one transform's worth of residues is live in registers.
-  T* ysm = reinterpret_cast<T*>(smem_raw) + 2 * SmemImage<T, LOGN>::WORDS + threadIdx.x;
+  T* tw_sm = reinterpret_cast<T*>(smem_raw);
+  Exchanger<T, LOGN> ex{tw_sm + TW_WORDS};
+  T* ysm = tw_sm + TW_WORDS + 2 * SmemImage<T, LOGN>::WORDS + threadIdx.x;
+
   const int limb = blockIdx.x % L;
-  const size_t b = blockIdx.x / L;
+  const uint32_t first = blockIdx.x / L;
+  const uint32_t stride = (gridDim.x - limb + L - 1) / L;  // CTAs serving this limb
   PrimeRegs<T> pr(tabs + limb);
   const T tmod = tabs[limb].tmod;
-  T x[Sh::E];
-  {
-    const uint64_t* ppt = pt + b * Sh::N + coef_base<LOGN>();
-#pragma unroll
-    for (int k = 0; k < Sh::E; ++k) {
-      const uint64_t v = __ldg(ppt + coef_off<LOGN>(k));
-      T r = csub(pr.reduce_u64_lazy(v), pr.p);         // v mod p
-      if (v > t_half) r = sub_mod(r, tmod, pr.p);       // centred lift: v - t (he.py:325-327)
-      x[k] = r;
-    }
-    ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
-#pragma unroll
-    for (int k = 0; k < Sh::E; ++k) ysm[k * Sh::THREADS] = shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p);
+  const T* twp = pr.fwd;
+  if constexpr (SMEM_TW) {
+    const uint4* src = reinterpret_cast<const uint4*>(pr.fwd);
+    uint4* dst = reinterpret_cast<uint4*>(tw_sm);
+    for (int i = threadIdx.x; i < TW_WORDS * (int)sizeof(T) / 16; i += Sh::THREADS) dst[i] = __ldg(src + i);
+    __syncthreads();
+    twp = tw_sm;
   }
+  const TwSrc<T, SMEM_TW> tw{twp};
+
+  T x[Sh::E];
 #pragma unroll 1
-  for (int part = 0; part < 2; ++part) {
-    const size_t off = ((b * 2 + part) * L + limb) * (size_t)Sh::N + coef_base<LOGN>();
+  for (uint32_t b = first; b < batch; b += stride) {
+    {
+      const uint64_t* ppt = pt + (size_t)b * Sh::N + coef_base<LOGN>();
 #pragma unroll
-    for (int k = 0; k < Sh::E; ++k) x[k] = ct[off + coef_off<LOGN>(k)];
-    ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
+      for (int k = 0; k < Sh::E; ++k) {
+        const uint64_t v = __ldg(ppt + coef_off<LOGN>(k));
+        T r = csub(pr.reduce_u64_lazy(v), pr.p);         // v mod p
+        if (v > t_half) r = sub_mod(r, tmod, pr.p);       // centred lift: v - t
+        x[k] = r;
+      }
+      ntt_fwd_regs<T, LOGN, 0, SMEM_TW>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
-    for (int k = 0; k < Sh::E; ++k) x[k] = mont_mul(x[k], ysm[k * Sh::THREADS], pr.p, pr.pinv);
-    ntt_inv_regs<T, LOGN>(x, ex, pr.inv, pr.p, pr.p2);
+      for (int k = 0; k < Sh::E; ++k) ysm[k * Sh::THREADS] = shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p);
+    }
+#pragma unroll 1
+    for (int part = 0; part < 2; ++part) {
+      const size_t off = (((size_t)b * 2 + part) * L + limb) * (size_t)Sh::N + coef_base<LOGN>();
 #pragma unroll
-    for (int k = 0; k < Sh::E; ++k) out[off + coef_off<LOGN>(k)] = csub(x[k], pr.p);
+      for (int k = 0; k < Sh::E; ++k) x[k] = ct[off + coef_off<LOGN>(k)];
+      ntt_fwd_regs<T, LOGN, 0, SMEM_TW>(x, ex, tw, pr.p, pr.p2);
+#pragma unroll
+      for (int k = 0; k < Sh::E; ++k) x[k] = mont_mul(x[k], ysm[k * Sh::THREADS], pr.p, pr.pinv);
+      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW>(x, ex, tw, pr.p, pr.p2);
+#pragma unroll
+      for (int k = 0; k < Sh::E; ++k) out[off + coef_off<LOGN>(k)] = csub(x[k], pr.p);
+    }
   }
 }
 
@@ -285,22 +307,37 @@ extern "C" int ctb_ring_mul(const ctb_ctx_t* ctx, int base, const void* a, uint6
   return cuda_status(e, "ctb_ring_mul");
 }
 
+template <typename T, int LOGN>
+static cudaError_t launch_cpmul(const Ctx* c, const Base* b, const void* ct, const uint64_t* pt, void* out,
+                                uint64_t batch, cudaStream_t s) {
+  using Sh = NttShape<LOGN>;
+  // twiddles in shared memory when the table fits beside the exchange image
+  constexpr size_t tw_bytes = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
+  constexpr size_t base_bytes = (2 * (size_t)SmemImage<T, LOGN>::WORDS + Sh::N) * sizeof(T);
+  constexpr bool SMEM_TW = sizeof(T) == 4 && LOGN >= 9 && tw_bytes + base_bytes <= 200 * 1024;
+  auto kern = k_cpmul<T, LOGN, SMEM_TW>;
+  const size_t smem = base_bytes + (SMEM_TW ? tw_bytes : 0);
+  const int L = b->size();
+  const uint64_t items = batch * (uint64_t)L;
+  if (items == 0) return cudaSuccess;
+  uint32_t grid = persistent_grid((const void*)kern, Sh::THREADS, smem);
+  grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(grid / L * L, (uint64_t)L), items);
+  return launch_kernel_grid(kern, grid, Sh::THREADS, smem, s, (const T*)ct, pt, (T*)out,
+                            (const PrimeTab<T>*)b->d_tabs, L, c->t_half, (uint32_t)batch);
+}
+
 extern "C" int ctb_cpmul(const ctb_ctx_t* ctx, const void* ct, const uint64_t* pt, void* out, uint64_t batch,
                          void* stream) {
   const Base* b = base_of(ctx, BASE_Q);
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
   if (!b || !c->t || !ct || !pt || !out) { set_error("ctb_cpmul: bad context (needs cipher+plain ring) or buffer"); return ERR_ARG; }
-  const size_t nblk = batch * b->size();
+  if (batch >= (1ull << 32)) { set_error("ctb_cpmul: batch too large"); return ERR_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
   if (b->word == 4) {
-    using T = uint32_t;
-    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN, 1>(k_cpmul<T, LOGN>, nblk, s, (const T*)ct, pt, (T*)out,
-                                                         (const PrimeTab<T>*)b->d_tabs, b->size(), c->t_half)));
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_cpmul<uint32_t, LOGN>(c, b, ct, pt, out, batch, s)));
   } else {
-    using T = uint64_t;
-    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN, 1>(k_cpmul<T, LOGN>, nblk, s, (const T*)ct, pt, (T*)out,
-                                                         (const PrimeTab<T>*)b->d_tabs, b->size(), c->t_half)));
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_cpmul<uint64_t, LOGN>(c, b, ct, pt, out, batch, s)));
   }
   return cuda_status(e, "ctb_cpmul");
 }

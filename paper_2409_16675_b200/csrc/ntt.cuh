@@ -35,8 +35,8 @@ struct PrimeTab {
   T rr;                 // 2^(2W) mod p (leaves the Montgomery domain)
   T tmod;               // plain modulus t mod p (cipher base only: centred lift)
   T delta, delta_q;     // floor(q/t) mod p and Shoup quotient (cipher base only)
-  const T* fwd;         // pass-major (w, w') pairs, w = psi^bitrev(m + b)   (shape_tw_off)
-  const T* inv;         // same layout, psi^-bitrev(m + b)
+  const T* fwd;         // (w, w') pairs, pass-major / entry-major (see TwSrc); serves both directions
+  const T* inv;         // == fwd (kept for layout stability)
 };
 
 // Pass schedule of the CTA transform, as runtime-capable constexpr functions
@@ -121,18 +121,35 @@ __host__ __device__ constexpr int pass_index(int t, int k) {
   return B * (Sh::N >> S0) + o + j * S;
 }
 
-// Twiddle pair (w, w') load through the read-only path.  volatile keeps the
-// compiler from CSE-ing the same table entries across the several transforms
-// of one kernel (that would pin ~180 registers and wreck occupancy); the
-// reloads hit L1.
-template <typename T>
-__device__ __forceinline__ void load_tw(const T* tab, int i, T& w, T& wq) {
-  if constexpr (sizeof(T) == 4) {
-    asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(w), "=r"(wq) : "l"(tab + 2 * i));
-  } else {
-    asm volatile("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(w), "=l"(wq) : "l"(tab + 2 * i));
+// Twiddle table: ONE table per prime serves both directions.  Entry for
+// forward stage s+i, butterfly block b = B*2^i + jb (pass k, group B) holds
+// (w, w') with w = psi^bitrev(2^(s+i) + b).  Entries are stored entry-major
+// inside a pass -- pair index tw_off(k) + e*2^s + B with e = 2^i - 1 + jb --
+// so the lanes of a warp (distinct or equal B) read consecutive or identical
+// pairs: coalesced from global, bank-conflict-free from shared memory.
+// The inverse transform reads the same table mirrored (group 2^s-1-B, block
+// 2^i-1-jb) because psi^-bitrev(m+b) = -psi^bitrev(2m-1-b); the sign is
+// folded into the Gentleman-Sande butterfly as (Y - X) * w.
+// Loads are volatile so the compiler cannot CSE table entries across the
+// several transforms of one kernel (which pinned ~180 registers).
+template <typename T, bool SMEM>
+struct TwSrc {
+  const T* tab;  // generic pointer to pair 0 of this prime's table (global or shared)
+  __device__ __forceinline__ void load(const T* at, T& w, T& wq) const {
+    if constexpr (SMEM) {
+      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(at);
+      if constexpr (sizeof(T) == 4)
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w), "=r"(wq) : "r"(sa));
+      else
+        asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(w), "=l"(wq) : "r"(sa));
+    } else {
+      if constexpr (sizeof(T) == 4)
+        asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(w), "=r"(wq) : "l"(at));
+      else
+        asm volatile("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(w), "=l"(wq) : "l"(at));
+    }
   }
-}
+};
 
 // Harvey CT butterfly: X, Y in [0,4p) -> X+WY, X-WY in [0,4p).
 template <typename T>
@@ -143,17 +160,18 @@ __device__ __forceinline__ void ct_bfly(T& X, T& Y, T w, T wq, T p, T p2) {
   Y = x - t + p2;
 }
 
-// Harvey GS butterfly: X, Y in [0,2p) -> X+Y, (X-Y)W in [0,2p).
+// Harvey GS butterfly with the mirrored (negated) twiddle:
+// X, Y in [0,2p) -> X+Y, (Y-X)W in [0,2p).
 template <typename T>
 __device__ __forceinline__ void gs_bfly(T& X, T& Y, T w, T wq, T p, T p2) {
   T u = csub(X + Y, p2);
-  T v = X - Y + p2;
+  T v = Y - X + p2;
   Y = shoup_mul(v, w, wq, p);
   X = u;
 }
 
-template <typename T, int LOGN, int K>
-__device__ __forceinline__ void fwd_pass(T (&x)[NttShape<LOGN>::E], const T* tw, T p, T p2) {
+template <typename T, int LOGN, int K, bool SMEM>
+__device__ __forceinline__ void fwd_pass(T (&x)[NttShape<LOGN>::E], TwSrc<T, SMEM> tw, T p, T p2) {
   using Sh = NttShape<LOGN>;
   constexpr int S0 = Sh::pass_s(K), R = Sh::pass_r(K);
   constexpr int G = 1 << R;
@@ -161,14 +179,14 @@ __device__ __forceinline__ void fwd_pass(T (&x)[NttShape<LOGN>::E], const T* tw,
   for (int gg = 0; gg < Sh::E / G; ++gg) {
     const int g = gg * Sh::THREADS + pass_thread<LOGN, S0 + R == LOGN>(threadIdx.x);
     const int B = g >> (LOGN - S0 - R);
-    const T* tg = tw + 2 * (Sh::tw_off(K) + B * G);
+    const T* tg = tw.tab + 2 * (Sh::tw_off(K) + B);
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const int h = 1 << (R - i - 1);
 #pragma unroll
       for (int jb = 0; jb < (1 << i); ++jb) {
         T w, wq;
-        load_tw(tg, (1 << i) - 1 + jb, w, wq);
+        tw.load(tg + 2 * (((1 << i) - 1 + jb) << S0), w, wq);
 #pragma unroll
         for (int jj = 0; jj < h; ++jj) {
           const int a = gg * G + jb * 2 * h + jj;
@@ -179,23 +197,23 @@ __device__ __forceinline__ void fwd_pass(T (&x)[NttShape<LOGN>::E], const T* tw,
   }
 }
 
-template <typename T, int LOGN, int K>
-__device__ __forceinline__ void inv_pass(T (&x)[NttShape<LOGN>::E], const T* tw, T p, T p2) {
+template <typename T, int LOGN, int K, bool SMEM>
+__device__ __forceinline__ void inv_pass(T (&x)[NttShape<LOGN>::E], TwSrc<T, SMEM> tw, T p, T p2) {
   using Sh = NttShape<LOGN>;
   constexpr int S0 = Sh::pass_s(K), R = Sh::pass_r(K);
   constexpr int G = 1 << R;
 #pragma unroll
   for (int gg = 0; gg < Sh::E / G; ++gg) {
     const int g = gg * Sh::THREADS + pass_thread<LOGN, S0 + R == LOGN>(threadIdx.x);
-    const int B = g >> (LOGN - S0 - R);
-    const T* tg = tw + 2 * (Sh::tw_off(K) + B * G);
+    const int Bm = (1 << S0) - 1 - (g >> (LOGN - S0 - R));  // mirrored group
+    const T* tg = tw.tab + 2 * (Sh::tw_off(K) + Bm);
 #pragma unroll
     for (int i = R - 1; i >= 0; --i) {
       const int h = 1 << (R - i - 1);
 #pragma unroll
       for (int jb = 0; jb < (1 << i); ++jb) {
         T w, wq;
-        load_tw(tg, (1 << i) - 1 + jb, w, wq);
+        tw.load(tg + 2 * (((1 << i) - 1 + ((1 << i) - 1 - jb)) << S0), w, wq);
 #pragma unroll
         for (int jj = 0; jj < h; ++jj) {
           const int a = gg * G + jb * 2 * h + jj;
@@ -226,28 +244,40 @@ struct Exchanger {
   }
 };
 
-template <typename T, int LOGN, int K = 0>
+template <typename T, int LOGN, int K = 0, bool SMEM>
 __device__ __forceinline__ void ntt_fwd_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN>& ex,
-                                             const T* tw, T p, T p2) {
+                                             TwSrc<T, SMEM> tw, T p, T p2) {
   using Sh = NttShape<LOGN>;
   constexpr int S = Sh::pass_s(K), R = Sh::pass_r(K);
-  fwd_pass<T, LOGN, K>(x, tw, p, p2);
+  fwd_pass<T, LOGN, K, SMEM>(x, tw, p, p2);
   if constexpr (K + 1 < Sh::NPASS) {
     ex.template run<S, R, Sh::pass_s(K + 1), Sh::pass_r(K + 1)>(x);
-    ntt_fwd_regs<T, LOGN, K + 1>(x, ex, tw, p, p2);
+    ntt_fwd_regs<T, LOGN, K + 1, SMEM>(x, ex, tw, p, p2);
   }
 }
 
-template <typename T, int LOGN, int K = NttShape<LOGN>::NPASS - 1>
+template <typename T, int LOGN, int K = NttShape<LOGN>::NPASS - 1, bool SMEM>
 __device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN>& ex,
-                                             const T* tw, T p, T p2) {
+                                             TwSrc<T, SMEM> tw, T p, T p2) {
   using Sh = NttShape<LOGN>;
   constexpr int S = Sh::pass_s(K), R = Sh::pass_r(K);
-  inv_pass<T, LOGN, K>(x, tw, p, p2);
+  inv_pass<T, LOGN, K, SMEM>(x, tw, p, p2);
   if constexpr (K > 0) {
     ex.template run<S, R, Sh::pass_s(K - 1), Sh::pass_r(K - 1)>(x);
-    ntt_inv_regs<T, LOGN, K - 1>(x, ex, tw, p, p2);
+    ntt_inv_regs<T, LOGN, K - 1, SMEM>(x, ex, tw, p, p2);
   }
+}
+
+// Convenience wrappers reading the twiddles through the global read-only path.
+template <typename T, int LOGN>
+__device__ __forceinline__ void ntt_fwd_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN>& ex,
+                                             const T* tw, T p, T p2) {
+  ntt_fwd_regs<T, LOGN, 0, false>(x, ex, TwSrc<T, false>{tw}, p, p2);
+}
+template <typename T, int LOGN>
+__device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN>& ex,
+                                             const T* tw, T p, T p2) {
+  ntt_inv_regs<T, LOGN, NttShape<LOGN>::NPASS - 1, false>(x, ex, TwSrc<T, false>{tw}, p, p2);
 }
 
 // Coefficient-domain layout (first pass, coalesced: thread t owns t + j*THREADS):
