@@ -101,7 +101,8 @@ static int build_typed(Base& b, uint32_t logn, std::string& err, const uint64_t*
         for (int i = 0; i < r; ++i)
           for (int jb = 0; jb < (1 << i); ++jb) {
             const uint32_t mb = (1u << (s + i)) + ((uint32_t)B << i) + jb;
-            const size_t e = (size_t)shape_tw_off((int)logn, k) + ((size_t)((1u << i) - 1 + jb) << s) + B;
+            const size_t e = (size_t)shape_tw_off((int)logn, k) + ((size_t)((1u << i) - 1 + jb) << s) +
+                             tw_group_slot((int)logn, s, r, B);
             const uint64_t w = pw[bitrev(mb, logn)];
             f[2 * e] = (T)w;  f[2 * e + 1] = shoup_q<T>(w, p);
           }

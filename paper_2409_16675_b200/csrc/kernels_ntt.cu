@@ -105,6 +105,8 @@ __global__ void k_pointwise(const T* a, const T* b, T* out, const PrimeTab<T>* _
 // part: NTT, slotwise Montgomery product, INTT, canonical store.  The 7 limb
 // groups advance through the batch together, so a plaintext read by all 7
 // limbs is an L2 hit after the first.
+constexpr int CPMUL_NBUF = 1;
+
 template <typename T, int LOGN, bool SMEM_TW>
 __global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
 k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>* __restrict__ tabs,
@@ -113,8 +115,8 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
   constexpr int TW_WORDS = SMEM_TW ? 2 * shape_tw_entries(LOGN) : 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
-  Exchanger<T, LOGN> ex{tw_sm + TW_WORDS};
-  T* ysm = tw_sm + TW_WORDS + 2 * SmemImage<T, LOGN>::WORDS + threadIdx.x;
+  Exchanger<T, LOGN, CPMUL_NBUF> ex{tw_sm + TW_WORDS};
+  T* ysm = tw_sm + TW_WORDS + Exchanger<T, LOGN, CPMUL_NBUF>::WORDS + threadIdx.x;
 
   const int limb = blockIdx.x % L;
   const uint32_t first = blockIdx.x / L;
@@ -143,7 +145,7 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
         if (v > t_half) r = sub_mod(r, tmod, pr.p);       // centred lift: v - t
         x[k] = r;
       }
-      ntt_fwd_regs<T, LOGN, 0, SMEM_TW>(x, ex, tw, pr.p, pr.p2);
+      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) ysm[k * Sh::THREADS] = shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p);
     }
@@ -152,10 +154,10 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
       const size_t off = (((size_t)b * 2 + part) * L + limb) * (size_t)Sh::N + coef_base<LOGN>();
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) x[k] = ct[off + coef_off<LOGN>(k)];
-      ntt_fwd_regs<T, LOGN, 0, SMEM_TW>(x, ex, tw, pr.p, pr.p2);
+      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) x[k] = mont_mul(x[k], ysm[k * Sh::THREADS], pr.p, pr.pinv);
-      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW>(x, ex, tw, pr.p, pr.p2);
+      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, CPMUL_NBUF>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) out[off + coef_off<LOGN>(k)] = csub(x[k], pr.p);
     }
@@ -313,7 +315,7 @@ static cudaError_t launch_cpmul(const Ctx* c, const Base* b, const void* ct, con
   using Sh = NttShape<LOGN>;
   // twiddles in shared memory when the table fits beside the exchange image
   constexpr size_t tw_bytes = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
-  constexpr size_t base_bytes = (2 * (size_t)SmemImage<T, LOGN>::WORDS + Sh::N) * sizeof(T);
+  constexpr size_t base_bytes = ((size_t)Exchanger<T, LOGN, CPMUL_NBUF>::WORDS + Sh::N) * sizeof(T);
   constexpr bool SMEM_TW = sizeof(T) == 4 && LOGN >= 9 && tw_bytes + base_bytes <= 200 * 1024;
   auto kern = k_cpmul<T, LOGN, SMEM_TW>;
   const size_t smem = base_bytes + (SMEM_TW ? tw_bytes : 0);

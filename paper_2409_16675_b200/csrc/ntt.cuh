@@ -132,6 +132,28 @@ __host__ __device__ constexpr int pass_index(int t, int k) {
 // folded into the Gentleman-Sande butterfly as (Y - X) * w.
 // Loads are volatile so the compiler cannot CSE table entries across the
 // several transforms of one kernel (which pinned ~180 registers).
+// Storage slot of the twiddle group served by (thread, gg) in pass (S0, R).
+// Groups are stored in thread order: for the last pass, whose thread -> group
+// map is permuted (pass_thread), slot = gg*THREADS + t rather than the group
+// number, so consecutive lanes read consecutive pairs.  Complementing a group
+// (the inverse's mirror) commutes with that bit permutation.
+template <int LOGN, int S0, int R>
+__device__ __forceinline__ int tw_slot(int gg) {
+  using Sh = NttShape<LOGN>;
+  if constexpr (S0 + R == LOGN) {
+    return gg * Sh::THREADS + threadIdx.x;
+  } else {
+    const int g = gg * Sh::THREADS + threadIdx.x;
+    return g >> (LOGN - S0 - R);
+  }
+}
+
+// Host helper: storage slot of group B in pass (s, r) (inverse of the above).
+__host__ __device__ constexpr int tw_group_slot(int logn, int s, int r, int B) {
+  if (s + r == logn && logn >= 10) return ((B >> 1) & 31) | ((B & 1) << 5) | (B & ~63);
+  return B;
+}
+
 template <typename T, bool SMEM>
 struct TwSrc {
   const T* tab;  // generic pointer to pair 0 of this prime's table (global or shared)
@@ -177,9 +199,8 @@ __device__ __forceinline__ void fwd_pass(T (&x)[NttShape<LOGN>::E], TwSrc<T, SME
   constexpr int G = 1 << R;
 #pragma unroll
   for (int gg = 0; gg < Sh::E / G; ++gg) {
-    const int g = gg * Sh::THREADS + pass_thread<LOGN, S0 + R == LOGN>(threadIdx.x);
-    const int B = g >> (LOGN - S0 - R);
-    const T* tg = tw.tab + 2 * (Sh::tw_off(K) + B);
+    const int slot = tw_slot<LOGN, S0, R>(gg);
+    const T* tg = tw.tab + 2 * (Sh::tw_off(K) + slot);
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const int h = 1 << (R - i - 1);
@@ -204,9 +225,8 @@ __device__ __forceinline__ void inv_pass(T (&x)[NttShape<LOGN>::E], TwSrc<T, SME
   constexpr int G = 1 << R;
 #pragma unroll
   for (int gg = 0; gg < Sh::E / G; ++gg) {
-    const int g = gg * Sh::THREADS + pass_thread<LOGN, S0 + R == LOGN>(threadIdx.x);
-    const int Bm = (1 << S0) - 1 - (g >> (LOGN - S0 - R));  // mirrored group
-    const T* tg = tw.tab + 2 * (Sh::tw_off(K) + Bm);
+    const int slot = (1 << S0) - 1 - tw_slot<LOGN, S0, R>(gg);  // mirrored group
+    const T* tg = tw.tab + 2 * (Sh::tw_off(K) + slot);
 #pragma unroll
     for (int i = R - 1; i >= 0; --i) {
       const int h = 1 << (R - i - 1);
@@ -224,16 +244,20 @@ __device__ __forceinline__ void inv_pass(T (&x)[NttShape<LOGN>::E], TwSrc<T, SME
   }
 }
 
-// Double-buffered shared-memory exchange between two pass layouts.
-template <typename T, int LOGN>
+// Shared-memory exchange between two pass layouts.  NBUF = 2 double-buffers
+// (one barrier per exchange); NBUF = 1 halves the footprint for one more
+// resident CTA at the price of a second barrier (write-after-read guard).
+template <typename T, int LOGN, int NBUF = 2>
 struct Exchanger {
-  T* buf;      // 2 * SmemImage::WORDS words
+  T* buf;      // NBUF * SmemImage::WORDS words
   int cur = 0;
+  static constexpr int WORDS = NBUF * SmemImage<T, LOGN>::WORDS;
   template <int SA, int RA, int SB, int RB>
   __device__ __forceinline__ void run(T (&x)[NttShape<LOGN>::E]) {
     using Sh = NttShape<LOGN>;
     T* b = buf + cur * SmemImage<T, LOGN>::WORDS;
-    cur ^= 1;
+    if constexpr (NBUF == 2) cur ^= 1;
+    else __syncthreads();
     T* wa = b + phys<T, LOGN>(pass_index<LOGN, SA, RA>(threadIdx.x, 0));
     T* wb = b + phys<T, LOGN>(pass_index<LOGN, SB, RB>(threadIdx.x, 0));
 #pragma unroll
@@ -244,27 +268,27 @@ struct Exchanger {
   }
 };
 
-template <typename T, int LOGN, int K = 0, bool SMEM>
-__device__ __forceinline__ void ntt_fwd_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN>& ex,
+template <typename T, int LOGN, int K = 0, bool SMEM, int NBUF>
+__device__ __forceinline__ void ntt_fwd_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN, NBUF>& ex,
                                              TwSrc<T, SMEM> tw, T p, T p2) {
   using Sh = NttShape<LOGN>;
   constexpr int S = Sh::pass_s(K), R = Sh::pass_r(K);
   fwd_pass<T, LOGN, K, SMEM>(x, tw, p, p2);
   if constexpr (K + 1 < Sh::NPASS) {
     ex.template run<S, R, Sh::pass_s(K + 1), Sh::pass_r(K + 1)>(x);
-    ntt_fwd_regs<T, LOGN, K + 1, SMEM>(x, ex, tw, p, p2);
+    ntt_fwd_regs<T, LOGN, K + 1, SMEM, NBUF>(x, ex, tw, p, p2);
   }
 }
 
-template <typename T, int LOGN, int K = NttShape<LOGN>::NPASS - 1, bool SMEM>
-__device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN>& ex,
+template <typename T, int LOGN, int K = NttShape<LOGN>::NPASS - 1, bool SMEM, int NBUF>
+__device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN, NBUF>& ex,
                                              TwSrc<T, SMEM> tw, T p, T p2) {
   using Sh = NttShape<LOGN>;
   constexpr int S = Sh::pass_s(K), R = Sh::pass_r(K);
   inv_pass<T, LOGN, K, SMEM>(x, tw, p, p2);
   if constexpr (K > 0) {
     ex.template run<S, R, Sh::pass_s(K - 1), Sh::pass_r(K - 1)>(x);
-    ntt_inv_regs<T, LOGN, K - 1, SMEM>(x, ex, tw, p, p2);
+    ntt_inv_regs<T, LOGN, K - 1, SMEM, NBUF>(x, ex, tw, p, p2);
   }
 }
 
@@ -272,12 +296,12 @@ __device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchange
 template <typename T, int LOGN>
 __device__ __forceinline__ void ntt_fwd_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN>& ex,
                                              const T* tw, T p, T p2) {
-  ntt_fwd_regs<T, LOGN, 0, false>(x, ex, TwSrc<T, false>{tw}, p, p2);
+  ntt_fwd_regs<T, LOGN, 0, false, 2>(x, ex, TwSrc<T, false>{tw}, p, p2);
 }
 template <typename T, int LOGN>
 __device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN>& ex,
                                              const T* tw, T p, T p2) {
-  ntt_inv_regs<T, LOGN, NttShape<LOGN>::NPASS - 1, false>(x, ex, TwSrc<T, false>{tw}, p, p2);
+  ntt_inv_regs<T, LOGN, NttShape<LOGN>::NPASS - 1, false, 2>(x, ex, TwSrc<T, false>{tw}, p, p2);
 }
 
 // Coefficient-domain layout (first pass, coalesced: thread t owns t + j*THREADS):
