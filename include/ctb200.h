@@ -76,6 +76,16 @@ int ctb_pointwise_mul(const ctb_ctx_t* ctx, int base, const void* a, const void*
 int ctb_ring_mul(const ctb_ctx_t* ctx, int base, const void* a, uint64_t a_stride, const void* b,
                  uint64_t b_stride, void* out, uint64_t n_polys, void* stream);
 
+/* Prepared operand for repeated products: out = NTT(in) scaled into the
+ * Montgomery domain with N^-1 folded (layout [poly][L][N], evaluation order).
+ * Keys (public, secret, relinearisation) are prepared once per session. */
+int ctb_prepare_operand(const ctb_ctx_t* ctx, int base, const void* in, void* out, uint64_t n_polys,
+                        void* stream);
+/* out[i] = a[i] * b[i*b_stride] (+ addend[i] if non-NULL) with b prepared by
+ * ctb_prepare_operand: ring.ring_mul followed by ring.ring_add (ring.py:363-427). */
+int ctb_mul_prepared(const ctb_ctx_t* ctx, int base, const void* a, const void* bprep, uint64_t b_stride,
+                     const void* addend, void* out, uint64_t n_polys, void* stream);
+
 /* CPMul: out[k] = (c0*lift(pt[k]), c1*lift(pt[k])) for `batch` 2-part
  * ciphertexts ct[k] ([batch][2][L][N]) and plain polys pt[k] ([batch][N]
  * uint64 in [0,t)).  He.cp_mul (he.py:366-382) with He._lift (he.py:325-327).
@@ -87,6 +97,57 @@ int ctb_cpmul(const ctb_ctx_t* ctx, const void* ct, const uint64_t* pt, void* ou
  * plain primes + 2-prime CRT (ring.py:477-485). */
 int ctb_pp_mul(const ctb_ctx_t* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out,
                uint64_t n_polys, void* stream);
+
+/* Coefficient-wise ring operations (ring.py:363-401) on residues [n][L][N]:
+ * op 0 = add, 1 = sub (a - b), 2 = neg (b unused).  In-place allowed. */
+int ctb_rns_elementwise(const ctb_ctx_t* ctx, int base, int op, const void* a, const void* b, void* out,
+                        uint64_t n_polys, void* stream);
+/* out = a * c mod q with c given per limb (host array of L words, c_i < q_i). */
+int ctb_rns_scalar_mul(const ctb_ctx_t* ctx, int base, const void* a, const uint64_t* scalars, void* out,
+                       uint64_t n_polys, void* stream);
+/* Small signed integers [n][N] (int64; ternary s/u, Gaussian e) -> residues [n][L][N]. */
+int ctb_rns_from_small(const ctb_ctx_t* ctx, int base, const int64_t* in, void* out, uint64_t n_polys,
+                       void* stream);
+/* out = scale * lift(m) mod q: m [n][N] uint64 in [0,t), centred lift of he.py:325-327,
+ * scale per limb (host array; Delta mod q_i for encryption, 1 for a plain lift). */
+int ctb_lift_plain(const ctb_ctx_t* ctx, const uint64_t* m, const uint64_t* scale, void* out, uint64_t n_polys,
+                   void* stream);
+/* Plain ring (mod t) coefficient ops on uint64 [n][N]: op 0 add, 1 sub, 2 neg, 3 scalar multiply. */
+int ctb_plain_elementwise(const ctb_ctx_t* ctx, int op, const uint64_t* a, const uint64_t* b, uint64_t scalar,
+                          uint64_t* out, uint64_t n_polys, void* stream);
+
+/* Decrypt's exact scale-and-round: v [n][L][N] residues of c0 + c1 s (+ c2 s^2)
+ * -> out [n][N] = floor((v t + floor(q/2)) / q) mod t   (He.decrypt, he.py:347-349). */
+int ctb_decrypt_round(const ctb_ctx_t* ctx, const void* v, uint64_t* out, uint64_t n_polys, void* stream);
+/* Wire format: residues [n][L][N] <-> positional little-endian 64-bit words
+ * [n][N][W], W = ctb_ctx_pos_words = ring.RingParams.limb_count (ring.py:147,
+ * ring_to_bytes / ring_from_bytes ring.py:592-615; input words reduced mod q). */
+int ctb_ctx_pos_words(const ctb_ctx_t* ctx);
+int ctb_rns_to_pos(const ctb_ctx_t* ctx, const void* x, uint64_t* out, uint64_t n_polys, void* stream);
+int ctb_pos_to_rns(const ctb_ctx_t* ctx, const uint64_t* in, void* x, uint64_t n_polys, void* stream);
+
+/* CCMul tensoring (He.cc_mul_raw, he.py:384-407; ring.int_negacyclic_mul,
+ * ring.py:516-541), exact: a, b [batch][2][L][N] -> out3 [batch][3][L][N] =
+ * round(h_k t / q) mod q.  `workspace` holds ctb_ccmul_workspace_words(batch)
+ * uint32 words.  The auxiliary 30-bit NTT base is built on first use. */
+uint64_t ctb_ccmul_workspace_words(const ctb_ctx_t* ctx, uint64_t batch);
+int ctb_ccmul_raw(const ctb_ctx_t* ctx, const void* a, const void* b, void* out3, uint32_t* workspace,
+                  uint64_t batch, void* stream);
+/* The three stages of ctb_ccmul_raw, exposed for pipelining: centred lift onto the
+ * auxiliary base ([batch][2][K][N] uint32), tensor products ([batch][3][K][N]),
+ * and the exact scale-and-round back to the cipher base. */
+int ctb_tensor_aux_size(const ctb_ctx_t* ctx);
+int ctb_tensor_lift(const ctb_ctx_t* ctx, const void* ct, uint32_t* out, uint64_t batch, void* stream);
+int ctb_tensor_product(const ctb_ctx_t* ctx, const uint32_t* a_aux, const uint32_t* b_aux, uint32_t* h_aux,
+                       uint64_t batch, void* stream);
+int ctb_tensor_round(const ctb_ctx_t* ctx, const uint32_t* h_aux, void* out, uint64_t batch, void* stream);
+/* Relinearisation (He.relinearize, he.py:409-432): ct3 [batch][3][L][N] and the
+ * relinearisation keys prepared by ctb_prepare_operand as [D][2][L][N]
+ * ((b_i, a_i), D = ctb_relin_digit_count) -> out [batch][2][L][N].
+ * digits_ws: batch * D * N uint32 words of scratch. */
+int ctb_relin_digit_count(const ctb_ctx_t* ctx);
+int ctb_relinearize(const ctb_ctx_t* ctx, const void* ct3, const void* keyprep, uint32_t* digits_ws, void* out,
+                    uint64_t batch, void* stream);
 
 /* Instrumentation (not a reference interface): launch a register-resident
  * Shoup modmul throughput probe on `stream` (grid = 8 x SM count, 256 threads,

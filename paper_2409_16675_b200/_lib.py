@@ -33,8 +33,27 @@ SIGNATURES: dict[str, tuple] = {
     "ctb_ntt_inverse": (_int, [_c_void_p, _int, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_pointwise_mul": (_int, [_c_void_p, _int, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_ring_mul": (_int, [_c_void_p, _int, _c_void_p, _u64, _c_void_p, _u64, _c_void_p, _u64, _c_void_p]),
+    "ctb_prepare_operand": (_int, [_c_void_p, _int, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_mul_prepared": (_int, [_c_void_p, _int, _c_void_p, _c_void_p, _u64, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_cpmul": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_pp_mul": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_rns_elementwise": (_int, [_c_void_p, _int, _int, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_rns_scalar_mul": (_int, [_c_void_p, _int, _c_void_p, ctypes.POINTER(_u64), _c_void_p, _u64, _c_void_p]),
+    "ctb_rns_from_small": (_int, [_c_void_p, _int, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_lift_plain": (_int, [_c_void_p, _c_void_p, ctypes.POINTER(_u64), _c_void_p, _u64, _c_void_p]),
+    "ctb_plain_elementwise": (_int, [_c_void_p, _int, _c_void_p, _c_void_p, _u64, _c_void_p, _u64, _c_void_p]),
+    "ctb_decrypt_round": (_int, [_c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_ctx_pos_words": (_int, [_c_void_p]),
+    "ctb_rns_to_pos": (_int, [_c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_pos_to_rns": (_int, [_c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_ccmul_workspace_words": (_u64, [_c_void_p, _u64]),
+    "ctb_ccmul_raw": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_tensor_aux_size": (_int, [_c_void_p]),
+    "ctb_tensor_lift": (_int, [_c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_tensor_product": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_tensor_round": (_int, [_c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_relin_digit_count": (_int, [_c_void_p]),
+    "ctb_relinearize": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_probe_modmul": (_int, [_int, _u64, _c_void_p, ctypes.POINTER(_u64), _c_void_p]),
 }
 

@@ -9,6 +9,8 @@ using namespace ctb;
 
 namespace ctb {
 Ctx::~Ctx() {
+  free_tensor_consts(tensor);
+  free_rns_consts(rns);
   for (auto& b : base) free_base(b);
 }
 }  // namespace ctb
@@ -64,6 +66,8 @@ extern "C" int ctb_ctx_create(ctb_ctx_t** out, uint32_t n, const uint64_t* q_pri
   int rc = build_base(c->base[BASE_Q], q_primes, (int)n_q, logn, err, n_t ? tmod.data() : nullptr,
                       n_t ? delta.data() : nullptr);
   if (rc) { delete c; set_error("cipher base: " + err); return rc == -2 ? ERR_CUDA : ERR_ARG; }
+  rc = build_rns_consts(c, err);
+  if (rc) { delete c; set_error("conversion constants: " + err); return rc == -2 ? ERR_CUDA : (rc == -3 ? ERR_UNSUPPORTED : ERR_ARG); }
   *out = reinterpret_cast<ctb_ctx_t*>(c);
   return OK;
 }

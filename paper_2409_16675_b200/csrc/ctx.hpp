@@ -26,6 +26,7 @@ struct Base {
 // Constants for exact RNS <-> integer work (mixed-radix / Garner), filled by
 // rns.cu.  All device arrays are uint64 words regardless of the base word.
 struct RnsConsts;
+struct TensorState;
 
 struct Ctx {
   uint32_t n = 0, logn = 0;
@@ -35,6 +36,7 @@ struct Ctx {
   uint32_t relin_base_bits = 16;
   uint32_t wave_chunk = 296;    // items per limb-major chunk (= 2 x SM count, set at creation)
   RnsConsts* rns = nullptr;
+  TensorState* tensor = nullptr;  // built lazily on first CCMul (tensor.cu)
   ~Ctx();
 };
 
@@ -62,5 +64,11 @@ inline uint64_t invmod(uint64_t a, uint64_t m) { return powmod(a, m - 2, m); }  
 int build_base(Base& b, const uint64_t* primes, int count, uint32_t logn, std::string& err,
                const uint64_t* tmod = nullptr, const uint64_t* delta = nullptr);
 void free_base(Base& b);
+// rns.cu: exact conversion constants of the cipher base (needs BASE_Q and BASE_T built)
+int build_rns_consts(Ctx* c, std::string& err);
+void free_rns_consts(RnsConsts* rc);
+// tensor.cu: auxiliary base + constants for exact tensoring / relinearisation
+int build_tensor_consts(Ctx* c, std::string& err);
+void free_tensor_consts(TensorState* t);
 
 }  // namespace ctb

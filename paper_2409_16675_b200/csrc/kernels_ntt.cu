@@ -78,6 +78,58 @@ k_ring_mul(const T* a, uint64_t sa, const T* b, uint64_t sb, T* out,
   for (int k = 0; k < Sh::E; ++k) po[coef_base<LOGN>() + coef_off<LOGN>(k)] = csub(x[k], pr.p);
 }
 
+// Prepared operand: out = NTT(b) * N^-1 * 2^W (Montgomery domain, N^-1 folded),
+// the form k_mul_prepared consumes.  Used for keys (pk, s, relin keys) that
+// multiply many polynomials: one forward NTT per key instead of per product.
+template <typename T, int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
+k_prepare(const T* in, T* out, const PrimeTab<T>* __restrict__ tabs, int L) {
+  using Sh = NttShape<LOGN>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Exchanger<T, LOGN> ex{reinterpret_cast<T*>(smem_raw)};
+  const int limb = blockIdx.x % L;
+  const size_t off = (size_t)blockIdx.x * Sh::N;
+  PrimeRegs<T> pr(tabs + limb);
+  T x[Sh::E];
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) x[k] = in[off + coef_base<LOGN>() + coef_off<LOGN>(k)];
+  ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k)
+    out[off + eval_base<LOGN>() + eval_off<LOGN>(k)] = csub(shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p), pr.p);
+}
+
+// out[i] = a[i] * b (+ addend[i]) with b a prepared operand ([nb][L][N], nb = 1
+// broadcasts, else one per product) -- ring.ring_mul then ring.ring_add
+// (ring.py:363-427) fused: 1 forward + 1 inverse NTT per product.
+template <typename T, int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
+k_mul_prepared(const T* a, const T* bprep, uint64_t b_stride, const T* addend, T* out,
+               const PrimeTab<T>* __restrict__ tabs, int L) {
+  using Sh = NttShape<LOGN>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Exchanger<T, LOGN> ex{reinterpret_cast<T*>(smem_raw)};
+  const int limb = blockIdx.x % L;
+  const size_t poly = blockIdx.x / L;
+  const size_t off = (size_t)blockIdx.x * Sh::N;
+  const T* pb = bprep + (poly * b_stride * L + limb) * (size_t)Sh::N + eval_base<LOGN>();
+  PrimeRegs<T> pr(tabs + limb);
+  T x[Sh::E];
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) x[k] = a[off + coef_base<LOGN>() + coef_off<LOGN>(k)];
+  ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) x[k] = mont_mul(x[k], __ldg(pb + eval_off<LOGN>(k)), pr.p, pr.pinv);
+  ntt_inv_regs<T, LOGN>(x, ex, pr.inv, pr.p, pr.p2);
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) {
+    const size_t i = off + coef_base<LOGN>() + coef_off<LOGN>(k);
+    T v = csub(x[k], pr.p);
+    if (addend) v = add_mod(v, addend[i], pr.p);
+    out[i] = v;
+  }
+}
+
 // Eval-domain slotwise product (ring.pointwise_mul, ring.py:572-584).
 template <typename T>
 __global__ void k_pointwise(const T* a, const T* b, T* out, const PrimeTab<T>* __restrict__ tabs,
@@ -267,6 +319,48 @@ extern "C" int ctb_ntt_inverse(const ctb_ctx_t* ctx, int base, const void* in, v
                                                       (const PrimeTab<T>*)b->d_tabs, b->size())));
   }
   return cuda_status(e, "ctb_ntt_inverse");
+}
+
+extern "C" int ctb_prepare_operand(const ctb_ctx_t* ctx, int base, const void* in, void* out, uint64_t n_polys,
+                                   void* stream) {
+  const Base* b = base_of(ctx, base);
+  if (!b || !in || !out) { set_error("ctb_prepare_operand: bad context, base or buffer"); return ERR_ARG; }
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  const size_t nblk = n_polys * b->size();
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  if (b->word == 4) {
+    using T = uint32_t;
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_prepare<T, LOGN>, nblk, s, (const T*)in, (T*)out,
+                                                      (const PrimeTab<T>*)b->d_tabs, b->size())));
+  } else {
+    using T = uint64_t;
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_prepare<T, LOGN>, nblk, s, (const T*)in, (T*)out,
+                                                      (const PrimeTab<T>*)b->d_tabs, b->size())));
+  }
+  return cuda_status(e, "ctb_prepare_operand");
+}
+
+extern "C" int ctb_mul_prepared(const ctb_ctx_t* ctx, int base, const void* a, const void* bprep, uint64_t b_stride,
+                                const void* addend, void* out, uint64_t n_polys, void* stream) {
+  const Base* b = base_of(ctx, base);
+  if (!b || !a || !bprep || !out) { set_error("ctb_mul_prepared: bad context, base or buffer"); return ERR_ARG; }
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  const size_t nblk = n_polys * b->size();
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  if (b->word == 4) {
+    using T = uint32_t;
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_mul_prepared<T, LOGN>, nblk, s, (const T*)a,
+                                                      (const T*)bprep, b_stride, (const T*)addend, (T*)out,
+                                                      (const PrimeTab<T>*)b->d_tabs, b->size())));
+  } else {
+    using T = uint64_t;
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_mul_prepared<T, LOGN>, nblk, s, (const T*)a,
+                                                      (const T*)bprep, b_stride, (const T*)addend, (T*)out,
+                                                      (const PrimeTab<T>*)b->d_tabs, b->size())));
+  }
+  return cuda_status(e, "ctb_mul_prepared");
 }
 
 extern "C" int ctb_pointwise_mul(const ctb_ctx_t* ctx, int base, const void* a, const void* bb, void* out,

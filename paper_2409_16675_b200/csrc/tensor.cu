@@ -1,0 +1,622 @@
+// CCMul on device: exact tensoring (K4) and relinearisation (K5).
+//
+// Reference semantics (he.py:384-432):
+//   cc_mul_raw: centred lifts c0,c1,d0,d1 of the two ciphertexts; exact integer
+//     negacyclic products h0 = c0 d0, h1 = c0 d1 + c1 d0, h2 = c1 d1
+//     (ring.int_negacyclic_mul, ring.py:516-541); part_k = round(h_k t / q) mod q,
+//     ties away from zero (he.py:527-531 -- ties cannot occur, q odd, gcd(t,q)=1).
+//   relinearize: digits d_i = (c2 >> w i) & (2^w - 1) of c2 in [0,q);
+//     (c0 + sum d_i b_i, c1 + sum d_i a_i) mod q.
+//
+// Device algorithm, all exact:
+//  1 k_tensor_lift   per coefficient: Garner digits of x over Q; x > (Q-1)/2 is
+//    decided digit-wise against the digits of (Q-1)/2; residues of the centred
+//    value over the auxiliary base A (30-bit NTT primes, a superset of Q when
+//    Q's primes are 30-bit) by Horner evaluation minus Q mod p.
+//  2 k_tensor_product  per (ciphertext, aux prime) CTA: 4 forward NTTs, the
+//    3 slotwise tensor products, 3 inverse NTTs -> h residues over A.
+//  3 k_tensor_round  per coefficient, with z = h t + (Q-1)/2 (so the result is
+//    floor(z / Q) for either sign of h): r = z mod Q from z's residues mod Q
+//    (Garner), y = (z - r) Q^-1 modulo each prime of P2 (aux primes outside Q,
+//    product > 2|y|+1), then the centred y is base-extended from P2 to Q.  When
+//    Q's primes are not in A (50-bit limbs), h itself is first extended exactly
+//    from A to Q (product of A > 2|h|+1).
+//  4 k_relin_digits  Garner digits of c2 -> positional 32-bit words -> w-bit digits.
+//  5 k_relin_accum   per (ciphertext, limb) CTA: sum over digits of
+//    NTT(d_i) * prepared(b_i), NTT(d_i) * prepared(a_i) in registers, 2 INTT,
+//    + (c0, c1).
+#include <algorithm>
+#include <cstring>
+#include <vector>
+#include "bigint.hpp"
+#include "ctb200.h"
+#include "kernels.hpp"
+#include "rns.cuh"
+
+namespace ctb {
+
+constexpr int MAXA = 20;  // auxiliary primes
+constexpr int MAXQ = 8;   // cipher primes on the tensoring path
+
+template <typename TQ>
+struct TensorConsts {
+  int L, K, K2, ext_h, relin_w, relin_d, qwords;
+  MrcTab<TQ> mrcQ;
+  TQ halfQ_dig[MAXQ];                 // Garner digits of (Q-1)/2 over Q
+  int aux_is_q[MAXA];                 // aux k -> index in Q or -1
+  int q_in_aux[MAXQ];                 // q_i -> aux index or -1
+  uint32_t ap[MAXA], a_oneq[MAXA], a_r2[MAXA], a_r2q[MAXA];
+  ShoupC<uint32_t> lift_hc[MAXA][MAXQ];  // q_j mod p_k
+  uint32_t Q_aux[MAXA];               // Q mod p_k
+  ShoupC<uint32_t> t_aux[MAXA];       // t mod p_k
+  uint32_t hQ_aux[MAXA];              // (Q-1)/2 mod p_k
+  ShoupC<TQ> t_q[MAXQ];               // t mod q_i
+  TQ hQ_q[MAXQ];                      // (Q-1)/2 mod q_i
+  int p2_idx[MAXA];                   // aux index of P2 prime k
+  ShoupC<uint32_t> r_hc[MAXA][MAXQ];  // q_j mod p2_k
+  ShoupC<uint32_t> Qinv_p2[MAXA];     // Q^-1 mod p2_k
+  uint32_t Ky_p2[MAXA];               // floor(P2/2) mod p2_k
+  MrcTab<uint32_t> mrcP2;
+  ShoupC<TQ> y_hc[MAXQ][MAXA];        // p2_k mod q_i
+  TQ Ky_q[MAXQ];                      // floor(P2/2) mod q_i
+  MrcTab<uint32_t> mrcA;              // Garner over all aux (exact h extension)
+  uint32_t Kh_aux[MAXA];              // floor(M_A/2) mod p_k
+  ShoupC<TQ> h_hc[MAXQ][MAXA];        // p_k mod q_i
+  TQ Kh_q[MAXQ];                      // floor(M_A/2) mod q_i
+};
+
+struct TensorState {
+  void* d_consts = nullptr;
+  int K = 0, K2 = 0, L = 0;
+  ~TensorState() {
+    if (d_consts) cudaFree(d_consts);
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ void load_consts(const T* src, T* dst) {
+  const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
+  uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+  for (int i = threadIdx.x; i < (int)(sizeof(T) / 4); i += blockDim.x) d[i] = s[i];
+  __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t red_u32(uint64_t v, uint32_t m, uint32_t oneq, uint32_t r2, uint32_t r2q) {
+  const uint32_t a = shoup_mul<uint32_t>((uint32_t)(v >> 32), r2, r2q, m);
+  const uint32_t b = shoup_mul<uint32_t>((uint32_t)v, 1u, oneq, m);
+  return csub(csub(a + b, 2 * m), m);
+}
+
+// u32 value (< 2^32) into a TQ residue mod q
+template <typename TQ>
+__device__ __forceinline__ TQ small_to_q(uint32_t v, TQ q, TQ oneq) {
+  if constexpr (sizeof(TQ) == 8) return (TQ)v;  // q > 2^32
+  else return csub(shoup_mul<TQ>((TQ)v, (TQ)1, oneq, q), q);
+}
+
+// Horner of u32 digits dig[0..n) (radices r_k, constants hc[k] = r_k mod q) mod a TQ prime.
+template <typename TQ>
+__device__ __forceinline__ TQ horner_to_q(int n, const uint32_t* dig, const ShoupC<TQ>* hc, TQ q, TQ oneq) {
+  TQ acc = small_to_q<TQ>(dig[n - 1], q, oneq);
+  for (int k = n - 2; k >= 0; --k) {
+    acc = csub(shoup_mul<TQ>(acc, hc[k].w, hc[k].wq, q), q);
+    acc = add_mod(acc, small_to_q<TQ>(dig[k], q, oneq), q);
+  }
+  return acc;
+}
+
+// Horner of TQ digits (Q mixed radix) mod an aux u32 prime.
+template <typename TQ>
+__device__ __forceinline__ uint32_t horner_to_aux(int n, const TQ* dig, const ShoupC<uint32_t>* hc, uint32_t p,
+                                                  uint32_t oneq, uint32_t r2, uint32_t r2q) {
+  uint32_t acc = red_u32((uint64_t)dig[n - 1], p, oneq, r2, r2q);
+  for (int k = n - 2; k >= 0; --k) {
+    acc = csub(shoup_mul<uint32_t>(acc, hc[k].w, hc[k].wq, p), p);
+    acc = add_mod(acc, red_u32((uint64_t)dig[k], p, oneq, r2, r2q), p);
+  }
+  return acc;
+}
+
+// ----------------------------------------------------------------------------- 1 lift
+// in: [B][2][L][N] (TQ) -> out: [B][2][K][N] (u32), centred lifts over the aux base.
+template <typename TQ>
+__global__ void __launch_bounds__(256) k_tensor_lift(const TQ* in, uint32_t* out, const TensorConsts<TQ>* gc,
+                                                     uint32_t n, uint64_t total) {
+  __shared__ TensorConsts<TQ> c;
+  load_consts(gc, &c);
+  const int L = c.L, K = c.K;
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t poly = g / n, i = g % n;   // poly = b * 2 + part
+    TQ r[MAXQ], a[MAXQ];
+    for (int l = 0; l < L; ++l) r[l] = in[(poly * L + l) * n + i];
+    mrc_digits(c.mrcQ, r, a);
+    // x > (Q-1)/2 ?  lexicographic from the most significant digit
+    bool neg = false;
+    for (int l = L - 1; l >= 0; --l) {
+      if (a[l] != c.halfQ_dig[l]) { neg = a[l] > c.halfQ_dig[l]; break; }
+    }
+    for (int k = 0; k < K; ++k) {
+      uint32_t v;
+      const int qi = c.aux_is_q[k];
+      if (qi >= 0) {
+        v = (uint32_t)r[qi];  // x == centred value (mod q_i)
+      } else {
+        v = horner_to_aux<TQ>(L, a, c.lift_hc[k], c.ap[k], c.a_oneq[k], c.a_r2[k], c.a_r2q[k]);
+        if (neg) v = sub_mod(v, c.Q_aux[k], c.ap[k]);
+      }
+      out[(poly * K + k) * n + i] = v;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------- 2 products
+// A, Bt: [B][2][K][N] lifted operands -> H: [B][3][K][N]; CTA per (ciphertext, aux prime).
+template <int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
+k_tensor_product(const uint32_t* A, const uint32_t* Bt, uint32_t* H, const PrimeTab<uint32_t>* __restrict__ tabs,
+                 int K) {
+  using Sh = NttShape<LOGN>;
+  using T = uint32_t;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Exchanger<T, LOGN> ex{reinterpret_cast<T*>(smem_raw)};
+  T* strip = reinterpret_cast<T*>(smem_raw) + Exchanger<T, LOGN>::WORDS + threadIdx.x;  // 3 polys
+  const int k = blockIdx.x % K;
+  const size_t b = blockIdx.x / K;
+  PrimeRegs<T> pr(tabs + k);
+  const size_t N = Sh::N;
+  auto src = [&](const T* base, int part) { return base + ((b * 2 + part) * K + k) * N + coef_base<LOGN>(); };
+  T x[Sh::E];
+  // NTT(a0) -> strip 0, NTT(a1) -> strip 1 (Montgomery form, N^-1 folded), NTT(b0) -> strip 2
+  for (int s = 0; s < 3; ++s) {
+    const T* p = s < 2 ? src(A, s) : src(Bt, 0);
+#pragma unroll
+    for (int j = 0; j < Sh::E; ++j) x[j] = p[coef_off<LOGN>(j)];
+    ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
+#pragma unroll
+    for (int j = 0; j < Sh::E; ++j) {
+      T v = x[j];
+      if (s < 2) v = shoup_mul(v, pr.ninvr, pr.ninvr_q, pr.p);  // [0,2p)
+      strip[(s * Sh::E + j) * Sh::THREADS] = v;
+    }
+  }
+  // NTT(b1) in registers
+  {
+    const T* p = src(Bt, 1);
+#pragma unroll
+    for (int j = 0; j < Sh::E; ++j) x[j] = p[coef_off<LOGN>(j)];
+    ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
+  }
+  T y[Sh::E];
+  // h2 = a1 b1 ; h1 = a0 b1 + a1 b0 ; h0 = a0 b0
+  for (int part = 2; part >= 0; --part) {
+#pragma unroll
+    for (int j = 0; j < Sh::E; ++j) {
+      const T a0 = strip[(0 * Sh::E + j) * Sh::THREADS];
+      const T a1 = strip[(1 * Sh::E + j) * Sh::THREADS];
+      const T b0 = strip[(2 * Sh::E + j) * Sh::THREADS];
+      T v;
+      if (part == 2) v = mont_mul(x[j], a1, pr.p, pr.pinv);
+      else if (part == 1) v = csub(mont_mul(x[j], a0, pr.p, pr.pinv) + mont_mul(b0, a1, pr.p, pr.pinv), pr.p2);
+      else v = mont_mul(b0, a0, pr.p, pr.pinv);
+      y[j] = v;
+    }
+    ntt_inv_regs<T, LOGN>(y, ex, pr.inv, pr.p, pr.p2);
+    T* dst = H + ((b * 3 + part) * K + k) * N + coef_base<LOGN>();
+#pragma unroll
+    for (int j = 0; j < Sh::E; ++j) dst[coef_off<LOGN>(j)] = csub(y[j], pr.p);
+  }
+}
+
+// ----------------------------------------------------------------------------- 3 round
+// H: [B][3][K][N] -> out [B][3][L][N] (TQ): round(h t / Q) mod Q.
+template <typename TQ>
+__global__ void __launch_bounds__(256) k_tensor_round(const uint32_t* H, TQ* out, const TensorConsts<TQ>* gc,
+                                                      uint32_t n, uint64_t total) {
+  __shared__ TensorConsts<TQ> c;
+  load_consts(gc, &c);
+  const int L = c.L, K = c.K, K2 = c.K2;
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t poly = g / n, i = g % n;   // poly = b * 3 + part
+    uint32_t h[MAXA];
+    for (int k = 0; k < K; ++k) h[k] = H[(poly * K + k) * n + i];
+    // h mod q_i
+    TQ hq[MAXQ];
+    if (c.ext_h) {
+      uint32_t hs[MAXA], dig[MAXA];
+      for (int k = 0; k < K; ++k) hs[k] = add_mod(h[k], c.Kh_aux[k], c.ap[k]);   // h + floor(M/2) in [0, M)
+      mrc_digits(c.mrcA, hs, dig);
+      for (int l = 0; l < L; ++l) {
+        const TQ q = c.mrcQ.q[l];
+        const TQ v = horner_to_q<TQ>(K, dig, c.h_hc[l], q, c.mrcQ.one_q[l]);
+        hq[l] = sub_mod(v, c.Kh_q[l], q);
+      }
+    } else {
+      for (int l = 0; l < L; ++l) hq[l] = (TQ)h[c.q_in_aux[l]];
+    }
+    // z = h t + (Q-1)/2 mod q_i ; r = z mod Q (Garner digits)
+    TQ z[MAXQ], rd[MAXQ];
+    for (int l = 0; l < L; ++l) {
+      const TQ q = c.mrcQ.q[l];
+      z[l] = add_mod(csub(shoup_mul<TQ>(hq[l], c.t_q[l].w, c.t_q[l].wq, q), q), c.hQ_q[l], q);
+    }
+    mrc_digits(c.mrcQ, z, rd);
+    // y' = (z - r) Q^-1 + floor(P2/2) mod each P2 prime
+    uint32_t ys[MAXA], yd[MAXA];
+    for (int k = 0; k < K2; ++k) {
+      const int ai = c.p2_idx[k];
+      const uint32_t p = c.ap[ai];
+      const uint32_t zk = add_mod(csub(shoup_mul<uint32_t>(h[ai], c.t_aux[ai].w, c.t_aux[ai].wq, p), p), c.hQ_aux[ai], p);
+      const uint32_t rk = horner_to_aux<TQ>(L, rd, c.r_hc[k], p, c.a_oneq[ai], c.a_r2[ai], c.a_r2q[ai]);
+      uint32_t yk = csub(shoup_mul<uint32_t>(sub_mod(zk, rk, p), c.Qinv_p2[k].w, c.Qinv_p2[k].wq, p), p);
+      ys[k] = add_mod(yk, c.Ky_p2[k], p);
+    }
+    mrc_digits(c.mrcP2, ys, yd);
+    for (int l = 0; l < L; ++l) {
+      const TQ q = c.mrcQ.q[l];
+      const TQ v = horner_to_q<TQ>(K2, yd, c.y_hc[l], q, c.mrcQ.one_q[l]);
+      out[(poly * L + l) * n + i] = sub_mod(v, c.Ky_q[l], q);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------- 4 relin digits
+// ct3: [B][3][L][N] -> digits [B][D][N] (u32 < 2^w), d_j = (c2 >> w j) & (2^w - 1).
+template <typename TQ>
+__global__ void __launch_bounds__(256) k_relin_digits(const TQ* ct3, uint32_t* digits, const TensorConsts<TQ>* gc,
+                                                      uint32_t n, uint64_t total) {
+  __shared__ MrcTab<TQ> m;
+  __shared__ int meta[4];
+  load_consts(&gc->mrcQ, &m);
+  if (threadIdx.x == 0) { meta[0] = gc->relin_w; meta[1] = gc->relin_d; meta[2] = gc->qwords; }
+  __syncthreads();
+  const int L = m.L, w = meta[0], D = meta[1], words = meta[2];
+  const uint32_t mask = (w >= 32) ? 0xffffffffu : ((1u << w) - 1u);
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t b = g / n, i = g % n;
+    TQ r[MAXQ], a[MAXQ];
+    for (int l = 0; l < L; ++l) r[l] = ct3[((b * 3 + 2) * L + l) * n + i];
+    mrc_digits(m, r, a);
+    uint32_t X[20];
+    mrc_positional(m, a, X, words);
+    for (int j = 0; j < D; ++j) {
+      const int bit = j * w, wi = bit >> 5, sh = bit & 31;
+      uint64_t v = (uint64_t)X[wi] >> sh;
+      if (sh + w > 32 && wi + 1 < words) v |= (uint64_t)X[wi + 1] << (32 - sh);
+      digits[(b * D + j) * n + i] = (uint32_t)v & mask;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------- 5 relin accumulate
+// out [B][2][L][N] = (c0, c1) + sum_j NTT^-1(NTT(d_j) * keyprep[j][0|1]); CTA per (ciphertext, limb).
+template <typename T, int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
+k_relin_accum(const T* ct3, const uint32_t* digits, const T* keyprep, T* out,
+              const PrimeTab<T>* __restrict__ tabs, int L, int D) {
+  using Sh = NttShape<LOGN>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Exchanger<T, LOGN> ex{reinterpret_cast<T*>(smem_raw)};
+  const int limb = blockIdx.x % L;
+  const size_t b = blockIdx.x / L;
+  const size_t N = Sh::N;
+  PrimeRegs<T> pr(tabs + limb);
+  T acc0[Sh::E], acc1[Sh::E], x[Sh::E];
+#pragma unroll
+  for (int j = 0; j < Sh::E; ++j) acc0[j] = acc1[j] = 0;
+#pragma unroll 1
+  for (int d = 0; d < D; ++d) {
+    const uint32_t* src = digits + (b * D + d) * N + coef_base<LOGN>();
+#pragma unroll
+    for (int j = 0; j < Sh::E; ++j) x[j] = csub((T)src[coef_off<LOGN>(j)], pr.p);  // digit < 2^w < 2p
+    ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
+    const T* kb = keyprep + (((size_t)d * 2 + 0) * L + limb) * N + eval_base<LOGN>();
+    const T* ka = keyprep + (((size_t)d * 2 + 1) * L + limb) * N + eval_base<LOGN>();
+#pragma unroll
+    for (int j = 0; j < Sh::E; ++j) {
+      acc0[j] = csub(acc0[j] + mont_mul(x[j], __ldg(kb + eval_off<LOGN>(j)), pr.p, pr.pinv), pr.p2);
+      acc1[j] = csub(acc1[j] + mont_mul(x[j], __ldg(ka + eval_off<LOGN>(j)), pr.p, pr.pinv), pr.p2);
+    }
+  }
+  for (int part = 0; part < 2; ++part) {
+    T* acc = part == 0 ? acc0 : acc1;
+#pragma unroll
+    for (int j = 0; j < Sh::E; ++j) x[j] = acc[j];
+    ntt_inv_regs<T, LOGN>(x, ex, pr.inv, pr.p, pr.p2);
+    const size_t off = ((b * 3 + part) * L + limb) * N + coef_base<LOGN>();
+    const size_t oo = ((b * 2 + part) * L + limb) * N + coef_base<LOGN>();
+#pragma unroll
+    for (int j = 0; j < Sh::E; ++j) out[oo + coef_off<LOGN>(j)] = add_mod(csub(x[j], pr.p), ct3[off + coef_off<LOGN>(j)], pr.p);
+  }
+}
+
+// ----------------------------------------------------------------------------- host constants
+template <typename T>
+static ShoupC<T> spair(uint64_t w, uint64_t p) {
+  constexpr int W = 8 * sizeof(T);
+  return ShoupC<T>{(T)w, (T)(((unsigned __int128)w << W) / p)};
+}
+
+template <typename T>
+static void fill_mrc_tab(MrcTab<T>& m, const std::vector<uint64_t>& q) {
+  constexpr int W = 8 * sizeof(T);
+  m.L = (int)q.size();
+  for (int j = 0; j < m.L; ++j) {
+    m.q[j] = (T)q[j];
+    m.q2[j] = (T)(2 * q[j]);
+    m.one_q[j] = (T)(((unsigned __int128)1 << W) / q[j]);
+    for (int i = 0; i < j; ++i) m.inv[j * (j - 1) / 2 + i] = spair<T>(invmod(q[i] % q[j], q[j]), q[j]);
+  }
+}
+
+static bool is_prime_u64(uint64_t n) {
+  if (n < 2) return false;
+  for (uint64_t p : {2ull, 3ull, 5ull, 7ull, 11ull, 13ull, 17ull, 19ull, 23ull, 29ull, 31ull, 37ull}) {
+    if (n % p == 0) return n == p;
+  }
+  uint64_t d = n - 1;
+  int s = 0;
+  while (!(d & 1)) { d >>= 1; ++s; }
+  for (uint64_t a : {2ull, 3ull, 5ull, 7ull, 11ull, 13ull, 17ull, 19ull, 23ull, 29ull, 31ull, 37ull}) {
+    uint64_t x = powmod(a, d, n);
+    if (x == 1 || x == n - 1) continue;
+    bool comp = true;
+    for (int r = 1; r < s; ++r) {
+      x = mulmod(x, x, n);
+      if (x == n - 1) { comp = false; break; }
+    }
+    if (comp) return false;
+  }
+  return true;
+}
+
+template <typename TQ>
+static int build_tensor(Ctx* c, std::string& err) {
+  const std::vector<uint64_t>& q = c->base[BASE_Q].primes;
+  const int L = (int)q.size();
+  if (L > MAXQ) { err = "tensoring supports at most 8 cipher primes"; return -3; }
+  if (!c->t) { err = "tensoring needs the plain modulus"; return -1; }
+  const uint64_t n = c->n;
+  BigU Q(1);
+  for (uint64_t p : q) Q.mul_small(p);
+  BigU hQ = BigU::sub(Q, BigU(1));
+  hQ.shr1();                                     // (Q-1)/2
+  // |h| <= 2 N ((Q+1)/2)^2 ; |y| <= |h| t / Q + 1
+  BigU half1 = Q; half1.add_small(1); half1.shr1();
+  BigU hmax = BigU::mul(half1, half1); hmax.mul_small(2 * n);
+  BigU ymax = hmax; ymax.mul_small(c->t);
+  ymax = big_div(ymax, Q); ymax.add_small(2);
+  BigU need_y = ymax; need_y.mul_small(2); need_y.add_small(1);   // P2 > 2 ymax + 1
+  BigU need_h = hmax; need_h.mul_small(2); need_h.add_small(1);   // M_A > 2 hmax + 1
+  const bool q_in = sizeof(TQ) == 4;             // 30-bit cipher primes are themselves aux primes
+  std::vector<uint64_t> aux, p2;
+  if (q_in) aux = q;
+  // candidate 30-bit NTT primes, descending, skipping Q
+  const uint64_t step = 2 * n;
+  uint64_t cand = ((1ull << 30) - 2) / step * step + 1;
+  BigU P2(1), MA(1);
+  for (uint64_t p : aux) MA.mul_small(p);
+  while (BigU::cmp(P2, need_y) <= 0 || (!q_in && BigU::cmp(MA, need_h) <= 0)) {
+    if (cand <= step) { err = "ran out of 30-bit auxiliary primes"; return -3; }
+    if (is_prime_u64(cand) && std::find(q.begin(), q.end(), cand) == q.end()) {
+      aux.push_back(cand);
+      MA.mul_small(cand);
+      if (BigU::cmp(P2, need_y) <= 0) { p2.push_back(cand); P2.mul_small(cand); }
+    }
+    cand -= step;
+  }
+  if ((int)aux.size() > MAXA) { err = "tensoring needs more than 20 auxiliary primes"; return -3; }
+  std::string e2;
+  int rc = build_base(c->base[BASE_B], aux.data(), (int)aux.size(), c->logn, e2);
+  if (rc) { err = "aux base: " + e2; return rc; }
+
+  auto* h = new TensorConsts<TQ>();
+  std::memset((void*)h, 0, sizeof(TensorConsts<TQ>));
+  h->L = L; h->K = (int)aux.size(); h->K2 = (int)p2.size(); h->ext_h = q_in ? 0 : 1;
+  h->relin_w = (int)c->relin_base_bits;
+  h->relin_d = (int)((Q.bit_length() + c->relin_base_bits - 1) / c->relin_base_bits);
+  h->qwords = (int)((Q.bit_length() + 31) / 32) + 2;
+  if (h->qwords > 20) { delete h; err = "cipher modulus too wide for relinearisation digits"; return -3; }
+  fill_mrc_tab(h->mrcQ, q);
+  // digits of (Q-1)/2 over Q
+  {
+    BigU x = hQ;
+    for (int l = 0; l < L; ++l) h->halfQ_dig[l] = (TQ)x.divmod_small(q[l]);
+  }
+  for (int l = 0; l < L; ++l) h->q_in_aux[l] = -1;
+  for (int k = 0; k < h->K; ++k) {
+    const uint64_t p = aux[k];
+    h->aux_is_q[k] = -1;
+    for (int l = 0; l < L; ++l)
+      if (q[l] == p) { h->aux_is_q[k] = l; h->q_in_aux[l] = k; }
+    h->ap[k] = (uint32_t)p;
+    h->a_oneq[k] = (uint32_t)((1ull << 32) / p);
+    const uint64_t r2 = (1ull << 32) % p;
+    h->a_r2[k] = (uint32_t)r2;
+    h->a_r2q[k] = (uint32_t)((r2 << 32) / p);
+    for (int j = 0; j + 1 < L; ++j) h->lift_hc[k][j] = spair<uint32_t>(q[j] % p, p);
+    h->Q_aux[k] = (uint32_t)Q.mod_small(p);
+    h->t_aux[k] = spair<uint32_t>(c->t % p, p);
+    h->hQ_aux[k] = (uint32_t)hQ.mod_small(p);
+  }
+  for (int l = 0; l < L; ++l) {
+    h->t_q[l] = spair<TQ>(c->t % q[l], q[l]);
+    h->hQ_q[l] = (TQ)hQ.mod_small(q[l]);
+  }
+  BigU Ky = P2; Ky.shr1();
+  for (int k = 0; k < h->K2; ++k) {
+    const uint64_t p = p2[k];
+    h->p2_idx[k] = (int)(std::find(aux.begin(), aux.end(), p) - aux.begin());
+    for (int j = 0; j + 1 < L; ++j) h->r_hc[k][j] = spair<uint32_t>(q[j] % p, p);
+    h->Qinv_p2[k] = spair<uint32_t>(invmod(Q.mod_small(p), p), p);
+    h->Ky_p2[k] = (uint32_t)Ky.mod_small(p);
+  }
+  fill_mrc_tab(h->mrcP2, p2);
+  for (int l = 0; l < L; ++l) {
+    for (int k = 0; k + 1 < h->K2; ++k) h->y_hc[l][k] = spair<TQ>(p2[k] % q[l], q[l]);
+    h->Ky_q[l] = (TQ)Ky.mod_small(q[l]);
+  }
+  if (h->ext_h) {
+    fill_mrc_tab(h->mrcA, aux);
+    BigU Kh = MA; Kh.shr1();
+    for (int k = 0; k < h->K; ++k) h->Kh_aux[k] = (uint32_t)Kh.mod_small(aux[k]);
+    for (int l = 0; l < L; ++l) {
+      for (int k = 0; k + 1 < h->K; ++k) h->h_hc[l][k] = spair<TQ>(aux[k] % q[l], q[l]);
+      h->Kh_q[l] = (TQ)Kh.mod_small(q[l]);
+    }
+  }
+  auto* st = new TensorState();
+  st->K = h->K; st->K2 = h->K2; st->L = L;
+  cudaError_t ce = cudaMalloc(&st->d_consts, sizeof(TensorConsts<TQ>));
+  if (ce == cudaSuccess) ce = cudaMemcpy(st->d_consts, h, sizeof(TensorConsts<TQ>), cudaMemcpyHostToDevice);
+  delete h;
+  if (ce != cudaSuccess) { delete st; err = std::string("tensor constants: ") + cudaGetErrorString(ce); return -2; }
+  c->tensor = st;
+  return 0;
+}
+
+int build_tensor_consts(Ctx* c, std::string& err) {
+  return c->base[BASE_Q].word == 4 ? build_tensor<uint32_t>(c, err) : build_tensor<uint64_t>(c, err);
+}
+void free_tensor_consts(TensorState* t) { delete t; }
+int tensor_aux_count(const TensorState* t) { return t ? t->K : 0; }
+
+}  // namespace ctb
+
+using namespace ctb;
+
+static unsigned grid_pc(uint64_t total) {
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148ull * 4));
+}
+
+static int ensure_tensor(const ctb_ctx_t* ctx, const Ctx*& c) {
+  c = reinterpret_cast<const Ctx*>(ctx);
+  if (!c) { set_error("null context"); return ERR_ARG; }
+  if (!c->tensor) {
+    std::string err;
+    const int rc = build_tensor_consts(const_cast<Ctx*>(c), err);
+    if (rc) { set_error("tensoring setup: " + err); return rc == -2 ? ERR_CUDA : (rc == -3 ? ERR_UNSUPPORTED : ERR_ARG); }
+  }
+  return OK;
+}
+
+extern "C" int ctb_tensor_aux_size(const ctb_ctx_t* ctx) {
+  const Ctx* c;
+  const int rc = ensure_tensor(ctx, c);
+  return rc ? rc : tensor_aux_count(c->tensor);
+}
+
+extern "C" int ctb_tensor_lift(const ctb_ctx_t* ctx, const void* ct, uint32_t* out, uint64_t batch, void* stream) {
+  const Ctx* c;
+  int rc = ensure_tensor(ctx, c);
+  if (rc) return rc;
+  if (!ct || !out) { set_error("ctb_tensor_lift: null buffer"); return ERR_ARG; }
+  const uint64_t total = batch * 2 * c->n;
+  if (!total) return OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (c->base[BASE_Q].word == 4)
+    k_tensor_lift<uint32_t><<<grid_pc(total), 256, 0, s>>>((const uint32_t*)ct, out,
+                                                           (const TensorConsts<uint32_t>*)c->tensor->d_consts, c->n, total);
+  else
+    k_tensor_lift<uint64_t><<<grid_pc(total), 256, 0, s>>>((const uint64_t*)ct, out,
+                                                           (const TensorConsts<uint64_t>*)c->tensor->d_consts, c->n, total);
+  return cuda_status(cudaGetLastError(), "ctb_tensor_lift");
+}
+
+extern "C" int ctb_tensor_product(const ctb_ctx_t* ctx, const uint32_t* a_aux, const uint32_t* b_aux, uint32_t* h_aux,
+                                  uint64_t batch, void* stream) {
+  const Ctx* c;
+  int rc = ensure_tensor(ctx, c);
+  if (rc) return rc;
+  if (!a_aux || !b_aux || !h_aux) { set_error("ctb_tensor_product: null buffer"); return ERR_ARG; }
+  const Base& B = c->base[BASE_B];
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<uint32_t, LOGN, 3>(k_tensor_product<LOGN>, batch * B.size(), s,
+                                                                      a_aux, b_aux, h_aux,
+                                                                      (const PrimeTab<uint32_t>*)B.d_tabs, B.size())));
+  return cuda_status(e, "ctb_tensor_product");
+}
+
+extern "C" int ctb_tensor_round(const ctb_ctx_t* ctx, const uint32_t* h_aux, void* out, uint64_t batch, void* stream) {
+  const Ctx* c;
+  int rc = ensure_tensor(ctx, c);
+  if (rc) return rc;
+  if (!h_aux || !out) { set_error("ctb_tensor_round: null buffer"); return ERR_ARG; }
+  const uint64_t total = batch * 3 * c->n;
+  if (!total) return OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (c->base[BASE_Q].word == 4)
+    k_tensor_round<uint32_t><<<grid_pc(total), 256, 0, s>>>(h_aux, (uint32_t*)out,
+                                                            (const TensorConsts<uint32_t>*)c->tensor->d_consts, c->n, total);
+  else
+    k_tensor_round<uint64_t><<<grid_pc(total), 256, 0, s>>>(h_aux, (uint64_t*)out,
+                                                            (const TensorConsts<uint64_t>*)c->tensor->d_consts, c->n, total);
+  return cuda_status(cudaGetLastError(), "ctb_tensor_round");
+}
+
+extern "C" uint64_t ctb_ccmul_workspace_words(const ctb_ctx_t* ctx, uint64_t batch) {
+  const Ctx* c;
+  if (ensure_tensor(ctx, c)) return 0;
+  return batch * 7ull * c->tensor->K * c->n;  // lifted a (2K) + lifted b (2K) + h (3K) polys, uint32
+}
+
+extern "C" int ctb_ccmul_raw(const ctb_ctx_t* ctx, const void* a, const void* b, void* out3, uint32_t* workspace,
+                             uint64_t batch, void* stream) {
+  const Ctx* c;
+  int rc = ensure_tensor(ctx, c);
+  if (rc) return rc;
+  if (!a || !b || !out3 || !workspace) { set_error("ctb_ccmul_raw: null buffer"); return ERR_ARG; }
+  const uint64_t poly = (uint64_t)c->tensor->K * c->n;
+  uint32_t* la = workspace;
+  uint32_t* lb = la + batch * 2 * poly;
+  uint32_t* hh = lb + batch * 2 * poly;
+  if ((rc = ctb_tensor_lift(ctx, a, la, batch, stream))) return rc;
+  if ((rc = ctb_tensor_lift(ctx, b, lb, batch, stream))) return rc;
+  if ((rc = ctb_tensor_product(ctx, la, lb, hh, batch, stream))) return rc;
+  return ctb_tensor_round(ctx, hh, out3, batch, stream);
+}
+
+extern "C" int ctb_relin_digit_count(const ctb_ctx_t* ctx) {
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (!c) return ERR_ARG;
+  BigU Q(1);
+  for (uint64_t p : c->base[BASE_Q].primes) Q.mul_small(p);
+  return (int)((Q.bit_length() + c->relin_base_bits - 1) / c->relin_base_bits);
+}
+
+extern "C" int ctb_relinearize(const ctb_ctx_t* ctx, const void* ct3, const void* keyprep, uint32_t* digits_ws,
+                               void* out, uint64_t batch, void* stream) {
+  const Ctx* c;
+  int rc = ensure_tensor(ctx, c);
+  if (rc) return rc;
+  if (!ct3 || !keyprep || !digits_ws || !out) { set_error("ctb_relinearize: null buffer"); return ERR_ARG; }
+  if (c->relin_base_bits < 1 || c->relin_base_bits > 29) { set_error("relinearisation base must be 1..29 bits"); return ERR_UNSUPPORTED; }
+  const Base& B = c->base[BASE_Q];
+  const int D = ctb_relin_digit_count(ctx);
+  const uint64_t total = batch * c->n;
+  if (!total) return OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  if (B.word == 4) {
+    using T = uint32_t;
+    k_relin_digits<T><<<grid_pc(total), 256, 0, s>>>((const T*)ct3, digits_ws,
+                                                     (const TensorConsts<T>*)c->tensor->d_consts, c->n, total);
+    e = cudaGetLastError();
+    if (e == cudaSuccess)
+      CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_relin_accum<T, LOGN>, batch * B.size(), s,
+                                                                (const T*)ct3, (const uint32_t*)digits_ws,
+                                                                (const T*)keyprep, (T*)out,
+                                                                (const PrimeTab<T>*)B.d_tabs, B.size(), D)));
+  } else {
+    using T = uint64_t;
+    k_relin_digits<T><<<grid_pc(total), 256, 0, s>>>((const T*)ct3, digits_ws,
+                                                     (const TensorConsts<T>*)c->tensor->d_consts, c->n, total);
+    e = cudaGetLastError();
+    if (e == cudaSuccess)
+      CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_relin_accum<T, LOGN>, batch * B.size(), s,
+                                                                (const T*)ct3, (const uint32_t*)digits_ws,
+                                                                (const T*)keyprep, (T*)out,
+                                                                (const PrimeTab<T>*)B.d_tabs, B.size(), D)));
+  }
+  return cuda_status(e, "ctb_relinearize");
+}

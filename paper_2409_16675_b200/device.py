@@ -58,9 +58,11 @@ class RnsContext:
         check(self._lib.ctb_ctx_create(ctypes.byref(h), self.n, q, len(self.q_primes), t, len(self.t_primes),
                                        relin_base_bits), "ctb_ctx_create")
         self._h = h
-        self.t = 1
-        for p in self.t_primes:
-            self.t *= p
+        self.t = 0
+        if self.t_primes:
+            self.t = 1
+            for p in self.t_primes:
+                self.t *= p
 
     def __del__(self):
         h = getattr(self, "_h", None)

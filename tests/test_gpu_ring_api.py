@@ -1,0 +1,80 @@
+"""GPU parity of the ring mirror (ring.py surface) against the oracle."""
+import numpy as np
+import pytest
+
+from conftest import has_gpu
+from oracle import ring_ref as R
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
+
+
+def test_wrap_and_monomials():
+    from paper_2409_16675_b200 import ring
+    from paper_2409_16675_b200.ring import RingElem, RingParams
+    P = RingParams(4, 17)
+    x3 = RingElem.monomial(P, 1, 3)
+    x1 = RingElem.monomial(P, 1, 1)
+    assert ring.ring_mul(x3, x1).to_ints() == [16, 0, 0, 0]
+    for n in (8, 16, 32):
+        p = R.ntt_primes(n, 18, 1)[0]
+        Pn = RingParams(n, p)
+        for i in range(n):
+            a = RingElem.monomial(Pn, 3, i)
+            b = RingElem.monomial(Pn, 5, (i * 7) % n)
+            want = R.negacyclic_mul_mod(np.asarray(a.coeffs), np.asarray(b.coeffs), p)
+            assert ring.ring_mul(a, b).coeffs.tolist() == [int(v) for v in want]
+
+
+def test_cipher_ring_ops_match_oracle():
+    from paper_2409_16675_b200 import ring
+    from paper_2409_16675_b200.params import default_he_params
+    from paper_2409_16675_b200.ring import RingElem
+    P = default_he_params(4096)
+    q = P.q
+    rng = np.random.default_rng(5)
+    a = RingElem.random(P.cipher_ring, rng)
+    b = RingElem.random(P.cipher_ring, rng)
+    ai = [int(v) for v in a.coeffs]
+    bi = [int(v) for v in b.coeffs]
+    assert [int(v) for v in ring.ring_add(a, b).coeffs[:64]] == [(x + y) % q for x, y in zip(ai[:64], bi[:64])]
+    assert [int(v) for v in ring.ring_sub(a, b).coeffs[:64]] == [(x - y) % q for x, y in zip(ai[:64], bi[:64])]
+    assert [int(v) for v in ring.ring_neg(a).coeffs[:64]] == [(-x) % q for x in ai[:64]]
+    c = 123456789123456789123
+    assert [int(v) for v in ring.ring_scalar_mul(a, c).coeffs[:64]] == [x * c % q for x in ai[:64]]
+    prod = ring.ring_mul(a, b)
+    want = R.ring_mul_rns(R.to_rns(ai, P.cipher_ring.primes), R.to_rns(bi, P.cipher_ring.primes), P.cipher_ring.primes)
+    assert np.array_equal(prod.data.cpu().numpy().astype(np.uint64), want)
+    # from_ints with signed big ints
+    vals = [(-1) ** i * (i * 10 ** 40 + 7) for i in range(P.n)]
+    e = RingElem.from_ints(P.cipher_ring, np.array(vals, dtype=object))
+    assert [int(v) for v in e.coeffs[:32]] == [v % q for v in vals[:32]]
+
+
+def test_plain_ring_ops_and_ntt_surface():
+    from paper_2409_16675_b200 import ring
+    from paper_2409_16675_b200.ring import RingElem, RingParams
+    from paper_2409_16675_b200.params import default_plain_params
+    T = default_plain_params(4096)
+    rng = np.random.default_rng(8)
+    a = RingElem.random(T, rng)
+    b = RingElem.random(T, rng)
+    t = T.modulus
+    av, bv = a.coeffs.astype(object), b.coeffs.astype(object)
+    assert np.array_equal(ring.ring_add(a, b).coeffs, ((av + bv) % t).astype(np.uint64))
+    assert np.array_equal(ring.ring_sub(a, b).coeffs, ((av - bv) % t).astype(np.uint64))
+    assert np.array_equal(ring.ring_scalar_mul(a, 10 ** 15 + 3).coeffs, (av * (10 ** 15 + 3) % t).astype(np.uint64))
+    # single-prime eval-domain surface (ring.py:549-584)
+    p = R.ntt_primes(32, 18, 1)[0]
+    P = RingParams(32, p)
+    x = RingElem.random(P, rng)
+    y = RingElem.random(P, rng)
+    fx = ring.ntt_forward(x)
+    assert fx.domain == "eval"
+    assert np.array_equal(fx.coeffs, R.NttPlan(32, p).forward(x.coeffs))
+    assert ring.ntt_inverse(fx) == x
+    ptw = ring.ntt_inverse(ring.pointwise_mul(fx, ring.ntt_forward(y)))
+    assert ptw == ring.ring_mul(x, y)
+    with pytest.raises(ring.NttUnavailableError):
+        ring.ntt_forward(RingElem.zeros(RingParams(8, 19)))
+    with pytest.raises(ring.ParamsMismatchError):
+        ring.ring_add(RingElem.zeros(RingParams(4, 17)), RingElem.zeros(RingParams(4, 97)))
