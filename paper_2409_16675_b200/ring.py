@@ -372,7 +372,7 @@ def ring_from_bytes(data: bytes, params: RingParams) -> RingElem:
         pad = np.zeros((n, wc), dtype=np.uint64)
         pad[:, :min(wc, limbs)] = body[:, :min(wc, limbs)]
         body = pad
-    words = torch.from_numpy(np.ascontiguousarray(body).view(np.int64)).cuda()
+    words = torch.from_numpy(np.array(body, dtype=np.uint64).view(np.int64)).cuda()
     out = torch.empty((ctx.L, params.n), dtype=ctx.dtype(), device="cuda")
     _lib.check(ctx._lib.ctb_pos_to_rns(ctx._h, _ptr(words), _ptr(out), 1, _stream()), "ctb_pos_to_rns")
     return RingElem(params, out)
