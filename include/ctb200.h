@@ -149,6 +149,33 @@ int ctb_relin_digit_count(const ctb_ctx_t* ctx);
 int ctb_relinearize(const ctb_ctx_t* ctx, const void* ct3, const void* keyprep, uint32_t* digits_ws, void* out,
                     uint64_t batch, void* stream);
 
+/* Prepared lifted plaintext: NTT(lift(m)) in the Montgomery domain, N^-1
+ * folded (m [n][N] uint64 in [0,t)) -> [n][L][N]. */
+int ctb_lift_prepare(const ctb_ctx_t* ctx, const uint64_t* m, void* out, uint64_t n_polys, void* stream);
+
+/* K3 -- server step of the precompute protocol for one linear job
+ * (linprot.precompute_online_server, linprot.py:455-485), exact:
+ *   out_ct[o] = sum_{(x,w,o) in sites} ( ct_x[x] * lift(mw[w]) + ct_w[w] * lift(mx[x]) ) + maskprod[o]
+ *   out_p[o]  = sum_{(x,w,o) in sites} mx[x] * mw[w]       (plain ring)
+ * ct_x [n_x][2][L][N], ct_w [n_w][2][L][N] ciphertexts; mx [n_x][N], mw [n_w][N]
+ * masked plaintexts (x - r_x, w - r_w); sites_host: HOST array of n_sites
+ * (x index, w index, out slot) triples (linprot.JobShape.sites); maskprod
+ * [n_out][2][L][N] or NULL; out_ct [n_out][2][L][N]; out_p [n_out][N].
+ * workspace: ctb_linear_online_workspace_bytes() bytes of device memory.
+ * Every ciphertext part and masked plaintext is NTT'd once; each slot is
+ * accumulated in the evaluation domain and inverse-transformed once. */
+uint64_t ctb_linear_online_workspace_bytes(const ctb_ctx_t* ctx, uint32_t n_x, uint32_t n_w, uint32_t n_out,
+                                           uint32_t n_sites);
+int ctb_linear_online(const ctb_ctx_t* ctx, const void* ct_x, uint32_t n_x, const void* ct_w, uint32_t n_w,
+                      const uint64_t* mx, const uint64_t* mw, const uint32_t* sites_host, uint32_t n_sites,
+                      uint32_t n_out, const void* maskprod, void* out_ct, uint64_t* out_p, void* workspace,
+                      void* stream);
+/* Segmented sum (the CCAdd accumulation of linprot._accumulate, linprot.py:343-344):
+ * out[o] = sum_{s in [slot_ptr[o], slot_ptr[o+1])} in[members[s]] over [*][parts][L][N]
+ * (slot_ptr / members are DEVICE int32 arrays). */
+int ctb_slot_sum(const ctb_ctx_t* ctx, int base, const void* in, uint32_t parts, const int32_t* slot_ptr,
+                 const int32_t* members, uint32_t n_out, void* out, void* stream);
+
 /* Instrumentation (not a reference interface): launch a register-resident
  * Shoup modmul throughput probe on `stream` (grid = 8 x SM count, 256 threads,
  * 8 chains) for word width 4 or 8; *modmuls receives the number of modular

@@ -54,6 +54,12 @@ SIGNATURES: dict[str, tuple] = {
     "ctb_tensor_round": (_int, [_c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_relin_digit_count": (_int, [_c_void_p]),
     "ctb_relinearize": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_lift_prepare": (_int, [_c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_linear_online_workspace_bytes": (_u64, [_c_void_p, _u32, _u32, _u32, _u32]),
+    "ctb_linear_online": (_int, [_c_void_p, _c_void_p, _u32, _c_void_p, _u32, _c_void_p, _c_void_p,
+                                 ctypes.POINTER(_u32), _u32, _u32, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
+                                 _c_void_p]),
+    "ctb_slot_sum": (_int, [_c_void_p, _int, _c_void_p, _u32, _c_void_p, _c_void_p, _u32, _c_void_p, _c_void_p]),
     "ctb_probe_modmul": (_int, [_int, _u64, _c_void_p, ctypes.POINTER(_u64), _c_void_p]),
 }
 

@@ -487,6 +487,74 @@ class He:
         nu = self._pessimistic_noise() if noise is None else noise
         return Ciphertext(parts, nu, self.backend)
 
+    # -- batched wire format (one conversion kernel per batch) ------------------
+    def batch_to_bytes(self, batch: CiphertextBatch) -> list[bytes]:
+        """[ct_to_bytes(c) for c in batch], byte-identical, one rns->positional kernel."""
+        B, k = len(batch), batch.nparts
+        n = self.params.n
+        limbs = self.params.cipher_ring.limb_count
+        wc = self.ctx._lib.ctb_ctx_pos_words(self.ctx._h)
+        words = torch.empty((B * k, n, wc), dtype=torch.int64, device="cuda")
+        _lib.check(self.ctx._lib.ctb_rns_to_pos(self.ctx._h, _ptr(batch.data.contiguous()), _ptr(words), B * k,
+                                                _stream()), "ctb_rns_to_pos")
+        host = words.cpu().numpy().view("<u8")[:, :, :limbs]
+        head = struct.pack("<IB", n, limbs)
+        out = []
+        for b in range(B):
+            parts = [struct.pack("<B", k)]
+            for j in range(k):
+                parts.append(head)
+                parts.append(np.ascontiguousarray(host[b * k + j]).tobytes())
+            out.append(b"".join(parts))
+        return out
+
+    def batch_from_bytes(self, blobs: Sequence[bytes], noise: int | None = None) -> CiphertextBatch:
+        """Inverse of batch_to_bytes / a list of ct_to_bytes blobs (ct_from_bytes, he.py:463-482)."""
+        if not blobs:
+            raise HeError("empty ciphertext batch")
+        n = self.params.n
+        limbs = self.params.cipher_ring.limb_count
+        size = 5 + n * 8 * limbs
+        k = blobs[0][0]
+        body = np.empty((len(blobs) * k, n, limbs), dtype=np.uint64)
+        for b, blob in enumerate(blobs):
+            if blob[0] != k:
+                raise PartCountError("ciphertexts in one batch must have the same part count")
+            for j in range(k):
+                off = 1 + j * size
+                nn, lc = struct.unpack_from("<IB", blob, off)
+                if nn != n or lc != limbs:
+                    raise ring.RingError("serialized header does not match the ring parameters")
+                body[b * k + j] = np.frombuffer(blob, dtype="<u8", count=n * limbs, offset=off + 5).reshape(n, limbs)
+        wc = self.ctx._lib.ctb_ctx_pos_words(self.ctx._h)
+        if wc != limbs:
+            pad = np.zeros((body.shape[0], n, wc), dtype=np.uint64)
+            pad[:, :, :min(wc, limbs)] = body[:, :, :min(wc, limbs)]
+            body = pad
+        words = torch.from_numpy(body.view(np.int64)).cuda()
+        out = torch.empty((len(blobs), k, self.L, n), dtype=self.ctx.dtype(), device="cuda")
+        _lib.check(self.ctx._lib.ctb_pos_to_rns(self.ctx._h, _ptr(words), _ptr(out), len(blobs) * k, _stream()),
+                   "ctb_pos_to_rns")
+        nu = self._pessimistic_noise() if noise is None else noise
+        return CiphertextBatch(out, nu, self.backend, self.params.cipher_ring)
+
+    def plain_to_bytes(self, polys: torch.Tensor) -> list[bytes]:
+        """[ring_to_bytes(p) for p in polys] for plain-ring values [B, N] (one limb per coefficient)."""
+        head = struct.pack("<IB", self.params.n, 1)
+        host = polys.cpu().numpy().astype("<u8")
+        return [head + host[i].tobytes() for i in range(host.shape[0])]
+
+    def plain_from_bytes(self, blobs: Sequence[bytes]) -> torch.Tensor:
+        n = self.params.n
+        rows = []
+        for blob in blobs:
+            nn, lc = struct.unpack_from("<IB", blob, 0)
+            if nn != n or lc != 1:
+                raise ring.RingError("serialized header does not match the ring parameters")
+            rows.append(np.frombuffer(blob, dtype="<u8", count=n, offset=5))
+        host = (np.stack(rows) % np.uint64(self.params.t)).astype(np.int64)
+        return torch.from_numpy(host).cuda()
+
     def _pessimistic_noise(self) -> int:
         p = self.params
         per_site = p.cc_mul_noise(p.fresh_noise, p.fresh_noise) + 2 * p.cp_mul_noise(p.fresh_noise)

@@ -19,7 +19,7 @@ from pathlib import Path
 import numpy as np
 
 sys.path.insert(0, "/root/reference/pkg/src")
-from privtrain import he, linprot, packing, ring  # noqa: E402
+from privtrain import he, linprot, packing, ring, transport  # noqa: E402
 from privtrain.ring import RingElem, RingParams  # noqa: E402
 
 
@@ -153,6 +153,52 @@ def main():
                           packing.ConvShape(32, 32, 3, 1), P.plain_ring).shape
     out["jobs"] = {"cfg4_fwd": [js.n_x, js.n_w, js.n_out, len(js.sites)],
                    "cfg4_fwd_sites_digest": hashlib.sha256(json.dumps(js.sites).encode()).hexdigest()}
+
+    # ------------------------------------------------------------ two-party precompute protocol transcripts
+    def protocol_case(params, job, keygen_seed=3, offline_seed=2, online_seed=4):
+        cli, srv = he.He(params, he.BACKEND_RLWE), he.He(params, he.BACKEND_RLWE)
+        keys = cli.keygen(keygen_seed)
+        cpool, spool = linprot.TriplePool(), linprot.TriplePool()
+
+        def client(end):
+            linprot.setup_client(end, cli, keys)
+            linprot.precompute_offline_client(end, cli, keys, np.random.default_rng(offline_seed), job.shape, 1, cpool)
+            return linprot.precompute_online_client(end, cli, keys, np.random.default_rng(online_seed), job, cpool)
+
+        def server(end):
+            pks = linprot.setup_server(end, srv)
+            linprot.precompute_offline_server(end, srv, pks, spool)
+            linprot.precompute_online_server(end, srv, pks, spool)
+
+        ce, se = transport.inproc_pair(capture=True)
+        res, _ = transport.run_pair(client, server, ce, se)
+        tr = ce.stats.transcript
+        signed = np.asarray(packing.to_signed_matrix(np.asarray(res.tensor), params.t), dtype=np.int64)
+        return {"c2s": hashlib.sha256(bytes(tr[transport.CLIENT])).hexdigest(),
+                "s2c": hashlib.sha256(bytes(tr[transport.SERVER])).hexdigest(),
+                "c2s_len": len(tr[transport.CLIENT]), "s2c_len": len(tr[transport.SERVER]),
+                "tensor": digest(signed.astype(np.uint64)), "tensor_shape": list(signed.shape),
+                "server_counts": srv.meter.snapshot()["counts"]}
+
+    rng = np.random.default_rng(21)
+    x = rng.integers(-40, 40, size=(2, 8, 8))
+    w = rng.integers(-9, 9, size=(2, 2, 3, 3))
+    proto = {"small_conv": {"x": x.tolist(), "w": w.tolist(),
+                            **protocol_case(Ps, linprot.conv_job("c", x, w, packing.ConvShape(8, 8, 3, 1), Ps.plain_ring))}}
+    rng = np.random.default_rng(22)
+    x = rng.integers(-30, 30, size=(2, 6, 6))
+    gy = rng.integers(-5, 5, size=(3, 4, 4))
+    proto["small_gradw"] = {"x": x.tolist(), "gy": gy.tolist(),
+                            **protocol_case(Ps, linprot.conv_grad_w_job("g", x, gy, packing.ConvShape(6, 6, 4, 1), Ps.plain_ring))}
+    rng = np.random.default_rng(23)
+    xf = rng.integers(-30, 30, size=40)
+    wf = rng.integers(-30, 30, size=(5, 40))
+    proto["small_fc"] = {"x": xf.tolist(), "w": wf.tolist(), **protocol_case(Ps, linprot.fc_job("fc", xf, wf, Ps.plain_ring))}
+    rng = np.random.default_rng(3)
+    x = rng.integers(0, 256, size=(1, 28, 28))
+    w = rng.integers(-128, 128, size=(5, 1, 5, 5))
+    proto["cfg3_image"] = {"x_seed": 3, **protocol_case(P, linprot.conv_job("cfg3", x, w, packing.ConvShape(28, 28, 5, 0), P.plain_ring))}
+    out["protocol"] = proto
 
     path = Path(__file__).with_name("golden.json")
     path.write_text(json.dumps(out, indent=1, sort_keys=True))
