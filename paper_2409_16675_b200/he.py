@@ -73,6 +73,8 @@ class OpMeter:
         self.phase = phase
 
     def tick(self, op: str, secs: float = 0.0, count: int = 1):
+        if count <= 0:
+            return
         with self._lock:
             key = (self.phase, op)
             self.counts[key] = self.counts.get(key, 0) + count
