@@ -41,6 +41,7 @@ def parse_args():
     ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU baseline sample")
+    ap.add_argument("--no-extras", action="store_true", help="skip the cfg2b/cfg3/cfg4 extra measurements")
     return ap.parse_args()
 
 
@@ -170,6 +171,79 @@ def probe_modmul_peak(torch, lib, word: int):
     return best
 
 
+def _time_cpmul(torch, ctx, B, qs, t, steps, warm):
+    """Device-resident batched CPMul timing (CUDA events) for an extra configuration."""
+    dt = ctx.dtype()
+    ct = torch.empty((B, 2, len(qs), ctx.n), dtype=dt, device="cuda")
+    for i, q in enumerate(qs):
+        ct[:, :, i, :] = torch.randint(0, q, (B, 2, ctx.n), device="cuda", dtype=torch.int64).to(dt)
+    pt = torch.randint(0, t, (B, ctx.n), device="cuda", dtype=torch.int64)
+    out = torch.empty_like(ct)
+    for _ in range(warm):
+        ctx.cpmul(ct, pt, out=out)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s.record()
+    for _ in range(steps):
+        ctx.cpmul(ct, pt, out=out)
+    e.record()
+    e.synchronize()
+    ms = s.elapsed_time(e) / steps
+    del ct, out, pt
+    return ms
+
+
+def run_extras(torch, steps):
+    """cfg2b (N=8192, 3 x 50-bit), cfg3 (64 images), cfg4 (32 images: fwd + grad-w + grad-x)."""
+    from paper_2409_16675_b200 import packing, workloads as W
+    from paper_2409_16675_b200.device import RnsContext
+    from paper_2409_16675_b200.params import default_he_params, p8192_he_params
+    extras = {}
+    P8 = p8192_he_params()
+    ctx8 = RnsContext.get(P8.n, P8.cipher_ring.primes, P8.plain_ring.primes)
+    ms = _time_cpmul(torch, ctx8, 4096, P8.cipher_ring.primes, P8.t, max(3, steps // 4), 2)
+    extras["cfg2b_p8192_cpmul"] = {"value": 4096 / (ms * 1e-3), "unit": UNIT, "ms_per_batch": ms,
+                                   "workload": "4096 CPMul, N=8192, q=3x50-bit (u64 residues), t=163841*147457"}
+    P = default_he_params(4096)
+    sess = W.Session.create(P)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(11)
+    # cfg3: 64 images, 1x28x28, 5 filters 5x5, stride 2 (stride-1 job + subsample)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)
+    x3 = torch.randint(0, 256, (64, 1, 28, 28), generator=g, device="cuda", dtype=torch.int64)
+    w3 = torch.randint(-128, 128, (5, 1, 5, 5), generator=g, device="cuda", dtype=torch.int64)
+    jobs3 = {"fwd": [__import__("paper_2409_16675_b200.linprot", fromlist=["x"]).conv_job(
+        f"c3_{b}", x3[b], w3, packing.ConvShape(28, 28, 5, 0), P.plain_ring) for b in range(64)]}
+    W.run_config(sess, jobs3, gen)  # warm
+    r3 = W.run_config(sess, jobs3, gen)
+    out3 = W.signed(r3["outputs"]["fwd"], P.t)[:, :, ::2, ::2]
+    ok3 = bool(torch.equal(out3, W.conv_reference_float(x3, w3, 0)[:, :, ::2, ::2]))
+    extras["cfg3_conv_stride2_b64"] = {"online_ms": r3["online_ms"], "offline_ms": r3["offline_ms"],
+                                       "sites": r3["sites"], "exact_vs_float64_conv": ok3}
+    # cfg4: 32 images fwd + gw + gx
+    (x, w, gy), jobs4 = W.cfg4_jobs(P, 32)
+    W.run_config(sess, jobs4, gen)  # warm
+    runs = [W.run_config(sess, jobs4, gen) for _ in range(3)]
+    r4 = min(runs, key=lambda r: r["online_ms"])
+    fwd = W.signed(r4["outputs"]["fwd"], P.t)
+    wrot = torch.flip(w, dims=(2, 3)).transpose(0, 1).contiguous()
+    ok4 = bool(torch.equal(fwd, W.conv_reference_float(x, w, 1))) and bool(
+        torch.equal(W.signed(r4["outputs"]["gx"], P.t), W.conv_reference_float(gy, wrot, 1)))
+    extras["cfg4_he_conv_fwd_bwd_ms"] = {
+        "value": r4["online_ms"], "unit": "ms", "higher_is_better": False,
+        "online_ms_runs": [round(r["online_ms"], 2) for r in runs],
+        "offline_ms": r4["offline_ms"], "offline_ccmul": r4["ccmul"],
+        "offline_ccmul_per_s": r4["ccmul"] / (r4["offline_ms"] * 1e-3),
+        "sites": r4["sites"], "exact_vs_float64_conv": ok4,
+        "workload": "batch 32: conv 3->64 3x3 pad 1 fwd + grad-w + grad-x (train.py:478-494 lowering), "
+                    "precompute protocol, client+server co-resident, device RNG sampling",
+        "reference_cpu_single_core_s_per_image": {"online": 93.3, "offline": 304.9,
+                                                  "source": "SURVEY.md 6 (reference run in the survey container)"},
+    }
+    return extras
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -276,6 +350,8 @@ def run_ours(args):
     t_hbm = bytes_per * B / (hbm_peak * 1e9)
     bound = "int" if t_int >= t_hbm else "hbm"
 
+    extras = run_extras(torch, args.steps) if not args.no_extras else {}
+
     line = None
     if rank == 0:
         clocks = clk.summary()
@@ -305,6 +381,7 @@ def run_ours(args):
                     "path": "RnsContext.cpmul (ctypes -> ctb_cpmul) on pinned host buffers"},
             "gpu_launches": args.steps,
             "clocks": clocks,
+            "extras": extras,
         }
     if world > 1:
         dist.barrier()

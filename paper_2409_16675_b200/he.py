@@ -322,31 +322,58 @@ class He:
         """he.py:307-323: c0 = b u + e1 + Delta lift(m), c1 = a u + e2."""
         return self.encrypt_many([m], keys, rng)[0]
 
-    def encrypt_many(self, ms: Sequence[RingElem], keys, rng: np.random.Generator) -> CiphertextBatch:
-        """Encrypt a list of plain polys; identical draws to calling encrypt() in order."""
+    def encrypt_many(self, ms, keys, rng) -> CiphertextBatch:
+        """Encrypt plain polys (list of RingElem or an int64 tensor [B, N] of values in [0, t)).
+
+        With a numpy Generator the draws are the reference's, in the reference's
+        order (identical to calling encrypt() B times).  With a torch.Generator
+        on the device, u / e1 / e2 come from the same distributions (uniform
+        ternary; rounded N(0, sigma^2) clipped to +-error_bound, he.py:292-303)
+        drawn by the device Philox stream -- the production mode, which does not
+        reproduce numpy's stream.
+        """
         t0 = self._t0()
-        for m in ms:
-            if not m.params.compatible(self.params.plain_ring):
-                raise HeError("payload must live in the plain ring")
-        B = len(ms)
-        draws = np.empty((B, 3, self.params.n), dtype=np.int64)
-        for k in range(B):
-            draws[k, 0] = self._ternary(rng)
-            draws[k, 1] = self._error(rng)
-            draws[k, 2] = self._error(rng)
-        small = self._small(draws.reshape(B * 3, self.params.n)).view(B, 3, self.L, self.params.n)
+        if isinstance(ms, torch.Tensor):
+            mt = ms.contiguous()
+        else:
+            for m in ms:
+                if not m.params.compatible(self.params.plain_ring):
+                    raise HeError("payload must live in the plain ring")
+            mt = self._plain_tensor(ms)
+        B, n = mt.shape[0], self.params.n
+        if isinstance(rng, torch.Generator):
+            draws = self._device_draws(B, rng)
+        else:
+            host = np.empty((B, 3, n), dtype=np.int64)
+            for k in range(B):
+                host[k, 0] = self._ternary(rng)
+                host[k, 1] = self._error(rng)
+                host[k, 2] = self._error(rng)
+            draws = torch.from_numpy(host.reshape(B * 3, n)).cuda()
+        small = torch.empty((B * 3, self.L, n), dtype=self.ctx.dtype(), device="cuda")
+        _lib.check(self.ctx._lib.ctb_rns_from_small(self.ctx._h, BASE_Q, _ptr(draws), _ptr(small), B * 3, _stream()),
+                   "ctb_rns_from_small")
+        small = small.view(B, 3, self.L, n)
         u = small[:, 0].contiguous()
-        mt = self._plain_tensor(ms)
-        dm = torch.empty((B, self.L, self.params.n), dtype=self.ctx.dtype(), device="cuda")
+        dm = torch.empty((B, self.L, n), dtype=self.ctx.dtype(), device="cuda")
         _lib.check(self.ctx._lib.ctb_lift_plain(self.ctx._h, _ptr(mt), _lib.u64_array(self._delta_res), _ptr(dm), B,
                                                 _stream()), "ctb_lift_plain")
         add0 = self._rns(0, small[:, 1].contiguous(), dm)
         pk = self._pk_prep(keys)
-        out = torch.empty((B, 2, self.L, self.params.n), dtype=self.ctx.dtype(), device="cuda")
+        out = torch.empty((B, 2, self.L, n), dtype=self.ctx.dtype(), device="cuda")
         out[:, 0] = self._mul_prepared(u, pk[0], add0)
         out[:, 1] = self._mul_prepared(u, pk[1], small[:, 2].contiguous())
         self.meter.tick("Enc", self._elapsed(t0), count=B)
         return CiphertextBatch(out, self.params.fresh_noise, self.backend, self.params.cipher_ring)
+
+    def _device_draws(self, B: int, gen: torch.Generator) -> torch.Tensor:
+        n = self.params.n
+        bound = self.params.error_bound
+        out = torch.empty((B, 3, n), dtype=torch.int64, device="cuda")
+        out[:, 0] = torch.randint(-1, 2, (B, n), generator=gen, device="cuda", dtype=torch.int64)
+        g = torch.randn((B, 2, n), generator=gen, device="cuda", dtype=torch.float64) * self.params.noise_stddev
+        out[:, 1:] = torch.clamp(torch.round(g), -bound, bound).to(torch.int64)
+        return out.view(B * 3, n)
 
     def _s_prep(self, keys, power: int) -> torch.Tensor:
         s = keys.secret.data
