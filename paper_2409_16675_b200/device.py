@@ -150,6 +150,56 @@ class RnsContext:
         check(self._lib.ctb_cpmul(self._h, _ptr(ct), _ptr(pt), _ptr(out), ct.shape[0], _stream()), "ctb_cpmul")
         return out
 
+    def cpmul_host(self, ct_h: torch.Tensor, pt_h: torch.Tensor, out_h: torch.Tensor, chunks: int = 8,
+                   slots: int = 3) -> None:
+        """CPMul of host-resident (pinned) batches: chunked H2D / k_cpmul / D2H on three
+        streams so both copy directions overlap each other and the kernel.  Returns
+        after enqueueing; the caller synchronises (or records an event on the
+        current stream, which is made to wait for the last D2H)."""
+        B = ct_h.shape[0]
+        if B == 0:
+            return
+        step = -(-B // max(1, chunks))
+        cur = torch.cuda.current_stream()
+        if not hasattr(self, "_pipe"):
+            self._pipe = [torch.cuda.Stream() for _ in range(3)]
+        s_in, s_comp, s_out = self._pipe
+        shape_ct = (step,) + tuple(ct_h.shape[1:])
+        key = (shape_ct, ct_h.dtype, pt_h.shape[1:])
+        if getattr(self, "_pipe_key", None) != key:
+            self._pipe_buf = [(torch.empty(shape_ct, dtype=ct_h.dtype, device="cuda"),
+                               torch.empty((step,) + tuple(pt_h.shape[1:]), dtype=pt_h.dtype, device="cuda"),
+                               torch.empty(shape_ct, dtype=ct_h.dtype, device="cuda")) for _ in range(slots)]
+            self._pipe_key = key
+        ev_in = [torch.cuda.Event() for _ in range(slots)]
+        ev_comp = [torch.cuda.Event() for _ in range(slots)]
+        ev_out = [None] * slots
+        start = torch.cuda.Event()
+        start.record(cur)
+        for s in (s_in, s_comp, s_out):
+            s.wait_event(start)
+        for i, lo in enumerate(range(0, B, step)):
+            hi = min(B, lo + step)
+            n = hi - lo
+            k = i % slots
+            ct_d, pt_d, out_d = self._pipe_buf[k]
+            if ev_out[k] is not None:
+                s_in.wait_event(ev_out[k])
+            with torch.cuda.stream(s_in):
+                ct_d[:n].copy_(ct_h[lo:hi], non_blocking=True)
+                pt_d[:n].copy_(pt_h[lo:hi], non_blocking=True)
+            ev_in[k].record(s_in)
+            s_comp.wait_event(ev_in[k])
+            with torch.cuda.stream(s_comp):
+                self.cpmul(ct_d[:n], pt_d[:n], out=out_d[:n])
+            ev_comp[k].record(s_comp)
+            s_out.wait_event(ev_comp[k])
+            with torch.cuda.stream(s_out):
+                out_h[lo:hi].copy_(out_d[:n], non_blocking=True)
+            ev_out[k] = torch.cuda.Event()
+            ev_out[k].record(s_out)
+        cur.wait_stream(s_out)
+
     def pp_mul(self, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
         na = self._check_plain(a, "pp_mul")
         if b.shape != a.shape:
