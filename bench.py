@@ -125,7 +125,7 @@ def run_reference(args):
         return
     from oracle.cpu_baseline import CpuPool, usable_cores
     pool = CpuPool(usable_cores())
-    per_step = 2  # CPMuls per process per step (bounded sample of the 4096-ciphertext workload)
+    per_step = 8  # CPMuls per process per step (bounded sample of the 4096-ciphertext workload)
     try:
         for _ in range(args.warmup):
             pool.run(per_step)
