@@ -151,3 +151,109 @@ def conv_reference_float(x, w, pad):
 
 def signed(t: torch.Tensor, modulus: int) -> torch.Tensor:
     return packing.to_signed_tensor(t, modulus)
+
+
+# ---------------------------------------------------------------------------------------- cfg5
+
+def upsample2(g: torch.Tensor, size: int) -> torch.Tensor:
+    """Zero-upsample a stride-2 output gradient onto the stride-1 grid."""
+    out = torch.zeros((*g.shape[:-2], size, size), dtype=g.dtype, device=g.device)
+    out[..., ::2, ::2] = g
+    return out
+
+
+def cfg5_tensors(images: int = 32, seed: int = 5):
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+
+    def r(lo, hi, *shape):
+        return torch.randint(lo, hi, shape, generator=g, device="cuda", dtype=torch.int64)
+
+    return {
+        "x": r(0, 256, images, 3, 32, 32), "w1": r(-128, 128, 64, 3, 3, 3), "gy1": r(-128, 128, images, 64, 32, 32),
+        "a1": r(0, 256, images, 64, 32, 32), "w2": r(-128, 128, 64, 64, 3, 3), "gy2": r(-128, 128, images, 64, 16, 16),
+        "a2": r(0, 256, images, 64, 16, 16), "wfc": r(-128, 128, 10, 64 * 16 * 16), "gfc": r(-128, 128, images, 10),
+    }
+
+
+def cfg5_image_jobs(params, T: dict, b: int, n_chunk: int) -> dict:
+    """Per image: the trainer's linear jobs (train.py:353-494 lowering) plus the stride-2 and
+    FC-chunk lowerings the reference lacks; 12,733 sites at N=8192."""
+    pr = params.plain_ring
+    CS = packing.ConvShape
+    w2rot = torch.flip(T["w2"], dims=(2, 3)).transpose(0, 1).contiguous()
+    gy2u = upsample2(T["gy2"][b], 32)
+    xfc = T["a2"][b].reshape(-1)
+    jobs = {
+        "conv1_fwd": linprot.conv_job(f"c1f{b}", T["x"][b], T["w1"], CS(32, 32, 3, 1), pr),
+        "conv1_gw": linprot.conv_grad_w_job(f"c1w{b}", T["x"][b], T["gy1"][b], CS(32, 32, 32, 1), pr),
+        "conv2_fwd": linprot.conv_job(f"c2f{b}", T["a1"][b], T["w2"], CS(32, 32, 3, 1), pr),
+        "conv2_gx": linprot.conv_job(f"c2x{b}", gy2u, w2rot, CS(32, 32, 3, 1), pr),
+        "conv2_gw": linprot.conv_grad_w_job(f"c2w{b}", T["a1"][b], gy2u, CS(32, 32, 32, 1), pr),
+        "fc_gx": linprot.fc_job(f"fcx{b}", T["gfc"][b], T["wfc"].t().contiguous(), pr),
+    }
+    for c, lo in enumerate(range(0, xfc.numel(), n_chunk)):
+        hi = lo + n_chunk
+        jobs[f"fc_fwd{c}"] = linprot.fc_job(f"fcf{b}_{c}", xfc[lo:hi], T["wfc"][:, lo:hi], pr)
+        jobs[f"fc_gw{c}"] = linprot.outer_job(f"fcw{b}_{c}", T["gfc"][b], xfc[lo:hi], pr)
+    return jobs
+
+
+WEIGHT_GRADIENT_FAMILIES = ("conv1_gw", "conv2_gw", "fc_gw0", "fc_gw1")
+
+
+def run_cfg5(sess: Session, T: dict, gen, group: int = 4, families=None) -> dict:
+    """Offline + online for every image (processed in groups of `group` images to bound HBM),
+    outputs decoded per family; timings in ms (device-synchronised)."""
+    P = sess.client.params
+    images = T["x"].shape[0]
+    res = {"offline_ms": {}, "online_ms": {}, "sites": {}, "outputs": {}}
+    for g0 in range(0, images, group):
+        per_image = [cfg5_image_jobs(P, T, b, P.n) for b in range(g0, min(images, g0 + group))]
+        fams = families or list(per_image[0])
+        for fam in fams:
+            jobs = [pi[fam] for pi in per_image]
+            job, shapes = concat_jobs(jobs, fam)
+            _sync()
+            t0 = time.perf_counter()
+            bundle, mp = offline(sess, job, gen)
+            _sync()
+            t1 = time.perf_counter()
+            out = online(sess, job, bundle, mp, gen)
+            _sync()
+            t2 = time.perf_counter()
+            res["offline_ms"][fam] = res["offline_ms"].get(fam, 0.0) + 1e3 * (t1 - t0)
+            res["online_ms"][fam] = res["online_ms"].get(fam, 0.0) + 1e3 * (t2 - t1)
+            res["sites"][fam] = res["sites"].get(fam, 0) + len(job.shape.sites)
+            o, parts = 0, []
+            for img_job, s in zip(jobs, shapes):
+                parts.append(img_job.extract(out[o:o + s.n_out]))
+                o += s.n_out
+            res["outputs"].setdefault(fam, []).extend(parts)
+            del bundle, mp, out
+    res["outputs"] = {k: torch.stack(v) for k, v in res["outputs"].items()}
+    return res
+
+
+def cfg5_reference_float(T: dict) -> dict:
+    """Plain GPU float64 results of every cfg5 family (exact at these magnitudes)."""
+    x, w1, gy1, a1, w2, gy2, a2, wfc, gfc = (T[k] for k in ("x", "w1", "gy1", "a1", "w2", "gy2", "a2", "wfc", "gfc"))
+    B = x.shape[0]
+    gy2u = upsample2(gy2, 32)
+    w2rot = torch.flip(w2, dims=(2, 3)).transpose(0, 1).contiguous()
+    conv = conv_reference_float
+    ref = {
+        "conv1_fwd": conv(x, w1, 1),
+        "conv1_gw": torch.stack([conv(x[b][:, None], gy1[b][:, None], 1).transpose(0, 1) for b in range(B)]),
+        "conv2_fwd": conv(a1, w2, 1),
+        "conv2_gx": conv(gy2u, w2rot, 1),
+        "conv2_gw": torch.stack([conv(a1[b][:, None], gy2u[b][:, None], 1).transpose(0, 1) for b in range(B)]),
+        "fc_gx": (gfc.double() @ wfc.double()).round().to(torch.int64),
+    }
+    xf = a2.reshape(B, -1)
+    n = xf.shape[1] // 2
+    for c in range(2):
+        sl = slice(c * n, (c + 1) * n)
+        ref[f"fc_fwd{c}"] = (xf[:, sl].double() @ wfc[:, sl].double().t()).round().to(torch.int64)
+        ref[f"fc_gw{c}"] = (gfc[:, :, None].double() * xf[:, None, sl].double()).round().to(torch.int64)
+    return ref
