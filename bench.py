@@ -241,6 +241,24 @@ def run_extras(torch, steps):
         "reference_cpu_single_core_s_per_image": {"online": 93.3, "offline": 304.9,
                                                   "source": "SURVEY.md 6 (reference run in the survey container)"},
     }
+    # cfg5: linear portion of one training step at N=8192, q = 3 x 50-bit, batch 32
+    sess8 = W.Session.create(P8)
+    W.run_cfg5(sess8, W.cfg5_tensors(1, seed=99), gen, group=1)   # builds the lazily-created constants
+    T5 = W.cfg5_tensors(32)
+    r5 = W.run_cfg5(sess8, T5, gen, group=4)
+    ref5 = W.cfg5_reference_float(T5)
+    ok5 = all(bool(torch.equal(W.signed(v, P8.t), ref5[k])) for k, v in r5["outputs"].items())
+    wg = W.WEIGHT_GRADIENT_FAMILIES
+    extras["cfg5_train_step_linear_n8192"] = {
+        "online_ms": sum(r5["online_ms"].values()), "offline_ms": sum(r5["offline_ms"].values()),
+        "offline_ms_weight_gradient_jobs": sum(r5["offline_ms"][k] for k in wg),
+        "ccmul_weight_gradient_jobs": sum(r5["sites"][k] for k in wg),
+        "sites_total": sum(r5["sites"].values()), "exact_vs_float64": ok5,
+        "per_family_online_ms": {k: round(v, 2) for k, v in r5["online_ms"].items()},
+        "per_family_offline_ms": {k: round(v, 2) for k, v in r5["offline_ms"].items()},
+        "workload": "batch 32: conv1 3->64 fwd+gw, conv2 64->64 s2 fwd+gx+gw (stride-1 + subsample / zero-upsampled gy),"
+                    " FC 16384->10 fwd+gw (2 chunks of N) + gx; precompute protocol incl. offline CCMul for every job",
+    }
     return extras
 
 
