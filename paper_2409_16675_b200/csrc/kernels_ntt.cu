@@ -159,27 +159,39 @@ __global__ void k_pointwise(const T* a, const T* b, T* out, const PrimeTab<T>* _
 // limbs is an L2 hit after the first.
 constexpr int CPMUL_NBUF = 1;
 
+// Groups of THREADS threads per CTA for the persistent CPMul: each group runs
+// its own ciphertext of the CTA's limb, all groups share the CTA's twiddle
+// table (2 groups at N >= 2048: 512-thread CTAs, 2 per SM, 32 warps).
+template <typename T, int LOGN>
+__host__ __device__ constexpr int cpmul_groups() { return sizeof(T) == 4 && (LOGN == 12 || LOGN == 11) ? 2 : 1; }
+
 template <typename T, int LOGN, bool SMEM_TW>
-__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS * cpmul_groups<T, LOGN>(),
+                                  cpmul_groups<T, LOGN>() == 2 ? 2 : NttShape<LOGN>::MINB)
 k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>* __restrict__ tabs,
         int L, uint64_t t_half, uint32_t batch) {
   using Sh = NttShape<LOGN>;
+  constexpr int GROUPS = cpmul_groups<T, LOGN>();
+  using Ex = Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>;
   constexpr int TW_WORDS = SMEM_TW ? 2 * shape_tw_entries(LOGN) : 0;
+  constexpr int GROUP_WORDS = Ex::WORDS + Sh::N;  // exchange image + NTT(pt) strip
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
-  Exchanger<T, LOGN, CPMUL_NBUF> ex{tw_sm + TW_WORDS};
-  T* ysm = tw_sm + TW_WORDS + Exchanger<T, LOGN, CPMUL_NBUF>::WORDS + threadIdx.x;
+  const int group = (int)(threadIdx.x / Sh::THREADS);
+  T* gsm = tw_sm + TW_WORDS + group * GROUP_WORDS;
+  Ex ex{gsm};
+  T* ysm = gsm + Ex::WORDS + ntt_tid<LOGN>();
 
   const int limb = blockIdx.x % L;
-  const uint32_t first = blockIdx.x / L;
-  const uint32_t stride = (gridDim.x - limb + L - 1) / L;  // CTAs serving this limb
+  const uint32_t slot = blockIdx.x / L;
+  const uint32_t nslots = (gridDim.x - limb + L - 1) / L;  // CTAs serving this limb
   PrimeRegs<T> pr(tabs + limb);
   const T tmod = tabs[limb].tmod;
   const T* twp = pr.fwd;
   if constexpr (SMEM_TW) {
     const uint4* src = reinterpret_cast<const uint4*>(pr.fwd);
     uint4* dst = reinterpret_cast<uint4*>(tw_sm);
-    for (int i = threadIdx.x; i < TW_WORDS * (int)sizeof(T) / 16; i += Sh::THREADS) dst[i] = __ldg(src + i);
+    for (int i = threadIdx.x; i < TW_WORDS * (int)sizeof(T) / 16; i += Sh::THREADS * GROUPS) dst[i] = __ldg(src + i);
     __syncthreads();
     twp = tw_sm;
   }
@@ -187,7 +199,7 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
 
   T x[Sh::E];
 #pragma unroll 1
-  for (uint32_t b = first; b < batch; b += stride) {
+  for (uint32_t b = slot * GROUPS + group; b < batch; b += nslots * GROUPS) {
     {
       const uint64_t* ppt = pt + (size_t)b * Sh::N + coef_base<LOGN>();
 #pragma unroll
@@ -197,7 +209,7 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
         if (v > t_half) r = sub_mod(r, tmod, pr.p);       // centred lift: v - t
         x[k] = r;
       }
-      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF>(x, ex, tw, pr.p, pr.p2);
+      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) ysm[k * Sh::THREADS] = shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p);
     }
@@ -206,10 +218,10 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
       const size_t off = (((size_t)b * 2 + part) * L + limb) * (size_t)Sh::N + coef_base<LOGN>();
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) x[k] = ct[off + coef_off<LOGN>(k)];
-      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF>(x, ex, tw, pr.p, pr.p2);
+      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) x[k] = mont_mul(x[k], ysm[k * Sh::THREADS], pr.p, pr.pinv);
-      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, CPMUL_NBUF>(x, ex, tw, pr.p, pr.p2);
+      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) out[off + coef_off<LOGN>(k)] = csub(x[k], pr.p);
     }
@@ -408,17 +420,20 @@ static cudaError_t launch_cpmul(const Ctx* c, const Base* b, const void* ct, con
                                 uint64_t batch, cudaStream_t s) {
   using Sh = NttShape<LOGN>;
   // twiddles in shared memory when the table fits beside the exchange image
+  constexpr int GROUPS = cpmul_groups<T, LOGN>();
   constexpr size_t tw_bytes = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
-  constexpr size_t base_bytes = ((size_t)Exchanger<T, LOGN, CPMUL_NBUF>::WORDS + Sh::N) * sizeof(T);
-  constexpr bool SMEM_TW = sizeof(T) == 4 && LOGN >= 9 && tw_bytes + base_bytes <= 200 * 1024;
+  constexpr size_t group_bytes = ((size_t)Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>::WORDS + Sh::N) * sizeof(T);
+  constexpr bool SMEM_TW = sizeof(T) == 4 && LOGN >= 9 && tw_bytes + GROUPS * group_bytes <= 200 * 1024;
   auto kern = k_cpmul<T, LOGN, SMEM_TW>;
-  const size_t smem = base_bytes + (SMEM_TW ? tw_bytes : 0);
+  const size_t smem = GROUPS * group_bytes + (SMEM_TW ? tw_bytes : 0);
   const int L = b->size();
   const uint64_t items = batch * (uint64_t)L;
   if (items == 0) return cudaSuccess;
-  uint32_t grid = persistent_grid((const void*)kern, Sh::THREADS, smem);
-  grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(grid / L * L, (uint64_t)L), items);
-  return launch_kernel_grid(kern, grid, Sh::THREADS, smem, s, (const T*)ct, pt, (T*)out,
+  const int threads = Sh::THREADS * GROUPS;
+  uint32_t grid = persistent_grid((const void*)kern, threads, smem);
+  const uint64_t max_grid = (batch + GROUPS - 1) / GROUPS * (uint64_t)L;
+  grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(grid / L * L, (uint64_t)L), max_grid);
+  return launch_kernel_grid(kern, grid, threads, smem, s, (const T*)ct, pt, (T*)out,
                             (const PrimeTab<T>*)b->d_tabs, L, c->t_half, (uint32_t)batch);
 }
 

@@ -71,6 +71,14 @@ struct NttShape {
   __host__ __device__ static constexpr int tw_off(int k) { return shape_tw_off(LOGN, k); }
 };
 
+// Thread index inside the transform's thread group.  Kernels that run several
+// independent transforms per CTA (one per group of THREADS threads) get the
+// lane of the group; for one transform per CTA this is threadIdx.x.
+template <int LOGN>
+__device__ __forceinline__ int ntt_tid() {
+  return (int)(threadIdx.x & (NttShape<LOGN>::THREADS - 1));
+}
+
 // Shared-memory image of a polynomial: element idx lives at word
 // phys(idx) = sum over set bits b of idx of WEIGHT[b].  The weights are
 // 2^b plus a little padding chosen so that, in every pass layout, the 32
@@ -141,9 +149,9 @@ template <int LOGN, int S0, int R>
 __device__ __forceinline__ int tw_slot(int gg) {
   using Sh = NttShape<LOGN>;
   if constexpr (S0 + R == LOGN) {
-    return gg * Sh::THREADS + threadIdx.x;
+    return gg * Sh::THREADS + ntt_tid<LOGN>();
   } else {
-    const int g = gg * Sh::THREADS + threadIdx.x;
+    const int g = gg * Sh::THREADS + ntt_tid<LOGN>();
     return g >> (LOGN - S0 - R);
   }
 }
@@ -244,10 +252,23 @@ __device__ __forceinline__ void inv_pass(T (&x)[NttShape<LOGN>::E], TwSrc<T, SME
   }
 }
 
+// Barrier over the THREADS threads of one transform: the whole CTA (GROUPS = 1)
+// or one named barrier per group (ids 1..GROUPS) when a CTA runs GROUPS
+// independent transforms.
+template <int LOGN, int GROUPS>
+__device__ __forceinline__ void group_sync() {
+  if constexpr (GROUPS == 1) {
+    __syncthreads();
+  } else {
+    const int id = 1 + (int)(threadIdx.x / NttShape<LOGN>::THREADS);
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(NttShape<LOGN>::THREADS) : "memory");
+  }
+}
+
 // Shared-memory exchange between two pass layouts.  NBUF = 2 double-buffers
 // (one barrier per exchange); NBUF = 1 halves the footprint for one more
 // resident CTA at the price of a second barrier (write-after-read guard).
-template <typename T, int LOGN, int NBUF = 2>
+template <typename T, int LOGN, int NBUF = 2, int GROUPS = 1>
 struct Exchanger {
   T* buf;      // NBUF * SmemImage::WORDS words
   int cur = 0;
@@ -257,38 +278,38 @@ struct Exchanger {
     using Sh = NttShape<LOGN>;
     T* b = buf + cur * SmemImage<T, LOGN>::WORDS;
     if constexpr (NBUF == 2) cur ^= 1;
-    else __syncthreads();
-    T* wa = b + phys<T, LOGN>(pass_index<LOGN, SA, RA>(threadIdx.x, 0));
-    T* wb = b + phys<T, LOGN>(pass_index<LOGN, SB, RB>(threadIdx.x, 0));
+    else group_sync<LOGN, GROUPS>();
+    T* wa = b + phys<T, LOGN>(pass_index<LOGN, SA, RA>(ntt_tid<LOGN>(), 0));
+    T* wb = b + phys<T, LOGN>(pass_index<LOGN, SB, RB>(ntt_tid<LOGN>(), 0));
 #pragma unroll
     for (int k = 0; k < Sh::E; ++k) wa[phys<T, LOGN>(pass_index<LOGN, SA, RA>(0, k))] = x[k];
-    __syncthreads();
+    group_sync<LOGN, GROUPS>();
 #pragma unroll
     for (int k = 0; k < Sh::E; ++k) x[k] = wb[phys<T, LOGN>(pass_index<LOGN, SB, RB>(0, k))];
   }
 };
 
-template <typename T, int LOGN, int K = 0, bool SMEM, int NBUF>
-__device__ __forceinline__ void ntt_fwd_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN, NBUF>& ex,
+template <typename T, int LOGN, int K = 0, bool SMEM, int NBUF, int GROUPS>
+__device__ __forceinline__ void ntt_fwd_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN, NBUF, GROUPS>& ex,
                                              TwSrc<T, SMEM> tw, T p, T p2) {
   using Sh = NttShape<LOGN>;
   constexpr int S = Sh::pass_s(K), R = Sh::pass_r(K);
   fwd_pass<T, LOGN, K, SMEM>(x, tw, p, p2);
   if constexpr (K + 1 < Sh::NPASS) {
     ex.template run<S, R, Sh::pass_s(K + 1), Sh::pass_r(K + 1)>(x);
-    ntt_fwd_regs<T, LOGN, K + 1, SMEM, NBUF>(x, ex, tw, p, p2);
+    ntt_fwd_regs<T, LOGN, K + 1, SMEM, NBUF, GROUPS>(x, ex, tw, p, p2);
   }
 }
 
-template <typename T, int LOGN, int K = NttShape<LOGN>::NPASS - 1, bool SMEM, int NBUF>
-__device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN, NBUF>& ex,
+template <typename T, int LOGN, int K = NttShape<LOGN>::NPASS - 1, bool SMEM, int NBUF, int GROUPS>
+__device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN, NBUF, GROUPS>& ex,
                                              TwSrc<T, SMEM> tw, T p, T p2) {
   using Sh = NttShape<LOGN>;
   constexpr int S = Sh::pass_s(K), R = Sh::pass_r(K);
   inv_pass<T, LOGN, K, SMEM>(x, tw, p, p2);
   if constexpr (K > 0) {
     ex.template run<S, R, Sh::pass_s(K - 1), Sh::pass_r(K - 1)>(x);
-    ntt_inv_regs<T, LOGN, K - 1, SMEM, NBUF>(x, ex, tw, p, p2);
+    ntt_inv_regs<T, LOGN, K - 1, SMEM, NBUF, GROUPS>(x, ex, tw, p, p2);
   }
 }
 
@@ -296,19 +317,19 @@ __device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchange
 template <typename T, int LOGN>
 __device__ __forceinline__ void ntt_fwd_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN>& ex,
                                              const T* tw, T p, T p2) {
-  ntt_fwd_regs<T, LOGN, 0, false, 2>(x, ex, TwSrc<T, false>{tw}, p, p2);
+  ntt_fwd_regs<T, LOGN, 0, false, 2, 1>(x, ex, TwSrc<T, false>{tw}, p, p2);
 }
 template <typename T, int LOGN>
 __device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN>& ex,
                                              const T* tw, T p, T p2) {
-  ntt_inv_regs<T, LOGN, NttShape<LOGN>::NPASS - 1, false, 2>(x, ex, TwSrc<T, false>{tw}, p, p2);
+  ntt_inv_regs<T, LOGN, NttShape<LOGN>::NPASS - 1, false, 2, 1>(x, ex, TwSrc<T, false>{tw}, p, p2);
 }
 
 // Coefficient-domain layout (first pass, coalesced: thread t owns t + j*THREADS):
 // element index = coef_base() + coef_off(k).
 template <int LOGN>
 __device__ __forceinline__ int coef_base() {
-  return pass_index<LOGN, 0, NttShape<LOGN>::FIRST_R>(threadIdx.x, 0);
+  return pass_index<LOGN, 0, NttShape<LOGN>::FIRST_R>(ntt_tid<LOGN>(), 0);
 }
 template <int LOGN>
 __host__ __device__ constexpr int coef_off(int k) {
@@ -318,7 +339,7 @@ __host__ __device__ constexpr int coef_off(int k) {
 template <int LOGN>
 __device__ __forceinline__ int eval_base() {
   using Sh = NttShape<LOGN>;
-  return pass_index<LOGN, Sh::pass_s(Sh::NPASS - 1), Sh::pass_r(Sh::NPASS - 1)>(threadIdx.x, 0);
+  return pass_index<LOGN, Sh::pass_s(Sh::NPASS - 1), Sh::pass_r(Sh::NPASS - 1)>(ntt_tid<LOGN>(), 0);
 }
 template <int LOGN>
 __host__ __device__ constexpr int eval_off(int k) {
