@@ -26,7 +26,7 @@ k_ntt_fwd(const T* in, T* out, const PrimeTab<T>* __restrict__ tabs, int L) {
   for (int k = 0; k < Sh::E; ++k) x[k] = in[off + coef_base<LOGN>() + coef_off<LOGN>(k)];
   ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
 #pragma unroll
-  for (int k = 0; k < Sh::E; ++k) out[off + eval_base<LOGN>() + eval_off<LOGN>(k)] = reduce4(x[k], pr.p);
+  for (int k = 0; k < Sh::E; ++k) out[off + eval_base<LOGN>() + eval_off<LOGN>(k)] = pr.canon_fwd(x[k]);
 }
 
 template <typename T, int LOGN>

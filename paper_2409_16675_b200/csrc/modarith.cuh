@@ -43,6 +43,19 @@ __device__ __forceinline__ T shoup_mul(T a, T w, T wq, T p) {
   return a * w - q * p;
 }
 
+// 64-bit Shoup with an approximate high product: the lowest 32x32 partial
+// product and the carries of the middle ones are dropped, so the quotient may
+// be low by at most 2 and the result lies in [0, 4p) (p < 2^62, any a).  Three
+// IMAD.WIDE instead of the exact __umul64hi sequence.
+__device__ __forceinline__ uint64_t mulhi64_approx(uint64_t a, uint64_t b) {
+  const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32), b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
+  const uint64_t m1 = (uint64_t)a1 * b0, m2 = (uint64_t)a0 * b1, hh = (uint64_t)a1 * b1;
+  return hh + (m1 >> 32) + (m2 >> 32);
+}
+__device__ __forceinline__ uint64_t shoup_mul_lazy4(uint64_t a, uint64_t w, uint64_t wq, uint64_t p) {
+  return a * w - mulhi64_approx(a, wq) * p;
+}
+
 // Montgomery REDC of a*b with R = 2^W: returns a*b*R^-1 mod p in [0, 2p)
 // provided a*b < 2p * R (true for a < 4p, b < 2p, p < 2^(W-2)... see DESIGN.md).
 // pinv = p^-1 mod 2^W.

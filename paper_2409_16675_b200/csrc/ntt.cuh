@@ -181,23 +181,46 @@ struct TwSrc {
   }
 };
 
-// Harvey CT butterfly: X, Y in [0,4p) -> X+WY, X-WY in [0,4p).
+// Harvey CT butterfly.
+//  u32 (p < 2^30): X, Y in [0,4p) -> X+WY, X-WY in [0,4p).
+//  u64 (p < 2^50 in practice, < 2^57 required): no conditional subtraction --
+//    t = WY in [0,4p) (approximate Shoup), X+t and X-t+4p grow by < 4p per
+//    stage, so canonical inputs stay below 53p after 13 stages (far below
+//    2^64); consumers are Shoup / Montgomery products (valid for any such
+//    input) or canon_fwd().
 template <typename T>
 __device__ __forceinline__ void ct_bfly(T& X, T& Y, T w, T wq, T p, T p2) {
-  T x = csub(X, p2);
-  T t = shoup_mul(Y, w, wq, p);
-  X = x + t;
-  Y = x - t + p2;
+  if constexpr (sizeof(T) == 8) {
+    const T t = shoup_mul_lazy4(Y, w, wq, p);
+    const T x = X;
+    X = x + t;
+    Y = x + 2 * p2 - t;
+  } else {
+    T x = csub(X, p2);
+    T t = shoup_mul(Y, w, wq, p);
+    X = x + t;
+    Y = x - t + p2;
+  }
 }
 
-// Harvey GS butterfly with the mirrored (negated) twiddle:
-// X, Y in [0,2p) -> X+Y, (Y-X)W in [0,2p).
+// Harvey GS butterfly with the mirrored (negated) twiddle.
+//  u32: X, Y in [0,2p) -> X+Y, (Y-X)W in [0,2p).
+//  u64: X, Y in [0,4p) -> same, in [0,4p) (approximate Shoup); ntt_inv_regs
+//       brings the outputs back below 2p after the last stage.
 template <typename T>
 __device__ __forceinline__ void gs_bfly(T& X, T& Y, T w, T wq, T p, T p2) {
-  T u = csub(X + Y, p2);
-  T v = Y - X + p2;
-  Y = shoup_mul(v, w, wq, p);
-  X = u;
+  if constexpr (sizeof(T) == 8) {
+    const T p4 = 2 * p2;
+    const T u = csub(X + Y, p4);
+    const T v = Y - X + p4;
+    Y = shoup_mul_lazy4(v, w, wq, p);
+    X = u;
+  } else {
+    T u = csub(X + Y, p2);
+    T v = Y - X + p2;
+    Y = shoup_mul(v, w, wq, p);
+    X = u;
+  }
 }
 
 template <typename T, int LOGN, int K, bool SMEM>
@@ -310,6 +333,9 @@ __device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchange
   if constexpr (K > 0) {
     ex.template run<S, R, Sh::pass_s(K - 1), Sh::pass_r(K - 1)>(x);
     ntt_inv_regs<T, LOGN, K - 1, SMEM, NBUF, GROUPS>(x, ex, tw, p, p2);
+  } else if constexpr (sizeof(T) == 8) {
+#pragma unroll
+    for (int k = 0; k < Sh::E; ++k) x[k] = csub(x[k], p2);  // [0,4p) -> [0,2p), as the u32 path
   }
 }
 
@@ -359,6 +385,11 @@ struct PrimeRegs {
     ninvr = tab->ninvr; ninvr_q = tab->ninvr_q;
     one_q = tab->one_q; r2 = tab->r2; r2_q = tab->r2_q; rr = tab->rr;
     fwd = tab->fwd; inv = tab->inv;
+  }
+  // Canonical [0, p) from a forward-transform output (u32: < 4p; u64: < 2^64).
+  __device__ __forceinline__ T canon_fwd(T x) const {
+    if constexpr (sizeof(T) == 4) return reduce4(x, p);
+    else return csub(shoup_mul<uint64_t>(x, 1ull, one_q, p), p);
   }
   // Reduce an arbitrary 64-bit value mod p into [0, 2p).
   __device__ __forceinline__ T reduce_u64_lazy(uint64_t v) const {
