@@ -93,6 +93,14 @@ int ctb_mul_prepared(const ctb_ctx_t* ctx, int base, const void* a, const void* 
 int ctb_cpmul(const ctb_ctx_t* ctx, const void* ct, const uint64_t* pt, void* out, uint64_t batch,
               void* stream);
 
+/* Encryption (He.encrypt, he.py:307-323), fused: out[k] = (b u + e1 + Delta lift(m), a u + e2)
+ * for m [batch][N] uint64 in [0,t), draws [batch][3][N] int64 = (u, e1, e2) small signed
+ * integers sampled by the caller (ternary u, rounded-Gaussian e clipped to the error
+ * bound), pkprep = ctb_prepare_operand of the public key (b, a) as [2][L][N];
+ * out [batch][2][L][N]. */
+int ctb_encrypt(const ctb_ctx_t* ctx, const uint64_t* m, const int64_t* draws, const void* pkprep, void* out,
+                uint64_t batch, void* stream);
+
 /* PPMul in the plain ring: He.pp_mul (he.py:441-445) = ring.ring_mul over the
  * plain primes + 2-prime CRT (ring.py:477-485). */
 int ctb_pp_mul(const ctb_ctx_t* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out,

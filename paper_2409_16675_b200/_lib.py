@@ -36,6 +36,7 @@ SIGNATURES: dict[str, tuple] = {
     "ctb_prepare_operand": (_int, [_c_void_p, _int, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_mul_prepared": (_int, [_c_void_p, _int, _c_void_p, _c_void_p, _u64, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_cpmul": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_encrypt": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_pp_mul": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_rns_elementwise": (_int, [_c_void_p, _int, _int, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_rns_scalar_mul": (_int, [_c_void_p, _int, _c_void_p, ctypes.POINTER(_u64), _c_void_p, _u64, _c_void_p]),

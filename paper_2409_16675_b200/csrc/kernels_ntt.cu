@@ -26,7 +26,8 @@ k_ntt_fwd(const T* in, T* out, const PrimeTab<T>* __restrict__ tabs, int L) {
   for (int k = 0; k < Sh::E; ++k) x[k] = in[off + coef_base<LOGN>() + coef_off<LOGN>(k)];
   ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
 #pragma unroll
-  for (int k = 0; k < Sh::E; ++k) out[off + eval_base<LOGN>() + eval_off<LOGN>(k)] = pr.canon_fwd(x[k]);
+  for (int k = 0; k < Sh::E; ++k) x[k] = pr.canon_fwd(x[k]);
+  store_eval<T, LOGN>(out + off, x);
 }
 
 template <typename T, int LOGN>
@@ -39,8 +40,7 @@ k_ntt_inv(const T* in, T* out, const PrimeTab<T>* __restrict__ tabs, int L) {
   const size_t off = (size_t)blockIdx.x * Sh::N;
   PrimeRegs<T> pr(tabs + limb);
   T x[Sh::E];
-#pragma unroll
-  for (int k = 0; k < Sh::E; ++k) x[k] = in[off + eval_base<LOGN>() + eval_off<LOGN>(k)];
+  load_eval<T, LOGN>(in + off, x);
   ntt_inv_regs<T, LOGN>(x, ex, pr.inv, pr.p, pr.p2);
 #pragma unroll
   for (int k = 0; k < Sh::E; ++k)
@@ -95,8 +95,8 @@ k_prepare(const T* in, T* out, const PrimeTab<T>* __restrict__ tabs, int L) {
   for (int k = 0; k < Sh::E; ++k) x[k] = in[off + coef_base<LOGN>() + coef_off<LOGN>(k)];
   ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
 #pragma unroll
-  for (int k = 0; k < Sh::E; ++k)
-    out[off + eval_base<LOGN>() + eval_off<LOGN>(k)] = csub(shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p), pr.p);
+  for (int k = 0; k < Sh::E; ++k) x[k] = csub(shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p), pr.p);
+  store_eval<T, LOGN>(out + off, x);
 }
 
 // out[i] = a[i] * b (+ addend[i]) with b a prepared operand ([nb][L][N], nb = 1
@@ -112,14 +112,20 @@ k_mul_prepared(const T* a, const T* bprep, uint64_t b_stride, const T* addend, T
   const int limb = blockIdx.x % L;
   const size_t poly = blockIdx.x / L;
   const size_t off = (size_t)blockIdx.x * Sh::N;
-  const T* pb = bprep + (poly * b_stride * L + limb) * (size_t)Sh::N + eval_base<LOGN>();
+  const T* pb = bprep + (poly * b_stride * L + limb) * (size_t)Sh::N;
   PrimeRegs<T> pr(tabs + limb);
   T x[Sh::E];
 #pragma unroll
   for (int k = 0; k < Sh::E; ++k) x[k] = a[off + coef_base<LOGN>() + coef_off<LOGN>(k)];
   ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
+  using EV = EvalVec<T, LOGN>;
 #pragma unroll
-  for (int k = 0; k < Sh::E; ++k) x[k] = mont_mul(x[k], __ldg(pb + eval_off<LOGN>(k)), pr.p, pr.pinv);
+  for (int i = 0; i < EV::CHUNKS; ++i) {
+    T v[EV::VEC];
+    EV::load(pb, i, v);
+#pragma unroll
+    for (int c = 0; c < EV::VEC; ++c) x[i * EV::VEC + c] = mont_mul(x[i * EV::VEC + c], v[c], pr.p, pr.pinv);
+  }
   ntt_inv_regs<T, LOGN>(x, ex, pr.inv, pr.p, pr.p2);
 #pragma unroll
   for (int k = 0; k < Sh::E; ++k) {
@@ -224,6 +230,90 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
       ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) out[off + coef_off<LOGN>(k)] = csub(x[k], pr.p);
+    }
+  }
+}
+
+// Fused encryption (He.encrypt, he.py:307-323): per (ciphertext, limb)
+//   c0 = INTT(NTT(u) * b^) + e1 + Delta * lift(m),   c1 = INTT(NTT(u) * a^) + e2
+// with (b^, a^) the prepared public key ([2][L][N], ctb_prepare_operand) and
+// draws [B][3][N] int64 = (u, e1, e2) small signed integers sampled by the
+// caller (the reference's numpy stream, or the device generator).  One forward
+// and two inverse transforms per limb; persistent and limb-stationary like
+// k_cpmul, twiddles in shared memory.
+template <typename T, int LOGN, bool SMEM_TW>
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS * cpmul_groups<T, LOGN>(),
+                                  cpmul_groups<T, LOGN>() == 2 ? 2 : NttShape<LOGN>::MINB)
+k_encrypt(const uint64_t* __restrict__ m, const int64_t* __restrict__ draws, const T* __restrict__ pkprep, T* out,
+          const PrimeTab<T>* __restrict__ tabs, int L, uint64_t t_half, uint32_t batch) {
+  using Sh = NttShape<LOGN>;
+  constexpr int GROUPS = cpmul_groups<T, LOGN>();
+  using Ex = Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>;
+  constexpr int TW_WORDS = SMEM_TW ? 2 * shape_tw_entries(LOGN) : 0;
+  constexpr int GROUP_WORDS = Ex::WORDS + Sh::N;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* tw_sm = reinterpret_cast<T*>(smem_raw);
+  const int group = (int)(threadIdx.x / Sh::THREADS);
+  T* gsm = tw_sm + TW_WORDS + group * GROUP_WORDS;
+  Ex ex{gsm};
+  T* usm = gsm + Ex::WORDS + ntt_tid<LOGN>();   // NTT(u), thread-private strip
+
+  const int limb = blockIdx.x % L;
+  const uint32_t slot = blockIdx.x / L;
+  const uint32_t nslots = (gridDim.x - limb + L - 1) / L;
+  PrimeRegs<T> pr(tabs + limb);
+  const T tmod = tabs[limb].tmod, delta = tabs[limb].delta, delta_q = tabs[limb].delta_q;
+  const T* twp = pr.fwd;
+  if constexpr (SMEM_TW) {
+    const uint4* src = reinterpret_cast<const uint4*>(pr.fwd);
+    uint4* dst = reinterpret_cast<uint4*>(tw_sm);
+    for (int i = threadIdx.x; i < TW_WORDS * (int)sizeof(T) / 16; i += Sh::THREADS * GROUPS) dst[i] = __ldg(src + i);
+    __syncthreads();
+    twp = tw_sm;
+  }
+  const TwSrc<T, SMEM_TW> tw{twp};
+  auto small = [&](int64_t v) -> T {  // signed small integer -> canonical residue
+    const uint64_t mag = v < 0 ? (uint64_t)(-(v + 1)) + 1 : (uint64_t)v;
+    T r = csub(pr.reduce_u64_lazy(mag), pr.p);
+    return v < 0 ? sub_mod((T)0, r, pr.p) : r;
+  };
+  const int cb = coef_base<LOGN>();
+  T x[Sh::E];
+#pragma unroll 1
+  for (uint32_t b = slot * GROUPS + group; b < batch; b += nslots * GROUPS) {
+    const int64_t* d = draws + (size_t)b * 3 * Sh::N + cb;
+#pragma unroll
+    for (int k = 0; k < Sh::E; ++k) x[k] = small(__ldg(d + coef_off<LOGN>(k)));
+    ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+#pragma unroll
+    for (int k = 0; k < Sh::E; ++k) usm[k * Sh::THREADS] = x[k];
+#pragma unroll 1
+    for (int part = 0; part < 2; ++part) {
+      const T* kp = pkprep + ((size_t)part * L + limb) * Sh::N;
+      using EV = EvalVec<T, LOGN>;
+#pragma unroll
+      for (int i = 0; i < EV::CHUNKS; ++i) {
+        T v[EV::VEC];
+        EV::load(kp, i, v);
+#pragma unroll
+        for (int c = 0; c < EV::VEC; ++c)
+          x[i * EV::VEC + c] = mont_mul(usm[(i * EV::VEC + c) * Sh::THREADS], v[c], pr.p, pr.pinv);
+      }
+      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+      const int64_t* e = d + (size_t)(1 + part) * Sh::N;
+      const uint64_t* mm = m + (size_t)b * Sh::N + cb;
+      T* o = out + (((size_t)b * 2 + part) * L + limb) * Sh::N + cb;
+#pragma unroll
+      for (int k = 0; k < Sh::E; ++k) {
+        T v = add_mod(csub(x[k], pr.p), small(__ldg(e + coef_off<LOGN>(k))), pr.p);
+        if (part == 0) {
+          const uint64_t mv = __ldg(mm + coef_off<LOGN>(k));
+          T l = csub(pr.reduce_u64_lazy(mv), pr.p);
+          if (mv > t_half) l = sub_mod(l, tmod, pr.p);
+          v = add_mod(v, csub(shoup_mul(l, delta, delta_q, pr.p), pr.p), pr.p);
+        }
+        o[coef_off<LOGN>(k)] = v;
+      }
     }
   }
 }
@@ -451,6 +541,42 @@ extern "C" int ctb_cpmul(const ctb_ctx_t* ctx, const void* ct, const uint64_t* p
     CTB_DISPATCH_LOGN(c->logn, e = (launch_cpmul<uint64_t, LOGN>(c, b, ct, pt, out, batch, s)));
   }
   return cuda_status(e, "ctb_cpmul");
+}
+
+template <typename T, int LOGN>
+static cudaError_t launch_encrypt(const Ctx* c, const Base* b, const uint64_t* m, const int64_t* draws,
+                                  const void* pkprep, void* out, uint64_t batch, cudaStream_t s) {
+  using Sh = NttShape<LOGN>;
+  constexpr int GROUPS = cpmul_groups<T, LOGN>();
+  constexpr size_t tw_bytes = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
+  constexpr size_t group_bytes = ((size_t)Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>::WORDS + Sh::N) * sizeof(T);
+  constexpr bool SMEM_TW = sizeof(T) == 4 && LOGN >= 9 && tw_bytes + GROUPS * group_bytes <= 200 * 1024;
+  auto kern = k_encrypt<T, LOGN, SMEM_TW>;
+  const size_t smem = GROUPS * group_bytes + (SMEM_TW ? tw_bytes : 0);
+  const int L = b->size();
+  if (batch == 0) return cudaSuccess;
+  const int threads = Sh::THREADS * GROUPS;
+  uint32_t grid = persistent_grid((const void*)kern, threads, smem);
+  const uint64_t max_grid = (batch + GROUPS - 1) / GROUPS * (uint64_t)L;
+  grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(grid / L * L, (uint64_t)L), max_grid);
+  return launch_kernel_grid(kern, grid, threads, smem, s, m, draws, (const T*)pkprep, (T*)out,
+                            (const PrimeTab<T>*)b->d_tabs, L, c->t_half, (uint32_t)batch);
+}
+
+extern "C" int ctb_encrypt(const ctb_ctx_t* ctx, const uint64_t* m, const int64_t* draws, const void* pkprep,
+                           void* out, uint64_t batch, void* stream) {
+  const Base* b = base_of(ctx, BASE_Q);
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (!b || !c->t || !m || !draws || !pkprep || !out) { set_error("ctb_encrypt: bad context (needs plain ring) or buffer"); return ERR_ARG; }
+  if (batch >= (1ull << 32)) { set_error("ctb_encrypt: batch too large"); return ERR_ARG; }
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  if (b->word == 4) {
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_encrypt<uint32_t, LOGN>(c, b, m, draws, pkprep, out, batch, s)));
+  } else {
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_encrypt<uint64_t, LOGN>(c, b, m, draws, pkprep, out, batch, s)));
+  }
+  return cuda_status(e, "ctb_encrypt");
 }
 
 extern "C" int ctb_pp_mul(const ctb_ctx_t* ctx, const uint64_t* a, const uint64_t* bb, uint64_t* out,

@@ -44,9 +44,9 @@ k_lift_prepare(const uint64_t* __restrict__ m, T* out, const PrimeTab<T>* __rest
     x[k] = r;
   }
   ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
-  T* dst = out + (size_t)blockIdx.x * Sh::N + eval_base<LOGN>();
 #pragma unroll
-  for (int k = 0; k < Sh::E; ++k) dst[eval_off<LOGN>(k)] = csub(shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p), pr.p);
+  for (int k = 0; k < Sh::E; ++k) x[k] = csub(shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p), pr.p);
+  store_eval<T, LOGN>(out + (size_t)blockIdx.x * Sh::N, x);
 }
 
 // X [n_x][2][L][N], W [n_w][2][L][N]: canonical eval; MXp [n_x][L][N], MWp [n_w][L][N]: prepared.
@@ -62,7 +62,7 @@ k_lin_cipher(const T* X, const T* W, const T* MXp, const T* MWp, const int32_t* 
   const int slot = blockIdx.x / L;
   PrimeRegs<T> pr(tabs + limb);
   const size_t N = Sh::N, LN = (size_t)L * N;
-  const int eb = eval_base<LOGN>();
+  using EV = EvalVec<T, LOGN>;
   T a0[Sh::E], a1[Sh::E];
 #pragma unroll
   for (int k = 0; k < Sh::E; ++k) a0[k] = a1[k] = 0;
@@ -70,20 +70,25 @@ k_lin_cipher(const T* X, const T* W, const T* MXp, const T* MWp, const int32_t* 
 #pragma unroll 1
   for (int s = s0; s < s1; ++s) {
     const size_t xi = (size_t)site_x[s], wi = (size_t)site_w[s];
-    const T* x0 = X + (xi * 2 + 0) * LN + limb * N + eb;
-    const T* x1 = X + (xi * 2 + 1) * LN + limb * N + eb;
-    const T* w0 = W + (wi * 2 + 0) * LN + limb * N + eb;
-    const T* w1 = W + (wi * 2 + 1) * LN + limb * N + eb;
-    const T* mx = MXp + xi * LN + limb * N + eb;
-    const T* mw = MWp + wi * LN + limb * N + eb;
+    const T* x0 = X + (xi * 2 + 0) * LN + limb * N;
+    const T* x1 = X + (xi * 2 + 1) * LN + limb * N;
+    const T* w0 = W + (wi * 2 + 0) * LN + limb * N;
+    const T* w1 = W + (wi * 2 + 1) * LN + limb * N;
+    const T* mx = MXp + xi * LN + limb * N;
+    const T* mw = MWp + wi * LN + limb * N;
 #pragma unroll
-    for (int k = 0; k < Sh::E; ++k) {
-      const int o = eval_off<LOGN>(k);
-      const T m_w = __ldg(mw + o), m_x = __ldg(mx + o);
-      a0[k] = csub(a0[k] + mont_mul(__ldg(x0 + o), m_w, pr.p, pr.pinv), pr.p2);
-      a0[k] = csub(a0[k] + mont_mul(__ldg(w0 + o), m_x, pr.p, pr.pinv), pr.p2);
-      a1[k] = csub(a1[k] + mont_mul(__ldg(x1 + o), m_w, pr.p, pr.pinv), pr.p2);
-      a1[k] = csub(a1[k] + mont_mul(__ldg(w1 + o), m_x, pr.p, pr.pinv), pr.p2);
+    for (int i = 0; i < EV::CHUNKS; ++i) {
+      T vx0[EV::VEC], vx1[EV::VEC], vw0[EV::VEC], vw1[EV::VEC], vmx[EV::VEC], vmw[EV::VEC];
+      EV::load(x0, i, vx0); EV::load(x1, i, vx1); EV::load(w0, i, vw0);
+      EV::load(w1, i, vw1); EV::load(mx, i, vmx); EV::load(mw, i, vmw);
+#pragma unroll
+      for (int c = 0; c < EV::VEC; ++c) {
+        const int k = i * EV::VEC + c;
+        a0[k] = csub(a0[k] + mont_mul(vx0[c], vmw[c], pr.p, pr.pinv), pr.p2);
+        a0[k] = csub(a0[k] + mont_mul(vw0[c], vmx[c], pr.p, pr.pinv), pr.p2);
+        a1[k] = csub(a1[k] + mont_mul(vx1[c], vmw[c], pr.p, pr.pinv), pr.p2);
+        a1[k] = csub(a1[k] + mont_mul(vw1[c], vmx[c], pr.p, pr.pinv), pr.p2);
+      }
     }
   }
 #pragma unroll 1
@@ -116,19 +121,24 @@ k_lin_plain(const uint32_t* MXt, const uint32_t* MWtp, const int32_t* __restrict
   const int slot = blockIdx.x / LT;
   PrimeRegs<T> pr(tabs + j);
   const size_t N = Sh::N, LN = (size_t)LT * N;
-  const int eb = eval_base<LOGN>();
+  using EV = EvalVec<T, LOGN>;
   T acc[Sh::E];
 #pragma unroll
   for (int k = 0; k < Sh::E; ++k) acc[k] = 0;
   const int s0 = slot_ptr[slot], s1 = slot_ptr[slot + 1];
 #pragma unroll 1
   for (int s = s0; s < s1; ++s) {
-    const T* mx = MXt + (size_t)site_x[s] * LN + j * N + eb;
-    const T* mw = MWtp + (size_t)site_w[s] * LN + j * N + eb;
+    const T* mx = MXt + (size_t)site_x[s] * LN + j * N;
+    const T* mw = MWtp + (size_t)site_w[s] * LN + j * N;
 #pragma unroll
-    for (int k = 0; k < Sh::E; ++k)
-      acc[k] = csub(acc[k] + mont_mul(__ldg(mx + eval_off<LOGN>(k)), __ldg(mw + eval_off<LOGN>(k)), pr.p, pr.pinv),
-                    pr.p2);
+    for (int i = 0; i < EV::CHUNKS; ++i) {
+      T vx[EV::VEC], vw[EV::VEC];
+      EV::load(mx, i, vx);
+      EV::load(mw, i, vw);
+#pragma unroll
+      for (int c = 0; c < EV::VEC; ++c)
+        acc[i * EV::VEC + c] = csub(acc[i * EV::VEC + c] + mont_mul(vx[c], vw[c], pr.p, pr.pinv), pr.p2);
+    }
   }
   ntt_inv_regs<T, LOGN>(acc, ex, pr.inv, pr.p, pr.p2);
   T* dst = out + ((size_t)slot * LT + j) * N + coef_base<LOGN>();

@@ -373,6 +373,81 @@ __host__ __device__ constexpr int eval_off(int k) {
   return pass_index<LOGN, Sh::pass_s(Sh::NPASS - 1), Sh::pass_r(Sh::NPASS - 1)>(0, k);
 }
 
+// Vectorised global access in the evaluation layout.  In the last pass each
+// thread owns E contiguous slots (when E/G == 1), so a thread's E words are one
+// 16-byte-aligned run: 4 x 16-byte loads (u32) instead of 16 strided words that
+// touch a separate sector per lane.  base must point at element 0 of the poly.
+template <typename T, int LOGN>
+__device__ __forceinline__ void load_eval(const T* __restrict__ base, T (&x)[NttShape<LOGN>::E]) {
+  using Sh = NttShape<LOGN>;
+  constexpr bool CONTIG = Sh::pass_r(Sh::NPASS - 1) == Sh::LOGE && Sh::E * sizeof(T) % 16 == 0;
+  const T* p = base + eval_base<LOGN>();
+  if constexpr (CONTIG) {
+    const uint4* v = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+    for (int i = 0; i < Sh::E * (int)sizeof(T) / 16; ++i) {
+      const uint4 w = __ldg(v + i);
+      if constexpr (sizeof(T) == 4) {
+        x[4 * i] = w.x; x[4 * i + 1] = w.y; x[4 * i + 2] = w.z; x[4 * i + 3] = w.w;
+      } else {
+        x[2 * i] = (uint64_t)w.x | ((uint64_t)w.y << 32);
+        x[2 * i + 1] = (uint64_t)w.z | ((uint64_t)w.w << 32);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < Sh::E; ++k) x[k] = __ldg(p + eval_off<LOGN>(k));
+  }
+}
+
+// Chunked form: chunk i holds slots [i*VEC, (i+1)*VEC) of the thread (VEC words = 16 B).
+template <typename T, int LOGN>
+struct EvalVec {
+  using Sh = NttShape<LOGN>;
+  static constexpr bool CONTIG = Sh::pass_r(Sh::NPASS - 1) == Sh::LOGE && Sh::E * sizeof(T) % 16 == 0;
+  static constexpr int VEC = CONTIG ? 16 / (int)sizeof(T) : 1;
+  static constexpr int CHUNKS = Sh::E / VEC;
+  // base: element 0 of the polynomial
+  __device__ __forceinline__ static void load(const T* __restrict__ base, int i, T (&v)[VEC]) {
+    const T* p = base + eval_base<LOGN>();
+    if constexpr (CONTIG) {
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(p) + i);
+      if constexpr (sizeof(T) == 4) {
+        v[0] = w.x; v[1] = w.y; v[2] = w.z; v[3] = w.w;
+      } else {
+        v[0] = (uint64_t)w.x | ((uint64_t)w.y << 32);
+        v[1] = (uint64_t)w.z | ((uint64_t)w.w << 32);
+      }
+    } else {
+      v[0] = __ldg(p + eval_off<LOGN>(i));
+    }
+  }
+};
+
+template <typename T, int LOGN>
+__device__ __forceinline__ void store_eval(T* base, const T (&x)[NttShape<LOGN>::E]) {
+  using Sh = NttShape<LOGN>;
+  constexpr bool CONTIG = Sh::pass_r(Sh::NPASS - 1) == Sh::LOGE && Sh::E * sizeof(T) % 16 == 0;
+  T* p = base + eval_base<LOGN>();
+  if constexpr (CONTIG) {
+    uint4* v = reinterpret_cast<uint4*>(p);
+#pragma unroll
+    for (int i = 0; i < Sh::E * (int)sizeof(T) / 16; ++i) {
+      uint4 w;
+      if constexpr (sizeof(T) == 4) {
+        w.x = x[4 * i]; w.y = x[4 * i + 1]; w.z = x[4 * i + 2]; w.w = x[4 * i + 3];
+      } else {
+        w.x = (uint32_t)x[2 * i]; w.y = (uint32_t)(x[2 * i] >> 32);
+        w.z = (uint32_t)x[2 * i + 1]; w.w = (uint32_t)(x[2 * i + 1] >> 32);
+      }
+      v[i] = w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < Sh::E; ++k) p[eval_off<LOGN>(k)] = x[k];
+  }
+}
+
 // Load a PrimeTab into registers (uniform across the CTA).
 template <typename T>
 struct PrimeRegs {

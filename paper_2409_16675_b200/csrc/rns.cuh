@@ -37,13 +37,19 @@ struct MrcTab {
 };
 
 // Digits of x from its residues (canonical inputs; digits canonical).
-template <typename T>
+// LC > 0 fixes the number of primes at compile time (loops unroll, the digit
+// arrays stay in registers); LC = 0 reads it from the table.
+template <typename T, int LC = 0>
 __device__ __forceinline__ void mrc_digits(const MrcTab<T>& tab, const T* r, T* a) {
   a[0] = r[0];
-  for (int j = 1; j < tab.L; ++j) {
+  const int L = LC ? LC : tab.L;
+#pragma unroll
+  for (int j = 1; j < (LC ? LC : MAX_MRC); ++j) {
+    if (!LC && j >= L) break;
     const T qj = tab.q[j], oq = tab.one_q[j];
     T t = r[j];
     const ShoupC<T>* iv = tab.inv + j * (j - 1) / 2;
+#pragma unroll
     for (int i = 0; i < j; ++i) {
       // a_i mod q_j (a_i < q_i may exceed q_j): Shoup reduction then one csub
       const T ai = csub(shoup_mul<T>(a[i], (T)1, oq, qj), qj);

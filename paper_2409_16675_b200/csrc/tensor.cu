@@ -68,6 +68,7 @@ struct TensorConsts {
 struct TensorState {
   void* d_consts = nullptr;
   int K = 0, K2 = 0, L = 0;
+  bool q_lead = false;  // aux base = [Q primes in order] + [P2 primes in order] (index shortcuts valid)
   ~TensorState() {
     if (d_consts) cudaFree(d_consts);
   }
@@ -95,9 +96,12 @@ __device__ __forceinline__ TQ small_to_q(uint32_t v, TQ q, TQ oneq) {
 }
 
 // Horner of u32 digits dig[0..n) (radices r_k, constants hc[k] = r_k mod q) mod a TQ prime.
-template <typename TQ>
-__device__ __forceinline__ TQ horner_to_q(int n, const uint32_t* dig, const ShoupC<TQ>* hc, TQ q, TQ oneq) {
+// NC > 0: n fixed at compile time.
+template <typename TQ, int NC = 0>
+__device__ __forceinline__ TQ horner_to_q(int n_rt, const uint32_t* dig, const ShoupC<TQ>* hc, TQ q, TQ oneq) {
+  const int n = NC ? NC : n_rt;
   TQ acc = small_to_q<TQ>(dig[n - 1], q, oneq);
+#pragma unroll
   for (int k = n - 2; k >= 0; --k) {
     acc = csub(shoup_mul<TQ>(acc, hc[k].w, hc[k].wq, q), q);
     acc = add_mod(acc, small_to_q<TQ>(dig[k], q, oneq), q);
@@ -106,42 +110,58 @@ __device__ __forceinline__ TQ horner_to_q(int n, const uint32_t* dig, const Shou
 }
 
 // Horner of TQ digits (Q mixed radix) mod an aux u32 prime.
-template <typename TQ>
-__device__ __forceinline__ uint32_t horner_to_aux(int n, const TQ* dig, const ShoupC<uint32_t>* hc, uint32_t p,
+template <typename TQ, int NC = 0>
+__device__ __forceinline__ uint32_t horner_to_aux(int n_rt, const TQ* dig, const ShoupC<uint32_t>* hc, uint32_t p,
                                                   uint32_t oneq, uint32_t r2, uint32_t r2q) {
-  uint32_t acc = red_u32((uint64_t)dig[n - 1], p, oneq, r2, r2q);
+  const int n = NC ? NC : n_rt;
+  uint32_t acc;
+  if constexpr (sizeof(TQ) == 4) acc = csub(shoup_mul<uint32_t>((uint32_t)dig[n - 1], 1u, oneq, p), p);
+  else acc = red_u32((uint64_t)dig[n - 1], p, oneq, r2, r2q);
+#pragma unroll
   for (int k = n - 2; k >= 0; --k) {
     acc = csub(shoup_mul<uint32_t>(acc, hc[k].w, hc[k].wq, p), p);
-    acc = add_mod(acc, red_u32((uint64_t)dig[k], p, oneq, r2, r2q), p);
+    uint32_t dk;
+    if constexpr (sizeof(TQ) == 4) dk = csub(shoup_mul<uint32_t>((uint32_t)dig[k], 1u, oneq, p), p);
+    else dk = red_u32((uint64_t)dig[k], p, oneq, r2, r2q);
+    acc = add_mod(acc, dk, p);
   }
   return acc;
 }
 
 // ----------------------------------------------------------------------------- 1 lift
 // in: [B][2][L][N] (TQ) -> out: [B][2][K][N] (u32), centred lifts over the aux base.
-template <typename TQ>
-__global__ void __launch_bounds__(256) k_tensor_lift(const TQ* in, uint32_t* out, const TensorConsts<TQ>* gc,
+// LC / KC > 0: limb / aux counts fixed at compile time (register-resident digits).
+template <typename TQ, int LC, int KC>
+__global__ void __launch_bounds__(256, 2) k_tensor_lift(const TQ* in, uint32_t* out, const TensorConsts<TQ>* gc,
                                                      uint32_t n, uint64_t total) {
   __shared__ TensorConsts<TQ> c;
   load_consts(gc, &c);
-  const int L = c.L, K = c.K;
+  const int L = LC ? LC : c.L, K = KC ? KC : c.K;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t poly = g / n, i = g % n;   // poly = b * 2 + part
     TQ r[MAXQ], a[MAXQ];
-    for (int l = 0; l < L; ++l) r[l] = in[(poly * L + l) * n + i];
-    mrc_digits(c.mrcQ, r, a);
-    // x > (Q-1)/2 ?  lexicographic from the most significant digit
-    bool neg = false;
-    for (int l = L - 1; l >= 0; --l) {
-      if (a[l] != c.halfQ_dig[l]) { neg = a[l] > c.halfQ_dig[l]; break; }
+#pragma unroll
+    for (int l = 0; l < (LC ? LC : MAXQ); ++l) {
+      if (!LC && l >= L) break;
+      r[l] = in[(poly * L + l) * n + i];
     }
-    for (int k = 0; k < K; ++k) {
+    mrc_digits<TQ, LC>(c.mrcQ, r, a);
+    // x > (Q-1)/2 ?  lexicographic from the most significant digit
+    bool neg = false, decided = false;
+#pragma unroll
+    for (int l = (LC ? LC : MAXQ) - 1; l >= 0; --l) {
+      if (!LC && l >= L) continue;
+      if (!decided && a[l] != c.halfQ_dig[l]) { neg = a[l] > c.halfQ_dig[l]; decided = true; }
+    }
+#pragma unroll
+    for (int k = 0; k < (KC ? KC : MAXA); ++k) {
+      if (!KC && k >= K) break;
       uint32_t v;
       const int qi = c.aux_is_q[k];
       if (qi >= 0) {
-        v = (uint32_t)r[qi];  // x == centred value (mod q_i)
+        v = (uint32_t)r[KC && LC && sizeof(TQ) == 4 && k < LC ? k : qi];  // x == centred value (mod q_i)
       } else {
-        v = horner_to_aux<TQ>(L, a, c.lift_hc[k], c.ap[k], c.a_oneq[k], c.a_r2[k], c.a_r2q[k]);
+        v = horner_to_aux<TQ, LC>(L, a, c.lift_hc[k], c.ap[k], c.a_oneq[k], c.a_r2[k], c.a_r2q[k]);
         if (neg) v = sub_mod(v, c.Q_aux[k], c.ap[k]);
       }
       out[(poly * K + k) * n + i] = v;
@@ -150,110 +170,167 @@ __global__ void __launch_bounds__(256) k_tensor_lift(const TQ* in, uint32_t* out
 }
 
 // ----------------------------------------------------------------------------- 2 products
-// A, Bt: [B][2][K][N] lifted operands -> H: [B][3][K][N]; CTA per (ciphertext, aux prime).
-template <int LOGN>
+// A, Bt: [B][2][K][N] lifted operands -> H: [B][3][K][N].  Persistent and
+// prime-stationary: CTA k serves aux prime k % K for ciphertext pairs
+// k / K, k / K + n_k, ...; the prime's twiddle table lives in shared memory.
+template <int LOGN, bool SMEM_TW>
 __global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
 k_tensor_product(const uint32_t* A, const uint32_t* Bt, uint32_t* H, const PrimeTab<uint32_t>* __restrict__ tabs,
-                 int K) {
+                 int K, uint32_t batch) {
   using Sh = NttShape<LOGN>;
   using T = uint32_t;
+  constexpr int TW_WORDS = SMEM_TW ? 2 * shape_tw_entries(LOGN) : 0;
+  using Ex = Exchanger<T, LOGN, 1, 1>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Exchanger<T, LOGN> ex{reinterpret_cast<T*>(smem_raw)};
-  T* strip = reinterpret_cast<T*>(smem_raw) + Exchanger<T, LOGN>::WORDS + threadIdx.x;  // 3 polys
+  T* tw_sm = reinterpret_cast<T*>(smem_raw);
+  Ex ex{tw_sm + TW_WORDS};
+  T* strip = tw_sm + TW_WORDS + Ex::WORDS + threadIdx.x;  // 3 thread-private polys
   const int k = blockIdx.x % K;
-  const size_t b = blockIdx.x / K;
+  const uint32_t slot = blockIdx.x / K;
+  const uint32_t nslots = (gridDim.x - k + K - 1) / K;
   PrimeRegs<T> pr(tabs + k);
+  const T* twp = pr.fwd;
+  if constexpr (SMEM_TW) {
+    const uint4* src = reinterpret_cast<const uint4*>(pr.fwd);
+    uint4* dst = reinterpret_cast<uint4*>(tw_sm);
+    for (int i = threadIdx.x; i < TW_WORDS * 4 / 16; i += Sh::THREADS) dst[i] = __ldg(src + i);
+    __syncthreads();
+    twp = tw_sm;
+  }
+  const TwSrc<T, SMEM_TW> tw{twp};
   const size_t N = Sh::N;
-  auto src = [&](const T* base, int part) { return base + ((b * 2 + part) * K + k) * N + coef_base<LOGN>(); };
-  T x[Sh::E];
-  // NTT(a0) -> strip 0, NTT(a1) -> strip 1 (Montgomery form, N^-1 folded), NTT(b0) -> strip 2
-  for (int s = 0; s < 3; ++s) {
-    const T* p = s < 2 ? src(A, s) : src(Bt, 0);
+  T x[Sh::E], y[Sh::E];
+#pragma unroll 1
+  for (uint32_t b = slot; b < batch; b += nslots) {
+    auto src = [&](const T* base, int part) { return base + ((b * 2 + part) * K + k) * N + coef_base<LOGN>(); };
+    // NTT(a0) -> strip 0, NTT(a1) -> strip 1 (Montgomery form, N^-1 folded), NTT(b0) -> strip 2
+#pragma unroll 1
+    for (int s = 0; s < 3; ++s) {
+      const T* p = s < 2 ? src(A, s) : src(Bt, 0);
 #pragma unroll
-    for (int j = 0; j < Sh::E; ++j) x[j] = p[coef_off<LOGN>(j)];
-    ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
+      for (int j = 0; j < Sh::E; ++j) x[j] = __ldg(p + coef_off<LOGN>(j));
+      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, 1, 1>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
-    for (int j = 0; j < Sh::E; ++j) {
-      T v = x[j];
-      if (s < 2) v = shoup_mul(v, pr.ninvr, pr.ninvr_q, pr.p);  // [0,2p)
-      strip[(s * Sh::E + j) * Sh::THREADS] = v;
+      for (int j = 0; j < Sh::E; ++j) {
+        T v = x[j];
+        if (s < 2) v = shoup_mul(v, pr.ninvr, pr.ninvr_q, pr.p);  // [0,2p)
+        strip[(s * Sh::E + j) * Sh::THREADS] = v;
+      }
+    }
+    {  // NTT(b1) in registers
+      const T* p = src(Bt, 1);
+#pragma unroll
+      for (int j = 0; j < Sh::E; ++j) x[j] = __ldg(p + coef_off<LOGN>(j));
+      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, 1, 1>(x, ex, tw, pr.p, pr.p2);
+    }
+    // h2 = a1 b1 ; h1 = a0 b1 + a1 b0 ; h0 = a0 b0
+#pragma unroll 1
+    for (int part = 2; part >= 0; --part) {
+#pragma unroll
+      for (int j = 0; j < Sh::E; ++j) {
+        const T a0 = strip[(0 * Sh::E + j) * Sh::THREADS];
+        const T a1 = strip[(1 * Sh::E + j) * Sh::THREADS];
+        const T b0 = strip[(2 * Sh::E + j) * Sh::THREADS];
+        T v;
+        if (part == 2) v = mont_mul(x[j], a1, pr.p, pr.pinv);
+        else if (part == 1) v = csub(mont_mul(x[j], a0, pr.p, pr.pinv) + mont_mul(b0, a1, pr.p, pr.pinv), pr.p2);
+        else v = mont_mul(b0, a0, pr.p, pr.pinv);
+        y[j] = v;
+      }
+      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1>(y, ex, tw, pr.p, pr.p2);
+      T* dst = H + ((b * 3 + part) * K + k) * N + coef_base<LOGN>();
+#pragma unroll
+      for (int j = 0; j < Sh::E; ++j) dst[coef_off<LOGN>(j)] = csub(y[j], pr.p);
     }
   }
-  // NTT(b1) in registers
-  {
-    const T* p = src(Bt, 1);
-#pragma unroll
-    for (int j = 0; j < Sh::E; ++j) x[j] = p[coef_off<LOGN>(j)];
-    ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
-  }
-  T y[Sh::E];
-  // h2 = a1 b1 ; h1 = a0 b1 + a1 b0 ; h0 = a0 b0
-  for (int part = 2; part >= 0; --part) {
-#pragma unroll
-    for (int j = 0; j < Sh::E; ++j) {
-      const T a0 = strip[(0 * Sh::E + j) * Sh::THREADS];
-      const T a1 = strip[(1 * Sh::E + j) * Sh::THREADS];
-      const T b0 = strip[(2 * Sh::E + j) * Sh::THREADS];
-      T v;
-      if (part == 2) v = mont_mul(x[j], a1, pr.p, pr.pinv);
-      else if (part == 1) v = csub(mont_mul(x[j], a0, pr.p, pr.pinv) + mont_mul(b0, a1, pr.p, pr.pinv), pr.p2);
-      else v = mont_mul(b0, a0, pr.p, pr.pinv);
-      y[j] = v;
-    }
-    ntt_inv_regs<T, LOGN>(y, ex, pr.inv, pr.p, pr.p2);
-    T* dst = H + ((b * 3 + part) * K + k) * N + coef_base<LOGN>();
-#pragma unroll
-    for (int j = 0; j < Sh::E; ++j) dst[coef_off<LOGN>(j)] = csub(y[j], pr.p);
-  }
+}
+
+template <int LOGN>
+static cudaError_t launch_tensor_product(const Ctx* c, const uint32_t* a, const uint32_t* b, uint32_t* h,
+                                         uint64_t batch, cudaStream_t s) {
+  using Sh = NttShape<LOGN>;
+  const Base& B = c->base[BASE_B];
+  using T = uint32_t;
+  constexpr size_t tw_bytes = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
+  constexpr size_t base_bytes = ((size_t)Exchanger<T, LOGN, 1, 1>::WORDS + 3 * (size_t)Sh::N) * sizeof(T);
+  constexpr bool SMEM_TW = LOGN >= 9 && tw_bytes + base_bytes <= 200 * 1024;
+  auto kern = k_tensor_product<LOGN, SMEM_TW>;
+  const size_t smem = base_bytes + (SMEM_TW ? tw_bytes : 0);
+  const int K = B.size();
+  if (batch == 0) return cudaSuccess;
+  uint32_t grid = persistent_grid((const void*)kern, Sh::THREADS, smem);
+  grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(grid / K * K, (uint64_t)K), batch * (uint64_t)K);
+  return launch_kernel_grid(kern, grid, Sh::THREADS, smem, s, a, b, h, (const PrimeTab<T>*)B.d_tabs, K,
+                            (uint32_t)batch);
 }
 
 // ----------------------------------------------------------------------------- 3 round
 // H: [B][3][K][N] -> out [B][3][L][N] (TQ): round(h t / Q) mod Q.
-template <typename TQ>
-__global__ void __launch_bounds__(256) k_tensor_round(const uint32_t* H, TQ* out, const TensorConsts<TQ>* gc,
+template <typename TQ, int LC, int KC, int K2C>
+__global__ void __launch_bounds__(256, 2) k_tensor_round(const uint32_t* H, TQ* out, const TensorConsts<TQ>* gc,
                                                       uint32_t n, uint64_t total) {
   __shared__ TensorConsts<TQ> c;
   load_consts(gc, &c);
-  const int L = c.L, K = c.K, K2 = c.K2;
+  const int L = LC ? LC : c.L, K = KC ? KC : c.K, K2 = K2C ? K2C : c.K2;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t poly = g / n, i = g % n;   // poly = b * 3 + part
     uint32_t h[MAXA];
-    for (int k = 0; k < K; ++k) h[k] = H[(poly * K + k) * n + i];
+#pragma unroll
+    for (int k = 0; k < (KC ? KC : MAXA); ++k) {
+      if (!KC && k >= K) break;
+      h[k] = H[(poly * K + k) * n + i];
+    }
     // h mod q_i
     TQ hq[MAXQ];
     if (c.ext_h) {
       uint32_t hs[MAXA], dig[MAXA];
-      for (int k = 0; k < K; ++k) hs[k] = add_mod(h[k], c.Kh_aux[k], c.ap[k]);   // h + floor(M/2) in [0, M)
-      mrc_digits(c.mrcA, hs, dig);
-      for (int l = 0; l < L; ++l) {
+#pragma unroll
+      for (int k = 0; k < (KC ? KC : MAXA); ++k) {
+        if (!KC && k >= K) break;
+        hs[k] = add_mod(h[k], c.Kh_aux[k], c.ap[k]);   // h + floor(M/2) in [0, M)
+      }
+      mrc_digits<uint32_t, KC>(c.mrcA, hs, dig);
+#pragma unroll
+      for (int l = 0; l < (LC ? LC : MAXQ); ++l) {
+        if (!LC && l >= L) break;
         const TQ q = c.mrcQ.q[l];
-        const TQ v = horner_to_q<TQ>(K, dig, c.h_hc[l], q, c.mrcQ.one_q[l]);
+        const TQ v = horner_to_q<TQ, KC>(K, dig, c.h_hc[l], q, c.mrcQ.one_q[l]);
         hq[l] = sub_mod(v, c.Kh_q[l], q);
       }
     } else {
-      for (int l = 0; l < L; ++l) hq[l] = (TQ)h[c.q_in_aux[l]];
+#pragma unroll
+      for (int l = 0; l < (LC ? LC : MAXQ); ++l) {
+        if (!LC && l >= L) break;
+        hq[l] = (TQ)h[LC ? l : c.q_in_aux[l]];   // Q primes lead the aux base (build_tensor)
+      }
     }
     // z = h t + (Q-1)/2 mod q_i ; r = z mod Q (Garner digits)
     TQ z[MAXQ], rd[MAXQ];
-    for (int l = 0; l < L; ++l) {
+#pragma unroll
+    for (int l = 0; l < (LC ? LC : MAXQ); ++l) {
+      if (!LC && l >= L) break;
       const TQ q = c.mrcQ.q[l];
       z[l] = add_mod(csub(shoup_mul<TQ>(hq[l], c.t_q[l].w, c.t_q[l].wq, q), q), c.hQ_q[l], q);
     }
-    mrc_digits(c.mrcQ, z, rd);
+    mrc_digits<TQ, LC>(c.mrcQ, z, rd);
     // y' = (z - r) Q^-1 + floor(P2/2) mod each P2 prime
     uint32_t ys[MAXA], yd[MAXA];
-    for (int k = 0; k < K2; ++k) {
+#pragma unroll
+    for (int k = 0; k < (K2C ? K2C : MAXA); ++k) {
+      if (!K2C && k >= K2) break;
       const int ai = c.p2_idx[k];
       const uint32_t p = c.ap[ai];
-      const uint32_t zk = add_mod(csub(shoup_mul<uint32_t>(h[ai], c.t_aux[ai].w, c.t_aux[ai].wq, p), p), c.hQ_aux[ai], p);
-      const uint32_t rk = horner_to_aux<TQ>(L, rd, c.r_hc[k], p, c.a_oneq[ai], c.a_r2[ai], c.a_r2q[ai]);
+      const uint32_t zk = add_mod(csub(shoup_mul<uint32_t>(h[KC && LC && sizeof(TQ) == 4 ? LC + k : ai], c.t_aux[ai].w, c.t_aux[ai].wq, p), p), c.hQ_aux[ai], p);
+      const uint32_t rk = horner_to_aux<TQ, LC>(L, rd, c.r_hc[k], p, c.a_oneq[ai], c.a_r2[ai], c.a_r2q[ai]);
       uint32_t yk = csub(shoup_mul<uint32_t>(sub_mod(zk, rk, p), c.Qinv_p2[k].w, c.Qinv_p2[k].wq, p), p);
       ys[k] = add_mod(yk, c.Ky_p2[k], p);
     }
-    mrc_digits(c.mrcP2, ys, yd);
-    for (int l = 0; l < L; ++l) {
+    mrc_digits<uint32_t, K2C>(c.mrcP2, ys, yd);
+#pragma unroll
+    for (int l = 0; l < (LC ? LC : MAXQ); ++l) {
+      if (!LC && l >= L) break;
       const TQ q = c.mrcQ.q[l];
-      const TQ v = horner_to_q<TQ>(K2, yd, c.y_hc[l], q, c.mrcQ.one_q[l]);
+      const TQ v = horner_to_q<TQ, K2C>(K2, yd, c.y_hc[l], q, c.mrcQ.one_q[l]);
       out[(poly * L + l) * n + i] = sub_mod(v, c.Ky_q[l], q);
     }
   }
@@ -275,7 +352,7 @@ __global__ void __launch_bounds__(256) k_relin_digits(const TQ* ct3, uint32_t* d
     const uint64_t b = g / n, i = g % n;
     TQ r[MAXQ], a[MAXQ];
     for (int l = 0; l < L; ++l) r[l] = ct3[((b * 3 + 2) * L + l) * n + i];
-    mrc_digits(m, r, a);
+    mrc_digits<TQ>(m, r, a);
     uint32_t X[20];
     mrc_positional(m, a, X, words);
     for (int j = 0; j < D; ++j) {
@@ -288,45 +365,91 @@ __global__ void __launch_bounds__(256) k_relin_digits(const TQ* ct3, uint32_t* d
 }
 
 // ----------------------------------------------------------------------------- 5 relin accumulate
-// out [B][2][L][N] = (c0, c1) + sum_j NTT^-1(NTT(d_j) * keyprep[j][0|1]); CTA per (ciphertext, limb).
-template <typename T, int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
+// out [B][2][L][N] = (c0, c1) + sum_j NTT^-1(NTT(d_j) * keyprep[j][0|1]).  Persistent and
+// limb-stationary (CTA k serves limb k % L), the limb's twiddle table staged in shared
+// memory; both accumulators stay in registers across the D digit transforms.
+template <typename T, int LOGN, bool SMEM_TW>
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, (NttShape<LOGN>::THREADS == 256 && sizeof(T) == 4) ? 3
+                                                                : NttShape<LOGN>::MINB)
 k_relin_accum(const T* ct3, const uint32_t* digits, const T* keyprep, T* out,
-              const PrimeTab<T>* __restrict__ tabs, int L, int D) {
+              const PrimeTab<T>* __restrict__ tabs, int L, int D, uint32_t batch) {
   using Sh = NttShape<LOGN>;
+  constexpr int TW_WORDS = SMEM_TW ? 2 * shape_tw_entries(LOGN) : 0;
+  using Ex = Exchanger<T, LOGN, 1, 1>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Exchanger<T, LOGN> ex{reinterpret_cast<T*>(smem_raw)};
+  T* tw_sm = reinterpret_cast<T*>(smem_raw);
+  Ex ex{tw_sm + TW_WORDS};
   const int limb = blockIdx.x % L;
-  const size_t b = blockIdx.x / L;
+  const uint32_t slot = blockIdx.x / L;
+  const uint32_t nslots = (gridDim.x - limb + L - 1) / L;
   const size_t N = Sh::N;
   PrimeRegs<T> pr(tabs + limb);
+  const T* twp = pr.fwd;
+  if constexpr (SMEM_TW) {
+    const uint4* src = reinterpret_cast<const uint4*>(pr.fwd);
+    uint4* dst = reinterpret_cast<uint4*>(tw_sm);
+    for (int i = threadIdx.x; i < TW_WORDS * (int)sizeof(T) / 16; i += Sh::THREADS) dst[i] = __ldg(src + i);
+    __syncthreads();
+    twp = tw_sm;
+  }
+  const TwSrc<T, SMEM_TW> tw{twp};
+  const int cb = coef_base<LOGN>();
+  using EV = EvalVec<T, LOGN>;
   T acc0[Sh::E], acc1[Sh::E], x[Sh::E];
-#pragma unroll
-  for (int j = 0; j < Sh::E; ++j) acc0[j] = acc1[j] = 0;
 #pragma unroll 1
-  for (int d = 0; d < D; ++d) {
-    const uint32_t* src = digits + (b * D + d) * N + coef_base<LOGN>();
+  for (uint32_t b = slot; b < batch; b += nslots) {
 #pragma unroll
-    for (int j = 0; j < Sh::E; ++j) x[j] = csub((T)src[coef_off<LOGN>(j)], pr.p);  // digit < 2^w < 2p
-    ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
-    const T* kb = keyprep + (((size_t)d * 2 + 0) * L + limb) * N + eval_base<LOGN>();
-    const T* ka = keyprep + (((size_t)d * 2 + 1) * L + limb) * N + eval_base<LOGN>();
+    for (int j = 0; j < Sh::E; ++j) acc0[j] = acc1[j] = 0;
+#pragma unroll 1
+    for (int d = 0; d < D; ++d) {
+      const uint32_t* src = digits + ((size_t)b * D + d) * N + cb;
 #pragma unroll
-    for (int j = 0; j < Sh::E; ++j) {
-      acc0[j] = csub(acc0[j] + mont_mul(x[j], __ldg(kb + eval_off<LOGN>(j)), pr.p, pr.pinv), pr.p2);
-      acc1[j] = csub(acc1[j] + mont_mul(x[j], __ldg(ka + eval_off<LOGN>(j)), pr.p, pr.pinv), pr.p2);
+      for (int j = 0; j < Sh::E; ++j) x[j] = csub((T)__ldg(src + coef_off<LOGN>(j)), pr.p);  // digit < 2^w < 2p
+      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, 1, 1>(x, ex, tw, pr.p, pr.p2);
+      const T* kb = keyprep + (((size_t)d * 2 + 0) * L + limb) * N;
+      const T* ka = keyprep + (((size_t)d * 2 + 1) * L + limb) * N;
+#pragma unroll
+      for (int i = 0; i < EV::CHUNKS; ++i) {
+        T vb[EV::VEC], va[EV::VEC];
+        EV::load(kb, i, vb);
+        EV::load(ka, i, va);
+#pragma unroll
+        for (int c = 0; c < EV::VEC; ++c) {
+          const int j = i * EV::VEC + c;
+          acc0[j] = csub(acc0[j] + mont_mul(x[j], vb[c], pr.p, pr.pinv), pr.p2);
+          acc1[j] = csub(acc1[j] + mont_mul(x[j], va[c], pr.p, pr.pinv), pr.p2);
+        }
+      }
+    }
+#pragma unroll 1
+    for (int part = 0; part < 2; ++part) {
+#pragma unroll
+      for (int j = 0; j < Sh::E; ++j) x[j] = part == 0 ? acc0[j] : acc1[j];
+      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1>(x, ex, tw, pr.p, pr.p2);
+      const size_t off = ((b * 3 + part) * L + limb) * N + cb;
+      const size_t oo = ((b * 2 + part) * L + limb) * N + cb;
+#pragma unroll
+      for (int j = 0; j < Sh::E; ++j) out[oo + coef_off<LOGN>(j)] = add_mod(csub(x[j], pr.p), ct3[off + coef_off<LOGN>(j)], pr.p);
     }
   }
-  for (int part = 0; part < 2; ++part) {
-    T* acc = part == 0 ? acc0 : acc1;
-#pragma unroll
-    for (int j = 0; j < Sh::E; ++j) x[j] = acc[j];
-    ntt_inv_regs<T, LOGN>(x, ex, pr.inv, pr.p, pr.p2);
-    const size_t off = ((b * 3 + part) * L + limb) * N + coef_base<LOGN>();
-    const size_t oo = ((b * 2 + part) * L + limb) * N + coef_base<LOGN>();
-#pragma unroll
-    for (int j = 0; j < Sh::E; ++j) out[oo + coef_off<LOGN>(j)] = add_mod(csub(x[j], pr.p), ct3[off + coef_off<LOGN>(j)], pr.p);
-  }
+}
+
+template <typename T, int LOGN>
+static cudaError_t launch_relin_accum(const Ctx* c, const void* ct3, const uint32_t* digits, const void* keyprep,
+                                      void* out, uint64_t batch, int D, cudaStream_t s) {
+  using Sh = NttShape<LOGN>;
+  const Base& B = c->base[BASE_Q];
+  constexpr size_t tw_bytes = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
+  constexpr size_t ex_bytes = (size_t)Exchanger<T, LOGN, 1, 1>::WORDS * sizeof(T);
+  constexpr bool SMEM_TW = sizeof(T) == 4 && LOGN >= 9 && tw_bytes + ex_bytes <= 110 * 1024;
+  auto kern = k_relin_accum<T, LOGN, SMEM_TW>;
+  const size_t smem = ex_bytes + (SMEM_TW ? tw_bytes : 0);
+  const int L = B.size();
+  if (batch == 0) return cudaSuccess;
+  uint32_t grid = persistent_grid((const void*)kern, Sh::THREADS, smem);
+  grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(grid / L * L, (uint64_t)L), batch * (uint64_t)L);
+  return launch_kernel_grid(kern, grid, Sh::THREADS, smem, s, (const T*)ct3, digits, (const T*)keyprep, (T*)out,
+                            (const PrimeTab<T>*)B.d_tabs, L, D, (uint32_t)batch);
 }
 
 // ----------------------------------------------------------------------------- host constants
@@ -466,6 +589,8 @@ static int build_tensor(Ctx* c, std::string& err) {
   }
   auto* st = new TensorState();
   st->K = h->K; st->K2 = h->K2; st->L = L;
+  st->q_lead = q_in && (int)aux.size() == L + (int)p2.size();
+  for (int k = 0; st->q_lead && k < (int)p2.size(); ++k) st->q_lead = h->p2_idx[k] == L + k;
   cudaError_t ce = cudaMalloc(&st->d_consts, sizeof(TensorConsts<TQ>));
   if (ce == cudaSuccess) ce = cudaMemcpy(st->d_consts, h, sizeof(TensorConsts<TQ>), cudaMemcpyHostToDevice);
   delete h;
@@ -513,12 +638,17 @@ extern "C" int ctb_tensor_lift(const ctb_ctx_t* ctx, const void* ct, uint32_t* o
   const uint64_t total = batch * 2 * c->n;
   if (!total) return OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (c->base[BASE_Q].word == 4)
-    k_tensor_lift<uint32_t><<<grid_pc(total), 256, 0, s>>>((const uint32_t*)ct, out,
-                                                           (const TensorConsts<uint32_t>*)c->tensor->d_consts, c->n, total);
-  else
-    k_tensor_lift<uint64_t><<<grid_pc(total), 256, 0, s>>>((const uint64_t*)ct, out,
-                                                           (const TensorConsts<uint64_t>*)c->tensor->d_consts, c->n, total);
+  const int L = c->tensor->L, K = c->tensor->K;
+  const unsigned grid = grid_pc(total);
+  if (c->base[BASE_Q].word == 4) {
+    const auto* tc = (const TensorConsts<uint32_t>*)c->tensor->d_consts;
+    if (L == 7 && K == 17) k_tensor_lift<uint32_t, 7, 17><<<grid, 256, 0, s>>>((const uint32_t*)ct, out, tc, c->n, total);
+    else k_tensor_lift<uint32_t, 0, 0><<<grid, 256, 0, s>>>((const uint32_t*)ct, out, tc, c->n, total);
+  } else {
+    const auto* tc = (const TensorConsts<uint64_t>*)c->tensor->d_consts;
+    if (L == 3 && K == 11) k_tensor_lift<uint64_t, 3, 11><<<grid, 256, 0, s>>>((const uint64_t*)ct, out, tc, c->n, total);
+    else k_tensor_lift<uint64_t, 0, 0><<<grid, 256, 0, s>>>((const uint64_t*)ct, out, tc, c->n, total);
+  }
   return cuda_status(cudaGetLastError(), "ctb_tensor_lift");
 }
 
@@ -528,12 +658,9 @@ extern "C" int ctb_tensor_product(const ctb_ctx_t* ctx, const uint32_t* a_aux, c
   int rc = ensure_tensor(ctx, c);
   if (rc) return rc;
   if (!a_aux || !b_aux || !h_aux) { set_error("ctb_tensor_product: null buffer"); return ERR_ARG; }
-  const Base& B = c->base[BASE_B];
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
-  CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<uint32_t, LOGN, 3>(k_tensor_product<LOGN>, batch * B.size(), s,
-                                                                      a_aux, b_aux, h_aux,
-                                                                      (const PrimeTab<uint32_t>*)B.d_tabs, B.size())));
+  CTB_DISPATCH_LOGN(c->logn, e = (launch_tensor_product<LOGN>(c, a_aux, b_aux, h_aux, batch, s)));
   return cuda_status(e, "ctb_tensor_product");
 }
 
@@ -545,12 +672,19 @@ extern "C" int ctb_tensor_round(const ctb_ctx_t* ctx, const uint32_t* h_aux, voi
   const uint64_t total = batch * 3 * c->n;
   if (!total) return OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (c->base[BASE_Q].word == 4)
-    k_tensor_round<uint32_t><<<grid_pc(total), 256, 0, s>>>(h_aux, (uint32_t*)out,
-                                                            (const TensorConsts<uint32_t>*)c->tensor->d_consts, c->n, total);
-  else
-    k_tensor_round<uint64_t><<<grid_pc(total), 256, 0, s>>>(h_aux, (uint64_t*)out,
-                                                            (const TensorConsts<uint64_t>*)c->tensor->d_consts, c->n, total);
+  const int L = c->tensor->L, K = c->tensor->K, K2 = c->tensor->K2;
+  const unsigned grid = grid_pc(total);
+  if (c->base[BASE_Q].word == 4) {
+    const auto* tc = (const TensorConsts<uint32_t>*)c->tensor->d_consts;
+    if (L == 7 && K == 17 && K2 == 10 && c->tensor->q_lead)
+      k_tensor_round<uint32_t, 7, 17, 10><<<grid, 256, 0, s>>>(h_aux, (uint32_t*)out, tc, c->n, total);
+    else k_tensor_round<uint32_t, 0, 0, 0><<<grid, 256, 0, s>>>(h_aux, (uint32_t*)out, tc, c->n, total);
+  } else {
+    const auto* tc = (const TensorConsts<uint64_t>*)c->tensor->d_consts;
+    if (L == 3 && K == 11 && K2 == 7)
+      k_tensor_round<uint64_t, 3, 11, 7><<<grid, 256, 0, s>>>(h_aux, (uint64_t*)out, tc, c->n, total);
+    else k_tensor_round<uint64_t, 0, 0, 0><<<grid, 256, 0, s>>>(h_aux, (uint64_t*)out, tc, c->n, total);
+  }
   return cuda_status(cudaGetLastError(), "ctb_tensor_round");
 }
 
@@ -603,20 +737,14 @@ extern "C" int ctb_relinearize(const ctb_ctx_t* ctx, const void* ct3, const void
                                                      (const TensorConsts<T>*)c->tensor->d_consts, c->n, total);
     e = cudaGetLastError();
     if (e == cudaSuccess)
-      CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_relin_accum<T, LOGN>, batch * B.size(), s,
-                                                                (const T*)ct3, (const uint32_t*)digits_ws,
-                                                                (const T*)keyprep, (T*)out,
-                                                                (const PrimeTab<T>*)B.d_tabs, B.size(), D)));
+      CTB_DISPATCH_LOGN(c->logn, e = (launch_relin_accum<T, LOGN>(c, ct3, digits_ws, keyprep, out, batch, D, s)));
   } else {
     using T = uint64_t;
     k_relin_digits<T><<<grid_pc(total), 256, 0, s>>>((const T*)ct3, digits_ws,
                                                      (const TensorConsts<T>*)c->tensor->d_consts, c->n, total);
     e = cudaGetLastError();
     if (e == cudaSuccess)
-      CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_relin_accum<T, LOGN>, batch * B.size(), s,
-                                                                (const T*)ct3, (const uint32_t*)digits_ws,
-                                                                (const T*)keyprep, (T*)out,
-                                                                (const PrimeTab<T>*)B.d_tabs, B.size(), D)));
+      CTB_DISPATCH_LOGN(c->logn, e = (launch_relin_accum<T, LOGN>(c, ct3, digits_ws, keyprep, out, batch, D, s)));
   }
   return cuda_status(e, "ctb_relinearize");
 }

@@ -135,16 +135,31 @@ class Ciphertext:
 
 
 class CiphertextBatch:
-    """B ciphertexts with the same part count, residues [B, parts, L, N]."""
+    """B ciphertexts with the same part count, residues [B, parts, L, N].
 
-    __slots__ = ("data", "noise", "backend_tag", "_cipher")
+    Noise estimates are exact Python integers (he.py:103-132); a batch whose
+    members share one estimate stores it once (`uniform_noise`)."""
+
+    __slots__ = ("data", "_nu", "backend_tag", "_cipher")
 
     def __init__(self, data: torch.Tensor, noise, backend_tag: str, cipher: RingParams):
         self.data = data
-        b = data.shape[0]
-        self.noise = [int(noise)] * b if isinstance(noise, int) else [int(v) for v in noise]
+        self._nu = int(noise) if isinstance(noise, int) else [int(v) for v in noise]
         self.backend_tag = backend_tag
         self._cipher = cipher
+
+    @property
+    def uniform_noise(self) -> int | None:
+        return self._nu if isinstance(self._nu, int) else None
+
+    @property
+    def noise(self) -> list[int]:
+        if isinstance(self._nu, int):
+            return [self._nu] * int(self.data.shape[0])
+        return self._nu
+
+    def max_noise(self) -> int:
+        return self._nu if isinstance(self._nu, int) else (max(self._nu) if self._nu else 0)
 
     @staticmethod
     def stack(cts: Sequence[Ciphertext]) -> "CiphertextBatch":
@@ -163,7 +178,8 @@ class CiphertextBatch:
         return int(self.data.shape[1])
 
     def __getitem__(self, i) -> Ciphertext:
-        return Ciphertext(self.data[i], self.noise[i], self.backend_tag, self._cipher)
+        nu = self._nu if isinstance(self._nu, int) else self._nu[i]
+        return Ciphertext(self.data[i], nu, self.backend_tag, self._cipher)
 
     def unbind(self) -> list[Ciphertext]:
         return [self[i] for i in range(len(self))]
@@ -350,19 +366,10 @@ class He:
                 host[k, 1] = self._error(rng)
                 host[k, 2] = self._error(rng)
             draws = torch.from_numpy(host.reshape(B * 3, n)).cuda()
-        small = torch.empty((B * 3, self.L, n), dtype=self.ctx.dtype(), device="cuda")
-        _lib.check(self.ctx._lib.ctb_rns_from_small(self.ctx._h, BASE_Q, _ptr(draws), _ptr(small), B * 3, _stream()),
-                   "ctb_rns_from_small")
-        small = small.view(B, 3, self.L, n)
-        u = small[:, 0].contiguous()
-        dm = torch.empty((B, self.L, n), dtype=self.ctx.dtype(), device="cuda")
-        _lib.check(self.ctx._lib.ctb_lift_plain(self.ctx._h, _ptr(mt), _lib.u64_array(self._delta_res), _ptr(dm), B,
-                                                _stream()), "ctb_lift_plain")
-        add0 = self._rns(0, small[:, 1].contiguous(), dm)
         pk = self._pk_prep(keys)
         out = torch.empty((B, 2, self.L, n), dtype=self.ctx.dtype(), device="cuda")
-        out[:, 0] = self._mul_prepared(u, pk[0], add0)
-        out[:, 1] = self._mul_prepared(u, pk[1], small[:, 2].contiguous())
+        _lib.check(self.ctx._lib.ctb_encrypt(self.ctx._h, _ptr(mt), _ptr(draws.contiguous()), _ptr(pk), _ptr(out), B,
+                                             _stream()), "ctb_encrypt")
         self.meter.tick("Enc", self._elapsed(t0), count=B)
         return CiphertextBatch(out, self.params.fresh_noise, self.backend, self.params.cipher_ring)
 
@@ -387,6 +394,11 @@ class He:
 
     def decrypt_many(self, cts, keys: KeySet) -> list[RingElem]:
         """he.py:329-351 over a batch: v = c0 + c1 s (+ c2 s^2); floor((v t + q//2)/q) mod t."""
+        out = self.decrypt_values(cts, keys)
+        return [RingElem(self.params.plain_ring, out[i]) for i in range(out.shape[0])]
+
+    def decrypt_values(self, cts, keys: KeySet) -> torch.Tensor:
+        """decrypt_many as one int64 tensor [B, N] of plain values (no per-poly objects)."""
         t0 = self._t0()
         if isinstance(cts, CiphertextBatch):
             batch = cts
@@ -395,12 +407,12 @@ class He:
                 self._check_tag(c)
             batch = CiphertextBatch.stack(list(cts))
         self._check_tag(batch)
-        for nu in batch.noise:
-            if nu >= self.params.noise_budget:
-                raise NoiseOverflowError(
-                    f"noise estimate 2^{nu.bit_length()} is at or above "
-                    f"the budget 2^{self.params.noise_budget.bit_length()}"
-                )
+        nu = batch.max_noise()
+        if nu >= self.params.noise_budget:
+            raise NoiseOverflowError(
+                f"noise estimate 2^{nu.bit_length()} is at or above "
+                f"the budget 2^{self.params.noise_budget.bit_length()}"
+            )
         d = batch.data
         acc = self._mul_prepared(d[:, 1].contiguous(), self._s_prep(keys, 1), d[:, 0].contiguous())
         if batch.nparts == 3:
@@ -409,7 +421,7 @@ class He:
         _lib.check(self.ctx._lib.ctb_decrypt_round(self.ctx._h, _ptr(acc), _ptr(out), len(batch), _stream()),
                    "ctb_decrypt_round")
         self.meter.tick("Dec", self._elapsed(t0), count=len(batch))
-        return [RingElem(self.params.plain_ring, out[i]) for i in range(len(batch))]
+        return out
 
     # -- homomorphic ops --------------------------------------------------------
     def cc_add(self, a: Ciphertext, b: Ciphertext) -> Ciphertext:
@@ -443,8 +455,9 @@ class He:
         if batch.nparts != 2:
             raise PartCountError("CPMul needs a 2-part ciphertext; relinearize first")
         out = self.ctx.cpmul(batch.data.contiguous(), self._plain_tensor(pts))
-        res = CiphertextBatch(out, [self.params.cp_mul_noise(nu) for nu in batch.noise], self.backend,
-                              self.params.cipher_ring)
+        u = batch.uniform_noise
+        nu = self.params.cp_mul_noise(u) if u is not None else [self.params.cp_mul_noise(v) for v in batch.noise]
+        res = CiphertextBatch(out, nu, self.backend, self.params.cipher_ring)
         self.meter.tick("CPMul", self._elapsed(t0), count=len(batch))
         return res
 
@@ -466,7 +479,10 @@ class He:
             raise PartCountError("CCMul needs two 2-part ciphertexts")
         out = tensoring.tensor_round(self.ctx, a.data.contiguous(), b.data.contiguous())
         p = self.params
-        nu = [2 * p.n * p.t * (x + y) + 2 * p.n * p.n * p.t * p.t for x, y in zip(a.noise, b.noise)]
+        if a.uniform_noise is not None and b.uniform_noise is not None:
+            nu = 2 * p.n * p.t * (a.uniform_noise + b.uniform_noise) + 2 * p.n * p.n * p.t * p.t
+        else:
+            nu = [2 * p.n * p.t * (x + y) + 2 * p.n * p.n * p.t * p.t for x, y in zip(a.noise, b.noise)]
         return CiphertextBatch(out, nu, self.backend, p.cipher_ring)
 
     def _relin_prep(self, keys) -> torch.Tensor:
@@ -485,8 +501,9 @@ class He:
         if ct.nparts != 3:
             raise PartCountError("relinearization expects a 3-part ciphertext")
         out = tensoring.relinearize(self.ctx, ct.data.contiguous(), self._relin_prep(keys))
-        res = CiphertextBatch(out, [nu + self.params.relin_noise for nu in ct.noise], self.backend,
-                              self.params.cipher_ring)
+        u = ct.uniform_noise
+        nu = u + self.params.relin_noise if u is not None else [v + self.params.relin_noise for v in ct.noise]
+        res = CiphertextBatch(out, nu, self.backend, self.params.cipher_ring)
         self.meter.tick("Relin", self._elapsed(t0), count=len(ct))
         return res
 

@@ -86,8 +86,7 @@ def online(sess: Session, job: LinearJob, bundle: linprot.MaskBundle, maskprod: 
     mx = linprot._plain_sub(cli, job.x_plain, bundle.r_x)
     mw = linprot._plain_sub(cli, job.w_plain, bundle.r_w)
     c_slots, p_slots = linprot.linear_online(srv, cx, cw, mx, mw, js, maskprod)
-    dec = cli.decrypt_many(c_slots, sess.keys)
-    c = torch.stack([d.data for d in dec])
+    c = cli.decrypt_values(c_slots, sess.keys)
     return linprot._plain_sub(cli, c, p_slots)
 
 
