@@ -171,6 +171,16 @@ def probe_modmul_peak(torch, lib, word: int):
     return best
 
 
+def _ncu_traffic(kernel: str, batch: int):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture
+    (profiles/traffic.json), scaled to this run's batch; None if absent."""
+    try:
+        rec = json.loads((ROOT / "profiles" / "traffic.json").read_text())[kernel]
+        return rec["dram_bytes_per_launch"] * batch / rec["batch"]
+    except Exception:
+        return None
+
+
 def _time_cpmul(torch, ctx, B, qs, t, steps, warm):
     """Device-resident batched CPMul timing (CUDA events) for an extra configuration."""
     dt = ctx.dtype()
@@ -373,7 +383,7 @@ def run_ours(args):
                 "peak": modmul_peak / 1e9 if bound == "int" else hbm_peak,
                 "unit": "Gmodmul/s" if bound == "int" else "GB/s",
                 "frac": (achieved_mm / modmul_peak) if bound == "int" else (achieved_bw / hbm_peak),
-                "traffic": None,
+                "traffic": _ncu_traffic("k_cpmul<u32,12>", B),
                 "kernel": "k_cpmul<uint32_t,12>",
                 "algorithmic_per_cpmul": {"modmuls": modmuls_per, "bytes": bytes_per},
                 "peak_source": {"int": "measured now: ctb_probe_modmul (Shoup u32, register-resident)",
