@@ -66,6 +66,11 @@ extern "C" int ctb_ctx_create(ctb_ctx_t** out, uint32_t n, const uint64_t* q_pri
   int rc = build_base(c->base[BASE_Q], q_primes, (int)n_q, logn, err, n_t ? tmod.data() : nullptr,
                       n_t ? delta.data() : nullptr);
   if (rc) { delete c; set_error("cipher base: " + err); return rc == -2 ? ERR_CUDA : ERR_ARG; }
+  {
+    bool fast = c->t && c->t < (1ull << 57) && c->base[BASE_Q].word == 4;
+    for (uint32_t i = 0; i < n_q; ++i) fast = fast && q_primes[i] > (1ull << 25);
+    c->plain_fast = fast;
+  }
   rc = build_rns_consts(c, err);
   if (rc) { delete c; set_error("conversion constants: " + err); return rc == -2 ? ERR_CUDA : (rc == -3 ? ERR_UNSUPPORTED : ERR_ARG); }
   *out = reinterpret_cast<ctb_ctx_t*>(c);

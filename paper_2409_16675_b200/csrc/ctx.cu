@@ -121,6 +121,10 @@ static int build_typed(Base& b, uint32_t logn, std::string& err, const uint64_t*
     t.one_q = shoup_q<T>(1, p);
     t.r2 = (T)R; t.r2_q = shoup_q<T>(R, p);
     t.rr = (T)mulmod(R, R, p);
+    if (sizeof(T) == 4 && p > (1ull << 25)) {
+      const uint64_t c25 = (1ull << 25) % p;
+      t.c25 = (T)c25; t.c25_q = shoup_q<T>(c25, p);
+    }
     if (tmod) t.tmod = (T)(tmod[l] % p);
     if (delta) { t.delta = (T)(delta[l] % p); t.delta_q = shoup_q<T>(delta[l] % p, p); }
     t.fwd = d_tw + (size_t)l * 2 * ent;

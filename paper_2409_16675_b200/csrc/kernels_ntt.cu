@@ -175,7 +175,7 @@ template <typename T, int LOGN, bool SMEM_TW>
 __global__ void __launch_bounds__(NttShape<LOGN>::THREADS * cpmul_groups<T, LOGN>(),
                                   cpmul_groups<T, LOGN>() == 2 ? 2 : NttShape<LOGN>::MINB)
 k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>* __restrict__ tabs,
-        int L, uint64_t t_half, uint32_t batch) {
+        int L, uint64_t t_half, uint32_t batch, bool plain_fast) {
   using Sh = NttShape<LOGN>;
   constexpr int GROUPS = cpmul_groups<T, LOGN>();
   using Ex = Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>;
@@ -211,8 +211,8 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) {
         const uint64_t v = __ldg(ppt + coef_off<LOGN>(k));
-        T r = csub(pr.reduce_u64_lazy(v), pr.p);         // v mod p
-        if (v > t_half) r = sub_mod(r, tmod, pr.p);       // centred lift: v - t
+        T r = csub(pr.reduce_plain(v, plain_fast), pr.p);  // v mod p
+        if (v > t_half) r = sub_mod(r, tmod, pr.p);         // centred lift: v - t
         x[k] = r;
       }
       ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
@@ -524,7 +524,7 @@ static cudaError_t launch_cpmul(const Ctx* c, const Base* b, const void* ct, con
   const uint64_t max_grid = (batch + GROUPS - 1) / GROUPS * (uint64_t)L;
   grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(grid / L * L, (uint64_t)L), max_grid);
   return launch_kernel_grid(kern, grid, threads, smem, s, (const T*)ct, pt, (T*)out,
-                            (const PrimeTab<T>*)b->d_tabs, L, c->t_half, (uint32_t)batch);
+                            (const PrimeTab<T>*)b->d_tabs, L, c->t_half, (uint32_t)batch, c->plain_fast);
 }
 
 extern "C" int ctb_cpmul(const ctb_ctx_t* ctx, const void* ct, const uint64_t* pt, void* out, uint64_t batch,

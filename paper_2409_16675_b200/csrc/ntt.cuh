@@ -35,6 +35,7 @@ struct PrimeTab {
   T rr;                 // 2^(2W) mod p (leaves the Montgomery domain)
   T tmod;               // plain modulus t mod p (cipher base only: centred lift)
   T delta, delta_q;     // floor(q/t) mod p and Shoup quotient (cipher base only)
+  T c25, c25_q;         // 2^25 mod p and Shoup quotient (u32, p > 2^25): one-multiply plain reduction
   const T* fwd;         // (w, w') pairs, pass-major / entry-major (see TwSrc); serves both directions
   const T* inv;         // == fwd (kept for layout stability)
 };
@@ -451,7 +452,7 @@ __device__ __forceinline__ void store_eval(T* base, const T (&x)[NttShape<LOGN>:
 // Load a PrimeTab into registers (uniform across the CTA).
 template <typename T>
 struct PrimeRegs {
-  T p, p2, pinv, ninv, ninv_q, ninvr, ninvr_q, one_q, r2, r2_q, rr;
+  T p, p2, pinv, ninv, ninv_q, ninvr, ninvr_q, one_q, r2, r2_q, rr, c25, c25_q;
   const T* fwd;
   const T* inv;
   __device__ __forceinline__ explicit PrimeRegs(const PrimeTab<T>* tab) {
@@ -459,12 +460,24 @@ struct PrimeRegs {
     ninv = tab->ninv; ninv_q = tab->ninv_q;
     ninvr = tab->ninvr; ninvr_q = tab->ninvr_q;
     one_q = tab->one_q; r2 = tab->r2; r2_q = tab->r2_q; rr = tab->rr;
+    c25 = tab->c25; c25_q = tab->c25_q;
     fwd = tab->fwd; inv = tab->inv;
   }
   // Canonical [0, p) from a forward-transform output (u32: < 4p; u64: < 2^64).
   __device__ __forceinline__ T canon_fwd(T x) const {
     if constexpr (sizeof(T) == 4) return reduce4(x, p);
     else return csub(shoup_mul<uint64_t>(x, 1ull, one_q, p), p);
+  }
+  // Plain value v < 2^57 mod p into [0, 2p) with ONE Shoup product when p > 2^25
+  // (v = hi 2^25 + lo with lo < 2^25 < p); callers pass fast = (t < 2^57 and p > 2^25).
+  __device__ __forceinline__ T reduce_plain(uint64_t v, bool fast) const {
+    if constexpr (sizeof(T) == 4) {
+      if (fast) {
+        const uint32_t hi = (uint32_t)(v >> 25), lo = (uint32_t)v & ((1u << 25) - 1);
+        return csub(shoup_mul<uint32_t>(hi, c25, c25_q, p) + lo, p2);
+      }
+    }
+    return reduce_u64_lazy(v);
   }
   // Reduce an arbitrary 64-bit value mod p into [0, 2p).
   __device__ __forceinline__ T reduce_u64_lazy(uint64_t v) const {
