@@ -20,6 +20,8 @@
  *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
  *     asynchronous on that stream; a context is read-only after creation, so
  *     two threads may use one context on different streams concurrently.
+ *   - A call whose item count (n_polys / batch / n_out) is zero is a no-op
+ *     returning CTB_OK; its buffers may then be NULL.
  *   - Return value: CTB_OK (0) or a negative CTB_ERR_*; ctb_last_error()
  *     returns the thread-local message of the last failure.
  */

@@ -127,6 +127,7 @@ const Base* base_ptr(const ctb_ctx_t* ctx, int base) {
 
 extern "C" int ctb_rns_elementwise(const ctb_ctx_t* ctx, int base, int op, const void* a, const void* b, void* out,
                                    uint64_t n_polys, void* stream) {
+  if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Base* B = base_ptr(ctx, base);
   if (!B || op < 0 || op > 2 || !a || !out || (op < 2 && !b)) { set_error("ctb_rns_elementwise: bad arguments"); return ERR_ARG; }
   if (B->size() > MAXL) { set_error("ctb_rns_elementwise: too many limbs"); return ERR_UNSUPPORTED; }
@@ -147,6 +148,7 @@ extern "C" int ctb_rns_elementwise(const ctb_ctx_t* ctx, int base, int op, const
 
 extern "C" int ctb_rns_scalar_mul(const ctb_ctx_t* ctx, int base, const void* a, const uint64_t* scalars, void* out,
                                   uint64_t n_polys, void* stream) {
+  if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Base* B = base_ptr(ctx, base);
   if (!B || !a || !scalars || !out) { set_error("ctb_rns_scalar_mul: bad arguments"); return ERR_ARG; }
   if (B->size() > MAXL) { set_error("ctb_rns_scalar_mul: too many limbs"); return ERR_UNSUPPORTED; }
@@ -167,6 +169,7 @@ extern "C" int ctb_rns_scalar_mul(const ctb_ctx_t* ctx, int base, const void* a,
 
 extern "C" int ctb_rns_from_small(const ctb_ctx_t* ctx, int base, const int64_t* in, void* out, uint64_t n_polys,
                                   void* stream) {
+  if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Base* B = base_ptr(ctx, base);
   if (!B || !in || !out) { set_error("ctb_rns_from_small: bad arguments"); return ERR_ARG; }
   if (B->size() > MAXL) { set_error("ctb_rns_from_small: too many limbs"); return ERR_UNSUPPORTED; }
@@ -185,6 +188,7 @@ extern "C" int ctb_rns_from_small(const ctb_ctx_t* ctx, int base, const int64_t*
 
 extern "C" int ctb_lift_plain(const ctb_ctx_t* ctx, const uint64_t* m, const uint64_t* scale, void* out,
                               uint64_t n_polys, void* stream) {
+  if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Base* B = base_ptr(ctx, CTB_BASE_Q);
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
   if (!B || !c->t || !m || !scale || !out) { set_error("ctb_lift_plain: bad arguments (needs plain ring)"); return ERR_ARG; }
@@ -205,6 +209,7 @@ extern "C" int ctb_lift_plain(const ctb_ctx_t* ctx, const uint64_t* m, const uin
 
 extern "C" int ctb_plain_elementwise(const ctb_ctx_t* ctx, int op, const uint64_t* a, const uint64_t* b,
                                      uint64_t scalar, uint64_t* out, uint64_t n_polys, void* stream) {
+  if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
   if (!c || !c->t || op < 0 || op > 3 || !a || !out || (op < 2 && !b)) { set_error("ctb_plain_elementwise: bad arguments"); return ERR_ARG; }
   const uint64_t total = n_polys * (uint64_t)c->n;

@@ -385,6 +385,7 @@ static inline const Base* base_of(const ctb_ctx_t* ctx, int base) {
 
 extern "C" int ctb_ntt_forward(const ctb_ctx_t* ctx, int base, const void* in, void* out,
                                uint64_t n_polys, void* stream) {
+  if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Base* b = base_of(ctx, base);
   if (!b || !in || !out) { set_error("ctb_ntt_forward: bad context, base or buffer"); return ERR_ARG; }
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
@@ -405,6 +406,7 @@ extern "C" int ctb_ntt_forward(const ctb_ctx_t* ctx, int base, const void* in, v
 
 extern "C" int ctb_ntt_inverse(const ctb_ctx_t* ctx, int base, const void* in, void* out,
                                uint64_t n_polys, void* stream) {
+  if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Base* b = base_of(ctx, base);
   if (!b || !in || !out) { set_error("ctb_ntt_inverse: bad context, base or buffer"); return ERR_ARG; }
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
@@ -425,6 +427,7 @@ extern "C" int ctb_ntt_inverse(const ctb_ctx_t* ctx, int base, const void* in, v
 
 extern "C" int ctb_prepare_operand(const ctb_ctx_t* ctx, int base, const void* in, void* out, uint64_t n_polys,
                                    void* stream) {
+  if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Base* b = base_of(ctx, base);
   if (!b || !in || !out) { set_error("ctb_prepare_operand: bad context, base or buffer"); return ERR_ARG; }
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
@@ -445,6 +448,7 @@ extern "C" int ctb_prepare_operand(const ctb_ctx_t* ctx, int base, const void* i
 
 extern "C" int ctb_mul_prepared(const ctb_ctx_t* ctx, int base, const void* a, const void* bprep, uint64_t b_stride,
                                 const void* addend, void* out, uint64_t n_polys, void* stream) {
+  if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Base* b = base_of(ctx, base);
   if (!b || !a || !bprep || !out) { set_error("ctb_mul_prepared: bad context, base or buffer"); return ERR_ARG; }
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
@@ -467,6 +471,7 @@ extern "C" int ctb_mul_prepared(const ctb_ctx_t* ctx, int base, const void* a, c
 
 extern "C" int ctb_pointwise_mul(const ctb_ctx_t* ctx, int base, const void* a, const void* bb, void* out,
                                  uint64_t n_polys, void* stream) {
+  if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Base* b = base_of(ctx, base);
   if (!b || !a || !bb || !out) { set_error("ctb_pointwise_mul: bad context, base or buffer"); return ERR_ARG; }
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
@@ -485,6 +490,7 @@ extern "C" int ctb_pointwise_mul(const ctb_ctx_t* ctx, int base, const void* a, 
 
 extern "C" int ctb_ring_mul(const ctb_ctx_t* ctx, int base, const void* a, uint64_t a_stride, const void* bb,
                             uint64_t b_stride, void* out, uint64_t n_polys, void* stream) {
+  if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Base* b = base_of(ctx, base);
   if (!b || !a || !bb || !out) { set_error("ctb_ring_mul: bad context, base or buffer"); return ERR_ARG; }
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
@@ -529,6 +535,7 @@ static cudaError_t launch_cpmul(const Ctx* c, const Base* b, const void* ct, con
 
 extern "C" int ctb_cpmul(const ctb_ctx_t* ctx, const void* ct, const uint64_t* pt, void* out, uint64_t batch,
                          void* stream) {
+  if (batch == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Base* b = base_of(ctx, BASE_Q);
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
   if (!b || !c->t || !ct || !pt || !out) { set_error("ctb_cpmul: bad context (needs cipher+plain ring) or buffer"); return ERR_ARG; }
@@ -565,6 +572,7 @@ static cudaError_t launch_encrypt(const Ctx* c, const Base* b, const uint64_t* m
 
 extern "C" int ctb_encrypt(const ctb_ctx_t* ctx, const uint64_t* m, const int64_t* draws, const void* pkprep,
                            void* out, uint64_t batch, void* stream) {
+  if (batch == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Base* b = base_of(ctx, BASE_Q);
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
   if (!b || !c->t || !m || !draws || !pkprep || !out) { set_error("ctb_encrypt: bad context (needs plain ring) or buffer"); return ERR_ARG; }
@@ -581,6 +589,7 @@ extern "C" int ctb_encrypt(const ctb_ctx_t* ctx, const uint64_t* m, const int64_
 
 extern "C" int ctb_pp_mul(const ctb_ctx_t* ctx, const uint64_t* a, const uint64_t* bb, uint64_t* out,
                           uint64_t n_polys, void* stream) {
+  if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Base* b = base_of(ctx, BASE_T);
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
   if (!b || !a || !bb || !out) { set_error("ctb_pp_mul: context has no plain ring or bad buffer"); return ERR_ARG; }

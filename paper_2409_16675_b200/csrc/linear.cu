@@ -188,6 +188,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 }  // namespace
 
 extern "C" int ctb_lift_prepare(const ctb_ctx_t* ctx, const uint64_t* m, void* out, uint64_t n_polys, void* stream) {
+  if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Ctx* c = cctx(ctx);
   if (!c || !c->t || !m || !out) { set_error("ctb_lift_prepare: needs plain ring and buffers"); return ERR_ARG; }
   const Base& B = c->base[BASE_Q];
@@ -227,6 +228,7 @@ extern "C" int ctb_linear_online(const ctb_ctx_t* ctx, const void* ct_x, uint32_
                                  const uint64_t* mx, const uint64_t* mw, const uint32_t* sites_host, uint32_t n_sites,
                                  uint32_t n_out, const void* maskprod, void* out_ct, uint64_t* out_p, void* workspace,
                                  void* stream) {
+  if (n_out == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Ctx* c = cctx(ctx);
   if (!c || !c->t || !ct_x || !ct_w || !mx || !mw || !sites_host || !out_ct || !out_p || !workspace) {
     set_error("ctb_linear_online: bad context (needs plain ring) or buffer");
@@ -314,6 +316,7 @@ extern "C" int ctb_linear_online(const ctb_ctx_t* ctx, const void* ct_x, uint32_
 
 extern "C" int ctb_slot_sum(const ctb_ctx_t* ctx, int base, const void* in, uint32_t parts, const int32_t* slot_ptr,
                             const int32_t* members, uint32_t n_out, void* out, void* stream) {
+  if (n_out == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Ctx* c = cctx(ctx);
   if (!c || base < 0 || base >= BASE_COUNT || !in || !slot_ptr || !members || !out) {
     set_error("ctb_slot_sum: bad arguments");

@@ -259,6 +259,7 @@ static unsigned grid_for(uint64_t total) {
 
 extern "C" int ctb_decrypt_round(const ctb_ctx_t* ctx, const void* v, uint64_t* out, uint64_t n_polys,
                                  void* stream) {
+  if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
   if (!c || !c->rns || !c->t || !v || !out) { set_error("ctb_decrypt_round: context lacks plain ring or bad buffer"); return ERR_ARG; }
   const uint64_t total = n_polys * c->n;
@@ -274,6 +275,7 @@ extern "C" int ctb_decrypt_round(const ctb_ctx_t* ctx, const void* v, uint64_t* 
 }
 
 extern "C" int ctb_rns_to_pos(const ctb_ctx_t* ctx, const void* x, uint64_t* out, uint64_t n_polys, void* stream) {
+  if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
   if (!c || !c->rns || !x || !out) { set_error("ctb_rns_to_pos: bad context or buffer"); return ERR_ARG; }
   const uint64_t total = n_polys * c->n;
@@ -289,6 +291,7 @@ extern "C" int ctb_rns_to_pos(const ctb_ctx_t* ctx, const void* x, uint64_t* out
 }
 
 extern "C" int ctb_pos_to_rns(const ctb_ctx_t* ctx, const uint64_t* in, void* x, uint64_t n_polys, void* stream) {
+  if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
   if (!c || !c->rns || !in || !x) { set_error("ctb_pos_to_rns: bad context or buffer"); return ERR_ARG; }
   const uint64_t total = n_polys * c->n;

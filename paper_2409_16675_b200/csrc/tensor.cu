@@ -631,6 +631,7 @@ extern "C" int ctb_tensor_aux_size(const ctb_ctx_t* ctx) {
 }
 
 extern "C" int ctb_tensor_lift(const ctb_ctx_t* ctx, const void* ct, uint32_t* out, uint64_t batch, void* stream) {
+  if (batch == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Ctx* c;
   int rc = ensure_tensor(ctx, c);
   if (rc) return rc;
@@ -654,6 +655,7 @@ extern "C" int ctb_tensor_lift(const ctb_ctx_t* ctx, const void* ct, uint32_t* o
 
 extern "C" int ctb_tensor_product(const ctb_ctx_t* ctx, const uint32_t* a_aux, const uint32_t* b_aux, uint32_t* h_aux,
                                   uint64_t batch, void* stream) {
+  if (batch == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Ctx* c;
   int rc = ensure_tensor(ctx, c);
   if (rc) return rc;
@@ -665,6 +667,7 @@ extern "C" int ctb_tensor_product(const ctb_ctx_t* ctx, const uint32_t* a_aux, c
 }
 
 extern "C" int ctb_tensor_round(const ctb_ctx_t* ctx, const uint32_t* h_aux, void* out, uint64_t batch, void* stream) {
+  if (batch == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Ctx* c;
   int rc = ensure_tensor(ctx, c);
   if (rc) return rc;
@@ -696,6 +699,7 @@ extern "C" uint64_t ctb_ccmul_workspace_words(const ctb_ctx_t* ctx, uint64_t bat
 
 extern "C" int ctb_ccmul_raw(const ctb_ctx_t* ctx, const void* a, const void* b, void* out3, uint32_t* workspace,
                              uint64_t batch, void* stream) {
+  if (batch == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Ctx* c;
   int rc = ensure_tensor(ctx, c);
   if (rc) return rc;
@@ -720,6 +724,7 @@ extern "C" int ctb_relin_digit_count(const ctb_ctx_t* ctx) {
 
 extern "C" int ctb_relinearize(const ctb_ctx_t* ctx, const void* ct3, const void* keyprep, uint32_t* digits_ws,
                                void* out, uint64_t batch, void* stream) {
+  if (batch == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Ctx* c;
   int rc = ensure_tensor(ctx, c);
   if (rc) return rc;

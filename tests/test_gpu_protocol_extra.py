@@ -1,0 +1,231 @@
+"""Reference protocol/pool/hygiene tests (pkg/tests/test_linprot.py, test_he.py)
+restated for the device path (rlwe backend: the device path has no clear backend)."""
+import numpy as np
+import pytest
+
+from conftest import has_gpu
+from oracle.plainconv import conv2d
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
+
+
+@pytest.fixture(scope="module")
+def p512():
+    from paper_2409_16675_b200 import he
+    plain = he.default_plain_params(512, 17, 2)
+    return he.HeParams(he.default_cipher_params(512, plain.modulus), plain)
+
+
+def evaluators(params):
+    from paper_2409_16675_b200 import he
+    cli, srv = he.He(params), he.He(params)
+    return cli, srv, cli.keygen(3)
+
+
+def run_b(params, job):
+    from paper_2409_16675_b200 import channel, linprot
+    cli, srv, keys = evaluators(params)
+
+    def c(end):
+        linprot.setup_client(end, cli, keys)
+        return linprot.linear_b_client(end, cli, keys, np.random.default_rng(1), job)
+
+    def s(end):
+        pks = linprot.setup_server(end, srv)
+        linprot.linear_b_server(end, srv, pks)
+
+    ce, se = channel.inproc_pair()
+    res, _ = channel.run_pair(c, s, ce, se)
+    return res, cli, srv
+
+
+def run_pre(params, job, count=1, capture=False):
+    from paper_2409_16675_b200 import channel, linprot
+    cli, srv, keys = evaluators(params)
+    cpool, spool = linprot.TriplePool(), linprot.TriplePool()
+
+    def c(end):
+        linprot.setup_client(end, cli, keys)
+        linprot.precompute_offline_client(end, cli, keys, np.random.default_rng(2), job.shape, count, cpool)
+        return linprot.precompute_online_client(end, cli, keys, np.random.default_rng(4), job, cpool)
+
+    def s(end):
+        pks = linprot.setup_server(end, srv)
+        linprot.precompute_offline_server(end, srv, pks, spool)
+        linprot.precompute_online_server(end, srv, pks, spool)
+
+    ce, se = channel.inproc_pair(capture=capture)
+    res, _ = channel.run_pair(c, s, ce, se)
+    return res, cli, srv, keys, ce, cpool, spool
+
+
+def signed(t, modulus):
+    from paper_2409_16675_b200 import packing
+    return packing.to_signed_tensor(t, modulus).cpu().numpy().astype(np.int64)
+
+
+def test_protocol_b_equals_precompute_equals_plain(p512, rng):
+    from paper_2409_16675_b200 import linprot, packing
+    shape = packing.ConvShape(8, 8, 3, 1)
+    x = rng.integers(-40, 40, size=(1, 8, 8))
+    w = rng.integers(-9, 9, size=(1, 1, 3, 3))
+    rb, _, srv_b = run_b(p512, linprot.conv_job("c", x, w, shape, p512.plain_ring))
+    rp, *_ = run_pre(p512, linprot.conv_job("c", x, w, shape, p512.plain_ring))
+    plain = conv2d(x[0], w[0, 0], 1)
+    assert np.array_equal(signed(rb.tensor[0], p512.t), plain)
+    assert np.array_equal(signed(rp.tensor[0], p512.t), plain)
+    assert srv_b.meter.count("CCMul", "online") == 1
+
+
+def test_identity_kernel_and_toy(p512, rng):
+    from paper_2409_16675_b200 import linprot, packing
+    x = rng.integers(-50, 50, size=(1, 4, 4))
+    res, *_ = run_pre(p512, linprot.conv_job("ident", x, np.ones((1, 1, 1, 1), dtype=np.int64),
+                                              packing.ConvShape(4, 4, 1, 0), p512.plain_ring))
+    assert np.array_equal(signed(res.tensor[0], p512.t), x[0])
+    x = rng.integers(-20, 20, size=(1, 2, 2))
+    w = rng.integers(-9, 9, size=(1, 1, 2, 2))
+    res, *_ = run_pre(p512, linprot.conv_job("toy", x, w, packing.ConvShape(2, 2, 2, 1), p512.plain_ring))
+    assert np.array_equal(signed(res.tensor[0], p512.t), conv2d(x[0], w[0, 0], 1))
+
+
+def test_fc_outer_affine_and_bn(p512, rng):
+    from paper_2409_16675_b200 import channel, linprot
+    W = rng.integers(-30, 30, size=(4, 4))
+    x = rng.integers(-30, 30, size=4)
+    res, *_ = run_pre(p512, linprot.fc_job("fc", x, W, p512.plain_ring))
+    assert np.array_equal(signed(res.tensor, p512.t), W @ x)
+    g = rng.integers(-9, 9, size=3)
+    res, *_ = run_pre(p512, linprot.outer_job("outer", g, x, p512.plain_ring))
+    assert np.array_equal(signed(res.tensor, p512.t), np.outer(g, x))
+    xa = rng.integers(-100, 100, size=(5, 5))
+    res, *_ = run_pre(p512, linprot.affine_job("bn", xa, 7, p512.plain_ring))
+    assert np.array_equal(signed(res.tensor, p512.t), xa * 7)
+    beta = rng.integers(-10, 10, size=(5, 5))
+    cli, srv, keys = evaluators(p512)
+
+    def c(end):
+        linprot.setup_client(end, cli, keys)
+        return linprot.bn_affine_client(end, cli, keys, np.random.default_rng(1), "bn", xa, 3, beta)
+
+    def s(end):
+        linprot.linear_b_server(end, srv, linprot.setup_server(end, srv))
+
+    ce, se = channel.inproc_pair()
+    r, _ = channel.run_pair(c, s, ce, se)
+    assert np.array_equal(r.tensor, xa * 3 + beta)
+
+
+def test_online_meters_per_site(p512, rng):
+    from paper_2409_16675_b200 import linprot, packing
+    x = rng.integers(-5, 5, size=(1, 3, 3))
+    w = rng.integers(-5, 5, size=(1, 1, 2, 2))
+    job = linprot.conv_job("m", x, w, packing.ConvShape(3, 3, 2, 0), p512.plain_ring)
+    nsites = len(job.shape.sites)
+    _, cli, srv, *_ = run_pre(p512, job)
+    assert srv.meter.count("CCMul", "online") == 0
+    assert srv.meter.count("CCMul", "offline") == nsites
+    assert srv.meter.count("Relin", "offline") == nsites
+    assert srv.meter.count("CPMul", "online") == 2 * nsites
+    assert srv.meter.count("PPMul", "online") == nsites
+    assert srv.meter.count("CCAdd", "online") >= 2 * nsites
+
+
+def test_pool_discipline_and_mask_product(p512, rng, tmp_path):
+    from paper_2409_16675_b200 import channel, linprot, ring
+    from paper_2409_16675_b200.ring import RingElem
+    cli, srv, keys = evaluators(p512)
+    cpool, spool = linprot.TriplePool(), linprot.TriplePool()
+    js = linprot.JobShape("L", 1, 1, 1, ((0, 0, 0),))
+
+    def c(end):
+        linprot.setup_client(end, cli, keys)
+        linprot.precompute_offline_client(end, cli, keys, np.random.default_rng(0), js, 2, cpool)
+
+    def s(end):
+        pks = linprot.setup_server(end, srv)
+        linprot.precompute_offline_server(end, srv, pks, spool)
+
+    ce, se = channel.inproc_pair()
+    channel.run_pair(c, s, ce, se)
+    # persistence round trip
+    linprot.save_server_pool(spool, srv, str(tmp_path / "s.pool"))
+    linprot.save_client_pool(cpool, str(tmp_path / "c.pool"), cli)
+    spool2 = linprot.load_server_pool(srv, str(tmp_path / "s.pool"))
+    cpool2 = linprot.load_client_pool(cli, str(tmp_path / "c.pool"))
+    assert spool2.available("L") == 2 and cpool2.available("L") == 2
+    b1, b2 = cpool.take("L"), cpool2.take("L")
+    assert np.array_equal(b1.r_x.cpu().numpy(), b2.r_x.cpu().numpy())
+    p1, p2 = spool.take("L"), spool2.take("L")
+    # the server's slot decrypts to r_x * r_w (test secret key)
+    expect = ring.ring_mul(RingElem(p512.plain_ring, b1.r_x[0]), RingElem(p512.plain_ring, b1.r_w[0]))
+    assert srv.decrypt(p1.slots[0], keys) == expect
+    assert srv.decrypt(p2.slots[0], keys) == expect
+    with pytest.raises(linprot.SingleUseViolationError):
+        b1.consume()
+    cpool.take("L")
+    with pytest.raises(linprot.PoolExhaustedError):
+        cpool.take("L")
+
+
+def test_transcript_hygiene(p512, rng):
+    from paper_2409_16675_b200 import linprot, packing, ring
+    from paper_2409_16675_b200.ring import RingElem
+    x = rng.integers(100, 1 << 15, size=(1, 4, 4))
+    w = rng.integers(100, 1 << 15, size=(1, 1, 2, 2))
+    job = linprot.conv_job("h", x, w, packing.ConvShape(4, 4, 2, 1), p512.plain_ring)
+    _, cli, srv, keys, ce, *_ = run_pre(p512, job, capture=True)
+    blob = bytes(ce.stats.transcript["client"]) + bytes(ce.stats.transcript["server"])
+    assert ring.ring_to_bytes(job.x_polys[0])[5:] not in blob
+    assert ring.ring_to_bytes(job.w_polys[0])[5:] not in blob
+    assert cli.secret_key_to_bytes(keys)[5:] not in blob
+    r_x = RingElem.random(p512.plain_ring, np.random.default_rng(2))
+    masked = ring.ring_sub(job.x_polys[0], r_x)
+    assert ring.ring_to_bytes(masked)[5:] in blob
+
+
+def test_meter_relin_exactly_once_n64():
+    # reference tests/test_he.py:117-130 at N = 64
+    from paper_2409_16675_b200 import he
+    from paper_2409_16675_b200.ring import RingElem
+    plain = he.default_plain_params(64, prime_bits=17, primes=2)
+    params = he.HeParams(he.default_cipher_params(64, plain.modulus), plain)
+    ev = he.He(params)
+    keys = ev.keygen(3)
+    rng = np.random.default_rng(0)
+    a = ev.encrypt(RingElem.random(plain, rng), keys, rng)
+    b = ev.encrypt(RingElem.random(plain, rng), keys, rng)
+    ev.cc_mul(a, b, keys)
+    assert ev.meter.count("CCMul") == 1 and ev.meter.count("Relin") == 1
+    ev.cp_mul(a, RingElem.zeros(plain))
+    assert ev.meter.count("CPMul") == 1 and ev.meter.count("Relin") == 1
+
+
+def test_depth_budget_validation():
+    from paper_2409_16675_b200 import he
+    from paper_2409_16675_b200.params import RingParams, ntt_primes
+    plain = he.default_plain_params(64, prime_bits=17, primes=2)
+    thin = ntt_primes(64, 30, 2)
+    with pytest.raises(ValueError):
+        he.HeParams(RingParams(64, thin[0] * thin[1], primes=tuple(thin)), plain).check_depth_budget()
+
+
+def test_c_abi_errors_and_empty_batches():
+    import ctypes
+    import torch
+    from paper_2409_16675_b200 import _lib
+    from paper_2409_16675_b200.device import RnsContext
+    from paper_2409_16675_b200.params import default_he_params
+    lib = _lib.load()
+    P = default_he_params(4096)
+    ctx = RnsContext.get(P.n, P.cipher_ring.primes, P.plain_ring.primes)
+    assert lib.ctb_cpmul(ctx._h, None, None, None, 1, None) == _lib.CTB_ERR_ARG
+    assert b"ctb_cpmul" in lib.ctb_last_error()
+    assert lib.ctb_ntt_forward(ctx._h, 7, None, None, 1, None) == _lib.CTB_ERR_ARG
+    h = ctypes.c_void_p()
+    rc = lib.ctb_ctx_create(ctypes.byref(h), 4096, _lib.u64_array([1073692673 + 2]), 1, _lib.u64_array([]), 0, 16)
+    assert rc == _lib.CTB_ERR_ARG and b"1 mod 2N" in lib.ctb_last_error()
+    empty = torch.empty((0, 2, ctx.L, P.n), dtype=torch.int32, device="cuda")
+    assert ctx.cpmul(empty, torch.empty((0, P.n), dtype=torch.int64, device="cuda")).shape[0] == 0
+    with pytest.raises(ValueError):
+        ctx.cpmul(empty[:, :1], torch.empty((0, P.n), dtype=torch.int64, device="cuda"))
