@@ -87,3 +87,29 @@ def test_params_and_noise_algebra(golden):
     with pytest.raises(ValueError):
         from paper_2409_16675_b200.params import RingParams
         RingParams(4, 15, primes=(3, 5))
+
+
+def test_trainer_fixture_matches_plain_oracle():
+    """The recorded reference PlainEngine outputs agree with the plain oracle (fixture sanity)."""
+    from pathlib import Path
+    from oracle.plainconv import conv2d_multi
+    store = dict(np.load(Path(__file__).parent / "golden" / "trainer_calls.npz"))
+    seen = set()
+    for tag in ("toy", "bn"):
+        for ci in range(int(store[f"{tag}.ncalls"])):
+            pre = f"{tag}.call{ci:03d}"
+            m, a, b, out = str(store[f"{pre}.method"]), store[f"{pre}.a"], store[f"{pre}.b"], store[f"{pre}.out"]
+            seen.add(m)
+            if m == "conv_forward":
+                exp = conv2d_multi(a, b, int(store[f"{pre}.shape"][3]))
+            elif m == "conv_pairwise":
+                pad = int(store[f"{pre}.shape"][3])
+                exp = np.stack([conv2d_multi(a[ci:ci + 1], b[:, None], pad) for ci in range(a.shape[0])], axis=1)
+            elif m == "fc":
+                exp = a @ b
+            elif m == "outer":
+                exp = np.outer(a, b)
+            else:
+                exp = a * int(b)
+            assert np.array_equal(exp, out), (tag, ci, m)
+    assert seen == {"conv_forward", "conv_pairwise", "fc", "outer", "affine"}
