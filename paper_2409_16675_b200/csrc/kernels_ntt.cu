@@ -244,7 +244,7 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
 template <typename T, int LOGN, bool SMEM_TW>
 __global__ void __launch_bounds__(NttShape<LOGN>::THREADS * cpmul_groups<T, LOGN>(),
                                   cpmul_groups<T, LOGN>() == 2 ? 2 : NttShape<LOGN>::MINB)
-k_encrypt(const uint64_t* __restrict__ m, const int64_t* __restrict__ draws, const T* __restrict__ pkprep, T* out,
+k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, const T* __restrict__ pkprep, T* out,
           const PrimeTab<T>* __restrict__ tabs, int L, uint64_t t_half, uint32_t batch) {
   using Sh = NttShape<LOGN>;
   constexpr int GROUPS = cpmul_groups<T, LOGN>();
@@ -272,16 +272,14 @@ k_encrypt(const uint64_t* __restrict__ m, const int64_t* __restrict__ draws, con
     twp = tw_sm;
   }
   const TwSrc<T, SMEM_TW> tw{twp};
-  auto small = [&](int64_t v) -> T {  // signed small integer -> canonical residue
-    const uint64_t mag = v < 0 ? (uint64_t)(-(v + 1)) + 1 : (uint64_t)v;
-    T r = csub(pr.reduce_u64_lazy(mag), pr.p);
-    return v < 0 ? sub_mod((T)0, r, pr.p) : r;
+  auto small = [&](int8_t v) -> T {  // |v| <= 127 < p: canonical residue
+    return v < 0 ? pr.p - (T)(-(int)v) : (T)v;
   };
   const int cb = coef_base<LOGN>();
   T x[Sh::E];
 #pragma unroll 1
   for (uint32_t b = slot * GROUPS + group; b < batch; b += nslots * GROUPS) {
-    const int64_t* d = draws + (size_t)b * 3 * Sh::N + cb;
+    const int8_t* d = draws + (size_t)b * 3 * Sh::N + cb;
 #pragma unroll
     for (int k = 0; k < Sh::E; ++k) x[k] = small(__ldg(d + coef_off<LOGN>(k)));
     ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
@@ -300,7 +298,7 @@ k_encrypt(const uint64_t* __restrict__ m, const int64_t* __restrict__ draws, con
           x[i * EV::VEC + c] = mont_mul(usm[(i * EV::VEC + c) * Sh::THREADS], v[c], pr.p, pr.pinv);
       }
       ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
-      const int64_t* e = d + (size_t)(1 + part) * Sh::N;
+      const int8_t* e = d + (size_t)(1 + part) * Sh::N;
       const uint64_t* mm = m + (size_t)b * Sh::N + cb;
       T* o = out + (((size_t)b * 2 + part) * L + limb) * Sh::N + cb;
 #pragma unroll
@@ -551,7 +549,7 @@ extern "C" int ctb_cpmul(const ctb_ctx_t* ctx, const void* ct, const uint64_t* p
 }
 
 template <typename T, int LOGN>
-static cudaError_t launch_encrypt(const Ctx* c, const Base* b, const uint64_t* m, const int64_t* draws,
+static cudaError_t launch_encrypt(const Ctx* c, const Base* b, const uint64_t* m, const int8_t* draws,
                                   const void* pkprep, void* out, uint64_t batch, cudaStream_t s) {
   using Sh = NttShape<LOGN>;
   constexpr int GROUPS = cpmul_groups<T, LOGN>();
@@ -570,7 +568,7 @@ static cudaError_t launch_encrypt(const Ctx* c, const Base* b, const uint64_t* m
                             (const PrimeTab<T>*)b->d_tabs, L, c->t_half, (uint32_t)batch);
 }
 
-extern "C" int ctb_encrypt(const ctb_ctx_t* ctx, const uint64_t* m, const int64_t* draws, const void* pkprep,
+extern "C" int ctb_encrypt(const ctb_ctx_t* ctx, const uint64_t* m, const int8_t* draws, const void* pkprep,
                            void* out, uint64_t batch, void* stream) {
   if (batch == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Base* b = base_of(ctx, BASE_Q);

@@ -357,10 +357,12 @@ class He:
                     raise HeError("payload must live in the plain ring")
             mt = self._plain_tensor(ms)
         B, n = mt.shape[0], self.params.n
+        if self.params.error_bound > 127:
+            raise HeError("the device encryptor takes int8 draws: error bound must be <= 127")
         if isinstance(rng, torch.Generator):
             draws = self._device_draws(B, rng)
         else:
-            host = np.empty((B, 3, n), dtype=np.int64)
+            host = np.empty((B, 3, n), dtype=np.int8)
             for k in range(B):
                 host[k, 0] = self._ternary(rng)
                 host[k, 1] = self._error(rng)
@@ -374,13 +376,16 @@ class He:
         return CiphertextBatch(out, self.params.fresh_noise, self.backend, self.params.cipher_ring)
 
     def _device_draws(self, B: int, gen: torch.Generator) -> torch.Tensor:
-        n = self.params.n
-        bound = self.params.error_bound
-        out = torch.empty((B, 3, n), dtype=torch.int64, device="cuda")
-        out[:, 0] = torch.randint(-1, 2, (B, n), generator=gen, device="cuda", dtype=torch.int64)
-        g = torch.randn((B, 2, n), generator=gen, device="cuda", dtype=torch.float64) * self.params.noise_stddev
-        out[:, 1:] = torch.clamp(torch.round(g), -bound, bound).to(torch.int64)
-        return out.view(B * 3, n)
+        """int8 draws [B*3, N] from ctb_sample_draws, keyed by the generator's seed and
+        Philox offset (advanced by B, so successive calls draw fresh values)."""
+        out = torch.empty((B * 3, self.params.n), dtype=torch.int8, device="cuda")
+        seed = gen.initial_seed() & ((1 << 64) - 1)
+        first = gen.get_offset()
+        gen.set_offset(first + 4 * B)   # CUDA Philox offsets move in multiples of 4
+        _lib.check(self.ctx._lib.ctb_sample_draws(self.ctx._h, seed, first, float(self.params.noise_stddev),
+                                                  int(self.params.error_bound), _ptr(out), B, _stream()),
+                   "ctb_sample_draws")
+        return out
 
     def _s_prep(self, keys, power: int) -> torch.Tensor:
         s = keys.secret.data

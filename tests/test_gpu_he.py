@@ -221,3 +221,34 @@ def test_batched_apis_match_single_calls(p4096, ev4096, keys4096):
     from paper_2409_16675_b200 import ring
     for i in range(5):
         assert decs[i] == ring.ring_mul(ms[i], pts[i])
+
+
+def test_device_sampler_distribution():
+    """ctb_sample_draws: ternary u uniform on {-1,0,1}; e = clip(rint(N(0, sigma^2)), +-bound) (he.py:292-303)."""
+    import torch
+    from paper_2409_16675_b200 import _lib
+    from paper_2409_16675_b200.device import RnsContext, _ptr, _stream
+    from paper_2409_16675_b200.params import default_he_params
+    P = default_he_params(4096)
+    ctx = RnsContext.get(P.n, P.cipher_ring.primes, P.plain_ring.primes)
+    B = 256
+
+    def draw(seed, first):
+        out = torch.empty((B, 3, P.n), dtype=torch.int8, device="cuda")
+        _lib.check(ctx._lib.ctb_sample_draws(ctx._h, seed, first, P.noise_stddev, P.error_bound, _ptr(out), B,
+                                             _stream()), "ctb_sample_draws")
+        return out.to(torch.int64)
+
+    d = draw(7, 0)
+    u, e = d[:, 0].flatten(), d[:, 1:].flatten().double()
+    for v in (-1, 0, 1):
+        assert abs((u == v).double().mean().item() - 1 / 3) < 0.005
+    assert u.abs().max().item() == 1
+    assert abs(e.mean().item()) < 0.02
+    assert abs(e.var().item() - (P.noise_stddev ** 2 + 1 / 12)) < 0.1
+    assert e.abs().max().item() <= P.error_bound
+    assert torch.equal(draw(7, 0), d)
+    assert torch.equal(draw(7, 5)[:B - 5], d[5:])          # counter = global poly index
+    assert not torch.equal(draw(8, 0), d)
+    e1, e2 = d[:, 1].flatten().double(), d[:, 2].flatten().double()
+    assert abs(torch.corrcoef(torch.stack([e1, e2]))[0, 1].item()) < 0.01
