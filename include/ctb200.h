@@ -88,6 +88,13 @@ int ctb_prepare_operand(const ctb_ctx_t* ctx, int base, const void* in, void* ou
 int ctb_mul_prepared(const ctb_ctx_t* ctx, int base, const void* a, const void* bprep, uint64_t b_stride,
                      const void* addend, void* out, uint64_t n_polys, void* stream);
 
+/* ctb_mul_prepared over strided operands: item k reads a at poly k * a_stride and the
+ * addend at poly k * add_stride (strides in [L][N] polys), e.g. c0 + c1 * s straight from
+ * [B][2][L][N] ciphertexts (a = &ct[0][1], addend = &ct[0][0], strides 2). */
+int ctb_mul_prepared_strided(const ctb_ctx_t* ctx, int base, const void* a, uint64_t a_stride, const void* bprep,
+                             uint64_t b_stride, const void* addend, uint64_t add_stride, void* out,
+                             uint64_t n_polys, void* stream);
+
 /* CPMul: out[k] = (c0*lift(pt[k]), c1*lift(pt[k])) for `batch` 2-part
  * ciphertexts ct[k] ([batch][2][L][N]) and plain polys pt[k] ([batch][N]
  * uint64 in [0,t)).  He.cp_mul (he.py:366-382) with He._lift (he.py:325-327).
@@ -167,6 +174,22 @@ int ctb_tensor_round(const ctb_ctx_t* ctx, const uint32_t* h_aux, void* out, uin
 int ctb_relin_digit_count(const ctb_ctx_t* ctx);
 int ctb_relinearize(const ctb_ctx_t* ctx, const void* ct3, const void* keyprep, uint32_t* digits_ws, void* out,
                     uint64_t batch, void* stream);
+
+/* Fused per-slot CCMul sums -- the server side of the precompute protocol's offline
+ * phase (precompute_offline_server, linprot.py:407-427: per site cc_mul(r_x, r_w),
+ * relinearised, CCAdd into its slot) and of protocol b (linear_b_server, linprot.py:
+ * 371-379).  ct_x [n_x][2][L][N], ct_w [n_w][2][L][N]; sites_host [n_sites][3] = (x, w,
+ * slot) in HOST memory; keyprep as ctb_relinearize; out [n_out][2][L][N] with
+ * out[o] = sum over the sites of slot o of relinearize(cc_mul_raw(x, w)), identical to
+ * the per-site computation.  Each distinct ciphertext is lifted and transformed once and
+ * relinearisation runs once per slot (digit sums; a slot may hold at most
+ * (2^32 - 1) / (2^w - 1) sites).  workspace: ctb_ccmul_sum_workspace_bytes(..., largest
+ * slot's site count).  Synchronises `stream` once (site table upload). */
+uint64_t ctb_ccmul_sum_workspace_bytes(const ctb_ctx_t* ctx, uint32_t n_x, uint32_t n_w, uint32_t n_out,
+                                       uint32_t n_sites, uint32_t max_slot_sites);
+int ctb_ccmul_sum(const ctb_ctx_t* ctx, const void* ct_x, uint32_t n_x, const void* ct_w, uint32_t n_w,
+                  const uint32_t* sites_host, uint32_t n_sites, uint32_t n_out, const void* keyprep, void* out,
+                  void* workspace, uint64_t workspace_bytes, void* stream);
 
 /* Prepared lifted plaintext: NTT(lift(m)) in the Montgomery domain, N^-1
  * folded (m [n][N] uint64 in [0,t)) -> [n][L][N]. */

@@ -35,6 +35,8 @@ SIGNATURES: dict[str, tuple] = {
     "ctb_ring_mul": (_int, [_c_void_p, _int, _c_void_p, _u64, _c_void_p, _u64, _c_void_p, _u64, _c_void_p]),
     "ctb_prepare_operand": (_int, [_c_void_p, _int, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_mul_prepared": (_int, [_c_void_p, _int, _c_void_p, _c_void_p, _u64, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_mul_prepared_strided": (_int, [_c_void_p, _int, _c_void_p, _u64, _c_void_p, _u64, _c_void_p, _u64, _c_void_p, _u64,
+                                         _c_void_p]),
     "ctb_cpmul": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_encrypt": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_sample_draws": (_int, [_c_void_p, _u64, _u64, ctypes.c_double, _int, _c_void_p, _u64, _c_void_p]),
@@ -61,6 +63,9 @@ SIGNATURES: dict[str, tuple] = {
     "ctb_linear_online": (_int, [_c_void_p, _c_void_p, _u32, _c_void_p, _u32, _c_void_p, _c_void_p,
                                  ctypes.POINTER(_u32), _u32, _u32, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
                                  _c_void_p]),
+    "ctb_ccmul_sum_workspace_bytes": (_u64, [_c_void_p, _u32, _u32, _u32, _u32, _u32]),
+    "ctb_ccmul_sum": (_int, [_c_void_p, _c_void_p, _u32, _c_void_p, _u32, _c_void_p, _u32, _u32, _c_void_p, _c_void_p,
+                             _c_void_p, _u64, _c_void_p]),
     "ctb_slot_sum": (_int, [_c_void_p, _int, _c_void_p, _u32, _c_void_p, _c_void_p, _u32, _c_void_p, _c_void_p]),
     "ctb_probe_modmul": (_int, [_int, _u64, _c_void_p, ctypes.POINTER(_u64), _c_void_p]),
 }

@@ -83,4 +83,36 @@ inline cudaError_t launch_kernel_grid(void (*kern)(KArgs...), uint32_t grid, int
       return ERR_UNSUPPORTED;                                         \
   }
 
+// Same dispatch for helpers returning cudaError_t (unsupported degree -> cudaErrorInvalidValue).
+#define CTB_DISPATCH_LOGN_E(logn, ...)        \
+  switch (logn) {                             \
+    CTB_CASE_LOGN(2, __VA_ARGS__)             \
+    CTB_CASE_LOGN(3, __VA_ARGS__)             \
+    CTB_CASE_LOGN(4, __VA_ARGS__)             \
+    CTB_CASE_LOGN(5, __VA_ARGS__)             \
+    CTB_CASE_LOGN(6, __VA_ARGS__)             \
+    CTB_CASE_LOGN(7, __VA_ARGS__)             \
+    CTB_CASE_LOGN(8, __VA_ARGS__)             \
+    CTB_CASE_LOGN(9, __VA_ARGS__)             \
+    CTB_CASE_LOGN(10, __VA_ARGS__)            \
+    CTB_CASE_LOGN(11, __VA_ARGS__)            \
+    CTB_CASE_LOGN(12, __VA_ARGS__)            \
+    CTB_CASE_LOGN(13, __VA_ARGS__)            \
+    default:                                  \
+      return cudaErrorInvalidValue;           \
+  }
+
+// Unscaled inverse NTT of eval-domain [npoly][L][N] (+ coefficient addend), persistent
+// (kernels_ntt.cu k_stream InvAdd).  In place allowed.
+cudaError_t stream_inv_add(const Ctx* c, int base, const void* in, void* out, const void* addend, uint64_t npoly,
+                           cudaStream_t s);
+
+// Persistent forward NTT of [npoly][L][N] over base `base`: canonical eval, or prepared
+// (N^-1 2^W Montgomery operand) when `prepare` (k_stream Fwd / Prepare).  In place allowed.
+cudaError_t stream_forward(const Ctx* c, int base, bool prepare, const void* in, void* out, uint64_t npoly,
+                           cudaStream_t s);
+
+// NTT of the centred lift of plain [npoly][N] per cipher limb, prepared (N^-1 2^W) (k_stream LiftPrepare).
+cudaError_t stream_lift_prepare(const Ctx* c, const uint64_t* m, void* out, uint64_t npoly, cudaStream_t s);
+
 }  // namespace ctb

@@ -7,45 +7,11 @@
 //   He.pp_mul (plain-ring ring_mul + CRT)  he.py:441-445, ring.py:477-485 (ctb_pp_mul)
 // Layout: residues [poly][limb][N] (uint32 or uint64 words), plain [poly][N] uint64.
 #include <algorithm>
+#include "bulk.cuh"
 #include "kernels.hpp"
 #include "ctb200.h"
 
 namespace ctb {
-
-template <typename T, int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
-k_ntt_fwd(const T* in, T* out, const PrimeTab<T>* __restrict__ tabs, int L) {
-  using Sh = NttShape<LOGN>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Exchanger<T, LOGN> ex{reinterpret_cast<T*>(smem_raw)};
-  const int limb = blockIdx.x % L;
-  const size_t off = (size_t)blockIdx.x * Sh::N;
-  PrimeRegs<T> pr(tabs + limb);
-  T x[Sh::E];
-#pragma unroll
-  for (int k = 0; k < Sh::E; ++k) x[k] = in[off + coef_base<LOGN>() + coef_off<LOGN>(k)];
-  ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
-#pragma unroll
-  for (int k = 0; k < Sh::E; ++k) x[k] = pr.canon_fwd(x[k]);
-  store_eval<T, LOGN>(out + off, x);
-}
-
-template <typename T, int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
-k_ntt_inv(const T* in, T* out, const PrimeTab<T>* __restrict__ tabs, int L) {
-  using Sh = NttShape<LOGN>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Exchanger<T, LOGN> ex{reinterpret_cast<T*>(smem_raw)};
-  const int limb = blockIdx.x % L;
-  const size_t off = (size_t)blockIdx.x * Sh::N;
-  PrimeRegs<T> pr(tabs + limb);
-  T x[Sh::E];
-  load_eval<T, LOGN>(in + off, x);
-  ntt_inv_regs<T, LOGN>(x, ex, pr.inv, pr.p, pr.p2);
-#pragma unroll
-  for (int k = 0; k < Sh::E; ++k)
-    out[off + coef_base<LOGN>() + coef_off<LOGN>(k)] = csub(shoup_mul(x[k], pr.ninv, pr.ninv_q, pr.p), pr.p);
-}
 
 // out[i] = a[i * sa] * b[i * sb] in Z_q[x]/(x^N+1), per limb; sa/sb are poly strides (0 = broadcast).
 template <typename T, int LOGN>
@@ -76,64 +42,6 @@ k_ring_mul(const T* a, uint64_t sa, const T* b, uint64_t sb, T* out,
   T* po = out + poly * LN + (size_t)limb * Sh::N;
 #pragma unroll
   for (int k = 0; k < Sh::E; ++k) po[coef_base<LOGN>() + coef_off<LOGN>(k)] = csub(x[k], pr.p);
-}
-
-// Prepared operand: out = NTT(b) * N^-1 * 2^W (Montgomery domain, N^-1 folded),
-// the form k_mul_prepared consumes.  Used for keys (pk, s, relin keys) that
-// multiply many polynomials: one forward NTT per key instead of per product.
-template <typename T, int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
-k_prepare(const T* in, T* out, const PrimeTab<T>* __restrict__ tabs, int L) {
-  using Sh = NttShape<LOGN>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Exchanger<T, LOGN> ex{reinterpret_cast<T*>(smem_raw)};
-  const int limb = blockIdx.x % L;
-  const size_t off = (size_t)blockIdx.x * Sh::N;
-  PrimeRegs<T> pr(tabs + limb);
-  T x[Sh::E];
-#pragma unroll
-  for (int k = 0; k < Sh::E; ++k) x[k] = in[off + coef_base<LOGN>() + coef_off<LOGN>(k)];
-  ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
-#pragma unroll
-  for (int k = 0; k < Sh::E; ++k) x[k] = csub(shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p), pr.p);
-  store_eval<T, LOGN>(out + off, x);
-}
-
-// out[i] = a[i] * b (+ addend[i]) with b a prepared operand ([nb][L][N], nb = 1
-// broadcasts, else one per product) -- ring.ring_mul then ring.ring_add
-// (ring.py:363-427) fused: 1 forward + 1 inverse NTT per product.
-template <typename T, int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
-k_mul_prepared(const T* a, const T* bprep, uint64_t b_stride, const T* addend, T* out,
-               const PrimeTab<T>* __restrict__ tabs, int L) {
-  using Sh = NttShape<LOGN>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Exchanger<T, LOGN> ex{reinterpret_cast<T*>(smem_raw)};
-  const int limb = blockIdx.x % L;
-  const size_t poly = blockIdx.x / L;
-  const size_t off = (size_t)blockIdx.x * Sh::N;
-  const T* pb = bprep + (poly * b_stride * L + limb) * (size_t)Sh::N;
-  PrimeRegs<T> pr(tabs + limb);
-  T x[Sh::E];
-#pragma unroll
-  for (int k = 0; k < Sh::E; ++k) x[k] = a[off + coef_base<LOGN>() + coef_off<LOGN>(k)];
-  ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
-  using EV = EvalVec<T, LOGN>;
-#pragma unroll
-  for (int i = 0; i < EV::CHUNKS; ++i) {
-    T v[EV::VEC];
-    EV::load(pb, i, v);
-#pragma unroll
-    for (int c = 0; c < EV::VEC; ++c) x[i * EV::VEC + c] = mont_mul(x[i * EV::VEC + c], v[c], pr.p, pr.pinv);
-  }
-  ntt_inv_regs<T, LOGN>(x, ex, pr.inv, pr.p, pr.p2);
-#pragma unroll
-  for (int k = 0; k < Sh::E; ++k) {
-    const size_t i = off + coef_base<LOGN>() + coef_off<LOGN>(k);
-    T v = csub(x[k], pr.p);
-    if (addend) v = add_mod(v, addend[i], pr.p);
-    out[i] = v;
-  }
 }
 
 // Eval-domain slotwise product (ring.pointwise_mul, ring.py:572-584).
@@ -232,6 +140,237 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
       for (int k = 0; k < Sh::E; ++k) out[off + coef_off<LOGN>(k)] = csub(x[k], pr.p);
     }
   }
+}
+
+// Persistent limb-stationary streaming transforms (the k_cpmul layout without
+// the plaintext strip) over [npoly][L][N] batches:
+//   Fwd          ctb_ntt_forward   canonical eval, bit-reversed (ring.ntt_forward)
+//   Inv          ctb_ntt_inverse   (ring.ntt_inverse, N^-1 applied)
+//   Prepare      ctb_prepare_operand: NTT(b) N^-1 2^W, the Montgomery-domain operand
+//                that MulPrepared consumes (keys multiplying many polynomials: one
+//                forward NTT per key instead of per product)
+//   MulPrepared  ctb_mul_prepared: a * b (+ addend) with b prepared ([nb][L][N], stride
+//                0 broadcasts) -- ring.ring_mul then ring.ring_add (ring.py:363-427)
+//                fused: 1 forward + 1 inverse NTT per product.
+//   InvAdd       unscaled INTT (+ addend): eval-domain sums of products with prepared
+//                operands (N^-1 already folded in) back to coefficients, plus a
+//                coefficient-domain addend (K3's mask product).
+//   LiftPrepare  plain [npoly][N] in [0,t) -> NTT(centred lift) N^-1 2^W per limb (ctb_lift_prepare)  Twiddles staged once per CTA in
+// shared memory, GROUPS transforms per CTA sharing them.
+enum class StreamOp { Fwd, Inv, Prepare, MulPrepared, InvAdd, LiftPrepare };
+
+template <typename T>
+struct StreamArgs {
+  const T* in;             // [npoly * in_stride][L][N] (item b at poly b * in_stride)
+  T* out;                  // [npoly][L][N]
+  const T* bprep;          // MulPrepared: prepared operand, item b uses poly b * b_stride
+  const T* addend;         // MulPrepared / InvAdd: item b adds poly b * add_stride (may be null)
+  const uint64_t* plain;   // LiftPrepare: [npoly][N] values in [0, t)
+  uint64_t in_stride, b_stride, add_stride, t_half;
+  bool plain_fast;
+};
+
+template <typename T, int LOGN>
+struct StreamCfg {
+  using Sh = NttShape<LOGN>;
+  static constexpr int GROUPS = cpmul_groups<T, LOGN>();
+  using Ex = Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>;
+  static constexpr size_t TW_BYTES = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
+  static constexpr bool SMEM_TW = sizeof(T) == 4 && LOGN >= 9 &&
+                                  TW_BYTES + GROUPS * (size_t)Ex::WORDS * sizeof(T) <= 200 * 1024;
+  // TMA prefetch of the next item into an N-word staging buffer per group (u32, where the
+  // table + images + staging still fit two CTAs per SM)
+  static constexpr int EXW = (Ex::WORDS * (int)sizeof(T) + 15) / 16 * 16 / (int)sizeof(T);
+  static constexpr bool PF_OK = SMEM_TW && (TW_BYTES + GROUPS * ((size_t)EXW + Sh::N) * sizeof(T) + 64) * 2 <= 220 * 1024;
+  static constexpr int GW = EXW + (PF_OK ? Sh::N : 0);  // words per group
+  static constexpr size_t SMEM = (SMEM_TW ? TW_BYTES : 0) + GROUPS * (size_t)GW * sizeof(T) + (PF_OK ? 64 : 0);
+  static constexpr int THREADS = Sh::THREADS * GROUPS;
+  static constexpr int MINB = GROUPS == 2 ? 2 : Sh::MINB;
+};
+
+template <typename T, int LOGN, bool SMEM_TW, StreamOp OP>
+__global__ void __launch_bounds__(StreamCfg<T, LOGN>::THREADS, StreamCfg<T, LOGN>::MINB)
+k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uint32_t npoly) {
+  using C = StreamCfg<T, LOGN>;
+  using Sh = NttShape<LOGN>;
+  constexpr int GROUPS = C::GROUPS;
+  constexpr bool PF = C::PF_OK && OP != StreamOp::LiftPrepare;
+  constexpr int TW_WORDS = SMEM_TW ? 2 * shape_tw_entries(LOGN) : 0;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* tw_sm = reinterpret_cast<T*>(smem_raw);
+  const int group = (int)(threadIdx.x / Sh::THREADS);
+  T* gsm = tw_sm + TW_WORDS + group * C::GW;
+  typename C::Ex ex{gsm};
+  T* stg = gsm + C::EXW;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tw_sm + TW_WORDS + GROUPS * C::GW) + group;
+  const bool leader = ntt_tid<LOGN>() == 0;
+  const int limb = blockIdx.x % L;
+  const uint32_t slot = blockIdx.x / L;
+  const uint32_t nslots = (gridDim.x - limb + L - 1) / L;
+  const uint32_t step = nslots * GROUPS;
+  PrimeRegs<T> pr(tabs + limb);
+  const T* twp = pr.fwd;
+  if constexpr (SMEM_TW) {
+    const uint4* src = reinterpret_cast<const uint4*>(pr.fwd);
+    uint4* dst = reinterpret_cast<uint4*>(tw_sm);
+    for (int i = threadIdx.x; i < TW_WORDS * (int)sizeof(T) / 16; i += C::THREADS) dst[i] = __ldg(src + i);
+    twp = tw_sm;
+  }
+  uint32_t b = slot * GROUPS + group;
+  if constexpr (PF) {
+    if (leader) {
+      mbar_init(bar, 1);
+      mbar_init_fence();
+      if (b < npoly) bulk_load(stg, a.in + ((size_t)b * a.in_stride * L + limb) * Sh::N, Sh::N * sizeof(T), bar);
+    }
+  }
+  if constexpr (SMEM_TW || PF) __syncthreads();
+  const TwSrc<T, SMEM_TW> tw{twp};
+  const int cb = coef_base<LOGN>();
+  uint32_t phase = 0;
+  T x[Sh::E];
+#pragma unroll 1
+  for (; b < npoly; b += step) {
+    const size_t off = ((size_t)b * L + limb) * (size_t)Sh::N;               // output item
+    const size_t ioff = ((size_t)b * a.in_stride * L + limb) * (size_t)Sh::N;  // input item
+    const size_t aoff = ((size_t)b * a.add_stride * L + limb) * (size_t)Sh::N;
+    constexpr bool EVAL_IN = OP == StreamOp::Inv || OP == StreamOp::InvAdd;
+    if constexpr (PF) {
+      mbar_wait(bar, phase);
+      phase ^= 1;
+      if constexpr (EVAL_IN) {
+        load_eval_smem<T, LOGN>(stg, x);
+      } else {
+#pragma unroll
+        for (int k = 0; k < Sh::E; ++k) x[k] = stg[cb + coef_off<LOGN>(k)];
+      }
+      group_sync<LOGN, GROUPS>();  // staging buffer consumed
+      if (leader) {
+        if (b + step < npoly) {
+          fence_proxy_async_smem();
+          bulk_load(stg, a.in + ((size_t)(b + step) * a.in_stride * L + limb) * Sh::N, Sh::N * sizeof(T), bar);
+        }
+        // the epilogue's per-item operands: start them towards L2 while this item transforms
+        if ((OP == StreamOp::InvAdd || OP == StreamOp::MulPrepared) && a.addend)
+          bulk_prefetch_l2(a.addend + aoff, Sh::N * sizeof(T));
+        if (OP == StreamOp::MulPrepared && a.b_stride)
+          bulk_prefetch_l2(a.bprep + ((size_t)b * a.b_stride * L + limb) * (size_t)Sh::N, Sh::N * sizeof(T));
+      }
+    } else if constexpr (OP == StreamOp::LiftPrepare) {
+      const uint64_t* src = a.plain + (size_t)b * Sh::N + cb;
+      const T tmod = tabs[limb].tmod;
+#pragma unroll
+      for (int k = 0; k < Sh::E; ++k) {
+        const uint64_t v = __ldg(src + coef_off<LOGN>(k));
+        T r = csub(pr.reduce_plain(v, a.plain_fast), pr.p);  // v mod p
+        if (v > a.t_half) r = sub_mod(r, tmod, pr.p);           // centred lift: v - t
+        x[k] = r;
+      }
+    } else if constexpr (EVAL_IN) {
+      load_eval<T, LOGN>(a.in + ioff, x);
+    } else {
+#pragma unroll
+      for (int k = 0; k < Sh::E; ++k) x[k] = a.in[ioff + cb + coef_off<LOGN>(k)];
+    }
+    if constexpr (OP == StreamOp::Inv) {
+      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+#pragma unroll
+      for (int k = 0; k < Sh::E; ++k)
+        a.out[off + cb + coef_off<LOGN>(k)] = csub(shoup_mul(x[k], pr.ninv, pr.ninv_q, pr.p), pr.p);
+    } else if constexpr (OP == StreamOp::InvAdd) {
+      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+#pragma unroll
+      for (int k = 0; k < Sh::E; ++k) {
+        const int j = cb + coef_off<LOGN>(k);
+        T v = csub(x[k], pr.p);
+        if (a.addend) v = add_mod(v, a.addend[aoff + j], pr.p);
+        a.out[off + j] = v;
+      }
+    } else {
+      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+      if constexpr (OP == StreamOp::Fwd) {
+#pragma unroll
+        for (int k = 0; k < Sh::E; ++k) x[k] = pr.canon_fwd(x[k]);
+        store_eval<T, LOGN>(a.out + off, x);
+      } else if constexpr (OP == StreamOp::Prepare || OP == StreamOp::LiftPrepare) {
+#pragma unroll
+        for (int k = 0; k < Sh::E; ++k) x[k] = csub(shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p), pr.p);
+        store_eval<T, LOGN>(a.out + off, x);
+      } else {
+        const T* pb = a.bprep + ((size_t)b * a.b_stride * L + limb) * (size_t)Sh::N;
+        using EV = EvalVec<T, LOGN>;
+#pragma unroll
+        for (int i = 0; i < EV::CHUNKS; ++i) {
+          T v[EV::VEC];
+          EV::load(pb, i, v);
+#pragma unroll
+          for (int c = 0; c < EV::VEC; ++c) x[i * EV::VEC + c] = mont_mul(x[i * EV::VEC + c], v[c], pr.p, pr.pinv);
+        }
+        ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+#pragma unroll
+        for (int k = 0; k < Sh::E; ++k) {
+          const int j = cb + coef_off<LOGN>(k);
+          T v = csub(x[k], pr.p);
+          if (a.addend) v = add_mod(v, a.addend[aoff + j], pr.p);
+          a.out[off + j] = v;
+        }
+      }
+    }
+  }
+}
+
+template <typename T, int LOGN, StreamOp OP>
+static cudaError_t launch_stream(const Base* b, const StreamArgs<T>& args, uint64_t npoly, cudaStream_t s) {
+  using C = StreamCfg<T, LOGN>;
+  auto kern = k_stream<T, LOGN, C::SMEM_TW, OP>;
+  const int L = b->size();
+  if (npoly == 0) return cudaSuccess;
+  uint32_t grid = persistent_grid((const void*)kern, C::THREADS, C::SMEM);
+  const uint64_t max_grid = (npoly + C::GROUPS - 1) / C::GROUPS * (uint64_t)L;
+  grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(grid / L * L, (uint64_t)L), max_grid);
+  return launch_kernel_grid(kern, grid, C::THREADS, C::SMEM, s, args, (const PrimeTab<T>*)b->d_tabs, L,
+                            (uint32_t)npoly);
+}
+
+// Host-side builder of StreamArgs (untyped pointers from the C ABI).
+template <typename T>
+static StreamArgs<T> sargs(const void* in, void* out, const void* bprep = nullptr, uint64_t b_stride = 0,
+                           const void* addend = nullptr, uint64_t in_stride = 1, uint64_t add_stride = 1) {
+  StreamArgs<T> a{};
+  a.in = (const T*)in;
+  a.out = (T*)out;
+  a.bprep = (const T*)bprep;
+  a.addend = (const T*)addend;
+  a.in_stride = in_stride;
+  a.b_stride = b_stride;
+  a.add_stride = add_stride;
+  return a;
+}
+
+cudaError_t stream_forward(const Ctx* c, int base, bool prepare, const void* in, void* out, uint64_t npoly,
+                           cudaStream_t s) {
+  const Base* b = &c->base[base];
+  cudaError_t e = cudaSuccess;
+  if (b->word == 4) {
+    if (prepare) CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::Prepare>(b, sargs<uint32_t>(in, out), npoly, s)))
+    else CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::Fwd>(b, sargs<uint32_t>(in, out), npoly, s)))
+  } else {
+    if (prepare) CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::Prepare>(b, sargs<uint64_t>(in, out), npoly, s)))
+    else CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::Fwd>(b, sargs<uint64_t>(in, out), npoly, s)))
+  }
+  return e;
+}
+
+cudaError_t stream_inv_add(const Ctx* c, int base, const void* in, void* out, const void* addend, uint64_t npoly,
+                           cudaStream_t s) {
+  const Base* b = &c->base[base];
+  cudaError_t e = cudaSuccess;
+  if (b->word == 4) {
+    CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::InvAdd>(b, sargs<uint32_t>(in, out, nullptr, 0, addend), npoly, s)));
+  } else {
+    CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::InvAdd>(b, sargs<uint64_t>(in, out, nullptr, 0, addend), npoly, s)));
+  }
+  return e;
 }
 
 // Fused encryption (He.encrypt, he.py:307-323): per (ciphertext, limb)
@@ -387,17 +526,12 @@ extern "C" int ctb_ntt_forward(const ctb_ctx_t* ctx, int base, const void* in, v
   const Base* b = base_of(ctx, base);
   if (!b || !in || !out) { set_error("ctb_ntt_forward: bad context, base or buffer"); return ERR_ARG; }
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
-  const size_t nblk = n_polys * b->size();
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
   if (b->word == 4) {
-    using T = uint32_t;
-    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_ntt_fwd<T, LOGN>, nblk, s, (const T*)in, (T*)out,
-                                                      (const PrimeTab<T>*)b->d_tabs, b->size())));
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::Fwd>(b, sargs<uint32_t>(in, out), n_polys, s)));
   } else {
-    using T = uint64_t;
-    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_ntt_fwd<T, LOGN>, nblk, s, (const T*)in, (T*)out,
-                                                      (const PrimeTab<T>*)b->d_tabs, b->size())));
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::Fwd>(b, sargs<uint64_t>(in, out), n_polys, s)));
   }
   return cuda_status(e, "ctb_ntt_forward");
 }
@@ -408,17 +542,12 @@ extern "C" int ctb_ntt_inverse(const ctb_ctx_t* ctx, int base, const void* in, v
   const Base* b = base_of(ctx, base);
   if (!b || !in || !out) { set_error("ctb_ntt_inverse: bad context, base or buffer"); return ERR_ARG; }
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
-  const size_t nblk = n_polys * b->size();
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
   if (b->word == 4) {
-    using T = uint32_t;
-    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_ntt_inv<T, LOGN>, nblk, s, (const T*)in, (T*)out,
-                                                      (const PrimeTab<T>*)b->d_tabs, b->size())));
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::Inv>(b, sargs<uint32_t>(in, out), n_polys, s)));
   } else {
-    using T = uint64_t;
-    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_ntt_inv<T, LOGN>, nblk, s, (const T*)in, (T*)out,
-                                                      (const PrimeTab<T>*)b->d_tabs, b->size())));
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::Inv>(b, sargs<uint64_t>(in, out), n_polys, s)));
   }
   return cuda_status(e, "ctb_ntt_inverse");
 }
@@ -429,42 +558,54 @@ extern "C" int ctb_prepare_operand(const ctb_ctx_t* ctx, int base, const void* i
   const Base* b = base_of(ctx, base);
   if (!b || !in || !out) { set_error("ctb_prepare_operand: bad context, base or buffer"); return ERR_ARG; }
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
-  const size_t nblk = n_polys * b->size();
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
   if (b->word == 4) {
-    using T = uint32_t;
-    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_prepare<T, LOGN>, nblk, s, (const T*)in, (T*)out,
-                                                      (const PrimeTab<T>*)b->d_tabs, b->size())));
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::Prepare>(b, sargs<uint32_t>(in, out), n_polys, s)));
   } else {
-    using T = uint64_t;
-    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_prepare<T, LOGN>, nblk, s, (const T*)in, (T*)out,
-                                                      (const PrimeTab<T>*)b->d_tabs, b->size())));
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::Prepare>(b, sargs<uint64_t>(in, out), n_polys, s)));
   }
   return cuda_status(e, "ctb_prepare_operand");
 }
 
-extern "C" int ctb_mul_prepared(const ctb_ctx_t* ctx, int base, const void* a, const void* bprep, uint64_t b_stride,
-                                const void* addend, void* out, uint64_t n_polys, void* stream) {
+extern "C" int ctb_mul_prepared_strided(const ctb_ctx_t* ctx, int base, const void* a, uint64_t a_stride,
+                                        const void* bprep, uint64_t b_stride, const void* addend,
+                                        uint64_t add_stride, void* out, uint64_t n_polys, void* stream) {
   if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Base* b = base_of(ctx, base);
-  if (!b || !a || !bprep || !out) { set_error("ctb_mul_prepared: bad context, base or buffer"); return ERR_ARG; }
+  if (!b || !a || !bprep || !out || a_stride == 0 || (addend && add_stride == 0)) {
+    set_error("ctb_mul_prepared: bad context, base, buffer or stride");
+    return ERR_ARG;
+  }
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
-  const size_t nblk = n_polys * b->size();
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
   if (b->word == 4) {
-    using T = uint32_t;
-    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_mul_prepared<T, LOGN>, nblk, s, (const T*)a,
-                                                      (const T*)bprep, b_stride, (const T*)addend, (T*)out,
-                                                      (const PrimeTab<T>*)b->d_tabs, b->size())));
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::MulPrepared>(b, sargs<uint32_t>(a, out, bprep, b_stride, addend, a_stride, add_stride), n_polys, s)));
   } else {
-    using T = uint64_t;
-    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_mul_prepared<T, LOGN>, nblk, s, (const T*)a,
-                                                      (const T*)bprep, b_stride, (const T*)addend, (T*)out,
-                                                      (const PrimeTab<T>*)b->d_tabs, b->size())));
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::MulPrepared>(b, sargs<uint64_t>(a, out, bprep, b_stride, addend, a_stride, add_stride), n_polys, s)));
   }
   return cuda_status(e, "ctb_mul_prepared");
+}
+
+extern "C" int ctb_mul_prepared(const ctb_ctx_t* ctx, int base, const void* a, const void* bprep, uint64_t b_stride,
+                                const void* addend, void* out, uint64_t n_polys, void* stream) {
+  return ctb_mul_prepared_strided(ctx, base, a, 1, bprep, b_stride, addend, 1, out, n_polys, stream);
+}
+
+cudaError_t ctb::stream_lift_prepare(const Ctx* c, const uint64_t* m, void* out, uint64_t npoly, cudaStream_t s) {
+  const Base* b = &c->base[BASE_Q];
+  cudaError_t e = cudaSuccess;
+  if (b->word == 4) {
+    StreamArgs<uint32_t> a = sargs<uint32_t>(nullptr, out);
+    a.plain = m; a.t_half = c->t_half; a.plain_fast = c->plain_fast;
+    CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::LiftPrepare>(b, a, npoly, s)));
+  } else {
+    StreamArgs<uint64_t> a = sargs<uint64_t>(nullptr, out);
+    a.plain = m; a.t_half = c->t_half; a.plain_fast = c->plain_fast;
+    CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::LiftPrepare>(b, a, npoly, s)));
+  }
+  return e;
 }
 
 extern "C" int ctb_pointwise_mul(const ctb_ctx_t* ctx, int base, const void* a, const void* bb, void* out,

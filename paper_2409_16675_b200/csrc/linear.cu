@@ -11,8 +11,9 @@
 // products in registers, and each slot part is inverse-transformed ONCE --
 // instead of 2 x (3 forward + 2 inverse) NTTs per site in the reference.
 //
-//   k_lift_prepare  plain [P][N] -> NTT(lift(m)) N^-1 2^W per limb (prepared operand)
-//   k_lin_cipher    CTA per (slot, limb): 2 parts x sum over the slot's sites, INTT, + mask product
+//   LiftPrepare     plain [P][N] -> NTT(lift(m)) N^-1 2^W per limb (k_stream, kernels_ntt.cu)
+//   k_lin_accum     per (slot, limb, 16-byte vector): 2 parts x sum over the slot's sites (eval)
+//   k_stream InvAdd persistent INTT of the slot sums, + mask product (kernels_ntt.cu)
 //   k_lin_plain     CTA per (slot, plain prime): sum of prepared products, INTT
 //   k_plain_crt     plain residues -> uint64 mod t (ring._crt_combine, ring.py:478-485)
 //   k_slot_sum      segmented sum of ciphertexts per slot (offline CCAdd accumulation)
@@ -24,87 +25,76 @@
 
 namespace ctb {
 
-template <typename T, int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
-k_lift_prepare(const uint64_t* __restrict__ m, T* out, const PrimeTab<T>* __restrict__ tabs, int L, uint64_t t_half) {
-  using Sh = NttShape<LOGN>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Exchanger<T, LOGN> ex{reinterpret_cast<T*>(smem_raw)};
-  const int limb = blockIdx.x % L;
-  const size_t poly = blockIdx.x / L;
-  PrimeRegs<T> pr(tabs + limb);
-  const T tmod = tabs[limb].tmod;
-  const uint64_t* src = m + poly * Sh::N + coef_base<LOGN>();
-  T x[Sh::E];
-#pragma unroll
-  for (int k = 0; k < Sh::E; ++k) {
-    const uint64_t v = __ldg(src + coef_off<LOGN>(k));
-    T r = csub(pr.reduce_u64_lazy(v), pr.p);
-    if (v > t_half) r = sub_mod(r, tmod, pr.p);
-    x[k] = r;
-  }
-  ntt_fwd_regs<T, LOGN>(x, ex, pr.fwd, pr.p, pr.p2);
-#pragma unroll
-  for (int k = 0; k < Sh::E; ++k) x[k] = csub(shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p), pr.p);
-  store_eval<T, LOGN>(out + (size_t)blockIdx.x * Sh::N, x);
-}
-
 // X [n_x][2][L][N], W [n_w][2][L][N]: canonical eval; MXp [n_x][L][N], MWp [n_w][L][N]: prepared.
-template <typename T, int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
-k_lin_cipher(const T* X, const T* W, const T* MXp, const T* MWp, const int32_t* __restrict__ slot_ptr,
-             const int32_t* __restrict__ site_x, const int32_t* __restrict__ site_w, const T* maskprod, T* out,
-             const PrimeTab<T>* __restrict__ tabs, int L) {
-  using Sh = NttShape<LOGN>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Exchanger<T, LOGN> ex{reinterpret_cast<T*>(smem_raw)};
-  const int limb = blockIdx.x % L;
-  const int slot = blockIdx.x / L;
-  PrimeRegs<T> pr(tabs + limb);
-  const size_t N = Sh::N, LN = (size_t)L * N;
-  using EV = EvalVec<T, LOGN>;
-  T a0[Sh::E], a1[Sh::E];
+// ACC [n_out][2][L][N] (eval, [0,2p), N^-1 folded) = per slot the sum over its sites of
+// X (x) MW + W (x) MX.  Elementwise in the eval domain, so the thread mapping is free:
+// one thread per 16-byte vector of one (slot, limb), sites two at a time so a thread
+// has 12 independent 16-byte loads in flight -- this phase is a gather over HBM/L2 and
+// lives on memory-level parallelism, while the transforms run in k_stream (InvAdd).
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_lin_accum(const T* __restrict__ X, const T* __restrict__ W, const T* __restrict__ MXp, const T* __restrict__ MWp,
+            const int32_t* __restrict__ slot_ptr, const int32_t* __restrict__ site_x,
+            const int32_t* __restrict__ site_w, T* __restrict__ acc, const PrimeTab<T>* __restrict__ tabs, int L,
+            uint32_t n, uint32_t chunks) {
+  constexpr int VEC = 16 / sizeof(T);
+  union V { uint4 u; T t[VEC]; };
+  uint32_t bid = blockIdx.x;
+  const uint32_t chunk = bid % chunks;
+  bid /= chunks;
+  const int limb = (int)(bid % L);
+  const uint32_t slot = bid / L;
+  const uint32_t nv = n / VEC;
+  const uint32_t v = chunk * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  const T p = tabs[limb].p, p2 = 2 * p, pinv = tabs[limb].pinv;
+  const size_t LN = (size_t)L * n;
+  const uint4* X4 = reinterpret_cast<const uint4*>(X + (size_t)limb * n) + v;
+  const uint4* W4 = reinterpret_cast<const uint4*>(W + (size_t)limb * n) + v;
+  const uint4* MX4 = reinterpret_cast<const uint4*>(MXp + (size_t)limb * n) + v;
+  const uint4* MW4 = reinterpret_cast<const uint4*>(MWp + (size_t)limb * n) + v;
+  const size_t part4 = LN / VEC, poly4 = 2 * part4;  // uint4 strides
+  T a0[VEC], a1[VEC];
 #pragma unroll
-  for (int k = 0; k < Sh::E; ++k) a0[k] = a1[k] = 0;
-  const int s0 = slot_ptr[slot], s1 = slot_ptr[slot + 1];
-#pragma unroll 1
-  for (int s = s0; s < s1; ++s) {
-    const size_t xi = (size_t)site_x[s], wi = (size_t)site_w[s];
-    const T* x0 = X + (xi * 2 + 0) * LN + limb * N;
-    const T* x1 = X + (xi * 2 + 1) * LN + limb * N;
-    const T* w0 = W + (wi * 2 + 0) * LN + limb * N;
-    const T* w1 = W + (wi * 2 + 1) * LN + limb * N;
-    const T* mx = MXp + xi * LN + limb * N;
-    const T* mw = MWp + wi * LN + limb * N;
+  for (int c = 0; c < VEC; ++c) a0[c] = a1[c] = 0;
+  auto site = [&](const V& x0, const V& x1, const V& w0, const V& w1, const V& mx, const V& mw) {
 #pragma unroll
-    for (int i = 0; i < EV::CHUNKS; ++i) {
-      T vx0[EV::VEC], vx1[EV::VEC], vw0[EV::VEC], vw1[EV::VEC], vmx[EV::VEC], vmw[EV::VEC];
-      EV::load(x0, i, vx0); EV::load(x1, i, vx1); EV::load(w0, i, vw0);
-      EV::load(w1, i, vw1); EV::load(mx, i, vmx); EV::load(mw, i, vmw);
-#pragma unroll
-      for (int c = 0; c < EV::VEC; ++c) {
-        const int k = i * EV::VEC + c;
-        a0[k] = csub(a0[k] + mont_mul(vx0[c], vmw[c], pr.p, pr.pinv), pr.p2);
-        a0[k] = csub(a0[k] + mont_mul(vw0[c], vmx[c], pr.p, pr.pinv), pr.p2);
-        a1[k] = csub(a1[k] + mont_mul(vx1[c], vmw[c], pr.p, pr.pinv), pr.p2);
-        a1[k] = csub(a1[k] + mont_mul(vw1[c], vmx[c], pr.p, pr.pinv), pr.p2);
-      }
+    for (int c = 0; c < VEC; ++c) {
+      a0[c] = csub(a0[c] + mont_mul(x0.t[c], mw.t[c], p, pinv), p2);
+      a0[c] = csub(a0[c] + mont_mul(w0.t[c], mx.t[c], p, pinv), p2);
+      a1[c] = csub(a1[c] + mont_mul(x1.t[c], mw.t[c], p, pinv), p2);
+      a1[c] = csub(a1[c] + mont_mul(w1.t[c], mx.t[c], p, pinv), p2);
     }
-  }
+  };
+  int s = slot_ptr[slot];
+  const int s1 = slot_ptr[slot + 1];
 #pragma unroll 1
-  for (int part = 0; part < 2; ++part) {
-    T acc[Sh::E];
-#pragma unroll
-    for (int k = 0; k < Sh::E; ++k) acc[k] = part == 0 ? a0[k] : a1[k];
-    ntt_inv_regs<T, LOGN>(acc, ex, pr.inv, pr.p, pr.p2);
-    const size_t off = ((size_t)slot * 2 + part) * LN + limb * N + coef_base<LOGN>();
-#pragma unroll
-    for (int k = 0; k < Sh::E; ++k) {
-      T v = csub(acc[k], pr.p);
-      if (maskprod) v = add_mod(v, maskprod[off + coef_off<LOGN>(k)], pr.p);
-      out[off + coef_off<LOGN>(k)] = v;
-    }
+  for (; s + 1 < s1; s += 2) {
+    const size_t xa = site_x[s], wa = site_w[s], xb = site_x[s + 1], wb = site_w[s + 1];
+    V x0a, x1a, w0a, w1a, mxa, mwa, x0b, x1b, w0b, w1b, mxb, mwb;
+    x0a.u = __ldg(X4 + xa * poly4); x1a.u = __ldg(X4 + xa * poly4 + part4);
+    w0a.u = __ldg(W4 + wa * poly4); w1a.u = __ldg(W4 + wa * poly4 + part4);
+    mxa.u = __ldg(MX4 + xa * part4); mwa.u = __ldg(MW4 + wa * part4);
+    x0b.u = __ldg(X4 + xb * poly4); x1b.u = __ldg(X4 + xb * poly4 + part4);
+    w0b.u = __ldg(W4 + wb * poly4); w1b.u = __ldg(W4 + wb * poly4 + part4);
+    mxb.u = __ldg(MX4 + xb * part4); mwb.u = __ldg(MW4 + wb * part4);
+    site(x0a, x1a, w0a, w1a, mxa, mwa);
+    site(x0b, x1b, w0b, w1b, mxb, mwb);
   }
+  if (s < s1) {
+    const size_t xa = site_x[s], wa = site_w[s];
+    V x0a, x1a, w0a, w1a, mxa, mwa;
+    x0a.u = __ldg(X4 + xa * poly4); x1a.u = __ldg(X4 + xa * poly4 + part4);
+    w0a.u = __ldg(W4 + wa * poly4); w1a.u = __ldg(W4 + wa * poly4 + part4);
+    mxa.u = __ldg(MX4 + xa * part4); mwa.u = __ldg(MW4 + wa * part4);
+    site(x0a, x1a, w0a, w1a, mxa, mwa);
+  }
+  V o0, o1;
+#pragma unroll
+  for (int c = 0; c < VEC; ++c) { o0.t[c] = a0[c]; o1.t[c] = a1[c]; }
+  uint4* A4 = reinterpret_cast<uint4*>(acc + (size_t)limb * n) + v + (size_t)slot * poly4;
+  A4[0] = o0.u;
+  A4[part4] = o1.u;
 }
 
 // Plain side over the plain primes (u32): MXt canonical eval [n_x][LT][N], MWtp prepared.
@@ -191,19 +181,7 @@ extern "C" int ctb_lift_prepare(const ctb_ctx_t* ctx, const uint64_t* m, void* o
   if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Ctx* c = cctx(ctx);
   if (!c || !c->t || !m || !out) { set_error("ctb_lift_prepare: needs plain ring and buffers"); return ERR_ARG; }
-  const Base& B = c->base[BASE_Q];
-  cudaStream_t s = (cudaStream_t)stream;
-  cudaError_t e;
-  if (B.word == 4) {
-    using T = uint32_t;
-    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_lift_prepare<T, LOGN>, n_polys * B.size(), s, m, (T*)out,
-                                                      (const PrimeTab<T>*)B.d_tabs, B.size(), c->t_half)));
-  } else {
-    using T = uint64_t;
-    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_lift_prepare<T, LOGN>, n_polys * B.size(), s, m, (T*)out,
-                                                      (const PrimeTab<T>*)B.d_tabs, B.size(), c->t_half)));
-  }
-  return cuda_status(e, "ctb_lift_prepare");
+  return cuda_status(stream_lift_prepare(c, m, out, n_polys, (cudaStream_t)stream), "ctb_lift_prepare");
 }
 
 extern "C" uint64_t ctb_linear_online_workspace_bytes(const ctb_ctx_t* ctx, uint32_t n_x, uint32_t n_w, uint32_t n_out,
@@ -287,18 +265,22 @@ extern "C" int ctb_linear_online(const ctb_ctx_t* ctx, const void* ct_x, uint32_
   if ((rc = ctb_ntt_forward(ctx, CTB_BASE_T, MXt, MXt, n_x, stream))) return rc;
   if ((rc = ctb_rns_from_small(ctx, CTB_BASE_T, (const int64_t*)mw, MWt, n_w, stream))) return rc;
   if ((rc = ctb_prepare_operand(ctx, CTB_BASE_T, MWt, MWt, n_w, stream))) return rc;
-  if (B.word == 4) {
-    using T = uint32_t;
-    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_lin_cipher<T, LOGN>, (size_t)n_out * L, s,
-                                                      (const T*)X, (const T*)W, (const T*)MX, (const T*)MW, d_ptr,
-                                                      d_sx, d_sw, (const T*)maskprod, (T*)out_ct,
-                                                      (const PrimeTab<T>*)B.d_tabs, (int)L)));
-  } else {
-    using T = uint64_t;
-    CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<T, LOGN>(k_lin_cipher<T, LOGN>, (size_t)n_out * L, s,
-                                                      (const T*)X, (const T*)W, (const T*)MX, (const T*)MW, d_ptr,
-                                                      d_sx, d_sw, (const T*)maskprod, (T*)out_ct,
-                                                      (const PrimeTab<T>*)B.d_tabs, (int)L)));
+  {
+    // cipher side: gather-accumulate into out_ct (eval domain), then INTT in place + mask product
+    const uint32_t nv = (uint32_t)(N * w / 16);
+    const uint32_t chunks = (nv + 255) / 256;
+    const uint64_t blocks = (uint64_t)n_out * L * chunks;
+    if (blocks >= (1ull << 31)) { set_error("ctb_linear_online: job too large"); return ERR_ARG; }
+    if (B.word == 4)
+      k_lin_accum<uint32_t><<<(unsigned)blocks, 256, 0, s>>>((const uint32_t*)X, (const uint32_t*)W,
+          (const uint32_t*)MX, (const uint32_t*)MW, d_ptr, d_sx, d_sw, (uint32_t*)out_ct,
+          (const PrimeTab<uint32_t>*)B.d_tabs, (int)L, (uint32_t)N, chunks);
+    else
+      k_lin_accum<uint64_t><<<(unsigned)blocks, 256, 0, s>>>((const uint64_t*)X, (const uint64_t*)W,
+          (const uint64_t*)MX, (const uint64_t*)MW, d_ptr, d_sx, d_sw, (uint64_t*)out_ct,
+          (const PrimeTab<uint64_t>*)B.d_tabs, (int)L, (uint32_t)N, chunks);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = stream_inv_add(c, BASE_Q, out_ct, out_ct, maskprod, (uint64_t)n_out * 2, s);
   }
   if (e != cudaSuccess) return cuda_status(e, "ctb_linear_online cipher");
   CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<uint32_t, LOGN>(k_lin_plain<LOGN>, (size_t)n_out * LT, s,

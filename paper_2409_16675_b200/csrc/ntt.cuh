@@ -425,6 +425,29 @@ struct EvalVec {
   }
 };
 
+// load_eval from a shared-memory copy of the polynomial (natural word order).
+template <typename T, int LOGN>
+__device__ __forceinline__ void load_eval_smem(const T* base, T (&x)[NttShape<LOGN>::E]) {
+  using Sh = NttShape<LOGN>;
+  using EV = EvalVec<T, LOGN>;
+  const T* p = base + eval_base<LOGN>();
+  if constexpr (EV::CONTIG) {
+#pragma unroll
+    for (int i = 0; i < EV::CHUNKS; ++i) {
+      const uint4 w = reinterpret_cast<const uint4*>(p)[i];
+      if constexpr (sizeof(T) == 4) {
+        x[4 * i] = w.x; x[4 * i + 1] = w.y; x[4 * i + 2] = w.z; x[4 * i + 3] = w.w;
+      } else {
+        x[2 * i] = (uint64_t)w.x | ((uint64_t)w.y << 32);
+        x[2 * i + 1] = (uint64_t)w.z | ((uint64_t)w.w << 32);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < Sh::E; ++k) x[k] = p[eval_off<LOGN>(k)];
+  }
+}
+
 template <typename T, int LOGN>
 __device__ __forceinline__ void store_eval(T* base, const T (&x)[NttShape<LOGN>::E]) {
   using Sh = NttShape<LOGN>;
@@ -478,6 +501,10 @@ struct PrimeRegs {
       }
     }
     return reduce_u64_lazy(v);
+  }
+  // Any 32-bit value into [0, p).
+  __device__ __forceinline__ T reduce_digit(uint32_t v) const {
+    return csub(shoup_mul<T>((T)v, (T)1, one_q, p), p);
   }
   // Reduce an arbitrary 64-bit value mod p into [0, 2p).
   __device__ __forceinline__ T reduce_u64_lazy(uint64_t v) const {

@@ -67,6 +67,7 @@ struct TensorConsts {
 
 struct TensorState {
   void* d_consts = nullptr;
+  std::vector<unsigned char> host;  // the same constants, passed by value (constant bank) to the hot kernels
   int K = 0, K2 = 0, L = 0;
   bool q_lead = false;  // aux base = [Q primes in order] + [P2 primes in order] (index shortcuts valid)
   ~TensorState() {
@@ -132,10 +133,9 @@ __device__ __forceinline__ uint32_t horner_to_aux(int n_rt, const TQ* dig, const
 // in: [B][2][L][N] (TQ) -> out: [B][2][K][N] (u32), centred lifts over the aux base.
 // LC / KC > 0: limb / aux counts fixed at compile time (register-resident digits).
 template <typename TQ, int LC, int KC>
-__global__ void __launch_bounds__(256, 2) k_tensor_lift(const TQ* in, uint32_t* out, const TensorConsts<TQ>* gc,
-                                                     uint32_t n, uint64_t total) {
-  __shared__ TensorConsts<TQ> c;
-  load_consts(gc, &c);
+__global__ void __launch_bounds__(256, 2) k_tensor_lift(const TQ* in, uint32_t* out,
+                                                     const __grid_constant__ TensorConsts<TQ> c, uint32_t n,
+                                                     uint64_t total) {
   const int L = LC ? LC : c.L, K = KC ? KC : c.K;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t poly = g / n, i = g % n;   // poly = b * 2 + part
@@ -267,10 +267,9 @@ static cudaError_t launch_tensor_product(const Ctx* c, const uint32_t* a, const 
 // ----------------------------------------------------------------------------- 3 round
 // H: [B][3][K][N] -> out [B][3][L][N] (TQ): round(h t / Q) mod Q.
 template <typename TQ, int LC, int KC, int K2C>
-__global__ void __launch_bounds__(256, 2) k_tensor_round(const uint32_t* H, TQ* out, const TensorConsts<TQ>* gc,
-                                                      uint32_t n, uint64_t total) {
-  __shared__ TensorConsts<TQ> c;
-  load_consts(gc, &c);
+__global__ void __launch_bounds__(256, 2) k_tensor_round(const uint32_t* H, TQ* out,
+                                                      const __grid_constant__ TensorConsts<TQ> c, uint32_t n,
+                                                      uint64_t total) {
   const int L = LC ? LC : c.L, K = KC ? KC : c.K, K2 = K2C ? K2C : c.K2;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t poly = g / n, i = g % n;   // poly = b * 3 + part
@@ -371,7 +370,7 @@ __global__ void __launch_bounds__(256) k_relin_digits(const TQ* ct3, uint32_t* d
 template <typename T, int LOGN, bool SMEM_TW>
 __global__ void __launch_bounds__(NttShape<LOGN>::THREADS, (NttShape<LOGN>::THREADS == 256 && sizeof(T) == 4) ? 3
                                                                 : NttShape<LOGN>::MINB)
-k_relin_accum(const T* ct3, const uint32_t* digits, const T* keyprep, T* out,
+k_relin_accum(const T* ct3, int ct_parts, const uint32_t* digits, const T* keyprep, T* out,
               const PrimeTab<T>* __restrict__ tabs, int L, int D, uint32_t batch) {
   using Sh = NttShape<LOGN>;
   constexpr int TW_WORDS = SMEM_TW ? 2 * shape_tw_entries(LOGN) : 0;
@@ -404,7 +403,7 @@ k_relin_accum(const T* ct3, const uint32_t* digits, const T* keyprep, T* out,
     for (int d = 0; d < D; ++d) {
       const uint32_t* src = digits + ((size_t)b * D + d) * N + cb;
 #pragma unroll
-      for (int j = 0; j < Sh::E; ++j) x[j] = csub((T)__ldg(src + coef_off<LOGN>(j)), pr.p);  // digit < 2^w < 2p
+      for (int j = 0; j < Sh::E; ++j) x[j] = pr.reduce_digit(__ldg(src + coef_off<LOGN>(j)));  // any u32 -> [0,p)
       ntt_fwd_regs<T, LOGN, 0, SMEM_TW, 1, 1>(x, ex, tw, pr.p, pr.p2);
       const T* kb = keyprep + (((size_t)d * 2 + 0) * L + limb) * N;
       const T* ka = keyprep + (((size_t)d * 2 + 1) * L + limb) * N;
@@ -426,7 +425,7 @@ k_relin_accum(const T* ct3, const uint32_t* digits, const T* keyprep, T* out,
 #pragma unroll
       for (int j = 0; j < Sh::E; ++j) x[j] = part == 0 ? acc0[j] : acc1[j];
       ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1>(x, ex, tw, pr.p, pr.p2);
-      const size_t off = ((b * 3 + part) * L + limb) * N + cb;
+      const size_t off = (((size_t)b * ct_parts + part) * L + limb) * N + cb;
       const size_t oo = ((b * 2 + part) * L + limb) * N + cb;
 #pragma unroll
       for (int j = 0; j < Sh::E; ++j) out[oo + coef_off<LOGN>(j)] = add_mod(csub(x[j], pr.p), ct3[off + coef_off<LOGN>(j)], pr.p);
@@ -435,8 +434,8 @@ k_relin_accum(const T* ct3, const uint32_t* digits, const T* keyprep, T* out,
 }
 
 template <typename T, int LOGN>
-static cudaError_t launch_relin_accum(const Ctx* c, const void* ct3, const uint32_t* digits, const void* keyprep,
-                                      void* out, uint64_t batch, int D, cudaStream_t s) {
+static cudaError_t launch_relin_accum(const Ctx* c, const void* ct3, int ct_parts, const uint32_t* digits,
+                                      const void* keyprep, void* out, uint64_t batch, int D, cudaStream_t s) {
   using Sh = NttShape<LOGN>;
   const Base& B = c->base[BASE_Q];
   constexpr size_t tw_bytes = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
@@ -448,8 +447,149 @@ static cudaError_t launch_relin_accum(const Ctx* c, const void* ct3, const uint3
   if (batch == 0) return cudaSuccess;
   uint32_t grid = persistent_grid((const void*)kern, Sh::THREADS, smem);
   grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(grid / L * L, (uint64_t)L), batch * (uint64_t)L);
-  return launch_kernel_grid(kern, grid, Sh::THREADS, smem, s, (const T*)ct3, digits, (const T*)keyprep, (T*)out,
-                            (const PrimeTab<T>*)B.d_tabs, L, D, (uint32_t)batch);
+  return launch_kernel_grid(kern, grid, Sh::THREADS, smem, s, (const T*)ct3, ct_parts, digits, (const T*)keyprep,
+                            (T*)out, (const PrimeTab<T>*)B.d_tabs, L, D, (uint32_t)batch);
+}
+
+// ----------------------------------------------------------------------------- 6 fused site sums
+// Offline mask products / protocol-b slots (linprot.py:407-427, :371-379): for every output
+// slot o, sum over its sites s of relinearize(cc_mul_raw(x[xs], w[ws])).  Exact reorganisation:
+//  * each distinct ciphertext is lifted to the aux base and forward-transformed ONCE
+//    (x prepared, w canonical), not once per site;
+//  * per site only the three eval-domain tensor products and three inverse transforms
+//    (k_site_product) and the exact rounding (k_tensor_round) remain;
+//  * relinearisation is linear in the digits: sum_s relin(c_s) = (sum c0_s + sum_i (sum_s d_i,s) b_i,
+//    sum c1_s + sum_i (sum_s d_i,s) a_i) mod q, so the digits and (c0, c1) are summed per slot
+//    (k_slot_digits) and relinearised once per SLOT (k_relin_accum).
+
+// AX [*][2][K][N] prepared eval, AW [*][2][K][N] canonical eval (aux base) -> H [nsite][3][K][N].
+template <int LOGN, bool SMEM_TW>
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
+k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict__ sx,
+               const int32_t* __restrict__ sw, uint32_t* H, const PrimeTab<uint32_t>* __restrict__ tabs, int K,
+               uint32_t nsite) {
+  using Sh = NttShape<LOGN>;
+  using T = uint32_t;
+  constexpr int TW_WORDS = SMEM_TW ? 2 * shape_tw_entries(LOGN) : 0;
+  using Ex = Exchanger<T, LOGN, 1, 1>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* tw_sm = reinterpret_cast<T*>(smem_raw);
+  Ex ex{tw_sm + TW_WORDS};
+  T* strip = tw_sm + TW_WORDS + Ex::WORDS + threadIdx.x;  // 2 thread-private polys (h1, h0)
+  const int k = blockIdx.x % K;
+  const uint32_t slot = blockIdx.x / K;
+  const uint32_t nslots = (gridDim.x - k + K - 1) / K;
+  PrimeRegs<T> pr(tabs + k);
+  const T* twp = pr.fwd;
+  if constexpr (SMEM_TW) {
+    const uint4* src = reinterpret_cast<const uint4*>(pr.fwd);
+    uint4* dst = reinterpret_cast<uint4*>(tw_sm);
+    for (int i = threadIdx.x; i < TW_WORDS * 4 / 16; i += Sh::THREADS) dst[i] = __ldg(src + i);
+    __syncthreads();
+    twp = tw_sm;
+  }
+  const TwSrc<T, SMEM_TW> tw{twp};
+  const size_t N = Sh::N, KN = (size_t)K * N;
+  using EV = EvalVec<T, LOGN>;
+  T y[Sh::E];
+#pragma unroll 1
+  for (uint32_t s = slot; s < nsite; s += nslots) {
+    const T* a0p = AX + (size_t)sx[s] * 2 * KN + k * N;
+    const T* b0p = AW + (size_t)sw[s] * 2 * KN + k * N;
+#pragma unroll
+    for (int i = 0; i < EV::CHUNKS; ++i) {
+      T a0[EV::VEC], a1[EV::VEC], b0[EV::VEC], b1[EV::VEC];
+      EV::load(a0p, i, a0);
+      EV::load(a0p + KN, i, a1);
+      EV::load(b0p, i, b0);
+      EV::load(b0p + KN, i, b1);
+#pragma unroll
+      for (int c = 0; c < EV::VEC; ++c) {
+        const int j = i * EV::VEC + c;
+        y[j] = mont_mul(a1[c], b1[c], pr.p, pr.pinv);                                        // h2
+        strip[(0 * Sh::E + j) * Sh::THREADS] =
+            csub(mont_mul(a0[c], b1[c], pr.p, pr.pinv) + mont_mul(a1[c], b0[c], pr.p, pr.pinv), pr.p2);  // h1
+        strip[(1 * Sh::E + j) * Sh::THREADS] = mont_mul(a0[c], b0[c], pr.p, pr.pinv);        // h0
+      }
+    }
+#pragma unroll 1
+    for (int part = 2; part >= 0; --part) {
+      if (part < 2) {
+#pragma unroll
+        for (int j = 0; j < Sh::E; ++j) y[j] = strip[((1 - part) * Sh::E + j) * Sh::THREADS];
+      }
+      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1>(y, ex, tw, pr.p, pr.p2);
+      T* dst = H + ((size_t)s * 3 + part) * KN + k * N + coef_base<LOGN>();
+#pragma unroll
+      for (int j = 0; j < Sh::E; ++j) dst[coef_off<LOGN>(j)] = csub(y[j], pr.p);
+    }
+  }
+}
+
+template <int LOGN>
+static cudaError_t launch_site_product(const Ctx* c, const uint32_t* ax, const uint32_t* aw, const int32_t* sx,
+                                       const int32_t* sw, uint32_t* h, uint64_t nsite, cudaStream_t s) {
+  using Sh = NttShape<LOGN>;
+  const Base& B = c->base[BASE_B];
+  using T = uint32_t;
+  constexpr size_t tw_bytes = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
+  constexpr size_t base_bytes = ((size_t)Exchanger<T, LOGN, 1, 1>::WORDS + 2 * (size_t)Sh::N) * sizeof(T);
+  constexpr bool SMEM_TW = LOGN >= 9 && tw_bytes + base_bytes <= 200 * 1024;
+  auto kern = k_site_product<LOGN, SMEM_TW>;
+  const size_t smem = base_bytes + (SMEM_TW ? tw_bytes : 0);
+  const int K = B.size();
+  if (nsite == 0) return cudaSuccess;
+  uint32_t grid = persistent_grid((const void*)kern, Sh::THREADS, smem);
+  grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(grid / K * K, (uint64_t)K), nsite * (uint64_t)K);
+  return launch_kernel_grid(kern, grid, Sh::THREADS, smem, s, ax, aw, sx, sw, h, (const PrimeTab<T>*)B.d_tabs, K,
+                            (uint32_t)nsite);
+}
+
+// Per (slot, coefficient): over the slot's sites (contiguous in ct3, rows ptr[o]-base ..
+// ptr[o+1]-base): C01[o] = sum (c0, c1) mod q_i, DS[o][j] = sum of the w-bit digits of c2
+// (plain u32 sums: fewer than 2^(32-w) sites per slot, checked by the host).
+template <typename TQ>
+__global__ void __launch_bounds__(256) k_slot_digits(const TQ* ct3, const int32_t* __restrict__ ptr, int32_t base,
+                                                     TQ* c01, uint32_t* ds, const TensorConsts<TQ>* gc, uint32_t n,
+                                                     uint64_t total) {
+  __shared__ MrcTab<TQ> m;
+  __shared__ int meta[4];
+  load_consts(&gc->mrcQ, &m);
+  if (threadIdx.x == 0) { meta[0] = gc->relin_w; meta[1] = gc->relin_d; meta[2] = gc->qwords; }
+  __syncthreads();
+  const int L = m.L, w = meta[0], D = meta[1], words = meta[2];
+  const uint32_t mask = (w >= 32) ? 0xffffffffu : ((1u << w) - 1u);
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t o = g / n, i = g % n;
+    const int s0 = ptr[o] - base, s1 = ptr[o + 1] - base;
+    TQ acc0[MAXQ], acc1[MAXQ];
+    uint32_t dsum[24];
+    for (int l = 0; l < L; ++l) acc0[l] = acc1[l] = 0;
+    for (int j = 0; j < D; ++j) dsum[j] = 0;
+    for (int s = s0; s < s1; ++s) {
+      TQ r[MAXQ], a[MAXQ];
+      for (int l = 0; l < L; ++l) {
+        const TQ q = m.q[l];
+        acc0[l] = add_mod(acc0[l], ct3[(((uint64_t)s * 3 + 0) * L + l) * n + i], q);
+        acc1[l] = add_mod(acc1[l], ct3[(((uint64_t)s * 3 + 1) * L + l) * n + i], q);
+        r[l] = ct3[(((uint64_t)s * 3 + 2) * L + l) * n + i];
+      }
+      mrc_digits<TQ>(m, r, a);
+      uint32_t X[20];
+      mrc_positional(m, a, X, words);
+      for (int j = 0; j < D; ++j) {
+        const int bit = j * w, wi = bit >> 5, sh = bit & 31;
+        uint64_t v = (uint64_t)X[wi] >> sh;
+        if (sh + w > 32 && wi + 1 < words) v |= (uint64_t)X[wi + 1] << (32 - sh);
+        dsum[j] += (uint32_t)v & mask;
+      }
+    }
+    for (int l = 0; l < L; ++l) {
+      c01[((o * 2 + 0) * L + l) * n + i] = acc0[l];
+      c01[((o * 2 + 1) * L + l) * n + i] = acc1[l];
+    }
+    for (int j = 0; j < D; ++j) ds[(o * D + j) * n + i] = dsum[j];
+  }
 }
 
 // ----------------------------------------------------------------------------- host constants
@@ -591,6 +731,7 @@ static int build_tensor(Ctx* c, std::string& err) {
   st->K = h->K; st->K2 = h->K2; st->L = L;
   st->q_lead = q_in && (int)aux.size() == L + (int)p2.size();
   for (int k = 0; st->q_lead && k < (int)p2.size(); ++k) st->q_lead = h->p2_idx[k] == L + k;
+  st->host.assign(reinterpret_cast<const unsigned char*>(h), reinterpret_cast<const unsigned char*>(h) + sizeof(TensorConsts<TQ>));
   cudaError_t ce = cudaMalloc(&st->d_consts, sizeof(TensorConsts<TQ>));
   if (ce == cudaSuccess) ce = cudaMemcpy(st->d_consts, h, sizeof(TensorConsts<TQ>), cudaMemcpyHostToDevice);
   delete h;
@@ -642,11 +783,11 @@ extern "C" int ctb_tensor_lift(const ctb_ctx_t* ctx, const void* ct, uint32_t* o
   const int L = c->tensor->L, K = c->tensor->K;
   const unsigned grid = grid_pc(total);
   if (c->base[BASE_Q].word == 4) {
-    const auto* tc = (const TensorConsts<uint32_t>*)c->tensor->d_consts;
+    const auto& tc = *reinterpret_cast<const TensorConsts<uint32_t>*>(c->tensor->host.data());
     if (L == 7 && K == 17) k_tensor_lift<uint32_t, 7, 17><<<grid, 256, 0, s>>>((const uint32_t*)ct, out, tc, c->n, total);
     else k_tensor_lift<uint32_t, 0, 0><<<grid, 256, 0, s>>>((const uint32_t*)ct, out, tc, c->n, total);
   } else {
-    const auto* tc = (const TensorConsts<uint64_t>*)c->tensor->d_consts;
+    const auto& tc = *reinterpret_cast<const TensorConsts<uint64_t>*>(c->tensor->host.data());
     if (L == 3 && K == 11) k_tensor_lift<uint64_t, 3, 11><<<grid, 256, 0, s>>>((const uint64_t*)ct, out, tc, c->n, total);
     else k_tensor_lift<uint64_t, 0, 0><<<grid, 256, 0, s>>>((const uint64_t*)ct, out, tc, c->n, total);
   }
@@ -678,12 +819,12 @@ extern "C" int ctb_tensor_round(const ctb_ctx_t* ctx, const uint32_t* h_aux, voi
   const int L = c->tensor->L, K = c->tensor->K, K2 = c->tensor->K2;
   const unsigned grid = grid_pc(total);
   if (c->base[BASE_Q].word == 4) {
-    const auto* tc = (const TensorConsts<uint32_t>*)c->tensor->d_consts;
+    const auto& tc = *reinterpret_cast<const TensorConsts<uint32_t>*>(c->tensor->host.data());
     if (L == 7 && K == 17 && K2 == 10 && c->tensor->q_lead)
       k_tensor_round<uint32_t, 7, 17, 10><<<grid, 256, 0, s>>>(h_aux, (uint32_t*)out, tc, c->n, total);
     else k_tensor_round<uint32_t, 0, 0, 0><<<grid, 256, 0, s>>>(h_aux, (uint32_t*)out, tc, c->n, total);
   } else {
-    const auto* tc = (const TensorConsts<uint64_t>*)c->tensor->d_consts;
+    const auto& tc = *reinterpret_cast<const TensorConsts<uint64_t>*>(c->tensor->host.data());
     if (L == 3 && K == 11 && K2 == 7)
       k_tensor_round<uint64_t, 3, 11, 7><<<grid, 256, 0, s>>>(h_aux, (uint64_t*)out, tc, c->n, total);
     else k_tensor_round<uint64_t, 0, 0, 0><<<grid, 256, 0, s>>>(h_aux, (uint64_t*)out, tc, c->n, total);
@@ -742,14 +883,151 @@ extern "C" int ctb_relinearize(const ctb_ctx_t* ctx, const void* ct3, const void
                                                      (const TensorConsts<T>*)c->tensor->d_consts, c->n, total);
     e = cudaGetLastError();
     if (e == cudaSuccess)
-      CTB_DISPATCH_LOGN(c->logn, e = (launch_relin_accum<T, LOGN>(c, ct3, digits_ws, keyprep, out, batch, D, s)));
+      CTB_DISPATCH_LOGN(c->logn, e = (launch_relin_accum<T, LOGN>(c, ct3, 3, digits_ws, keyprep, out, batch, D, s)));
   } else {
     using T = uint64_t;
     k_relin_digits<T><<<grid_pc(total), 256, 0, s>>>((const T*)ct3, digits_ws,
                                                      (const TensorConsts<T>*)c->tensor->d_consts, c->n, total);
     e = cudaGetLastError();
     if (e == cudaSuccess)
-      CTB_DISPATCH_LOGN(c->logn, e = (launch_relin_accum<T, LOGN>(c, ct3, digits_ws, keyprep, out, batch, D, s)));
+      CTB_DISPATCH_LOGN(c->logn, e = (launch_relin_accum<T, LOGN>(c, ct3, 3, digits_ws, keyprep, out, batch, D, s)));
   }
   return cuda_status(e, "ctb_relinearize");
+}
+
+// ----------------------------------------------------------------------------- fused site sums (C ABI)
+namespace {
+constexpr uint64_t kSiteChunkBytes = 1ull << 30;  // H workspace budget per chunk
+
+size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct SumLayout {
+  size_t ax, aw, h, ct3, c01, ds, csr, total;
+  uint64_t chunk;
+};
+
+SumLayout sum_layout(const Ctx* c, uint32_t n_x, uint32_t n_w, uint32_t n_out, uint32_t n_sites, uint32_t max_slot) {
+  SumLayout l{};
+  const size_t N = c->n, K = c->tensor->K, L = c->tensor->L, w = c->base[BASE_Q].word;
+  const size_t D = (size_t)ctb_relin_digit_count(reinterpret_cast<const ctb_ctx_t*>(c));
+  uint64_t chunk = std::max<uint64_t>(1, kSiteChunkBytes / (3 * K * N * 4));
+  chunk = std::max<uint64_t>(chunk, max_slot);
+  chunk = std::min<uint64_t>(chunk, std::max<uint32_t>(n_sites, 1));
+  l.chunk = chunk;
+  l.ax = al256((size_t)n_x * 2 * K * N * 4);
+  l.aw = al256((size_t)n_w * 2 * K * N * 4);
+  l.h = al256(chunk * 3 * K * N * 4);
+  l.ct3 = al256(chunk * 3 * L * N * w);
+  l.c01 = al256(chunk * 2 * L * N * w);
+  l.ds = al256(chunk * D * N * 4);
+  l.csr = al256(((size_t)n_out + 1 + 2 * (size_t)n_sites) * 4);
+  l.total = l.ax + l.aw + l.h + l.ct3 + l.c01 + l.ds + l.csr;
+  return l;
+}
+}  // namespace
+
+extern "C" uint64_t ctb_ccmul_sum_workspace_bytes(const ctb_ctx_t* ctx, uint32_t n_x, uint32_t n_w, uint32_t n_out,
+                                                  uint32_t n_sites, uint32_t max_slot_sites) {
+  const Ctx* c;
+  if (ensure_tensor(ctx, c)) return 0;
+  return sum_layout(c, n_x, n_w, n_out, n_sites, max_slot_sites).total;
+}
+
+extern "C" int ctb_ccmul_sum(const ctb_ctx_t* ctx, const void* ct_x, uint32_t n_x, const void* ct_w, uint32_t n_w,
+                             const uint32_t* sites_host, uint32_t n_sites, uint32_t n_out, const void* keyprep,
+                             void* out, void* workspace, uint64_t workspace_bytes, void* stream) {
+  if (n_out == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
+  const Ctx* c;
+  int rc = ensure_tensor(ctx, c);
+  if (rc) return rc;
+  if (!ct_x || !ct_w || (n_sites && !sites_host) || !keyprep || !out || !workspace) {
+    set_error("ctb_ccmul_sum: null buffer");
+    return ERR_ARG;
+  }
+  if (c->relin_base_bits < 1 || c->relin_base_bits > 29) { set_error("relinearisation base must be 1..29 bits"); return ERR_UNSUPPORTED; }
+  const Base& B = c->base[BASE_Q];
+  const size_t N = c->n, L = B.size(), w = B.word, K = c->tensor->K;
+  const int D = ctb_relin_digit_count(ctx);
+  // CSR by output slot, reference site order kept within a slot
+  std::vector<int32_t> ptr(n_out + 1, 0), sx(n_sites), sw(n_sites);
+  for (uint32_t s = 0; s < n_sites; ++s) {
+    const uint32_t xi = sites_host[3 * s], wi = sites_host[3 * s + 1], oi = sites_host[3 * s + 2];
+    if (xi >= n_x || wi >= n_w || oi >= n_out) { set_error("ctb_ccmul_sum: site index out of range"); return ERR_ARG; }
+    ptr[oi + 1]++;
+  }
+  uint32_t max_slot = 0;
+  for (uint32_t o = 0; o < n_out; ++o) max_slot = std::max<uint32_t>(max_slot, ptr[o + 1]);
+  if ((uint64_t)max_slot * ((1ull << c->relin_base_bits) - 1) >= (1ull << 32)) {
+    set_error("ctb_ccmul_sum: too many sites in one output slot for 32-bit digit sums");
+    return ERR_UNSUPPORTED;
+  }
+  for (uint32_t o = 0; o < n_out; ++o) ptr[o + 1] += ptr[o];
+  {
+    std::vector<int32_t> fill(ptr.begin(), ptr.end() - 1);
+    for (uint32_t s = 0; s < n_sites; ++s) {
+      const int32_t pos = fill[sites_host[3 * s + 2]]++;
+      sx[pos] = (int32_t)sites_host[3 * s];
+      sw[pos] = (int32_t)sites_host[3 * s + 1];
+    }
+  }
+  const SumLayout lay = sum_layout(c, n_x, n_w, n_out, n_sites, max_slot);
+  if (workspace_bytes < lay.total) { set_error("ctb_ccmul_sum: workspace too small"); return ERR_ARG; }
+  char* ws = (char*)workspace;
+  uint32_t* AX = (uint32_t*)ws; ws += lay.ax;
+  uint32_t* AW = (uint32_t*)ws; ws += lay.aw;
+  uint32_t* H = (uint32_t*)ws; ws += lay.h;
+  void* CT3 = ws; ws += lay.ct3;
+  void* C01 = ws; ws += lay.c01;
+  uint32_t* DS = (uint32_t*)ws; ws += lay.ds;
+  int32_t* csr = (int32_t*)ws;
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<int32_t> packed(n_out + 1 + 2 * (size_t)n_sites);
+  std::copy(ptr.begin(), ptr.end(), packed.begin());
+  std::copy(sx.begin(), sx.end(), packed.begin() + n_out + 1);
+  std::copy(sw.begin(), sw.end(), packed.begin() + n_out + 1 + n_sites);
+  cudaError_t e = cudaMemcpyAsync(csr, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // the host vector dies at return
+  if (e != cudaSuccess) return cuda_status(e, "ctb_ccmul_sum csr");
+  const int32_t* d_ptr = csr;
+  const int32_t* d_sx = csr + n_out + 1;
+  const int32_t* d_sw = d_sx + n_sites;
+  // every distinct ciphertext: centred lift to the aux base, forward transform once
+  if ((rc = ctb_tensor_lift(ctx, ct_x, AX, n_x, stream))) return rc;
+  if ((rc = ctb_tensor_lift(ctx, ct_w, AW, n_w, stream))) return rc;
+  if ((e = stream_forward(c, BASE_B, true, AX, AX, (uint64_t)n_x * 2, s)) != cudaSuccess) return cuda_status(e, "ctb_ccmul_sum ntt");
+  if ((e = stream_forward(c, BASE_B, false, AW, AW, (uint64_t)n_w * 2, s)) != cudaSuccess) return cuda_status(e, "ctb_ccmul_sum ntt");
+  // chunks of whole slots
+  uint32_t o0 = 0;
+  while (o0 < n_out) {
+    uint32_t o1 = o0 + 1;
+    while (o1 < n_out && (uint64_t)(ptr[o1 + 1] - ptr[o0]) <= lay.chunk) ++o1;
+    const int32_t s0 = ptr[o0], ns = ptr[o1] - ptr[o0];
+    const uint32_t nslot = o1 - o0;
+    if (ns > 0) {
+      CTB_DISPATCH_LOGN(c->logn, e = (launch_site_product<LOGN>(c, AX, AW, d_sx + s0, d_sw + s0, H, (uint64_t)ns, s)));
+      if (e != cudaSuccess) return cuda_status(e, "ctb_ccmul_sum product");
+      if ((rc = ctb_tensor_round(ctx, H, CT3, (uint64_t)ns, stream))) return rc;
+    }
+    const uint64_t total = (uint64_t)nslot * N;
+    if (w == 4)
+      k_slot_digits<uint32_t><<<grid_pc(total), 256, 0, s>>>((const uint32_t*)CT3, d_ptr + o0, s0, (uint32_t*)C01, DS,
+                                                            (const TensorConsts<uint32_t>*)c->tensor->d_consts,
+                                                            (uint32_t)N, total);
+    else
+      k_slot_digits<uint64_t><<<grid_pc(total), 256, 0, s>>>((const uint64_t*)CT3, d_ptr + o0, s0, (uint64_t*)C01, DS,
+                                                            (const TensorConsts<uint64_t>*)c->tensor->d_consts,
+                                                            (uint32_t)N, total);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_status(e, "ctb_ccmul_sum digits");
+    char* o_ptr = (char*)out + (size_t)o0 * 2 * L * N * w;
+    if (w == 4) {
+      CTB_DISPATCH_LOGN(c->logn, e = (launch_relin_accum<uint32_t, LOGN>(c, C01, 2, DS, keyprep, o_ptr, nslot, D, s)));
+    } else {
+      CTB_DISPATCH_LOGN(c->logn, e = (launch_relin_accum<uint64_t, LOGN>(c, C01, 2, DS, keyprep, o_ptr, nslot, D, s)));
+    }
+    if (e != cudaSuccess) return cuda_status(e, "ctb_ccmul_sum relin");
+    o0 = o1;
+  }
+  (void)K;
+  return OK;
 }

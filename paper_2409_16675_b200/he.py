@@ -418,10 +418,17 @@ class He:
                 f"noise estimate 2^{nu.bit_length()} is at or above "
                 f"the budget 2^{self.params.noise_budget.bit_length()}"
             )
-        d = batch.data
-        acc = self._mul_prepared(d[:, 1].contiguous(), self._s_prep(keys, 1), d[:, 0].contiguous())
+        d = batch.data.contiguous()
+        B, P = d.shape[0], d.shape[1]
+        acc = torch.empty((B, self.L, self.params.n), dtype=d.dtype, device="cuda")
+        # c0 + c1 s (+ c2 s^2) read in place from the [B][parts][L][N] batch (strided operands)
+        _lib.check(self.ctx._lib.ctb_mul_prepared_strided(self.ctx._h, BASE_Q, _ptr(d[:, 1]), P,
+                                                          _ptr(self._s_prep(keys, 1)), 0, _ptr(d[:, 0]), P,
+                                                          _ptr(acc), B, _stream()), "ctb_mul_prepared_strided")
         if batch.nparts == 3:
-            acc = self._mul_prepared(d[:, 2].contiguous(), self._s_prep(keys, 2), acc)
+            _lib.check(self.ctx._lib.ctb_mul_prepared_strided(self.ctx._h, BASE_Q, _ptr(d[:, 2]), P,
+                                                              _ptr(self._s_prep(keys, 2)), 0, _ptr(acc), 1,
+                                                              _ptr(acc), B, _stream()), "ctb_mul_prepared_strided")
         out = torch.empty((len(batch), self.params.n), dtype=torch.int64, device="cuda")
         _lib.check(self.ctx._lib.ctb_decrypt_round(self.ctx._h, _ptr(acc), _ptr(out), len(batch), _stream()),
                    "ctb_decrypt_round")
