@@ -63,6 +63,21 @@ struct TensorConsts {
   uint32_t Kh_aux[MAXA];              // floor(M_A/2) mod p_k
   ShoupC<TQ> h_hc[MAXQ][MAXA];        // p_k mod q_i
   TQ Kh_q[MAXQ];                      // floor(M_A/2) mod q_i
+  // lazy (64-bit accumulated) forms, TQ = u32 only
+  uint32_t q_r2[MAXQ], q_r2q[MAXQ];   // 2^32 mod q_i and its Shoup quotient (64-bit reduction)
+  uint32_t gM[MAXQ][MAXQ];            // gM[j][i] = M_i mod q_j, M_i = q_0 ... q_{i-1}   (Garner)
+  ShoupC<uint32_t> gMinv[MAXQ];       // M_j^-1 mod q_j
+  uint32_t aM[MAXA][MAXQ];            // aM[k][i] = M_i mod p_k (mixed radix of Q -> aux prime)
+  // float-assisted exact CRT extension of a value x' in [M/4, 3M/4) (M = P2, or M_A for ext_h):
+  //   xi_k = x'_k (M/p_k)^-1 mod p_k ; v = floor(sum xi_k / p_k) ; x' = sum xi_k (M/p_k) - v M
+  ShoupC<uint32_t> p2_hinv[MAXA];     // (P2/p_k)^-1 mod p_k (P2 index)
+  float p2_rcp[MAXA];                 // 1/p_k
+  ShoupC<TQ> p2_hat_q[MAXQ][MAXA];    // (P2/p_k) mod q_l (Shoup pair; the u32 path uses .w lazily)
+  TQ p2_v_q[MAXQ][MAXA + 1];          // v * P2 mod q_l, v = 0..K2
+  ShoupC<uint32_t> a_hinv[MAXA];      // (M_A/p_k)^-1 mod p_k
+  float a_rcp[MAXA];
+  ShoupC<TQ> a_hat_q[MAXQ][MAXA];     // (M_A/p_k) mod q_l
+  TQ a_v_q[MAXQ][MAXA + 1];           // v * M_A mod q_l
 };
 
 struct TensorState {
@@ -129,6 +144,86 @@ __device__ __forceinline__ uint32_t horner_to_aux(int n_rt, const TQ* dig, const
   return acc;
 }
 
+// ----------------------------------------------------------------------------- lazy RNS helpers
+// Dot products of 30-bit digits with 30-bit constants accumulate exactly in 64 bits
+// (< 2^60 per term, folded every 8 terms) and are reduced once.
+
+// Garner digits over Q (u32 limbs): a_j = (r_j - sum_{i<j} a_i M_i) M_j^-1 mod q_j.
+template <int LC>
+__device__ __forceinline__ void garner_lazy(const TensorConsts<uint32_t>& c, int L, const uint32_t* r, uint32_t* a) {
+  a[0] = r[0];
+#pragma unroll
+  for (int j = 1; j < (LC ? LC : MAXQ); ++j) {
+    if (!LC && j >= L) break;
+    uint64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < j; ++i) s += (uint64_t)a[i] * c.gM[j][i];
+    const uint32_t q = c.mrcQ.q[j];
+    const uint32_t sj = red_u32(s, q, c.mrcQ.one_q[j], c.q_r2[j], c.q_r2q[j]);
+    a[j] = csub(shoup_mul<uint32_t>(sub_mod(r[j], sj, q), c.gMinv[j].w, c.gMinv[j].wq, q), q);
+  }
+}
+
+// x mod aux prime k from the Q mixed-radix digits of x (u32 digits).
+template <typename TQ, int LC>
+__device__ __forceinline__ uint32_t digits_to_aux(const TensorConsts<TQ>& c, int L, int k, const uint32_t* a) {
+  uint64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < (LC ? LC : MAXQ); ++i) {
+    if (!LC && i >= L) break;
+    s += (uint64_t)a[i] * c.aM[k][i];
+  }
+  return red_u32(s, c.ap[k], c.a_oneq[k], c.a_r2[k], c.a_r2q[k]);
+}
+
+// Float-assisted exact CRT: x' in [M/4, 3M/4) given by residues xs[k] modulo n primes
+// p_{idx(k)}; returns x' mod q_l for every l (then minus `shift`).  xi_k = x'_k (M/p_k)^-1,
+// v = floor(sum xi_k / p_k) (the fractional part x'/M is at least 1/4 away from an integer,
+// the float error is < 2^-17), x' = sum xi_k (M/p_k) - v M.
+template <typename TQ, int NC, int LC>
+__device__ __forceinline__ void crt_extend(const TensorConsts<TQ>& c, int n_rt, int L, const uint32_t* xs,
+                                           const ShoupC<uint32_t>* hinv, const float* rcp, const uint32_t* pmod,
+                                           const ShoupC<TQ> (*hat_q)[MAXA], const TQ (*v_q)[MAXA + 1],
+                                           const TQ* shift, TQ* out) {
+  const int n = NC ? NC : n_rt;
+  uint32_t xi[MAXA];
+  float S = 0.f;
+#pragma unroll
+  for (int k = 0; k < (NC ? NC : MAXA); ++k) {
+    if (!NC && k >= n) break;
+    const uint32_t p = pmod[k];
+    xi[k] = csub(shoup_mul<uint32_t>(xs[k], hinv[k].w, hinv[k].wq, p), p);
+    S = fmaf((float)xi[k], rcp[k], S);
+  }
+  const int v = (int)S;
+#pragma unroll
+  for (int l = 0; l < (LC ? LC : MAXQ); ++l) {
+    if (!LC && l >= L) break;
+    const TQ q = c.mrcQ.q[l];
+    TQ x;
+    if constexpr (sizeof(TQ) == 4) {
+      uint64_t acc = 0;
+#pragma unroll
+      for (int k = 0; k < (NC ? NC : MAXA); ++k) {
+        if (!NC && k >= n) break;
+        acc += (uint64_t)xi[k] * hat_q[l][k].w;
+        if ((k & 7) == 7) acc = red_u32(acc, q, c.mrcQ.one_q[l], c.q_r2[l], c.q_r2q[l]);
+      }
+      x = red_u32(acc, q, c.mrcQ.one_q[l], c.q_r2[l], c.q_r2q[l]);
+    } else {
+      TQ acc = 0;  // sum of terms in [0, 2q): < 40 q < 2^56
+#pragma unroll
+      for (int k = 0; k < (NC ? NC : MAXA); ++k) {
+        if (!NC && k >= n) break;
+        acc += shoup_mul<TQ>((TQ)xi[k], hat_q[l][k].w, hat_q[l][k].wq, q);
+      }
+      x = csub(shoup_mul<TQ>(acc, (TQ)1, c.mrcQ.one_q[l], q), q);
+    }
+    x = sub_mod(x, v_q[l][v], q);
+    out[l] = sub_mod(x, shift[l], q);
+  }
+}
+
 // ----------------------------------------------------------------------------- 1 lift
 // in: [B][2][L][N] (TQ) -> out: [B][2][K][N] (u32), centred lifts over the aux base.
 // LC / KC > 0: limb / aux counts fixed at compile time (register-resident digits).
@@ -145,7 +240,8 @@ __global__ void __launch_bounds__(256, 2) k_tensor_lift(const TQ* in, uint32_t* 
       if (!LC && l >= L) break;
       r[l] = in[(poly * L + l) * n + i];
     }
-    mrc_digits<TQ, LC>(c.mrcQ, r, a);
+    if constexpr (sizeof(TQ) == 4) garner_lazy<LC>(c, L, r, a);
+    else mrc_digits<TQ, LC>(c.mrcQ, r, a);
     // x > (Q-1)/2 ?  lexicographic from the most significant digit
     bool neg = false, decided = false;
 #pragma unroll
@@ -161,7 +257,8 @@ __global__ void __launch_bounds__(256, 2) k_tensor_lift(const TQ* in, uint32_t* 
       if (qi >= 0) {
         v = (uint32_t)r[KC && LC && sizeof(TQ) == 4 && k < LC ? k : qi];  // x == centred value (mod q_i)
       } else {
-        v = horner_to_aux<TQ, LC>(L, a, c.lift_hc[k], c.ap[k], c.a_oneq[k], c.a_r2[k], c.a_r2q[k]);
+        if constexpr (sizeof(TQ) == 4) v = digits_to_aux<TQ, LC>(c, L, k, a);
+        else v = horner_to_aux<TQ, LC>(L, a, c.lift_hc[k], c.ap[k], c.a_oneq[k], c.a_r2[k], c.a_r2q[k]);
         if (neg) v = sub_mod(v, c.Q_aux[k], c.ap[k]);
       }
       out[(poly * K + k) * n + i] = v;
@@ -282,20 +379,14 @@ __global__ void __launch_bounds__(256, 2) k_tensor_round(const uint32_t* H, TQ* 
     // h mod q_i
     TQ hq[MAXQ];
     if (c.ext_h) {
-      uint32_t hs[MAXA], dig[MAXA];
+      // exact extension A -> Q of h + floor(M_A/2) (in [M_A/4, 3 M_A/4)), then minus floor(M_A/2)
+      uint32_t hs[MAXA];
 #pragma unroll
       for (int k = 0; k < (KC ? KC : MAXA); ++k) {
         if (!KC && k >= K) break;
-        hs[k] = add_mod(h[k], c.Kh_aux[k], c.ap[k]);   // h + floor(M/2) in [0, M)
+        hs[k] = add_mod(h[k], c.Kh_aux[k], c.ap[k]);
       }
-      mrc_digits<uint32_t, KC>(c.mrcA, hs, dig);
-#pragma unroll
-      for (int l = 0; l < (LC ? LC : MAXQ); ++l) {
-        if (!LC && l >= L) break;
-        const TQ q = c.mrcQ.q[l];
-        const TQ v = horner_to_q<TQ, KC>(K, dig, c.h_hc[l], q, c.mrcQ.one_q[l]);
-        hq[l] = sub_mod(v, c.Kh_q[l], q);
-      }
+      crt_extend<TQ, KC, LC>(c, K, L, hs, c.a_hinv, c.a_rcp, c.ap, c.a_hat_q, c.a_v_q, c.Kh_q, hq);
     } else {
 #pragma unroll
       for (int l = 0; l < (LC ? LC : MAXQ); ++l) {
@@ -311,26 +402,30 @@ __global__ void __launch_bounds__(256, 2) k_tensor_round(const uint32_t* H, TQ* 
       const TQ q = c.mrcQ.q[l];
       z[l] = add_mod(csub(shoup_mul<TQ>(hq[l], c.t_q[l].w, c.t_q[l].wq, q), q), c.hQ_q[l], q);
     }
-    mrc_digits<TQ, LC>(c.mrcQ, z, rd);
+    if constexpr (sizeof(TQ) == 4) garner_lazy<LC>(c, L, z, rd);
+    else mrc_digits<TQ, LC>(c.mrcQ, z, rd);
     // y' = (z - r) Q^-1 + floor(P2/2) mod each P2 prime
-    uint32_t ys[MAXA], yd[MAXA];
+    uint32_t ys[MAXA], p2p[MAXA];
 #pragma unroll
     for (int k = 0; k < (K2C ? K2C : MAXA); ++k) {
       if (!K2C && k >= K2) break;
-      const int ai = c.p2_idx[k];
+      const int ai = (KC && LC && sizeof(TQ) == 4) ? LC + k : c.p2_idx[k];
       const uint32_t p = c.ap[ai];
-      const uint32_t zk = add_mod(csub(shoup_mul<uint32_t>(h[KC && LC && sizeof(TQ) == 4 ? LC + k : ai], c.t_aux[ai].w, c.t_aux[ai].wq, p), p), c.hQ_aux[ai], p);
-      const uint32_t rk = horner_to_aux<TQ, LC>(L, rd, c.r_hc[k], p, c.a_oneq[ai], c.a_r2[ai], c.a_r2q[ai]);
-      uint32_t yk = csub(shoup_mul<uint32_t>(sub_mod(zk, rk, p), c.Qinv_p2[k].w, c.Qinv_p2[k].wq, p), p);
+      p2p[k] = p;
+      const uint32_t zk = add_mod(csub(shoup_mul<uint32_t>(h[ai], c.t_aux[ai].w, c.t_aux[ai].wq, p), p), c.hQ_aux[ai], p);
+      uint32_t rk;
+      if constexpr (sizeof(TQ) == 4) rk = digits_to_aux<TQ, LC>(c, L, ai, rd);
+      else rk = horner_to_aux<TQ, LC>(L, rd, c.r_hc[k], p, c.a_oneq[ai], c.a_r2[ai], c.a_r2q[ai]);
+      const uint32_t yk = csub(shoup_mul<uint32_t>(sub_mod(zk, rk, p), c.Qinv_p2[k].w, c.Qinv_p2[k].wq, p), p);
       ys[k] = add_mod(yk, c.Ky_p2[k], p);
     }
-    mrc_digits<uint32_t, K2C>(c.mrcP2, ys, yd);
+    // exact extension P2 -> Q of y' (in [P2/4, 3 P2/4)), minus floor(P2/2)
+    TQ o[MAXQ];
+    crt_extend<TQ, K2C, LC>(c, K2, L, ys, c.p2_hinv, c.p2_rcp, p2p, c.p2_hat_q, c.p2_v_q, c.Ky_q, o);
 #pragma unroll
     for (int l = 0; l < (LC ? LC : MAXQ); ++l) {
       if (!LC && l >= L) break;
-      const TQ q = c.mrcQ.q[l];
-      const TQ v = horner_to_q<TQ, K2C>(K2, yd, c.y_hc[l], q, c.mrcQ.one_q[l]);
-      out[(poly * L + l) * n + i] = sub_mod(v, c.Ky_q[l], q);
+      out[(poly * L + l) * n + i] = o[l];
     }
   }
 }
@@ -648,8 +743,10 @@ static int build_tensor(Ctx* c, std::string& err) {
   BigU hmax = BigU::mul(half1, half1); hmax.mul_small(2 * n);
   BigU ymax = hmax; ymax.mul_small(c->t);
   ymax = big_div(ymax, Q); ymax.add_small(2);
-  BigU need_y = ymax; need_y.mul_small(2); need_y.add_small(1);   // P2 > 2 ymax + 1
-  BigU need_h = hmax; need_h.mul_small(2); need_h.add_small(1);   // M_A > 2 hmax + 1
+  // P2 > 4 (ymax + 1), M_A > 4 (hmax + 1): exactness needs 2x+1; the float-assisted CRT
+  // extensions need the shifted value inside [M/4, 3M/4)
+  BigU need_y = ymax; need_y.add_small(1); need_y.mul_small(4);
+  BigU need_h = hmax; need_h.add_small(1); need_h.mul_small(4);
   const bool q_in = sizeof(TQ) == 4;             // 30-bit cipher primes are themselves aux primes
   std::vector<uint64_t> aux, p2;
   if (q_in) aux = q;
@@ -726,6 +823,37 @@ static int build_tensor(Ctx* c, std::string& err) {
       for (int k = 0; k + 1 < h->K; ++k) h->h_hc[l][k] = spair<TQ>(aux[k] % q[l], q[l]);
       h->Kh_q[l] = (TQ)Kh.mod_small(q[l]);
     }
+  }
+  // lazy forms
+  {
+    std::vector<BigU> M(L + 1, BigU(1));
+    for (int i = 1; i <= L; ++i) { M[i] = M[i - 1]; M[i].mul_small(q[i - 1]); }
+    for (int j = 0; j < L; ++j) {
+      if (sizeof(TQ) == 4) {
+        const uint64_t r2 = (1ull << 32) % q[j];
+        h->q_r2[j] = (uint32_t)r2;
+        h->q_r2q[j] = (uint32_t)((r2 << 32) / q[j]);
+        for (int i = 0; i < j; ++i) h->gM[j][i] = (uint32_t)M[i].mod_small(q[j]);
+        h->gMinv[j] = spair<uint32_t>(invmod(M[j].mod_small(q[j]), q[j]), q[j]);
+      }
+    }
+    for (int k = 0; k < h->K; ++k)
+      for (int i = 0; i < L; ++i) h->aM[k][i] = (uint32_t)M[i].mod_small(aux[k]);
+    auto crt = [&](const std::vector<uint64_t>& ps, const BigU& MM, ShoupC<uint32_t>* hinv, float* rcp,
+                   ShoupC<TQ> (*hat_q)[MAXA], TQ (*v_q)[MAXA + 1]) {
+      for (size_t k = 0; k < ps.size(); ++k) {
+        BigU hat = big_div(MM, BigU(ps[k]));
+        hinv[k] = spair<uint32_t>(invmod(hat.mod_small(ps[k]), ps[k]), ps[k]);
+        rcp[k] = (float)(1.0 / (double)ps[k]);
+        for (int l = 0; l < L; ++l) hat_q[l][k] = spair<TQ>(hat.mod_small(q[l]), q[l]);
+      }
+      for (int l = 0; l < L; ++l) {
+        const uint64_t mq = MM.mod_small(q[l]);
+        for (size_t v = 0; v <= ps.size(); ++v) v_q[l][v] = (TQ)mulmod(v % q[l], mq, q[l]);
+      }
+    };
+    crt(p2, P2, h->p2_hinv, h->p2_rcp, h->p2_hat_q, h->p2_v_q);
+    if (h->ext_h) crt(aux, MA, h->a_hinv, h->a_rcp, h->a_hat_q, h->a_v_q);
   }
   auto* st = new TensorState();
   st->K = h->K; st->K2 = h->K2; st->L = L;
