@@ -37,6 +37,7 @@ namespace ctb {
 
 constexpr int MAXA = 20;  // auxiliary primes
 constexpr int MAXQ = 8;   // cipher primes on the tensoring path
+constexpr int MAXDIG = 32;  // relinearisation digits on the lazy path
 
 template <typename TQ>
 struct TensorConsts {
@@ -78,6 +79,8 @@ struct TensorConsts {
   float a_rcp[MAXA];
   ShoupC<TQ> a_hat_q[MAXQ][MAXA];     // (M_A/p_k) mod q_l
   TQ a_v_q[MAXQ][MAXA + 1];           // v * M_A mod q_l
+  int lazy_digits;                    // u32 limbs and D <= MAXDIG: digits by limb dot products
+  uint32_t dM[MAXQ][MAXDIG];          // dM[i][j] = j-th w-bit limb of M_i
 };
 
 struct TensorState {
@@ -431,29 +434,68 @@ __global__ void __launch_bounds__(256, 2) k_tensor_round(const uint32_t* H, TQ* 
 }
 
 // ----------------------------------------------------------------------------- 4 relin digits
-// ct3: [B][3][L][N] -> digits [B][D][N] (u32 < 2^w), d_j = (c2 >> w j) & (2^w - 1).
-template <typename TQ>
-__global__ void __launch_bounds__(256) k_relin_digits(const TQ* ct3, uint32_t* digits, const TensorConsts<TQ>* gc,
-                                                      uint32_t n, uint64_t total) {
-  __shared__ MrcTab<TQ> m;
-  __shared__ int meta[4];
-  load_consts(&gc->mrcQ, &m);
-  if (threadIdx.x == 0) { meta[0] = gc->relin_w; meta[1] = gc->relin_d; meta[2] = gc->qwords; }
-  __syncthreads();
-  const int L = m.L, w = meta[0], D = meta[1], words = meta[2];
+// w-bit digits of x in [0, Q) given by residues r (he.py:420-424 on the integer c2).
+// u32 limbs: Garner digits a_i, then X = sum a_i M_i limb by limb with M_i cut into w-bit
+// limbs (64-bit accumulators, carry between limbs); DC / WC > 0 fix D / w at compile time
+// (limbs of M_i above 2^(30 i) are zero and skipped).  ACC: add into dig[] instead of store.
+template <typename TQ, int LC, int DC, int WC, bool ACC>
+__device__ __forceinline__ void value_digits(const TensorConsts<TQ>& c, const TQ* r, uint32_t* dig) {
+  const int L = LC ? LC : c.L, D = DC ? DC : c.relin_d, w = WC ? WC : c.relin_w;
   const uint32_t mask = (w >= 32) ? 0xffffffffu : ((1u << w) - 1u);
+  if constexpr (sizeof(TQ) == 4) {
+    if (c.lazy_digits) {
+      uint32_t a[MAXQ];
+      garner_lazy<LC>(c, L, r, a);
+      uint64_t carry = 0;
+#pragma unroll
+      for (int j = 0; j < (DC ? DC : MAXDIG); ++j) {
+        if (!DC && j >= D) break;
+        uint64_t acc = carry;
+#pragma unroll
+        for (int i = 0; i < (LC ? LC : MAXQ); ++i) {
+          if (!LC && i >= L) break;
+          if (WC && LC && j * WC >= (i ? 30 * i : 1)) continue;  // M_i < 2^(30 i), M_0 = 1: limb j is zero
+          acc += (uint64_t)a[i] * c.dM[i][j];
+        }
+        const uint32_t d = (uint32_t)acc & mask;
+        carry = acc >> w;
+        if (ACC) dig[j] += d; else dig[j] = d;
+      }
+      return;
+    }
+  }
+  TQ a[MAXQ];
+  mrc_digits<TQ>(c.mrcQ, r, a);
+  uint32_t X[20];
+  mrc_positional(c.mrcQ, a, X, c.qwords);
+  for (int j = 0; j < D; ++j) {
+    const int bit = j * w, wi = bit >> 5, sh = bit & 31;
+    uint64_t v = (uint64_t)X[wi] >> sh;
+    if (sh + w > 32 && wi + 1 < c.qwords) v |= (uint64_t)X[wi + 1] << (32 - sh);
+    if (ACC) dig[j] += (uint32_t)v & mask; else dig[j] = (uint32_t)v & mask;
+  }
+}
+
+// ct3: [B][3][L][N] -> digits [B][D][N] (u32 < 2^w), d_j = (c2 >> w j) & (2^w - 1).
+template <typename TQ, int LC, int DC, int WC>
+__global__ void __launch_bounds__(256) k_relin_digits(const TQ* ct3, uint32_t* digits,
+                                                      const __grid_constant__ TensorConsts<TQ> c, uint32_t n,
+                                                      uint64_t total) {
+  const int L = LC ? LC : c.L, D = DC ? DC : c.relin_d;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t b = g / n, i = g % n;
-    TQ r[MAXQ], a[MAXQ];
-    for (int l = 0; l < L; ++l) r[l] = ct3[((b * 3 + 2) * L + l) * n + i];
-    mrc_digits<TQ>(m, r, a);
-    uint32_t X[20];
-    mrc_positional(m, a, X, words);
-    for (int j = 0; j < D; ++j) {
-      const int bit = j * w, wi = bit >> 5, sh = bit & 31;
-      uint64_t v = (uint64_t)X[wi] >> sh;
-      if (sh + w > 32 && wi + 1 < words) v |= (uint64_t)X[wi + 1] << (32 - sh);
-      digits[(b * D + j) * n + i] = (uint32_t)v & mask;
+    TQ r[MAXQ];
+#pragma unroll
+    for (int l = 0; l < (LC ? LC : MAXQ); ++l) {
+      if (!LC && l >= L) break;
+      r[l] = ct3[((b * 3 + 2) * L + l) * n + i];
+    }
+    uint32_t d[MAXDIG];
+    value_digits<TQ, LC, DC, WC, false>(c, r, d);
+#pragma unroll
+    for (int j = 0; j < (DC ? DC : MAXDIG); ++j) {
+      if (!DC && j >= D) break;
+      digits[(b * D + j) * n + i] = d[j];
     }
   }
 }
@@ -643,47 +685,43 @@ static cudaError_t launch_site_product(const Ctx* c, const uint32_t* ax, const u
 // Per (slot, coefficient): over the slot's sites (contiguous in ct3, rows ptr[o]-base ..
 // ptr[o+1]-base): C01[o] = sum (c0, c1) mod q_i, DS[o][j] = sum of the w-bit digits of c2
 // (plain u32 sums: fewer than 2^(32-w) sites per slot, checked by the host).
-template <typename TQ>
+template <typename TQ, int LC, int DC, int WC>
 __global__ void __launch_bounds__(256) k_slot_digits(const TQ* ct3, const int32_t* __restrict__ ptr, int32_t base,
-                                                     TQ* c01, uint32_t* ds, const TensorConsts<TQ>* gc, uint32_t n,
-                                                     uint64_t total) {
-  __shared__ MrcTab<TQ> m;
-  __shared__ int meta[4];
-  load_consts(&gc->mrcQ, &m);
-  if (threadIdx.x == 0) { meta[0] = gc->relin_w; meta[1] = gc->relin_d; meta[2] = gc->qwords; }
-  __syncthreads();
-  const int L = m.L, w = meta[0], D = meta[1], words = meta[2];
-  const uint32_t mask = (w >= 32) ? 0xffffffffu : ((1u << w) - 1u);
+                                                     TQ* c01, uint32_t* ds, const __grid_constant__ TensorConsts<TQ> c,
+                                                     uint32_t n, uint64_t total) {
+  const int L = LC ? LC : c.L, D = DC ? DC : c.relin_d;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t o = g / n, i = g % n;
     const int s0 = ptr[o] - base, s1 = ptr[o + 1] - base;
     TQ acc0[MAXQ], acc1[MAXQ];
-    uint32_t dsum[24];
-    for (int l = 0; l < L; ++l) acc0[l] = acc1[l] = 0;
-    for (int j = 0; j < D; ++j) dsum[j] = 0;
+    uint32_t dsum[MAXDIG];
+#pragma unroll
+    for (int l = 0; l < (LC ? LC : MAXQ); ++l) acc0[l] = acc1[l] = 0;
+#pragma unroll
+    for (int j = 0; j < (DC ? DC : MAXDIG); ++j) dsum[j] = 0;
     for (int s = s0; s < s1; ++s) {
-      TQ r[MAXQ], a[MAXQ];
-      for (int l = 0; l < L; ++l) {
-        const TQ q = m.q[l];
+      TQ r[MAXQ];
+#pragma unroll
+      for (int l = 0; l < (LC ? LC : MAXQ); ++l) {
+        if (!LC && l >= L) break;
+        const TQ q = c.mrcQ.q[l];
         acc0[l] = add_mod(acc0[l], ct3[(((uint64_t)s * 3 + 0) * L + l) * n + i], q);
         acc1[l] = add_mod(acc1[l], ct3[(((uint64_t)s * 3 + 1) * L + l) * n + i], q);
         r[l] = ct3[(((uint64_t)s * 3 + 2) * L + l) * n + i];
       }
-      mrc_digits<TQ>(m, r, a);
-      uint32_t X[20];
-      mrc_positional(m, a, X, words);
-      for (int j = 0; j < D; ++j) {
-        const int bit = j * w, wi = bit >> 5, sh = bit & 31;
-        uint64_t v = (uint64_t)X[wi] >> sh;
-        if (sh + w > 32 && wi + 1 < words) v |= (uint64_t)X[wi + 1] << (32 - sh);
-        dsum[j] += (uint32_t)v & mask;
-      }
+      value_digits<TQ, LC, DC, WC, true>(c, r, dsum);
     }
-    for (int l = 0; l < L; ++l) {
+#pragma unroll
+    for (int l = 0; l < (LC ? LC : MAXQ); ++l) {
+      if (!LC && l >= L) break;
       c01[((o * 2 + 0) * L + l) * n + i] = acc0[l];
       c01[((o * 2 + 1) * L + l) * n + i] = acc1[l];
     }
-    for (int j = 0; j < D; ++j) ds[(o * D + j) * n + i] = dsum[j];
+#pragma unroll
+    for (int j = 0; j < (DC ? DC : MAXDIG); ++j) {
+      if (!DC && j >= D) break;
+      ds[(o * D + j) * n + i] = dsum[j];
+    }
   }
 }
 
@@ -852,6 +890,18 @@ static int build_tensor(Ctx* c, std::string& err) {
         for (size_t v = 0; v <= ps.size(); ++v) v_q[l][v] = (TQ)mulmod(v % q[l], mq, q[l]);
       }
     };
+    h->lazy_digits = sizeof(TQ) == 4 && h->relin_d <= MAXDIG && h->relin_w >= 1 && h->relin_w <= 29;
+    if (h->lazy_digits) {
+      const uint32_t wmask = (1u << h->relin_w) - 1u;
+      for (int i = 0; i < L; ++i) {
+        BigU x = M[i];
+        for (int j = 0; j < h->relin_d; ++j) {
+          const uint64_t lo = x.w.empty() ? 0 : x.w[0];
+          h->dM[i][j] = (uint32_t)lo & wmask;
+          for (int b = 0; b < h->relin_w; ++b) x.shr1();
+        }
+      }
+    }
     crt(p2, P2, h->p2_hinv, h->p2_rcp, h->p2_hat_q, h->p2_v_q);
     if (h->ext_h) crt(aux, MA, h->a_hinv, h->a_rcp, h->a_hat_q, h->a_v_q);
   }
@@ -1005,17 +1055,24 @@ extern "C" int ctb_relinearize(const ctb_ctx_t* ctx, const void* ct3, const void
   if (!total) return OK;
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
+  const auto& st = *c->tensor;
   if (B.word == 4) {
     using T = uint32_t;
-    k_relin_digits<T><<<grid_pc(total), 256, 0, s>>>((const T*)ct3, digits_ws,
-                                                     (const TensorConsts<T>*)c->tensor->d_consts, c->n, total);
+    const auto& tc = *reinterpret_cast<const TensorConsts<T>*>(st.host.data());
+    if (st.L == 7 && D == 14 && c->relin_base_bits == 16 && tc.lazy_digits)
+      k_relin_digits<T, 7, 14, 16><<<grid_pc(total), 256, 0, s>>>((const T*)ct3, digits_ws, tc, c->n, total);
+    else
+      k_relin_digits<T, 0, 0, 0><<<grid_pc(total), 256, 0, s>>>((const T*)ct3, digits_ws, tc, c->n, total);
     e = cudaGetLastError();
     if (e == cudaSuccess)
       CTB_DISPATCH_LOGN(c->logn, e = (launch_relin_accum<T, LOGN>(c, ct3, 3, digits_ws, keyprep, out, batch, D, s)));
   } else {
     using T = uint64_t;
-    k_relin_digits<T><<<grid_pc(total), 256, 0, s>>>((const T*)ct3, digits_ws,
-                                                     (const TensorConsts<T>*)c->tensor->d_consts, c->n, total);
+    const auto& tc = *reinterpret_cast<const TensorConsts<T>*>(st.host.data());
+    if (st.L == 3 && D == 10 && c->relin_base_bits == 16)
+      k_relin_digits<T, 3, 10, 16><<<grid_pc(total), 256, 0, s>>>((const T*)ct3, digits_ws, tc, c->n, total);
+    else
+      k_relin_digits<T, 0, 0, 0><<<grid_pc(total), 256, 0, s>>>((const T*)ct3, digits_ws, tc, c->n, total);
     e = cudaGetLastError();
     if (e == cudaSuccess)
       CTB_DISPATCH_LOGN(c->logn, e = (launch_relin_accum<T, LOGN>(c, ct3, 3, digits_ws, keyprep, out, batch, D, s)));
@@ -1137,14 +1194,23 @@ extern "C" int ctb_ccmul_sum(const ctb_ctx_t* ctx, const void* ct_x, uint32_t n_
       if ((rc = ctb_tensor_round(ctx, H, CT3, (uint64_t)ns, stream))) return rc;
     }
     const uint64_t total = (uint64_t)nslot * N;
-    if (w == 4)
-      k_slot_digits<uint32_t><<<grid_pc(total), 256, 0, s>>>((const uint32_t*)CT3, d_ptr + o0, s0, (uint32_t*)C01, DS,
-                                                            (const TensorConsts<uint32_t>*)c->tensor->d_consts,
-                                                            (uint32_t)N, total);
-    else
-      k_slot_digits<uint64_t><<<grid_pc(total), 256, 0, s>>>((const uint64_t*)CT3, d_ptr + o0, s0, (uint64_t*)C01, DS,
-                                                            (const TensorConsts<uint64_t>*)c->tensor->d_consts,
-                                                            (uint32_t)N, total);
+    if (w == 4) {
+      const auto& tc = *reinterpret_cast<const TensorConsts<uint32_t>*>(c->tensor->host.data());
+      if (L == 7 && D == 14 && c->relin_base_bits == 16 && tc.lazy_digits)
+        k_slot_digits<uint32_t, 7, 14, 16><<<grid_pc(total), 256, 0, s>>>((const uint32_t*)CT3, d_ptr + o0, s0,
+                                                                        (uint32_t*)C01, DS, tc, (uint32_t)N, total);
+      else
+        k_slot_digits<uint32_t, 0, 0, 0><<<grid_pc(total), 256, 0, s>>>((const uint32_t*)CT3, d_ptr + o0, s0,
+                                                                       (uint32_t*)C01, DS, tc, (uint32_t)N, total);
+    } else {
+      const auto& tc = *reinterpret_cast<const TensorConsts<uint64_t>*>(c->tensor->host.data());
+      if (L == 3 && D == 10 && c->relin_base_bits == 16)
+        k_slot_digits<uint64_t, 3, 10, 16><<<grid_pc(total), 256, 0, s>>>((const uint64_t*)CT3, d_ptr + o0, s0,
+                                                                        (uint64_t*)C01, DS, tc, (uint32_t)N, total);
+      else
+        k_slot_digits<uint64_t, 0, 0, 0><<<grid_pc(total), 256, 0, s>>>((const uint64_t*)CT3, d_ptr + o0, s0,
+                                                                       (uint64_t*)C01, DS, tc, (uint32_t)N, total);
+    }
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_status(e, "ctb_ccmul_sum digits");
     char* o_ptr = (char*)out + (size_t)o0 * 2 * L * N * w;
