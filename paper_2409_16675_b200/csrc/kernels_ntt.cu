@@ -419,6 +419,11 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
 #pragma unroll 1
   for (uint32_t b = slot * GROUPS + group; b < batch; b += nslots * GROUPS) {
     const int8_t* d = draws + (size_t)b * 3 * Sh::N + cb;
+    if (ntt_tid<LOGN>() == 0 && b + nslots * GROUPS < batch) {  // next item's inputs towards L2
+      const uint32_t nb = b + nslots * GROUPS;
+      bulk_prefetch_l2(m + (size_t)nb * Sh::N, (uint32_t)(Sh::N * 8));
+      bulk_prefetch_l2(draws + (size_t)nb * 3 * Sh::N, (uint32_t)(Sh::N * 3));
+    }
 #pragma unroll
     for (int k = 0; k < Sh::E; ++k) x[k] = small(__ldg(d + coef_off<LOGN>(k)));
     ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);

@@ -29,6 +29,7 @@
 #include <cstring>
 #include <vector>
 #include "bigint.hpp"
+#include "bulk.cuh"
 #include "ctb200.h"
 #include "kernels.hpp"
 #include "rns.cuh"
@@ -504,17 +505,34 @@ __global__ void __launch_bounds__(256) k_relin_digits(const TQ* ct3, uint32_t* d
 // out [B][2][L][N] = (c0, c1) + sum_j NTT^-1(NTT(d_j) * keyprep[j][0|1]).  Persistent and
 // limb-stationary (CTA k serves limb k % L), the limb's twiddle table staged in shared
 // memory; both accumulators stay in registers across the D digit transforms.
+template <typename T, int LOGN>
+struct RelinCfg {
+  using Sh = NttShape<LOGN>;
+  using Ex = Exchanger<T, LOGN, 1, 1>;
+  static constexpr size_t TW_BYTES = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
+  static constexpr size_t EX_BYTES = ((size_t)Ex::WORDS * sizeof(T) + 15) / 16 * 16;
+  static constexpr bool SMEM_TW = sizeof(T) == 4 && LOGN >= 9 && TW_BYTES + EX_BYTES <= 110 * 1024;
+  // digits (u32 [N]) staged by TMA one transform ahead: measured slower here (an extra CTA
+  // barrier per digit, keys dominate the traffic), kept switchable
+  static constexpr bool PF = false;
+  static constexpr size_t SMEM = (SMEM_TW ? TW_BYTES : 0) + EX_BYTES + (PF ? Sh::N * 4 + 16 : 0);
+  static constexpr int MINB = (Sh::THREADS == 256 && sizeof(T) == 4) ? 3 : Sh::MINB;
+};
+
 template <typename T, int LOGN, bool SMEM_TW>
-__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, (NttShape<LOGN>::THREADS == 256 && sizeof(T) == 4) ? 3
-                                                                : NttShape<LOGN>::MINB)
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, RelinCfg<T, LOGN>::MINB)
 k_relin_accum(const T* ct3, int ct_parts, const uint32_t* digits, const T* keyprep, T* out,
               const PrimeTab<T>* __restrict__ tabs, int L, int D, uint32_t batch) {
   using Sh = NttShape<LOGN>;
+  using C = RelinCfg<T, LOGN>;
+  constexpr bool PF = C::PF;
   constexpr int TW_WORDS = SMEM_TW ? 2 * shape_tw_entries(LOGN) : 0;
-  using Ex = Exchanger<T, LOGN, 1, 1>;
+  using Ex = typename C::Ex;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
   Ex ex{tw_sm + TW_WORDS};
+  uint32_t* stg = reinterpret_cast<uint32_t*>(smem_raw + (SMEM_TW ? C::TW_BYTES : 0) + C::EX_BYTES);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stg + Sh::N);
   const int limb = blockIdx.x % L;
   const uint32_t slot = blockIdx.x / L;
   const uint32_t nslots = (gridDim.x - limb + L - 1) / L;
@@ -525,9 +543,17 @@ k_relin_accum(const T* ct3, int ct_parts, const uint32_t* digits, const T* keypr
     const uint4* src = reinterpret_cast<const uint4*>(pr.fwd);
     uint4* dst = reinterpret_cast<uint4*>(tw_sm);
     for (int i = threadIdx.x; i < TW_WORDS * (int)sizeof(T) / 16; i += Sh::THREADS) dst[i] = __ldg(src + i);
-    __syncthreads();
     twp = tw_sm;
   }
+  uint32_t phase = 0;
+  if constexpr (PF) {
+    if (threadIdx.x == 0) {
+      mbar_init(bar, 1);
+      mbar_init_fence();
+      if (slot < batch) bulk_load(stg, digits + (size_t)slot * D * N, (uint32_t)(N * 4), bar);
+    }
+  }
+  if constexpr (SMEM_TW || PF) __syncthreads();
   const TwSrc<T, SMEM_TW> tw{twp};
   const int cb = coef_base<LOGN>();
   using EV = EvalVec<T, LOGN>;
@@ -538,9 +564,26 @@ k_relin_accum(const T* ct3, int ct_parts, const uint32_t* digits, const T* keypr
     for (int j = 0; j < Sh::E; ++j) acc0[j] = acc1[j] = 0;
 #pragma unroll 1
     for (int d = 0; d < D; ++d) {
-      const uint32_t* src = digits + ((size_t)b * D + d) * N + cb;
+      if constexpr (PF) {
+        mbar_wait(bar, phase);
+        phase ^= 1;
 #pragma unroll
-      for (int j = 0; j < Sh::E; ++j) x[j] = pr.reduce_digit(__ldg(src + coef_off<LOGN>(j)));  // any u32 -> [0,p)
+        for (int j = 0; j < Sh::E; ++j) x[j] = pr.reduce_digit(stg[cb + coef_off<LOGN>(j)]);
+        __syncthreads();  // staging consumed
+        if (threadIdx.x == 0) {
+          // next digit of this item, else the first digit of the next item
+          const uint32_t nb = d + 1 < D ? b : b + nslots;
+          const int nd = d + 1 < D ? d + 1 : 0;
+          if (nb < batch) {
+            fence_proxy_async_smem();
+            bulk_load(stg, digits + ((size_t)nb * D + nd) * N, (uint32_t)(N * 4), bar);
+          }
+        }
+      } else {
+        const uint32_t* src = digits + ((size_t)b * D + d) * N + cb;
+#pragma unroll
+        for (int j = 0; j < Sh::E; ++j) x[j] = pr.reduce_digit(__ldg(src + coef_off<LOGN>(j)));  // any u32 -> [0,p)
+      }
       ntt_fwd_regs<T, LOGN, 0, SMEM_TW, 1, 1>(x, ex, tw, pr.p, pr.p2);
       const T* kb = keyprep + (((size_t)d * 2 + 0) * L + limb) * N;
       const T* ka = keyprep + (((size_t)d * 2 + 1) * L + limb) * N;
@@ -574,17 +617,14 @@ template <typename T, int LOGN>
 static cudaError_t launch_relin_accum(const Ctx* c, const void* ct3, int ct_parts, const uint32_t* digits,
                                       const void* keyprep, void* out, uint64_t batch, int D, cudaStream_t s) {
   using Sh = NttShape<LOGN>;
+  using C = RelinCfg<T, LOGN>;
   const Base& B = c->base[BASE_Q];
-  constexpr size_t tw_bytes = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
-  constexpr size_t ex_bytes = (size_t)Exchanger<T, LOGN, 1, 1>::WORDS * sizeof(T);
-  constexpr bool SMEM_TW = sizeof(T) == 4 && LOGN >= 9 && tw_bytes + ex_bytes <= 110 * 1024;
-  auto kern = k_relin_accum<T, LOGN, SMEM_TW>;
-  const size_t smem = ex_bytes + (SMEM_TW ? tw_bytes : 0);
+  auto kern = k_relin_accum<T, LOGN, C::SMEM_TW>;
   const int L = B.size();
   if (batch == 0) return cudaSuccess;
-  uint32_t grid = persistent_grid((const void*)kern, Sh::THREADS, smem);
+  uint32_t grid = persistent_grid((const void*)kern, Sh::THREADS, C::SMEM);
   grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(grid / L * L, (uint64_t)L), batch * (uint64_t)L);
-  return launch_kernel_grid(kern, grid, Sh::THREADS, smem, s, (const T*)ct3, ct_parts, digits, (const T*)keyprep,
+  return launch_kernel_grid(kern, grid, Sh::THREADS, C::SMEM, s, (const T*)ct3, ct_parts, digits, (const T*)keyprep,
                             (T*)out, (const PrimeTab<T>*)B.d_tabs, L, D, (uint32_t)batch);
 }
 
@@ -633,6 +673,14 @@ k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict
   for (uint32_t s = slot; s < nsite; s += nslots) {
     const T* a0p = AX + (size_t)sx[s] * 2 * KN + k * N;
     const T* b0p = AW + (size_t)sw[s] * 2 * KN + k * N;
+    if (threadIdx.x == 0 && s + nslots < nsite) {  // next item's operands towards L2
+      const T* na = AX + (size_t)sx[s + nslots] * 2 * KN + k * N;
+      const T* nb = AW + (size_t)sw[s + nslots] * 2 * KN + k * N;
+      bulk_prefetch_l2(na, (uint32_t)(N * 4));
+      bulk_prefetch_l2(na + KN, (uint32_t)(N * 4));
+      bulk_prefetch_l2(nb, (uint32_t)(N * 4));
+      bulk_prefetch_l2(nb + KN, (uint32_t)(N * 4));
+    }
 #pragma unroll
     for (int i = 0; i < EV::CHUNKS; ++i) {
       T a0[EV::VEC], a1[EV::VEC], b0[EV::VEC], b1[EV::VEC];

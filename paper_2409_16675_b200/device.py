@@ -150,7 +150,7 @@ class RnsContext:
         check(self._lib.ctb_cpmul(self._h, _ptr(ct), _ptr(pt), _ptr(out), ct.shape[0], _stream()), "ctb_cpmul")
         return out
 
-    def cpmul_host(self, ct_h: torch.Tensor, pt_h: torch.Tensor, out_h: torch.Tensor, chunks: int = 8,
+    def cpmul_host(self, ct_h: torch.Tensor, pt_h: torch.Tensor, out_h: torch.Tensor, chunks: int = 16,
                    slots: int = 3) -> None:
         """CPMul of host-resident (pinned) batches: chunked H2D / k_cpmul / D2H on three
         streams so both copy directions overlap each other and the kernel.  Returns
@@ -165,7 +165,7 @@ class RnsContext:
             self._pipe = [torch.cuda.Stream() for _ in range(3)]
         s_in, s_comp, s_out = self._pipe
         shape_ct = (step,) + tuple(ct_h.shape[1:])
-        key = (shape_ct, ct_h.dtype, pt_h.shape[1:])
+        key = (shape_ct, ct_h.dtype, pt_h.shape[1:], slots)
         if getattr(self, "_pipe_key", None) != key:
             self._pipe_buf = [(torch.empty(shape_ct, dtype=ct_h.dtype, device="cuda"),
                                torch.empty((step,) + tuple(pt_h.shape[1:]), dtype=pt_h.dtype, device="cuda"),
