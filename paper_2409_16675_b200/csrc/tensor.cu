@@ -232,7 +232,7 @@ __device__ __forceinline__ void crt_extend(const TensorConsts<TQ>& c, int n_rt, 
 // in: [B][2][L][N] (TQ) -> out: [B][2][K][N] (u32), centred lifts over the aux base.
 // LC / KC > 0: limb / aux counts fixed at compile time (register-resident digits).
 template <typename TQ, int LC, int KC>
-__global__ void __launch_bounds__(256, 2) k_tensor_lift(const TQ* in, uint32_t* out,
+__global__ void __launch_bounds__(256, 3) k_tensor_lift(const TQ* in, uint32_t* out,
                                                      const __grid_constant__ TensorConsts<TQ> c, uint32_t n,
                                                      uint64_t total) {
   const int L = LC ? LC : c.L, K = KC ? KC : c.K;
@@ -368,7 +368,7 @@ static cudaError_t launch_tensor_product(const Ctx* c, const uint32_t* a, const 
 // ----------------------------------------------------------------------------- 3 round
 // H: [B][3][K][N] -> out [B][3][L][N] (TQ): round(h t / Q) mod Q.
 template <typename TQ, int LC, int KC, int K2C>
-__global__ void __launch_bounds__(256, 2) k_tensor_round(const uint32_t* H, TQ* out,
+__global__ void __launch_bounds__(256, 3) k_tensor_round(const uint32_t* H, TQ* out,
                                                       const __grid_constant__ TensorConsts<TQ> c, uint32_t n,
                                                       uint64_t total) {
   const int L = LC ? LC : c.L, K = KC ? KC : c.K, K2 = K2C ? K2C : c.K2;
@@ -652,7 +652,10 @@ k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
   Ex ex{tw_sm + TW_WORDS};
-  T* strip = tw_sm + TW_WORDS + Ex::WORDS + threadIdx.x;  // 2 thread-private polys (h1, h0)
+  // thread-private strips: h1 (and h0 when two strips: N <= 4096; at N = 8192 h0 is
+  // recomputed from re-read operands, which measured faster than a second strip)
+  constexpr bool TWO = LOGN <= 12;
+  T* strip = tw_sm + TW_WORDS + Ex::WORDS + threadIdx.x;
   const int k = blockIdx.x % K;
   const uint32_t slot = blockIdx.x / K;
   const uint32_t nslots = (gridDim.x - k + K - 1) / K;
@@ -669,6 +672,11 @@ k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict
   const size_t N = Sh::N, KN = (size_t)K * N;
   using EV = EvalVec<T, LOGN>;
   T y[Sh::E];
+  auto store = [&](uint32_t s, int part) {
+    T* dst = H + ((size_t)s * 3 + part) * KN + k * N + coef_base<LOGN>();
+#pragma unroll
+    for (int j = 0; j < Sh::E; ++j) dst[coef_off<LOGN>(j)] = csub(y[j], pr.p);
+  };
 #pragma unroll 1
   for (uint32_t s = slot; s < nsite; s += nslots) {
     const T* a0p = AX + (size_t)sx[s] * 2 * KN + k * N;
@@ -681,6 +689,7 @@ k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict
       bulk_prefetch_l2(nb, (uint32_t)(N * 4));
       bulk_prefetch_l2(nb + KN, (uint32_t)(N * 4));
     }
+    // h2 = a1 b1 (registers), h1 = a0 b1 + a1 b0 (strip)
 #pragma unroll
     for (int i = 0; i < EV::CHUNKS; ++i) {
       T a0[EV::VEC], a1[EV::VEC], b0[EV::VEC], b1[EV::VEC];
@@ -691,23 +700,34 @@ k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict
 #pragma unroll
       for (int c = 0; c < EV::VEC; ++c) {
         const int j = i * EV::VEC + c;
-        y[j] = mont_mul(a1[c], b1[c], pr.p, pr.pinv);                                        // h2
-        strip[(0 * Sh::E + j) * Sh::THREADS] =
-            csub(mont_mul(a0[c], b1[c], pr.p, pr.pinv) + mont_mul(a1[c], b0[c], pr.p, pr.pinv), pr.p2);  // h1
-        strip[(1 * Sh::E + j) * Sh::THREADS] = mont_mul(a0[c], b0[c], pr.p, pr.pinv);        // h0
+        y[j] = mont_mul(a1[c], b1[c], pr.p, pr.pinv);
+        strip[j * Sh::THREADS] =
+            csub(mont_mul(a0[c], b1[c], pr.p, pr.pinv) + mont_mul(a1[c], b0[c], pr.p, pr.pinv), pr.p2);
+        if constexpr (TWO) strip[(Sh::E + j) * Sh::THREADS] = mont_mul(a0[c], b0[c], pr.p, pr.pinv);
       }
     }
-#pragma unroll 1
-    for (int part = 2; part >= 0; --part) {
-      if (part < 2) {
+    ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1>(y, ex, tw, pr.p, pr.p2);
+    store(s, 2);
 #pragma unroll
-        for (int j = 0; j < Sh::E; ++j) y[j] = strip[((1 - part) * Sh::E + j) * Sh::THREADS];
+    for (int j = 0; j < Sh::E; ++j) y[j] = strip[j * Sh::THREADS];
+    ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1>(y, ex, tw, pr.p, pr.p2);
+    store(s, 1);
+    if constexpr (TWO) {
+#pragma unroll
+      for (int j = 0; j < Sh::E; ++j) y[j] = strip[(Sh::E + j) * Sh::THREADS];
+    } else {
+      // h0 = a0 b0 (operands re-read: L1/L2 hits)
+#pragma unroll
+      for (int i = 0; i < EV::CHUNKS; ++i) {
+        T a0[EV::VEC], b0[EV::VEC];
+        EV::load(a0p, i, a0);
+        EV::load(b0p, i, b0);
+#pragma unroll
+        for (int c = 0; c < EV::VEC; ++c) y[i * EV::VEC + c] = mont_mul(a0[c], b0[c], pr.p, pr.pinv);
       }
-      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1>(y, ex, tw, pr.p, pr.p2);
-      T* dst = H + ((size_t)s * 3 + part) * KN + k * N + coef_base<LOGN>();
-#pragma unroll
-      for (int j = 0; j < Sh::E; ++j) dst[coef_off<LOGN>(j)] = csub(y[j], pr.p);
     }
+    ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1>(y, ex, tw, pr.p, pr.p2);
+    store(s, 0);
   }
 }
 
@@ -718,7 +738,7 @@ static cudaError_t launch_site_product(const Ctx* c, const uint32_t* ax, const u
   const Base& B = c->base[BASE_B];
   using T = uint32_t;
   constexpr size_t tw_bytes = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
-  constexpr size_t base_bytes = ((size_t)Exchanger<T, LOGN, 1, 1>::WORDS + 2 * (size_t)Sh::N) * sizeof(T);
+  constexpr size_t base_bytes = ((size_t)Exchanger<T, LOGN, 1, 1>::WORDS + (LOGN <= 12 ? 2 : 1) * (size_t)Sh::N) * sizeof(T);
   constexpr bool SMEM_TW = LOGN >= 9 && tw_bytes + base_bytes <= 200 * 1024;
   auto kern = k_site_product<LOGN, SMEM_TW>;
   const size_t smem = base_bytes + (SMEM_TW ? tw_bytes : 0);
