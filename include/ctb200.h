@@ -78,6 +78,11 @@ int ctb_pointwise_mul(const ctb_ctx_t* ctx, int base, const void* a, const void*
 int ctb_ring_mul(const ctb_ctx_t* ctx, int base, const void* a, uint64_t a_stride, const void* b,
                  uint64_t b_stride, void* out, uint64_t n_polys, void* stream);
 
+/* out = NTT(in) * N^-1 (canonical eval): the evaluation-domain form of a coefficient
+ * addend to sums of products with prepared operands, e.g. K3's mask products
+ * (ctb_linear_online maskprod_eval = 1).  In place allowed. */
+int ctb_eval_addend(const ctb_ctx_t* ctx, int base, const void* in, void* out, uint64_t n_polys, void* stream);
+
 /* Prepared operand for repeated products: out = NTT(in) scaled into the
  * Montgomery domain with N^-1 folded (layout [poly][L][N], evaluation order).
  * Keys (public, secret, relinearisation) are prepared once per session. */
@@ -202,7 +207,10 @@ int ctb_lift_prepare(const ctb_ctx_t* ctx, const uint64_t* m, void* out, uint64_
  * ct_x [n_x][2][L][N], ct_w [n_w][2][L][N] ciphertexts; mx [n_x][N], mw [n_w][N]
  * masked plaintexts (x - r_x, w - r_w); sites_host: HOST array of n_sites
  * (x index, w index, out slot) triples (linprot.JobShape.sites); maskprod
- * [n_out][2][L][N] or NULL; out_ct [n_out][2][L][N]; out_p [n_out][N].
+ * [n_out][2][L][N] or NULL, as ciphertexts (maskprod_eval = 0) or in the
+ * ctb_eval_addend form (maskprod_eval = 1: the server transformed its mask products
+ * offline, so the online step adds them in the evaluation domain);
+ * out_ct [n_out][2][L][N]; out_p [n_out][N].
  * workspace: ctb_linear_online_workspace_bytes() bytes of device memory.
  * Every ciphertext part and masked plaintext is NTT'd once; each slot is
  * accumulated in the evaluation domain and inverse-transformed once. */
@@ -210,8 +218,8 @@ uint64_t ctb_linear_online_workspace_bytes(const ctb_ctx_t* ctx, uint32_t n_x, u
                                            uint32_t n_sites);
 int ctb_linear_online(const ctb_ctx_t* ctx, const void* ct_x, uint32_t n_x, const void* ct_w, uint32_t n_w,
                       const uint64_t* mx, const uint64_t* mw, const uint32_t* sites_host, uint32_t n_sites,
-                      uint32_t n_out, const void* maskprod, void* out_ct, uint64_t* out_p, void* workspace,
-                      void* stream);
+                      uint32_t n_out, const void* maskprod, int maskprod_eval, void* out_ct, uint64_t* out_p,
+                      void* workspace, void* stream);
 /* Segmented sum (the CCAdd accumulation of linprot._accumulate, linprot.py:343-344):
  * out[o] = sum_{s in [slot_ptr[o], slot_ptr[o+1])} in[members[s]] over [*][parts][L][N]
  * (slot_ptr / members are DEVICE int32 arrays). */

@@ -155,9 +155,11 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
 //   InvAdd       unscaled INTT (+ addend): eval-domain sums of products with prepared
 //                operands (N^-1 already folded in) back to coefficients, plus a
 //                coefficient-domain addend (K3's mask product).
-//   LiftPrepare  plain [npoly][N] in [0,t) -> NTT(centred lift) N^-1 2^W per limb (ctb_lift_prepare)  Twiddles staged once per CTA in
+//   LiftPrepare  plain [npoly][N] in [0,t) -> NTT(centred lift) N^-1 2^W per limb (ctb_lift_prepare)
+//   FwdNinv      NTT(x) N^-1, canonical: the eval-domain form of a coefficient addend to
+//                sums of products with prepared operands (ctb_eval_addend)  Twiddles staged once per CTA in
 // shared memory, GROUPS transforms per CTA sharing them.
-enum class StreamOp { Fwd, Inv, Prepare, MulPrepared, InvAdd, LiftPrepare };
+enum class StreamOp { Fwd, Inv, Prepare, MulPrepared, InvAdd, LiftPrepare, FwdNinv };
 
 template <typename T>
 struct StreamArgs {
@@ -291,6 +293,10 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
       if constexpr (OP == StreamOp::Fwd) {
 #pragma unroll
         for (int k = 0; k < Sh::E; ++k) x[k] = pr.canon_fwd(x[k]);
+        store_eval<T, LOGN>(a.out + off, x);
+      } else if constexpr (OP == StreamOp::FwdNinv) {
+#pragma unroll
+        for (int k = 0; k < Sh::E; ++k) x[k] = csub(shoup_mul(x[k], pr.ninv, pr.ninv_q, pr.p), pr.p);
         store_eval<T, LOGN>(a.out + off, x);
       } else if constexpr (OP == StreamOp::Prepare || OP == StreamOp::LiftPrepare) {
 #pragma unroll
@@ -555,6 +561,22 @@ extern "C" int ctb_ntt_inverse(const ctb_ctx_t* ctx, int base, const void* in, v
     CTB_DISPATCH_LOGN(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::Inv>(b, sargs<uint64_t>(in, out), n_polys, s)));
   }
   return cuda_status(e, "ctb_ntt_inverse");
+}
+
+extern "C" int ctb_eval_addend(const ctb_ctx_t* ctx, int base, const void* in, void* out, uint64_t n_polys,
+                               void* stream) {
+  if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
+  const Base* b = base_of(ctx, base);
+  if (!b || !in || !out) { set_error("ctb_eval_addend: bad context, base or buffer"); return ERR_ARG; }
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  if (b->word == 4) {
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::FwdNinv>(b, sargs<uint32_t>(in, out), n_polys, s)));
+  } else {
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::FwdNinv>(b, sargs<uint64_t>(in, out), n_polys, s)));
+  }
+  return cuda_status(e, "ctb_eval_addend");
 }
 
 extern "C" int ctb_prepare_operand(const ctb_ctx_t* ctx, int base, const void* in, void* out, uint64_t n_polys,

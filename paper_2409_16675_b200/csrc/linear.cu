@@ -35,8 +35,8 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 k_lin_accum(const T* __restrict__ X, const T* __restrict__ W, const T* __restrict__ MXp, const T* __restrict__ MWp,
             const int32_t* __restrict__ slot_ptr, const int32_t* __restrict__ site_x,
-            const int32_t* __restrict__ site_w, T* __restrict__ acc, const PrimeTab<T>* __restrict__ tabs, int L,
-            uint32_t n, uint32_t chunks) {
+            const int32_t* __restrict__ site_w, const T* __restrict__ init, T* __restrict__ acc,
+            const PrimeTab<T>* __restrict__ tabs, int L, uint32_t n, uint32_t chunks) {
   constexpr int VEC = 16 / sizeof(T);
   union V { uint4 u; T t[VEC]; };
   uint32_t bid = blockIdx.x;
@@ -55,8 +55,18 @@ k_lin_accum(const T* __restrict__ X, const T* __restrict__ W, const T* __restric
   const uint4* MW4 = reinterpret_cast<const uint4*>(MWp + (size_t)limb * n) + v;
   const size_t part4 = LN / VEC, poly4 = 2 * part4;  // uint4 strides
   T a0[VEC], a1[VEC];
+  uint4* A4 = reinterpret_cast<uint4*>(acc + (size_t)limb * n) + v + (size_t)slot * poly4;
+  if (init) {  // eval-domain mask product (ctb_eval_addend form), same layout as acc
+    V i0, i1;
+    const uint4* I4 = reinterpret_cast<const uint4*>(init + (size_t)limb * n) + v + (size_t)slot * poly4;
+    i0.u = __ldg(I4);
+    i1.u = __ldg(I4 + part4);
 #pragma unroll
-  for (int c = 0; c < VEC; ++c) a0[c] = a1[c] = 0;
+    for (int c = 0; c < VEC; ++c) { a0[c] = i0.t[c]; a1[c] = i1.t[c]; }
+  } else {
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) a0[c] = a1[c] = 0;
+  }
   auto site = [&](const V& x0, const V& x1, const V& w0, const V& w1, const V& mx, const V& mw) {
 #pragma unroll
     for (int c = 0; c < VEC; ++c) {
@@ -92,7 +102,6 @@ k_lin_accum(const T* __restrict__ X, const T* __restrict__ W, const T* __restric
   V o0, o1;
 #pragma unroll
   for (int c = 0; c < VEC; ++c) { o0.t[c] = a0[c]; o1.t[c] = a1[c]; }
-  uint4* A4 = reinterpret_cast<uint4*>(acc + (size_t)limb * n) + v + (size_t)slot * poly4;
   A4[0] = o0.u;
   A4[part4] = o1.u;
 }
@@ -204,8 +213,8 @@ extern "C" uint64_t ctb_linear_online_workspace_bytes(const ctb_ctx_t* ctx, uint
 
 extern "C" int ctb_linear_online(const ctb_ctx_t* ctx, const void* ct_x, uint32_t n_x, const void* ct_w, uint32_t n_w,
                                  const uint64_t* mx, const uint64_t* mw, const uint32_t* sites_host, uint32_t n_sites,
-                                 uint32_t n_out, const void* maskprod, void* out_ct, uint64_t* out_p, void* workspace,
-                                 void* stream) {
+                                 uint32_t n_out, const void* maskprod, int maskprod_eval, void* out_ct, uint64_t* out_p,
+                                 void* workspace, void* stream) {
   if (n_out == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Ctx* c = cctx(ctx);
   if (!c || !c->t || !ct_x || !ct_w || !mx || !mw || !sites_host || !out_ct || !out_p || !workspace) {
@@ -273,14 +282,17 @@ extern "C" int ctb_linear_online(const ctb_ctx_t* ctx, const void* ct_x, uint32_
     if (blocks >= (1ull << 31)) { set_error("ctb_linear_online: job too large"); return ERR_ARG; }
     if (B.word == 4)
       k_lin_accum<uint32_t><<<(unsigned)blocks, 256, 0, s>>>((const uint32_t*)X, (const uint32_t*)W,
-          (const uint32_t*)MX, (const uint32_t*)MW, d_ptr, d_sx, d_sw, (uint32_t*)out_ct,
+          (const uint32_t*)MX, (const uint32_t*)MW, d_ptr, d_sx, d_sw,
+          maskprod_eval ? (const uint32_t*)maskprod : nullptr, (uint32_t*)out_ct,
           (const PrimeTab<uint32_t>*)B.d_tabs, (int)L, (uint32_t)N, chunks);
     else
       k_lin_accum<uint64_t><<<(unsigned)blocks, 256, 0, s>>>((const uint64_t*)X, (const uint64_t*)W,
-          (const uint64_t*)MX, (const uint64_t*)MW, d_ptr, d_sx, d_sw, (uint64_t*)out_ct,
+          (const uint64_t*)MX, (const uint64_t*)MW, d_ptr, d_sx, d_sw,
+          maskprod_eval ? (const uint64_t*)maskprod : nullptr, (uint64_t*)out_ct,
           (const PrimeTab<uint64_t>*)B.d_tabs, (int)L, (uint32_t)N, chunks);
     e = cudaGetLastError();
-    if (e == cudaSuccess) e = stream_inv_add(c, BASE_Q, out_ct, out_ct, maskprod, (uint64_t)n_out * 2, s);
+    if (e == cudaSuccess)
+      e = stream_inv_add(c, BASE_Q, out_ct, out_ct, maskprod_eval ? nullptr : maskprod, (uint64_t)n_out * 2, s);
   }
   if (e != cudaSuccess) return cuda_status(e, "ctb_linear_online cipher");
   CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<uint32_t, LOGN>(k_lin_plain<LOGN>, (size_t)n_out * LT, s,

@@ -140,10 +140,11 @@ class CiphertextBatch:
     Noise estimates are exact Python integers (he.py:103-132); a batch whose
     members share one estimate stores it once (`uniform_noise`)."""
 
-    __slots__ = ("data", "_nu", "backend_tag", "_cipher")
+    __slots__ = ("data", "_nu", "backend_tag", "_cipher", "eval_form")
 
     def __init__(self, data: torch.Tensor, noise, backend_tag: str, cipher: RingParams):
         self.data = data
+        self.eval_form = None   # optional ctb_eval_addend form of `data` (server-side mask products)
         self._nu = int(noise) if isinstance(noise, int) else [int(v) for v in noise]
         self.backend_tag = backend_tag
         self._cipher = cipher

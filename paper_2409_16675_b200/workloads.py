@@ -73,7 +73,7 @@ def offline(sess: Session, job: LinearJob, gen) -> tuple[linprot.MaskBundle, Cip
     fresh = sess.server.params.fresh_noise
     rx = CiphertextBatch(cts.data[:js.n_x], fresh, cts.backend_tag, cts._cipher)
     rw = CiphertextBatch(cts.data[js.n_x:], fresh, cts.backend_tag, cts._cipher)
-    prod = linprot._sites_ccmul_sum(sess.server, sess.pks, rx, rw, js)
+    prod = linprot.attach_eval_form(sess.server, linprot._sites_ccmul_sum(sess.server, sess.pks, rx, rw, js))
     return linprot.MaskBundle(js.job_id, r[:js.n_x], r[js.n_x:]), prod
 
 
