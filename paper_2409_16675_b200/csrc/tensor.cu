@@ -26,6 +26,7 @@
 //    NTT(d_i) * prepared(b_i), NTT(d_i) * prepared(a_i) in registers, 2 INTT,
 //    + (c0, c1).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 #include "bigint.hpp"
@@ -1152,6 +1153,16 @@ extern "C" int ctb_relinearize(const ctb_ctx_t* ctx, const void* ct3, const void
 namespace {
 constexpr uint64_t kSiteChunkBytes = 1ull << 30;  // H workspace budget per chunk
 
+// Sites per chunk; CTB_SITE_CHUNK (sites) overrides the memory-derived value (tests use it to
+// exercise the multi-chunk path on small jobs).
+uint64_t site_chunk(uint64_t per_site_bytes) {
+  static const uint64_t env = [] {
+    const char* e = getenv("CTB_SITE_CHUNK");
+    return e ? strtoull(e, nullptr, 10) : 0ull;
+  }();
+  return env ? env : std::max<uint64_t>(1, kSiteChunkBytes / per_site_bytes);
+}
+
 size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct SumLayout {
@@ -1163,7 +1174,7 @@ SumLayout sum_layout(const Ctx* c, uint32_t n_x, uint32_t n_w, uint32_t n_out, u
   SumLayout l{};
   const size_t N = c->n, K = c->tensor->K, L = c->tensor->L, w = c->base[BASE_Q].word;
   const size_t D = (size_t)ctb_relin_digit_count(reinterpret_cast<const ctb_ctx_t*>(c));
-  uint64_t chunk = std::max<uint64_t>(1, kSiteChunkBytes / (3 * K * N * 4));
+  uint64_t chunk = site_chunk(3 * K * N * 4);
   chunk = std::max<uint64_t>(chunk, max_slot);
   chunk = std::min<uint64_t>(chunk, std::max<uint32_t>(n_sites, 1));
   l.chunk = chunk;

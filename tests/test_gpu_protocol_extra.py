@@ -229,3 +229,55 @@ def test_c_abi_errors_and_empty_batches():
     assert ctx.cpmul(empty, torch.empty((0, P.n), dtype=torch.int64, device="cuda")).shape[0] == 0
     with pytest.raises(ValueError):
         ctx.cpmul(empty[:, :1], torch.empty((0, P.n), dtype=torch.int64, device="cuda"))
+
+
+def _ccmul_sum_case(p512, rng, job):
+    """Offline mask products of one job via the fused path; returned as host residues."""
+    from paper_2409_16675_b200 import linprot
+    from paper_2409_16675_b200.he import CiphertextBatch
+    cli, srv, keys = evaluators(p512)
+    pks = srv.public_keys_from_bytes(cli.public_keys_to_bytes(keys))
+    js = job.shape
+    r = linprot._plain_random(cli, js.n_x + js.n_w, np.random.default_rng(7))
+    cts = cli.encrypt_many(r, keys, np.random.default_rng(8))
+    fresh = srv.params.fresh_noise
+    rx = CiphertextBatch(cts.data[:js.n_x], fresh, cts.backend_tag, cts._cipher)
+    rw = CiphertextBatch(cts.data[js.n_x:], fresh, cts.backend_tag, cts._cipher)
+    out = linprot._sites_ccmul_sum(srv, pks, rx, rw, js)
+    # per-site reference through the single-CCMul API, CCAdd per slot
+    per = srv.cc_mul_many(
+        CiphertextBatch(rx.data[[s[0] for s in js.sites]].contiguous(), fresh, rx.backend_tag, rx._cipher),
+        CiphertextBatch(rw.data[[s[1] for s in js.sites]].contiguous(), fresh, rw.backend_tag, rw._cipher), pks)
+    ref = [None] * js.n_out
+    for k, (_, _, o) in enumerate(js.sites):
+        c = per[k]
+        ref[o] = c if ref[o] is None else srv.cc_add(ref[o], c)
+    return out, ref
+
+
+def test_ccmul_sum_matches_per_site_and_chunks(p512, rng):
+    """ctb_ccmul_sum == per-site cc_mul + relinearize + CCAdd (he.py:434-439, linprot.py:407-427),
+    single-chunk and with the multi-chunk path forced (CTB_SITE_CHUNK=2 in a subprocess)."""
+    import os
+    import subprocess
+    import sys
+    import torch
+    from paper_2409_16675_b200 import linprot, packing
+    x = rng.integers(0, 50, size=(2, 6, 6))
+    w = rng.integers(-9, 9, size=(3, 2, 3, 3))
+    job = linprot.conv_job("cs", x, w, packing.ConvShape(6, 6, 3, 1), p512.plain_ring)
+    out, ref = _ccmul_sum_case(p512, rng, job)
+    assert all(torch.equal(out.data[o], c.data) for o, c in enumerate(ref))
+    code = (
+        "import numpy as np, torch, sys; sys.path.insert(0, 'tests'); "
+        "import test_gpu_protocol_extra as t; from paper_2409_16675_b200 import he, linprot, packing; "
+        "plain = he.default_plain_params(512, 17, 2); "
+        "P = he.HeParams(he.default_cipher_params(512, plain.modulus), plain); "
+        "rng = np.random.default_rng(3); x = rng.integers(0, 50, size=(2, 6, 6)); "
+        "w = rng.integers(-9, 9, size=(3, 2, 3, 3)); "
+        "job = linprot.conv_job('cs', x, w, packing.ConvShape(6, 6, 3, 1), P.plain_ring); "
+        "out, ref = t._ccmul_sum_case(P, rng, job); "
+        "print('OK' if all(torch.equal(out.data[o], c.data) for o, c in enumerate(ref)) else 'BAD')")
+    env = dict(os.environ, CTB_SITE_CHUNK="2")
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
+    assert res.stdout.strip().endswith("OK"), res.stdout + res.stderr

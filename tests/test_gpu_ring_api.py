@@ -78,3 +78,22 @@ def test_plain_ring_ops_and_ntt_surface():
         ring.ntt_forward(RingElem.zeros(RingParams(8, 19)))
     with pytest.raises(ring.ParamsMismatchError):
         ring.ring_add(RingElem.zeros(RingParams(4, 17)), RingElem.zeros(RingParams(4, 97)))
+
+
+def test_eval_addend_is_scaled_forward_ntt():
+    """ctb_eval_addend(x) == NTT(x) * N^-1 mod p (canonical), the K3 mask-product form."""
+    import torch
+    from paper_2409_16675_b200 import _lib
+    from paper_2409_16675_b200.device import RnsContext, _ptr, _stream
+    from paper_2409_16675_b200.params import default_he_params
+    P = default_he_params(4096)
+    ctx = RnsContext.get(P.n, P.cipher_ring.primes, P.plain_ring.primes)
+    p = torch.tensor(P.cipher_ring.primes, dtype=torch.int64, device="cuda").view(1, -1, 1)
+    x = (torch.randint(0, 1 << 62, (3, ctx.L, P.n), device="cuda") % p).to(torch.int32)
+    ev = torch.empty_like(x)
+    _lib.check(ctx._lib.ctb_eval_addend(ctx._h, 0, _ptr(x), _ptr(ev), 3, _stream()), "ctb_eval_addend")
+    f = torch.empty_like(x)
+    _lib.check(ctx._lib.ctb_ntt_forward(ctx._h, 0, _ptr(x), _ptr(f), 3, _stream()), "ctb_ntt_forward")
+    ninv = torch.tensor([pow(P.n, -1, q) for q in P.cipher_ring.primes], dtype=torch.int64, device="cuda").view(1, -1, 1)
+    expect = (f.to(torch.int64) * ninv) % p
+    assert torch.equal(ev.to(torch.int64), expect)
