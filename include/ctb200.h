@@ -109,20 +109,26 @@ int ctb_cpmul(const ctb_ctx_t* ctx, const void* ct, const uint64_t* pt, void* ou
 
 /* Encryption (He.encrypt, he.py:307-323), fused: out[k] = (b u + e1 + Delta lift(m), a u + e2)
  * for m [batch][N] uint64 in [0,t), draws [batch][3][N] int8 = (u, e1, e2) small signed
- * integers (ternary u, rounded-Gaussian e clipped to the error bound, |e| <= 127) --
- * from the caller's sampler (the reference's numpy draws reproduce its ciphertexts) or
- * from ctb_sample_draws; pkprep = ctb_prepare_operand of the public key (b, a) as
- * [2][L][N]; out [batch][2][L][N]. */
+ * integers (ternary u, rounded-Gaussian e clipped to the error bound, |e| <= 127) in the
+ * DEVICE DRAW LAYOUT (thread-major: see ctb_sample_draws; convert natural-order draws,
+ * e.g. the reference's numpy draws, with ctb_draws_from_natural), pkprep =
+ * ctb_prepare_operand of the public key (b, a) as [2][L][N]; out [batch][2][L][N]. */
 int ctb_encrypt(const ctb_ctx_t* ctx, const uint64_t* m, const int8_t* draws, const void* pkprep, void* out,
                 uint64_t batch, void* stream);
 
 /* Device sampler for ctb_encrypt's draws (He._ternary / He._error, he.py:292-303):
  * Philox4x32-10 keyed by `seed`, counter = (first_poly + k, coefficient), so the
  * stream is launch-shape independent; u uniform over {-1,0,1}, e1/e2 = clip(rint(
- * sigma * z), -bound, bound) for z ~ N(0,1) by Box-Muller.  out [batch][3][N] int8.
+ * sigma * z), -bound, bound) for z ~ N(0,1) by Box-Muller.  out [batch][3][N] int8 in
+ * the device draw layout: position t*E + k of each row holds the draw of the coefficient
+ * owned by register k of transform thread t (E = 16 residues per thread for N >= 512).
  * The distribution is the reference's; the stream is not numpy's. */
 int ctb_sample_draws(const ctb_ctx_t* ctx, uint64_t seed, uint64_t first_poly, double sigma, int bound,
                      int8_t* out, uint64_t batch, void* stream);
+
+/* Natural-order draws [batch][3][N] (coefficient i at index i) -> device draw layout
+ * (not in place). */
+int ctb_draws_from_natural(const ctb_ctx_t* ctx, const int8_t* in, int8_t* out, uint64_t batch, void* stream);
 
 /* PPMul in the plain ring: He.pp_mul (he.py:441-445) = ring.ring_mul over the
  * plain primes + 2-prime CRT (ring.py:477-485). */

@@ -40,6 +40,7 @@ SIGNATURES: dict[str, tuple] = {
     "ctb_cpmul": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_encrypt": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_sample_draws": (_int, [_c_void_p, _u64, _u64, ctypes.c_double, _int, _c_void_p, _u64, _c_void_p]),
+    "ctb_draws_from_natural": (_int, [_c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_pp_mul": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_rns_elementwise": (_int, [_c_void_p, _int, _int, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_rns_scalar_mul": (_int, [_c_void_p, _int, _c_void_p, ctypes.POINTER(_u64), _c_void_p, _u64, _c_void_p]),

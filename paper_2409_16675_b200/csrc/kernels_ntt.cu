@@ -423,15 +423,32 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
   const int cb = coef_base<LOGN>();
   T x[Sh::E];
 #pragma unroll 1
+  // device draw layout (sample.cu): this thread's E draws of each kind are contiguous
+  const int tid = ntt_tid<LOGN>();
+  auto load_draws = [&](const int8_t* row, int8_t (&v)[Sh::E]) {
+    if constexpr (Sh::E == 16) {
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(row) + tid);
+      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = (int8_t)(ww[k >> 2] >> (8 * (k & 3)));
+    } else {
+#pragma unroll
+      for (int k = 0; k < Sh::E; ++k) v[k] = __ldg(row + tid * Sh::E + k);
+    }
+  };
   for (uint32_t b = slot * GROUPS + group; b < batch; b += nslots * GROUPS) {
-    const int8_t* d = draws + (size_t)b * 3 * Sh::N + cb;
+    const int8_t* drow = draws + (size_t)b * 3 * Sh::N;
     if (ntt_tid<LOGN>() == 0 && b + nslots * GROUPS < batch) {  // next item's inputs towards L2
       const uint32_t nb = b + nslots * GROUPS;
       bulk_prefetch_l2(m + (size_t)nb * Sh::N, (uint32_t)(Sh::N * 8));
       bulk_prefetch_l2(draws + (size_t)nb * 3 * Sh::N, (uint32_t)(Sh::N * 3));
     }
+    {
+      int8_t u[Sh::E];
+      load_draws(drow, u);
 #pragma unroll
-    for (int k = 0; k < Sh::E; ++k) x[k] = small(__ldg(d + coef_off<LOGN>(k)));
+      for (int k = 0; k < Sh::E; ++k) x[k] = small(u[k]);
+    }
     ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
     for (int k = 0; k < Sh::E; ++k) usm[k * Sh::THREADS] = x[k];
@@ -447,13 +464,14 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
         for (int c = 0; c < EV::VEC; ++c)
           x[i * EV::VEC + c] = mont_mul(usm[(i * EV::VEC + c) * Sh::THREADS], v[c], pr.p, pr.pinv);
       }
+      int8_t e[Sh::E];  // issued before the inverse transform, consumed after it
+      load_draws(drow + (size_t)(1 + part) * Sh::N, e);
       ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
-      const int8_t* e = d + (size_t)(1 + part) * Sh::N;
       const uint64_t* mm = m + (size_t)b * Sh::N + cb;
       T* o = out + (((size_t)b * 2 + part) * L + limb) * Sh::N + cb;
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) {
-        T v = add_mod(csub(x[k], pr.p), small(__ldg(e + coef_off<LOGN>(k))), pr.p);
+        T v = add_mod(csub(x[k], pr.p), small(e[k]), pr.p);
         if (part == 0) {
           const uint64_t mv = __ldg(mm + coef_off<LOGN>(k));
           T l = csub(pr.reduce_u64_lazy(mv), pr.p);

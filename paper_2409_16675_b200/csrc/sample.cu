@@ -6,7 +6,10 @@
 // Philox block per coefficient gives u (ternary, uniform over {-1, 0, 1}) and,
 // through Box-Muller, the two Gaussian errors e1, e2 ~ N(0, sigma^2), rounded
 // to the nearest integer and clipped to +-bound like the reference.  Output:
-// int8 draws [batch][3][N] = (u, e1, e2), the layout ctb_encrypt consumes.
+// int8 draws [batch][3][N] = (u, e1, e2) in the device draw layout ctb_encrypt consumes:
+// thread-major, position t*E + k holds the draw of the coefficient that register k of
+// NTT thread t owns (coef_base/coef_off of the first pass), so a thread loads its 16
+// draws of each kind with one 16-byte load.  ctb_draws_from_natural converts.
 #include <algorithm>
 #include <cstdint>
 #include "ctb200.h"
@@ -28,31 +31,54 @@ struct Philox4x32 {
   }
 };
 
-__global__ void k_sample_draws(int8_t* out, uint64_t seed, uint64_t first_poly, uint32_t n, uint64_t total,
-                               float sigma, int bound) {
+template <int LOGN>
+__host__ __device__ constexpr int draw_coef(int pos) {  // device position -> coefficient
+  using Sh = NttShape<LOGN>;
+  return pass_index<LOGN, 0, Sh::FIRST_R>(pos / Sh::E, pos % Sh::E);
+}
+
+template <int LOGN>
+__global__ void k_sample_draws(int8_t* out, uint64_t seed, uint64_t first_poly, uint64_t total, float sigma, int bound) {
+  constexpr uint32_t n = 1u << LOGN;
   const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t poly = g / n, i = g % n;
+    const uint64_t poly = g / n;
+    const uint32_t pos = (uint32_t)(g % n);
+    const uint32_t i = (uint32_t)draw_coef<LOGN>((int)pos);
     const uint64_t gp = first_poly + poly;
-    const uint4 r = Philox4x32::run(make_uint4((uint32_t)i, (uint32_t)gp, (uint32_t)(gp >> 32), 0x43544232u), key);
+    const uint4 r = Philox4x32::run(make_uint4(i, (uint32_t)gp, (uint32_t)(gp >> 32), 0x43544232u), key);
     const int u = (int)(((uint64_t)r.x * 3u) >> 32) - 1;
     const float u1 = ((float)r.y + 1.0f) * 2.3283064365386963e-10f;   // (0, 1]
     const float th = (float)r.z * 1.4629180792671596e-09f;             // 2 pi / 2^32
     const float rad = sqrtf(-2.0f * logf(u1));
-    float s, c;
-    sincosf(th, &s, &c);
-    const int e1 = max(-bound, min(bound, __float2int_rn(sigma * rad * c)));
-    const int e2 = max(-bound, min(bound, __float2int_rn(sigma * rad * s)));
-    int8_t* o = out + poly * 3 * n + i;
+    float sn, cs;
+    sincosf(th, &sn, &cs);
+    const int e1 = max(-bound, min(bound, __float2int_rn(sigma * rad * cs)));
+    const int e2 = max(-bound, min(bound, __float2int_rn(sigma * rad * sn)));
+    int8_t* o = out + poly * 3 * n + pos;
     o[0] = (int8_t)u;
     o[n] = (int8_t)e1;
     o[2 * n] = (int8_t)e2;
   }
 }
 
+template <int LOGN>
+__global__ void k_draws_layout(const int8_t* in, int8_t* out, uint64_t total) {
+  constexpr uint32_t n = 1u << LOGN;
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t row = g / n;   // poly * 3 + kind
+    const uint32_t pos = (uint32_t)(g % n);
+    out[g] = in[row * n + (uint32_t)draw_coef<LOGN>((int)pos)];
+  }
+}
+
 }  // namespace ctb
 
 using namespace ctb;
+
+static unsigned grid_for(uint64_t total) {
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148ull * 16));
+}
 
 extern "C" int ctb_sample_draws(const ctb_ctx_t* ctx, uint64_t seed, uint64_t first_poly, double sigma, int bound,
                                 int8_t* out, uint64_t batch, void* stream) {
@@ -61,7 +87,19 @@ extern "C" int ctb_sample_draws(const ctb_ctx_t* ctx, uint64_t seed, uint64_t fi
   if (!c || !out) { set_error("ctb_sample_draws: bad context or buffer"); return ERR_ARG; }
   if (bound < 0 || bound > 127 || !(sigma >= 0.0)) { set_error("ctb_sample_draws: bound must be in [0, 127], sigma >= 0"); return ERR_ARG; }
   const uint64_t total = batch * c->n;
-  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148ull * 16));
-  k_sample_draws<<<grid, 256, 0, (cudaStream_t)stream>>>(out, seed, first_poly, c->n, total, (float)sigma, bound);
+  cudaStream_t s = (cudaStream_t)stream;
+  CTB_DISPATCH_LOGN(c->logn, (k_sample_draws<LOGN><<<grid_for(total), 256, 0, s>>>(out, seed, first_poly, total,
+                                                                                (float)sigma, bound)));
   return cuda_status(cudaGetLastError(), "ctb_sample_draws");
+}
+
+extern "C" int ctb_draws_from_natural(const ctb_ctx_t* ctx, const int8_t* in, int8_t* out, uint64_t batch,
+                                      void* stream) {
+  if (batch == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (!c || !in || !out || in == out) { set_error("ctb_draws_from_natural: bad context or buffer (no in-place)"); return ERR_ARG; }
+  const uint64_t total = batch * 3 * c->n;
+  cudaStream_t s = (cudaStream_t)stream;
+  CTB_DISPATCH_LOGN(c->logn, (k_draws_layout<LOGN><<<grid_for(total), 256, 0, s>>>(in, out, total)));
+  return cuda_status(cudaGetLastError(), "ctb_draws_from_natural");
 }

@@ -368,7 +368,10 @@ class He:
                 host[k, 0] = self._ternary(rng)
                 host[k, 1] = self._error(rng)
                 host[k, 2] = self._error(rng)
-            draws = torch.from_numpy(host.reshape(B * 3, n)).cuda()
+            nat = torch.from_numpy(host.reshape(B * 3, n)).cuda()
+            draws = torch.empty_like(nat)
+            _lib.check(self.ctx._lib.ctb_draws_from_natural(self.ctx._h, _ptr(nat), _ptr(draws), B, _stream()),
+                       "ctb_draws_from_natural")
         pk = self._pk_prep(keys)
         out = torch.empty((B, 2, self.L, n), dtype=self.ctx.dtype(), device="cuda")
         _lib.check(self.ctx._lib.ctb_encrypt(self.ctx._h, _ptr(mt), _ptr(draws.contiguous()), _ptr(pk), _ptr(out), B,
