@@ -112,7 +112,9 @@ cudaError_t stream_inv_add(const Ctx* c, int base, const void* in, void* out, co
 cudaError_t stream_forward(const Ctx* c, int base, bool prepare, const void* in, void* out, uint64_t npoly,
                            cudaStream_t s);
 
-// NTT of the centred lift of plain [npoly][N] per cipher limb, prepared (N^-1 2^W) (k_stream LiftPrepare).
-cudaError_t stream_lift_prepare(const Ctx* c, const uint64_t* m, void* out, uint64_t npoly, cudaStream_t s);
+// NTT of the lift of plain [npoly][N] (centred for the cipher base) per limb of `base`:
+// prepared (N^-1 2^W, k_stream LiftPrepare) or canonical eval (LiftFwd).
+cudaError_t stream_lift(const Ctx* c, int base, bool prepare, const uint64_t* m, void* out, uint64_t npoly,
+                        cudaStream_t s);
 
 }  // namespace ctb

@@ -156,10 +156,11 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
 //                operands (N^-1 already folded in) back to coefficients, plus a
 //                coefficient-domain addend (K3's mask product).
 //   LiftPrepare  plain [npoly][N] in [0,t) -> NTT(centred lift) N^-1 2^W per limb (ctb_lift_prepare)
+//   LiftFwd      plain [npoly][N] -> canonical NTT of the (centred) lift per limb
 //   FwdNinv      NTT(x) N^-1, canonical: the eval-domain form of a coefficient addend to
 //                sums of products with prepared operands (ctb_eval_addend)  Twiddles staged once per CTA in
 // shared memory, GROUPS transforms per CTA sharing them.
-enum class StreamOp { Fwd, Inv, Prepare, MulPrepared, InvAdd, LiftPrepare, FwdNinv };
+enum class StreamOp { Fwd, Inv, Prepare, MulPrepared, InvAdd, LiftPrepare, FwdNinv, LiftFwd };
 
 template <typename T>
 struct StreamArgs {
@@ -196,7 +197,7 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
   using C = StreamCfg<T, LOGN>;
   using Sh = NttShape<LOGN>;
   constexpr int GROUPS = C::GROUPS;
-  constexpr bool PF = C::PF_OK && OP != StreamOp::LiftPrepare;
+  constexpr bool PF = C::PF_OK && OP != StreamOp::LiftPrepare && OP != StreamOp::LiftFwd;
   constexpr int TW_WORDS = SMEM_TW ? 2 * shape_tw_entries(LOGN) : 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
@@ -258,8 +259,9 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
         if (OP == StreamOp::MulPrepared && a.b_stride)
           bulk_prefetch_l2(a.bprep + ((size_t)b * a.b_stride * L + limb) * (size_t)Sh::N, Sh::N * sizeof(T));
       }
-    } else if constexpr (OP == StreamOp::LiftPrepare) {
+    } else if constexpr (OP == StreamOp::LiftPrepare || OP == StreamOp::LiftFwd) {
       const uint64_t* src = a.plain + (size_t)b * Sh::N + cb;
+      if (leader && b + step < npoly) bulk_prefetch_l2(a.plain + (size_t)(b + step) * Sh::N, Sh::N * 8);
       const T tmod = tabs[limb].tmod;
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) {
@@ -290,7 +292,7 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
       }
     } else {
       ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
-      if constexpr (OP == StreamOp::Fwd) {
+      if constexpr (OP == StreamOp::Fwd || OP == StreamOp::LiftFwd) {
 #pragma unroll
         for (int k = 0; k < Sh::E; ++k) x[k] = pr.canon_fwd(x[k]);
         store_eval<T, LOGN>(a.out + off, x);
@@ -638,17 +640,23 @@ extern "C" int ctb_mul_prepared(const ctb_ctx_t* ctx, int base, const void* a, c
   return ctb_mul_prepared_strided(ctx, base, a, 1, bprep, b_stride, addend, 1, out, n_polys, stream);
 }
 
-cudaError_t ctb::stream_lift_prepare(const Ctx* c, const uint64_t* m, void* out, uint64_t npoly, cudaStream_t s) {
-  const Base* b = &c->base[BASE_Q];
+cudaError_t ctb::stream_lift(const Ctx* c, int base, bool prepare, const uint64_t* m, void* out, uint64_t npoly,
+                             cudaStream_t s) {
+  const Base* b = &c->base[base];
+  // the plain base needs no centring: t = 0 mod t_j
+  const uint64_t t_half = base == BASE_Q ? c->t_half : ~0ull;
+  const bool fast = base == BASE_Q && c->plain_fast;
   cudaError_t e = cudaSuccess;
   if (b->word == 4) {
     StreamArgs<uint32_t> a = sargs<uint32_t>(nullptr, out);
-    a.plain = m; a.t_half = c->t_half; a.plain_fast = c->plain_fast;
-    CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::LiftPrepare>(b, a, npoly, s)));
+    a.plain = m; a.t_half = t_half; a.plain_fast = fast;
+    if (prepare) CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::LiftPrepare>(b, a, npoly, s)))
+    else CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::LiftFwd>(b, a, npoly, s)))
   } else {
     StreamArgs<uint64_t> a = sargs<uint64_t>(nullptr, out);
-    a.plain = m; a.t_half = c->t_half; a.plain_fast = c->plain_fast;
-    CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::LiftPrepare>(b, a, npoly, s)));
+    a.plain = m; a.t_half = t_half; a.plain_fast = fast;
+    if (prepare) CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::LiftPrepare>(b, a, npoly, s)))
+    else CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::LiftFwd>(b, a, npoly, s)))
   }
   return e;
 }

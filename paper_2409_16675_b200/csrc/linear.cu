@@ -190,7 +190,7 @@ extern "C" int ctb_lift_prepare(const ctb_ctx_t* ctx, const uint64_t* m, void* o
   if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Ctx* c = cctx(ctx);
   if (!c || !c->t || !m || !out) { set_error("ctb_lift_prepare: needs plain ring and buffers"); return ERR_ARG; }
-  return cuda_status(stream_lift_prepare(c, m, out, n_polys, (cudaStream_t)stream), "ctb_lift_prepare");
+  return cuda_status(stream_lift(c, BASE_Q, true, m, out, n_polys, (cudaStream_t)stream), "ctb_lift_prepare");
 }
 
 extern "C" uint64_t ctb_linear_online_workspace_bytes(const ctb_ctx_t* ctx, uint32_t n_x, uint32_t n_w, uint32_t n_out,
@@ -270,10 +270,8 @@ extern "C" int ctb_linear_online(const ctb_ctx_t* ctx, const void* ct_x, uint32_
   if ((rc = ctb_lift_prepare(ctx, mx, MX, n_x, stream))) return rc;
   if ((rc = ctb_lift_prepare(ctx, mw, MW, n_w, stream))) return rc;
   // plain side: residues mod t_j of mx (eval) and mw (prepared)
-  if ((rc = ctb_rns_from_small(ctx, CTB_BASE_T, (const int64_t*)mx, MXt, n_x, stream))) return rc;
-  if ((rc = ctb_ntt_forward(ctx, CTB_BASE_T, MXt, MXt, n_x, stream))) return rc;
-  if ((rc = ctb_rns_from_small(ctx, CTB_BASE_T, (const int64_t*)mw, MWt, n_w, stream))) return rc;
-  if ((rc = ctb_prepare_operand(ctx, CTB_BASE_T, MWt, MWt, n_w, stream))) return rc;
+  if ((e = stream_lift(c, BASE_T, false, mx, MXt, n_x, s)) != cudaSuccess) return cuda_status(e, "ctb_linear_online lift");
+  if ((e = stream_lift(c, BASE_T, true, mw, MWt, n_w, s)) != cudaSuccess) return cuda_status(e, "ctb_linear_online lift");
   {
     // cipher side: gather-accumulate into out_ct (eval domain), then INTT in place + mask product
     const uint32_t nv = (uint32_t)(N * w / 16);

@@ -40,10 +40,27 @@ struct QConsts {
   PlainEval pe;
 };
 
+// Decrypt rounding for u32 limbs by value (constant bank), lazy 64-bit accumulation:
+// Garner digits a_j = (R_j - sum_{i<j} a_i M_i) M_j^-1 mod q_j, and R mod t_j as one dot
+// product sum_i a_i (M_i mod t_j) (30-bit digits x 25-bit constants, one reduction).
+constexpr int DEC_MAXQ = 8;
+struct DecLazy {
+  int L, LT;
+  uint32_t q[DEC_MAXQ], one_q[DEC_MAXQ], r2[DEC_MAXQ], r2q[DEC_MAXQ], h_q[DEC_MAXQ];
+  ShoupC<uint32_t> t_q[DEC_MAXQ];
+  uint32_t gM[DEC_MAXQ][DEC_MAXQ];  // M_i mod q_j (i < j)
+  ShoupC<uint32_t> gMinv[DEC_MAXQ];
+  uint32_t tM[2][DEC_MAXQ];         // M_i mod t_j
+  uint32_t tp[2], t_oneq[2], t_r2[2], t_r2q[2], h_t[2];
+  ShoupC<uint32_t> qinv_t[2], crt;
+};
+
 struct RnsConsts {
   void* d_q = nullptr;  // QConsts<T> for the cipher base
   int word = 4;
   int W = 1;
+  bool lazy = false;
+  DecLazy dec{};
   ~RnsConsts() {
     if (d_q) cudaFree(d_q);
   }
@@ -109,6 +126,57 @@ __global__ void k_decrypt_round(const T* v, uint64_t* out, const QConsts<T>* __r
       const uint32_t w0m = red64_u32(w[0], m1, c.pe.oneq[1], c.pe.r2[1], c.pe.r2q[1]);
       const uint32_t d = csub(shoup_mul<uint32_t>(sub_mod(w[1], w0m, m1), c.pe.crt.w, c.pe.crt.wq, m1), m1);
       res = (uint64_t)w[0] + (uint64_t)c.pe.tp[0] * d;
+    }
+    out[g] = res;
+  }
+}
+
+template <int LC>
+__global__ void __launch_bounds__(256) k_decrypt_round_lazy(const uint32_t* v, uint64_t* out,
+                                                            const __grid_constant__ DecLazy c, uint32_t n,
+                                                            uint64_t total) {
+  const int L = LC ? LC : c.L;
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t b = g / n, i = g % n;
+    uint32_t a[DEC_MAXQ];
+#pragma unroll
+    for (int j = 0; j < (LC ? LC : DEC_MAXQ); ++j) {
+      if (!LC && j >= L) break;
+      const uint32_t q = c.q[j];
+      const uint32_t x = v[(b * L + j) * n + i];
+      const uint32_t r = add_mod(csub(shoup_mul<uint32_t>(x, c.t_q[j].w, c.t_q[j].wq, q), q), c.h_q[j], q);
+      if (j == 0) {
+        a[0] = r;
+      } else {
+        uint64_t sacc = 0;
+#pragma unroll
+        for (int k = 0; k < j; ++k) sacc += (uint64_t)a[k] * c.gM[j][k];
+        const uint32_t sj = red64_u32(sacc, q, c.one_q[j], c.r2[j], c.r2q[j]);
+        a[j] = csub(shoup_mul<uint32_t>(sub_mod(r, sj, q), c.gMinv[j].w, c.gMinv[j].wq, q), q);
+      }
+    }
+    uint32_t w[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      if (t >= c.LT) break;
+      uint64_t sacc = 0;
+#pragma unroll
+      for (int k = 0; k < (LC ? LC : DEC_MAXQ); ++k) {
+        if (!LC && k >= L) break;
+        sacc += (uint64_t)a[k] * c.tM[t][k];
+      }
+      const uint32_t m = c.tp[t];
+      const uint32_t Rj = red64_u32(sacc, m, c.t_oneq[t], c.t_r2[t], c.t_r2q[t]);
+      const uint32_t d = sub_mod(c.h_t[t], Rj, m);
+      w[t] = csub(shoup_mul<uint32_t>(d, c.qinv_t[t].w, c.qinv_t[t].wq, m), m);
+    }
+    uint64_t res = w[0];
+    if (c.LT == 2) {
+      const uint32_t m1 = c.tp[1];
+      const uint32_t w0m = red64_u32(w[0], m1, c.t_oneq[1], c.t_r2[1], c.t_r2q[1]);
+      const uint32_t d = csub(shoup_mul<uint32_t>(sub_mod(w[1], w0m, m1), c.crt.w, c.crt.wq, m1), m1);
+      res = (uint64_t)w[0] + (uint64_t)c.tp[0] * d;
     }
     out[g] = res;
   }
@@ -229,6 +297,30 @@ static int build_q_consts(Ctx* c, RnsConsts* rc, std::string& err) {
     pe.qinv_t[j] = shoup_pair<uint32_t>(invmod(Q.mod_small(m), m), m);
   }
   if (pe.LT == 2) pe.crt = shoup_pair<uint32_t>(invmod(tp[0] % tp[1], tp[1]), tp[1]);
+  if (sizeof(T) == 4 && (int)q.size() <= DEC_MAXQ && pe.LT >= 1) {
+    DecLazy& d = rc->dec;
+    d.L = (int)q.size();
+    d.LT = pe.LT;
+    std::vector<BigU> M(q.size() + 1, BigU(1));
+    for (size_t i = 1; i <= q.size(); ++i) { M[i] = M[i - 1]; M[i].mul_small(q[i - 1]); }
+    for (size_t j = 0; j < q.size(); ++j) {
+      d.q[j] = (uint32_t)q[j];
+      d.one_q[j] = (uint32_t)h->mrc.one_q[j];
+      d.r2[j] = (uint32_t)h->r2[j];
+      d.r2q[j] = (uint32_t)h->r2q[j];
+      d.h_q[j] = (uint32_t)h->h_q[j];
+      d.t_q[j] = ShoupC<uint32_t>{(uint32_t)h->t_q[j].w, (uint32_t)h->t_q[j].wq};
+      for (size_t i = 0; i < j; ++i) d.gM[j][i] = (uint32_t)M[i].mod_small(q[j]);
+      d.gMinv[j] = shoup_pair<uint32_t>(invmod(M[j].mod_small(q[j]), q[j]), q[j]);
+    }
+    for (int j = 0; j < pe.LT; ++j) {
+      d.tp[j] = pe.tp[j]; d.t_oneq[j] = pe.oneq[j]; d.t_r2[j] = pe.r2[j]; d.t_r2q[j] = pe.r2q[j];
+      d.h_t[j] = pe.h_t[j]; d.qinv_t[j] = pe.qinv_t[j];
+      for (size_t i = 0; i < q.size(); ++i) d.tM[j][i] = (uint32_t)M[i].mod_small(tp[j]);
+    }
+    d.crt = pe.crt;
+    rc->lazy = true;
+  }
   cudaError_t e = cudaMalloc(&rc->d_q, sizeof(QConsts<T>));
   if (e == cudaSuccess) e = cudaMemcpy(rc->d_q, h, sizeof(QConsts<T>), cudaMemcpyHostToDevice);
   rc->W = h->W;
@@ -265,7 +357,12 @@ extern "C" int ctb_decrypt_round(const ctb_ctx_t* ctx, const void* v, uint64_t* 
   const uint64_t total = n_polys * c->n;
   if (!total) return OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (c->rns->word == 4)
+  if (c->rns->lazy) {
+    if (c->rns->dec.L == 7)
+      k_decrypt_round_lazy<7><<<grid_for(total), 256, 0, s>>>((const uint32_t*)v, out, c->rns->dec, c->n, total);
+    else
+      k_decrypt_round_lazy<0><<<grid_for(total), 256, 0, s>>>((const uint32_t*)v, out, c->rns->dec, c->n, total);
+  } else if (c->rns->word == 4)
     k_decrypt_round<uint32_t><<<grid_for(total), 256, 0, s>>>((const uint32_t*)v, out,
                                                               (const QConsts<uint32_t>*)c->rns->d_q, c->n, total);
   else
