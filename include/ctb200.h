@@ -49,7 +49,7 @@ int ctb_version(void);
 
 /* Context: replaces ring._plan/_NttPlan (ring.py:164-229) and the derived
  * constants of he.HeParams (he.py:61-132).  q_primes: the declared factorisation
- * of the cipher (or single) ring modulus, each = 1 mod 2N, < 2^62.  t_primes:
+ * of the cipher (or single) ring modulus, each = 1 mod 2N, < 2^50.  t_primes:
  * factorisation of the plain modulus (n_t = 0 for a ring-only context).
  * relin_base_bits: he.HeParams.relin_base_bits (he.py:68). */
 int ctb_ctx_create(ctb_ctx_t** out, uint32_t n, const uint64_t* q_primes, uint32_t n_q,

@@ -104,12 +104,22 @@ static int build_typed(Base& b, uint32_t logn, std::string& err, const uint64_t*
             const size_t e = (size_t)shape_tw_off((int)logn, k) + ((size_t)((1u << i) - 1 + jb) << s) +
                              tw_group_slot((int)logn, s, r, B);
             const uint64_t w = pw[bitrev(mb, logn)];
-            f[2 * e] = (T)w;  f[2 * e + 1] = shoup_q<T>(w, p);
+            if (sizeof(T) == 4) {
+              f[2 * e] = (T)w;  f[2 * e + 1] = shoup_q<T>(w, p);
+            } else {  // 64-bit limbs run the FP64 butterflies (ntt.cuh): (w, w/p) as doubles
+              const double wd = (double)w, wp = (double)w / (double)p;
+              uint64_t bw, bq;
+              std::memcpy(&bw, &wd, 8);
+              std::memcpy(&bq, &wp, 8);
+              f[2 * e] = (T)bw;  f[2 * e + 1] = (T)bq;
+            }
           }
     }
     PrimeTab<T>& t = tabs[l];
     std::memset(&t, 0, sizeof(t));
     t.p = (T)p; t.p2 = (T)(2 * p);
+    t.dp = (double)p;
+    t.dpinv = 1.0 / (double)p;
     T x = 1;  // Newton: p^-1 mod 2^W
     for (int it = 0; it < 7; ++it) x = (T)(x * (T)(2 - (T)p * x));
     t.pinv = x;
@@ -144,7 +154,7 @@ int build_base(Base& b, const uint64_t* primes, int count, uint32_t logn, std::s
   bool small = true;
   for (uint64_t p : b.primes) {
     if (p < 3 || p % (2ull * n) != 1) { err = "prime " + std::to_string(p) + " is not 1 mod 2N"; return -1; }
-    if (p >= (1ull << 62)) { err = "prime " + std::to_string(p) + " exceeds 62 bits"; return -1; }
+    if (p >= (1ull << 50)) { err = "prime " + std::to_string(p) + " exceeds 50 bits (64-bit limbs run FP64 butterflies)"; return -1; }
     if (p >= (1ull << 30)) small = false;
   }
   b.word = small ? 4 : 8;

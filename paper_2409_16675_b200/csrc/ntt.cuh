@@ -36,7 +36,9 @@ struct PrimeTab {
   T tmod;               // plain modulus t mod p (cipher base only: centred lift)
   T delta, delta_q;     // floor(q/t) mod p and Shoup quotient (cipher base only)
   T c25, c25_q;         // 2^25 mod p and Shoup quotient (u32, p > 2^25): one-multiply plain reduction
+  double dp, dpinv;     // p and 1/p as doubles (64-bit limbs: FP64 butterflies)
   const T* fwd;         // (w, w') pairs, pass-major / entry-major (see TwSrc); serves both directions
+                        // (64-bit limbs: the bits of (double w, double w/p))
   const T* inv;         // == fwd (kept for layout stability)
 };
 
@@ -297,14 +299,15 @@ struct Exchanger {
   T* buf;      // NBUF * SmemImage::WORDS words
   int cur = 0;
   static constexpr int WORDS = NBUF * SmemImage<T, LOGN>::WORDS;
-  template <int SA, int RA, int SB, int RB>
-  __device__ __forceinline__ void run(T (&x)[NttShape<LOGN>::E]) {
+  template <int SA, int RA, int SB, int RB, typename U>
+  __device__ __forceinline__ void run(U (&x)[NttShape<LOGN>::E]) {
+    static_assert(sizeof(U) == sizeof(T), "exchange element width");
     using Sh = NttShape<LOGN>;
-    T* b = buf + cur * SmemImage<T, LOGN>::WORDS;
+    U* b = reinterpret_cast<U*>(buf + cur * SmemImage<T, LOGN>::WORDS);
     if constexpr (NBUF == 2) cur ^= 1;
     else group_sync<LOGN, GROUPS>();
-    T* wa = b + phys<T, LOGN>(pass_index<LOGN, SA, RA>(ntt_tid<LOGN>(), 0));
-    T* wb = b + phys<T, LOGN>(pass_index<LOGN, SB, RB>(ntt_tid<LOGN>(), 0));
+    U* wa = b + phys<T, LOGN>(pass_index<LOGN, SA, RA>(ntt_tid<LOGN>(), 0));
+    U* wb = b + phys<T, LOGN>(pass_index<LOGN, SB, RB>(ntt_tid<LOGN>(), 0));
 #pragma unroll
     for (int k = 0; k < Sh::E; ++k) wa[phys<T, LOGN>(pass_index<LOGN, SA, RA>(0, k))] = x[k];
     group_sync<LOGN, GROUPS>();
@@ -313,15 +316,152 @@ struct Exchanger {
   }
 };
 
+// ---- FP64 butterflies for 64-bit limbs (primes < 2^50) --------------------------------
+// Residues are held as exact integers in doubles, signed and lazily reduced.  For |x| < 2^51:
+//   mulmod(x, w): hi = fl(x w), lo = x w - hi (exact, fma), q = rint(x * fl(w/p)) is within 1
+//   of x w / p (relative error < 2^-52 on a value < 2^51), r = (hi - q p) + lo is exact and
+//   |r| < p;
+//   center(x) = x - p rint(x / p) in [-p/2, p/2] (tiny slack) for |x| < 2^51.
+// rint uses the 1.5 * 2^52 magic constant (exact for |y| < 2^51).  Forward (CT) invariant:
+// inputs in (-2p, 2p) -> outputs in (-1.5p, 1.5p); inverse (GS): (-p, p) -> (-p, p).
+// The integer Shoup product costs ~4x its 32-bit form; on B200's full-rate FP64 pipe this
+// costs ~11 FP64 operations per butterfly (2x the integer modmul throughput, measured by
+// tools/probe/f64_modmul.cu).
+struct F64Prime {
+  double p, pinv;
+};
+__device__ __forceinline__ double f64_rint(double y) {
+  constexpr double C = 6755399441055744.0;  // 1.5 * 2^52
+  return __dadd_rn(__dadd_rn(y, C), -C);
+}
+__device__ __forceinline__ double f64_mulmod(double x, double w, double wp, double p) {
+  const double hi = __dmul_rn(x, w);
+  const double lo = __fma_rn(x, w, -hi);
+  const double q = f64_rint(__dmul_rn(x, wp));
+  return __dadd_rn(__fma_rn(-q, p, hi), lo);
+}
+__device__ __forceinline__ double f64_center(double x, const F64Prime& P) {
+  const double q = f64_rint(__dmul_rn(x, P.pinv));
+  return __fma_rn(-q, P.p, x);
+}
+// u64 residue (< 2^52) <-> double, exact, by exponent-bit splicing.
+__device__ __forceinline__ double f64_from_u64(uint64_t x) {
+  return __dadd_rn(__longlong_as_double((long long)(x | 0x4330000000000000ull)), -4503599627370496.0);
+}
+__device__ __forceinline__ uint64_t f64_to_canon(double x, const F64Prime& P) {  // x in (-2p, 2p)
+  double y = f64_center(x, P);                   // [-p/2 - e, p/2 + e]
+  y = y < 0.0 ? __dadd_rn(y, P.p) : y;           // [0, p)
+  return (uint64_t)__double_as_longlong(__dadd_rn(y, 4503599627370496.0)) & 0x000FFFFFFFFFFFFFull;
+}
+
+template <typename T, bool SMEM>
+__device__ __forceinline__ void tw_load_f64(const TwSrc<T, SMEM>& tw, const T* at, double& w, double& wp) {
+  T a, b;
+  tw.load(at, a, b);
+  w = __longlong_as_double((long long)a);
+  wp = __longlong_as_double((long long)b);
+}
+
+template <typename T, int LOGN, int K, bool SMEM>
+__device__ __forceinline__ void fwd_pass_f64(double (&x)[NttShape<LOGN>::E], TwSrc<T, SMEM> tw, const F64Prime& P) {
+  using Sh = NttShape<LOGN>;
+  constexpr int S0 = Sh::pass_s(K), R = Sh::pass_r(K);
+  constexpr int G = 1 << R;
+#pragma unroll
+  for (int gg = 0; gg < Sh::E / G; ++gg) {
+    const int slot = tw_slot<LOGN, S0, R>(gg);
+    const T* tg = tw.tab + 2 * (Sh::tw_off(K) + slot);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int h = 1 << (R - i - 1);
+#pragma unroll
+      for (int jb = 0; jb < (1 << i); ++jb) {
+        double w, wp;
+        tw_load_f64(tw, tg + 2 * (((1 << i) - 1 + jb) << S0), w, wp);
+#pragma unroll
+        for (int jj = 0; jj < h; ++jj) {
+          const int a = gg * G + jb * 2 * h + jj;
+          const double X = f64_center(x[a], P);
+          const double t = f64_mulmod(x[a + h], w, wp, P.p);
+          x[a] = __dadd_rn(X, t);
+          x[a + h] = __dadd_rn(X, -t);
+        }
+      }
+    }
+  }
+}
+
+template <typename T, int LOGN, int K, bool SMEM>
+__device__ __forceinline__ void inv_pass_f64(double (&x)[NttShape<LOGN>::E], TwSrc<T, SMEM> tw, const F64Prime& P) {
+  using Sh = NttShape<LOGN>;
+  constexpr int S0 = Sh::pass_s(K), R = Sh::pass_r(K);
+  constexpr int G = 1 << R;
+#pragma unroll
+  for (int gg = 0; gg < Sh::E / G; ++gg) {
+    const int slot = (1 << S0) - 1 - tw_slot<LOGN, S0, R>(gg);
+    const T* tg = tw.tab + 2 * (Sh::tw_off(K) + slot);
+#pragma unroll
+    for (int i = R - 1; i >= 0; --i) {
+      const int h = 1 << (R - i - 1);
+#pragma unroll
+      for (int jb = 0; jb < (1 << i); ++jb) {
+        double w, wp;
+        tw_load_f64(tw, tg + 2 * (((1 << i) - 1 + ((1 << i) - 1 - jb)) << S0), w, wp);
+#pragma unroll
+        for (int jj = 0; jj < h; ++jj) {
+          const int a = gg * G + jb * 2 * h + jj;
+          const double X = x[a], Y = x[a + h];
+          x[a] = f64_center(__dadd_rn(X, Y), P);
+          x[a + h] = f64_mulmod(__dadd_rn(Y, -X), w, wp, P.p);
+        }
+      }
+    }
+  }
+}
+
+template <typename T, int LOGN, int K, bool SMEM, int NBUF, int GROUPS>
+__device__ __forceinline__ void ntt_fwd_f64(double (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN, NBUF, GROUPS>& ex,
+                                            TwSrc<T, SMEM> tw, const F64Prime& P) {
+  using Sh = NttShape<LOGN>;
+  fwd_pass_f64<T, LOGN, K, SMEM>(x, tw, P);
+  if constexpr (K + 1 < Sh::NPASS) {
+    ex.template run<Sh::pass_s(K), Sh::pass_r(K), Sh::pass_s(K + 1), Sh::pass_r(K + 1)>(x);
+    ntt_fwd_f64<T, LOGN, K + 1, SMEM, NBUF, GROUPS>(x, ex, tw, P);
+  }
+}
+
+template <typename T, int LOGN, int K, bool SMEM, int NBUF, int GROUPS>
+__device__ __forceinline__ void ntt_inv_f64(double (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN, NBUF, GROUPS>& ex,
+                                            TwSrc<T, SMEM> tw, const F64Prime& P) {
+  using Sh = NttShape<LOGN>;
+  inv_pass_f64<T, LOGN, K, SMEM>(x, tw, P);
+  if constexpr (K > 0) {
+    ex.template run<Sh::pass_s(K), Sh::pass_r(K), Sh::pass_s(K - 1), Sh::pass_r(K - 1)>(x);
+    ntt_inv_f64<T, LOGN, K - 1, SMEM, NBUF, GROUPS>(x, ex, tw, P);
+  }
+}
+
 template <typename T, int LOGN, int K = 0, bool SMEM, int NBUF, int GROUPS>
 __device__ __forceinline__ void ntt_fwd_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN, NBUF, GROUPS>& ex,
                                              TwSrc<T, SMEM> tw, T p, T p2) {
   using Sh = NttShape<LOGN>;
-  constexpr int S = Sh::pass_s(K), R = Sh::pass_r(K);
-  fwd_pass<T, LOGN, K, SMEM>(x, tw, p, p2);
-  if constexpr (K + 1 < Sh::NPASS) {
-    ex.template run<S, R, Sh::pass_s(K + 1), Sh::pass_r(K + 1)>(x);
-    ntt_fwd_regs<T, LOGN, K + 1, SMEM, NBUF, GROUPS>(x, ex, tw, p, p2);
+  if constexpr (sizeof(T) == 8) {
+    // 64-bit limbs: FP64 butterflies, inputs < 4p (< 2^52), outputs canonical [0, p)
+    static_assert(K == 0, "64-bit limbs transform whole polynomials");
+    const F64Prime P{(double)p, __drcp_rn((double)p)};
+    double d[Sh::E];
+#pragma unroll
+    for (int k = 0; k < Sh::E; ++k) d[k] = f64_center(f64_from_u64(x[k]), P);
+    ntt_fwd_f64<T, LOGN, 0, SMEM, NBUF, GROUPS>(d, ex, tw, P);
+#pragma unroll
+    for (int k = 0; k < Sh::E; ++k) x[k] = f64_to_canon(d[k], P);
+  } else {
+    constexpr int S = Sh::pass_s(K), R = Sh::pass_r(K);
+    fwd_pass<T, LOGN, K, SMEM>(x, tw, p, p2);
+    if constexpr (K + 1 < Sh::NPASS) {
+      ex.template run<S, R, Sh::pass_s(K + 1), Sh::pass_r(K + 1)>(x);
+      ntt_fwd_regs<T, LOGN, K + 1, SMEM, NBUF, GROUPS>(x, ex, tw, p, p2);
+    }
   }
 }
 
@@ -329,14 +469,23 @@ template <typename T, int LOGN, int K = NttShape<LOGN>::NPASS - 1, bool SMEM, in
 __device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN, NBUF, GROUPS>& ex,
                                              TwSrc<T, SMEM> tw, T p, T p2) {
   using Sh = NttShape<LOGN>;
-  constexpr int S = Sh::pass_s(K), R = Sh::pass_r(K);
-  inv_pass<T, LOGN, K, SMEM>(x, tw, p, p2);
-  if constexpr (K > 0) {
-    ex.template run<S, R, Sh::pass_s(K - 1), Sh::pass_r(K - 1)>(x);
-    ntt_inv_regs<T, LOGN, K - 1, SMEM, NBUF, GROUPS>(x, ex, tw, p, p2);
-  } else if constexpr (sizeof(T) == 8) {
+  if constexpr (sizeof(T) == 8) {
+    // 64-bit limbs: FP64 butterflies, inputs < 4p, outputs canonical [0, p)
+    static_assert(K == Sh::NPASS - 1, "64-bit limbs transform whole polynomials");
+    const F64Prime P{(double)p, __drcp_rn((double)p)};
+    double d[Sh::E];
 #pragma unroll
-    for (int k = 0; k < Sh::E; ++k) x[k] = csub(x[k], p2);  // [0,4p) -> [0,2p), as the u32 path
+    for (int k = 0; k < Sh::E; ++k) d[k] = f64_center(f64_from_u64(x[k]), P);
+    ntt_inv_f64<T, LOGN, Sh::NPASS - 1, SMEM, NBUF, GROUPS>(d, ex, tw, P);
+#pragma unroll
+    for (int k = 0; k < Sh::E; ++k) x[k] = f64_to_canon(d[k], P);
+  } else {
+    constexpr int S = Sh::pass_s(K), R = Sh::pass_r(K);
+    inv_pass<T, LOGN, K, SMEM>(x, tw, p, p2);
+    if constexpr (K > 0) {
+      ex.template run<S, R, Sh::pass_s(K - 1), Sh::pass_r(K - 1)>(x);
+      ntt_inv_regs<T, LOGN, K - 1, SMEM, NBUF, GROUPS>(x, ex, tw, p, p2);
+    }
   }
 }
 

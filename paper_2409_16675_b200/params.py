@@ -5,7 +5,7 @@ Mirrors the reference's parameter layer so the same parameter sets come out:
   is_prime / ntt_primes     ring.py:39-78   (deterministic Miller-Rabin, descending search)
   HeParams + noise algebra  he.py:61-132
   default_*_params          he.py:135-165
-One deliberate extension: declared primes may be up to 62 bits (the reference
+One deliberate extension: declared primes may be up to 50 bits (the reference
 caps them below 2^31 for its numpy uint64 kernels, ring.py:134-135); the
 device kernels carry 64-bit residues, which is what the N=8192 / 3 x 50-bit
 configurations need.
@@ -84,8 +84,8 @@ class RingParams:
             for p in self.primes:
                 if p % (2 * self.n) != 1:
                     raise ValueError(f"prime {p} is not 1 mod {2 * self.n}")
-                if p >= 1 << 62:
-                    raise ValueError(f"prime {p} too large for the 64-bit device kernels")
+                if p >= 1 << 50:
+                    raise ValueError(f"prime {p} too large for the device kernels (64-bit limbs: < 2^50)")
                 prod *= p
             if prod != self.modulus:
                 raise ValueError("declared primes do not multiply to the modulus")

@@ -15,7 +15,7 @@ through the exact positional conversion kernel.
 Deliberate differences: the degree must be >= 4 and <= 8192,
 moduli must carry an NTT-friendly factorisation (the reference's schoolbook
 fallback for non-NTT moduli, ring.py:427-439, has no device path and raises
-NttUnavailableError), and declared primes may reach 62 bits.
+NttUnavailableError), and declared primes may reach 50 bits.
 """
 from __future__ import annotations
 
