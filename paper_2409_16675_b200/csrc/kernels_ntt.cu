@@ -179,8 +179,10 @@ struct StreamCfg {
   static constexpr int GROUPS = cpmul_groups<T, LOGN>();
   using Ex = Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>;
   static constexpr size_t TW_BYTES = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
-  static constexpr bool SMEM_TW = sizeof(T) == 4 && LOGN >= 9 &&
-                                  TW_BYTES + GROUPS * (size_t)Ex::WORDS * sizeof(T) <= 200 * 1024;
+  // u32: table + images within 200 KB (two CTAs per SM with staging); 64-bit limbs: the
+  // (w, w/p) table (140 KB at N=8192) + image fill one CTA's 227 KB
+  static constexpr bool SMEM_TW = LOGN >= 9 && TW_BYTES + GROUPS * (size_t)Ex::WORDS * sizeof(T) <=
+                                                   (sizeof(T) == 4 ? 200 * 1024 : 226 * 1024);
   // TMA prefetch of the next item into an N-word staging buffer per group (u32, where the
   // table + images + staging still fit two CTAs per SM)
   static constexpr int EXW = (Ex::WORDS * (int)sizeof(T) + 15) / 16 * 16 / (int)sizeof(T);

@@ -334,14 +334,19 @@ __device__ __forceinline__ double f64_rint(double y) {
   constexpr double C = 6755399441055744.0;  // 1.5 * 2^52
   return __dadd_rn(__dadd_rn(y, C), -C);
 }
+// rint(a * b) for |a * b| < 2^51, the magic constant folded into the product's FMA
+__device__ __forceinline__ double f64_rint_mul(double a, double b) {
+  constexpr double C = 6755399441055744.0;  // 1.5 * 2^52
+  return __dadd_rn(__fma_rn(a, b, C), -C);
+}
 __device__ __forceinline__ double f64_mulmod(double x, double w, double wp, double p) {
   const double hi = __dmul_rn(x, w);
   const double lo = __fma_rn(x, w, -hi);
-  const double q = f64_rint(__dmul_rn(x, wp));
+  const double q = f64_rint_mul(x, wp);
   return __dadd_rn(__fma_rn(-q, p, hi), lo);
 }
 __device__ __forceinline__ double f64_center(double x, const F64Prime& P) {
-  const double q = f64_rint(__dmul_rn(x, P.pinv));
+  const double q = f64_rint_mul(x, P.pinv);
   return __fma_rn(-q, P.p, x);
 }
 // u64 residue (< 2^52) <-> double, exact, by exponent-bit splicing.

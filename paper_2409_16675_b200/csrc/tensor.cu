@@ -512,7 +512,7 @@ struct RelinCfg {
   using Ex = Exchanger<T, LOGN, 1, 1>;
   static constexpr size_t TW_BYTES = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
   static constexpr size_t EX_BYTES = ((size_t)Ex::WORDS * sizeof(T) + 15) / 16 * 16;
-  static constexpr bool SMEM_TW = sizeof(T) == 4 && LOGN >= 9 && TW_BYTES + EX_BYTES <= 110 * 1024;
+  static constexpr bool SMEM_TW = sizeof(T) == 4 && LOGN >= 9 && TW_BYTES + EX_BYTES <= 110 * 1024;  // u64: measured slower
   // digits (u32 [N]) staged by TMA one transform ahead: measured slower here (an extra CTA
   // barrier per digit, keys dominate the traffic), kept switchable
   static constexpr bool PF = false;
