@@ -216,13 +216,18 @@ __device__ __forceinline__ void crt_extend(const TensorConsts<TQ>& c, int n_rt, 
       }
       x = red_u32(acc, q, c.mrcQ.one_q[l], c.q_r2[l], c.q_r2q[l]);
     } else {
-      TQ acc = 0;  // sum of terms in [0, 2q): < 40 q < 2^56
+      // 50-bit q_l: FP64 products (ntt.cuh f64_mulmod; constants as (c, c/q) doubles), each in
+      // (-q, q), the running sum re-centred every 4 terms
+      const F64Prime P{(double)q, __drcp_rn((double)q)};
+      double acc = 0.0;
 #pragma unroll
       for (int k = 0; k < (NC ? NC : MAXA); ++k) {
         if (!NC && k >= n) break;
-        acc += shoup_mul<TQ>((TQ)xi[k], hat_q[l][k].w, hat_q[l][k].wq, q);
+        acc = __dadd_rn(acc, f64_mulmod((double)xi[k], __longlong_as_double((long long)hat_q[l][k].w),
+                                        __longlong_as_double((long long)hat_q[l][k].wq), P.p));
+        if ((k & 3) == 3) acc = f64_center(acc, P);
       }
-      x = csub(shoup_mul<TQ>(acc, (TQ)1, c.mrcQ.one_q[l], q), q);
+      x = (TQ)f64_to_canon(acc, P);
     }
     x = sub_mod(x, v_q[l][v], q);
     out[l] = sub_mod(x, shift[l], q);
@@ -952,7 +957,18 @@ static int build_tensor(Ctx* c, std::string& err) {
         BigU hat = big_div(MM, BigU(ps[k]));
         hinv[k] = spair<uint32_t>(invmod(hat.mod_small(ps[k]), ps[k]), ps[k]);
         rcp[k] = (float)(1.0 / (double)ps[k]);
-        for (int l = 0; l < L; ++l) hat_q[l][k] = spair<TQ>(hat.mod_small(q[l]), q[l]);
+        for (int l = 0; l < L; ++l) {
+          const uint64_t c = hat.mod_small(q[l]);
+          if (sizeof(TQ) == 4) {
+            hat_q[l][k] = spair<TQ>(c, q[l]);
+          } else {  // 50-bit limbs: the bits of (double c, double c/q) for the FP64 products
+            const double cd = (double)c, cq = (double)c / (double)q[l];
+            uint64_t bc, bq;
+            std::memcpy(&bc, &cd, 8);
+            std::memcpy(&bq, &cq, 8);
+            hat_q[l][k] = ShoupC<TQ>{(TQ)bc, (TQ)bq};
+          }
+        }
       }
       for (int l = 0; l < L; ++l) {
         const uint64_t mq = MM.mod_small(q[l]);
