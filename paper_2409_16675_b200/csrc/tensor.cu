@@ -9,22 +9,24 @@
 //     (c0 + sum d_i b_i, c1 + sum d_i a_i) mod q.
 //
 // Device algorithm, all exact:
-//  1 k_tensor_lift   per coefficient: Garner digits of x over Q; x > (Q-1)/2 is
-//    decided digit-wise against the digits of (Q-1)/2; residues of the centred
-//    value over the auxiliary base A (30-bit NTT primes, a superset of Q when
-//    Q's primes are 30-bit) by Horner evaluation minus Q mod p.
+//  1 k_tensor_lift   per coefficient: Garner digits of x over Q (u32 limbs: 64-bit
+//    accumulated, one reduction per digit); x > (Q-1)/2 is decided digit-wise against
+//    the digits of (Q-1)/2; residues of the centred value over the auxiliary base A
+//    (30-bit NTT primes, a superset of Q when Q's primes are 30-bit) as mixed-radix dot
+//    products, minus Q mod p when negative.
 //  2 k_tensor_product  per (ciphertext, aux prime) CTA: 4 forward NTTs, the
 //    3 slotwise tensor products, 3 inverse NTTs -> h residues over A.
 //  3 k_tensor_round  per coefficient, with z = h t + (Q-1)/2 (so the result is
 //    floor(z / Q) for either sign of h): r = z mod Q from z's residues mod Q
-//    (Garner), y = (z - r) Q^-1 modulo each prime of P2 (aux primes outside Q,
-//    product > 2|y|+1), then the centred y is base-extended from P2 to Q.  When
-//    Q's primes are not in A (50-bit limbs), h itself is first extended exactly
-//    from A to Q (product of A > 2|h|+1).
-//  4 k_relin_digits  Garner digits of c2 -> positional 32-bit words -> w-bit digits.
+//    (Garner), y = (z - r) Q^-1 modulo each prime of P2 (aux primes outside Q),
+//    then y + floor(P2/2) is extended to Q by the float-assisted exact CRT
+//    (crt_extend; P2 > 4(|y|max + 1)).  When Q's primes are not in A (50-bit limbs),
+//    h + floor(M_A/2) is first extended the same way from A to Q.
+//  4 k_relin_digits  w-bit digits of c2 from its Garner digits (limb dot products).
 //  5 k_relin_accum   per (ciphertext, limb) CTA: sum over digits of
 //    NTT(d_i) * prepared(b_i), NTT(d_i) * prepared(a_i) in registers, 2 INTT,
 //    + (c0, c1).
+//  6 ctb_ccmul_sum   the fused per-slot form of 1-5 (offline mask products).
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -59,12 +61,8 @@ struct TensorConsts {
   ShoupC<uint32_t> r_hc[MAXA][MAXQ];  // q_j mod p2_k
   ShoupC<uint32_t> Qinv_p2[MAXA];     // Q^-1 mod p2_k
   uint32_t Ky_p2[MAXA];               // floor(P2/2) mod p2_k
-  MrcTab<uint32_t> mrcP2;
-  ShoupC<TQ> y_hc[MAXQ][MAXA];        // p2_k mod q_i
   TQ Ky_q[MAXQ];                      // floor(P2/2) mod q_i
-  MrcTab<uint32_t> mrcA;              // Garner over all aux (exact h extension)
   uint32_t Kh_aux[MAXA];              // floor(M_A/2) mod p_k
-  ShoupC<TQ> h_hc[MAXQ][MAXA];        // p_k mod q_i
   TQ Kh_q[MAXQ];                      // floor(M_A/2) mod q_i
   // lazy (64-bit accumulated) forms, TQ = u32 only
   uint32_t q_r2[MAXQ], q_r2q[MAXQ];   // 2^32 mod q_i and its Shoup quotient (64-bit reduction)
@@ -922,19 +920,11 @@ static int build_tensor(Ctx* c, std::string& err) {
     h->Qinv_p2[k] = spair<uint32_t>(invmod(Q.mod_small(p), p), p);
     h->Ky_p2[k] = (uint32_t)Ky.mod_small(p);
   }
-  fill_mrc_tab(h->mrcP2, p2);
-  for (int l = 0; l < L; ++l) {
-    for (int k = 0; k + 1 < h->K2; ++k) h->y_hc[l][k] = spair<TQ>(p2[k] % q[l], q[l]);
-    h->Ky_q[l] = (TQ)Ky.mod_small(q[l]);
-  }
+  for (int l = 0; l < L; ++l) h->Ky_q[l] = (TQ)Ky.mod_small(q[l]);
   if (h->ext_h) {
-    fill_mrc_tab(h->mrcA, aux);
     BigU Kh = MA; Kh.shr1();
     for (int k = 0; k < h->K; ++k) h->Kh_aux[k] = (uint32_t)Kh.mod_small(aux[k]);
-    for (int l = 0; l < L; ++l) {
-      for (int k = 0; k + 1 < h->K; ++k) h->h_hc[l][k] = spair<TQ>(aux[k] % q[l], q[l]);
-      h->Kh_q[l] = (TQ)Kh.mod_small(q[l]);
-    }
+    for (int l = 0; l < L; ++l) h->Kh_q[l] = (TQ)Kh.mod_small(q[l]);
   }
   // lazy forms
   {
