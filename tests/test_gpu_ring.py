@@ -154,3 +154,27 @@ def test_encrypted_cpmul_decrypts(golden, p4096, ctx4096):
     out = _np(ctx4096.cpmul(_t(cte[None], ctx4096.dtype()), _t(pt[None], torch.int64)))[0]
     assert digest(out) == g["enc_cpmul"]
     assert digest(H.decrypt(P, out, keys["s"])) == g["dec"]
+
+
+@pytest.mark.parametrize("logn", [6, 12, 13])
+def test_fp64_butterflies_extreme_inputs(logn):
+    """50-bit limbs run FP64 butterflies (ntt.cuh): all-(p-1), alternating 0/(p-1) and
+    single-spike inputs on the largest primes below 2^50 must match the exact oracle."""
+    from paper_2409_16675_b200.device import RnsContext
+    n = 1 << logn
+    primes = R.ntt_primes(n, 50, 3)
+    ctx = RnsContext.get(n, primes)
+    pv = np.asarray(primes, dtype=np.uint64)[:, None]
+    full = np.broadcast_to(pv - 1, (3, n))
+    alt = np.where(np.arange(n) % 2 == 0, 0, pv - 1).astype(np.uint64)
+    spike = np.zeros((3, n), dtype=np.uint64)
+    spike[:, n - 1] = (pv - 1)[:, 0]
+    a = np.stack([full, alt, spike]).astype(np.uint64)
+    fa = _np(ctx.ntt_forward(_t(a, ctx.dtype())))
+    for b in range(3):
+        for i, p in enumerate(primes):
+            assert np.array_equal(fa[b, i], np.asarray(R.NttPlan(n, p).forward(a[b, i]), dtype=np.uint64)), (b, i)
+    back = _np(ctx.ntt_inverse(_t(fa.astype(np.int64), ctx.dtype())))
+    assert np.array_equal(back, a)
+    got = _np(ctx.ring_mul(_t(a, ctx.dtype()), _t(a[::-1].copy(), ctx.dtype())))
+    assert np.array_equal(got, R.ring_mul_rns(a, a[::-1].copy(), primes))
