@@ -280,15 +280,6 @@ class He:
                                                      _ptr(out), npoly, _stream()), "ctb_rns_elementwise")
         return out
 
-    def _mul_prepared(self, a: torch.Tensor, bprep: torch.Tensor, addend: torch.Tensor | None,
-                      broadcast: bool = True) -> torch.Tensor:
-        out = torch.empty_like(a)
-        npoly = a.numel() // (self.L * self.params.n)
-        _lib.check(self.ctx._lib.ctb_mul_prepared(self.ctx._h, BASE_Q, _ptr(a), _ptr(bprep), 0 if broadcast else 1,
-                                                  _ptr(addend) if addend is not None else None, _ptr(out), npoly,
-                                                  _stream()), "ctb_mul_prepared")
-        return out
-
     def _plain_tensor(self, pts) -> torch.Tensor:
         if isinstance(pts, torch.Tensor):
             return pts.contiguous()

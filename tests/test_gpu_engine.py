@@ -105,7 +105,7 @@ def test_engine_errors(params):
 
 def test_lowerings_and_batch(params, rng):
     from oracle.plainconv import conv2d_multi
-    from paper_2409_16675_b200 import engine, packing
+    from paper_2409_16675_b200 import engine, linprot, packing
     sess = engine.DeviceSession(params, auto_offline=True)
     eng = engine.DeviceSecureEngine(sess)
     x = rng.integers(-100, 100, size=(2, 10, 10))
@@ -122,4 +122,14 @@ def test_lowerings_and_batch(params, rng):
     got = eng.conv_forward_batch(xs, w, packing.ConvShape(10, 10, 3, 1))
     for bi in range(3):
         assert np.array_equal(got[bi], eng.conv_forward(xs[bi], w, packing.ConvShape(10, 10, 3, 1)))
+    gys = rng.integers(-20, 20, size=(3, 3, 10, 10))
+    gw = eng.conv_pairwise_batch(xs, gys, packing.ConvShape(10, 10, 10, 1))
+    for bi in range(3):
+        assert np.array_equal(gw[bi], eng.conv_pairwise(xs[bi], gys[bi], packing.ConvShape(10, 10, 10, 1)))
+    # precompute mode with explicit offline for the batch job shape
+    sess2 = engine.DeviceSession(params)
+    eng2 = engine.DeviceSecureEngine(sess2)
+    jobs = [linprot.conv_job(f"cb.b{b}", xs[b], w, packing.ConvShape(10, 10, 3, 1), eng2.ring) for b in range(3)]
+    sess2.ensure_offline([eng2.batch_shape(jobs, "cb")], 1)
+    assert np.array_equal(eng2.conv_forward_batch(xs, w, packing.ConvShape(10, 10, 3, 1), job_id="cb"), got)
 
