@@ -249,18 +249,8 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
 #pragma unroll
         for (int k = 0; k < Sh::E; ++k) x[k] = stg[cb + coef_off<LOGN>(k)];
       }
-      group_sync<LOGN, GROUPS>();  // staging buffer consumed
-      if (leader) {
-        if (b + step < npoly) {
-          fence_proxy_async_smem();
-          bulk_load(stg, a.in + ((size_t)(b + step) * a.in_stride * L + limb) * Sh::N, Sh::N * sizeof(T), bar);
-        }
-        // the epilogue's per-item operands: start them towards L2 while this item transforms
-        if ((OP == StreamOp::InvAdd || OP == StreamOp::MulPrepared) && a.addend)
-          bulk_prefetch_l2(a.addend + aoff, Sh::N * sizeof(T));
-        if (OP == StreamOp::MulPrepared && a.b_stride)
-          bulk_prefetch_l2(a.bprep + ((size_t)b * a.b_stride * L + limb) * (size_t)Sh::N, Sh::N * sizeof(T));
-      }
+      // the next item's staging load is issued after the transform's first exchange, whose
+      // barrier already orders every thread's staging read before it (see xform_fwd/xform_inv)
     } else if constexpr (OP == StreamOp::LiftPrepare || OP == StreamOp::LiftFwd) {
       const uint64_t* src = a.plain + (size_t)b * Sh::N + cb;
       if (leader && b + step < npoly) bulk_prefetch_l2(a.plain + (size_t)(b + step) * Sh::N, Sh::N * 8);
@@ -278,13 +268,57 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) x[k] = a.in[ioff + cb + coef_off<LOGN>(k)];
     }
+    auto issue_next = [&]() {
+      if constexpr (PF) {
+        if (leader) {
+          if (b + step < npoly) {
+            fence_proxy_async_smem();
+            bulk_load(stg, a.in + ((size_t)(b + step) * a.in_stride * L + limb) * Sh::N, Sh::N * sizeof(T), bar);
+          }
+          // the epilogue's per-item operands: start them towards L2 while this item transforms
+          if ((OP == StreamOp::InvAdd || OP == StreamOp::MulPrepared) && a.addend)
+            bulk_prefetch_l2(a.addend + aoff, Sh::N * sizeof(T));
+          if (OP == StreamOp::MulPrepared && a.b_stride)
+            bulk_prefetch_l2(a.bprep + ((size_t)b * a.b_stride * L + limb) * (size_t)Sh::N, Sh::N * sizeof(T));
+        }
+      }
+    };
+    // forward / inverse transform; with staging, split after the first exchange to issue the
+    // next item's load there (PF implies 32-bit limbs and >= 3 passes)
+    // (64-bit limbs transform whole polynomials on the FP64 path: issue after the transform)
+    constexpr bool SPLIT = PF && sizeof(T) == 4 && Sh::NPASS >= 2;
+    auto xform_fwd = [&]() {
+      if constexpr (SPLIT) {
+        fwd_pass<T, LOGN, 0, SMEM_TW>(x, tw, pr.p, pr.p2);
+        ex.template run<Sh::pass_s(0), Sh::pass_r(0), Sh::pass_s(1), Sh::pass_r(1)>(x);
+        issue_next();
+        ntt_fwd_regs<T, LOGN, 1, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+      } else {
+        ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+        issue_next();
+      }
+    };
+    auto xform_inv = [&](bool first_in_item) {
+      constexpr int K = Sh::NPASS - 1;
+      if constexpr (SPLIT) {
+        if (first_in_item) {
+          inv_pass<T, LOGN, K, SMEM_TW>(x, tw, pr.p, pr.p2);
+          ex.template run<Sh::pass_s(K), Sh::pass_r(K), Sh::pass_s(K - 1), Sh::pass_r(K - 1)>(x);
+          issue_next();
+          ntt_inv_regs<T, LOGN, K - 1, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+          return;
+        }
+      }
+      ntt_inv_regs<T, LOGN, K, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+      if (first_in_item) issue_next();
+    };
     if constexpr (OP == StreamOp::Inv) {
-      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+      xform_inv(true);
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k)
         a.out[off + cb + coef_off<LOGN>(k)] = csub(shoup_mul(x[k], pr.ninv, pr.ninv_q, pr.p), pr.p);
     } else if constexpr (OP == StreamOp::InvAdd) {
-      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+      xform_inv(true);
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) {
         const int j = cb + coef_off<LOGN>(k);
@@ -293,7 +327,7 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
         a.out[off + j] = v;
       }
     } else {
-      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+      xform_fwd();
       if constexpr (OP == StreamOp::Fwd || OP == StreamOp::LiftFwd) {
 #pragma unroll
         for (int k = 0; k < Sh::E; ++k) x[k] = pr.canon_fwd(x[k]);
@@ -316,7 +350,7 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
 #pragma unroll
           for (int c = 0; c < EV::VEC; ++c) x[i * EV::VEC + c] = mont_mul(x[i * EV::VEC + c], v[c], pr.p, pr.pinv);
         }
-        ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+        xform_inv(false);
 #pragma unroll
         for (int k = 0; k < Sh::E; ++k) {
           const int j = cb + coef_off<LOGN>(k);

@@ -450,9 +450,10 @@ template <typename T, int LOGN, int K = 0, bool SMEM, int NBUF, int GROUPS>
 __device__ __forceinline__ void ntt_fwd_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN, NBUF, GROUPS>& ex,
                                              TwSrc<T, SMEM> tw, T p, T p2) {
   using Sh = NttShape<LOGN>;
-  if constexpr (sizeof(T) == 8) {
+  if constexpr (sizeof(T) == 8 && K != 0) {
+    __trap();  // 64-bit limbs transform whole polynomials (never split)
+  } else if constexpr (sizeof(T) == 8) {
     // 64-bit limbs: FP64 butterflies, inputs < 4p (< 2^52), outputs canonical [0, p)
-    static_assert(K == 0, "64-bit limbs transform whole polynomials");
     const F64Prime P{(double)p, __drcp_rn((double)p)};
     double d[Sh::E];
 #pragma unroll
@@ -474,9 +475,10 @@ template <typename T, int LOGN, int K = NttShape<LOGN>::NPASS - 1, bool SMEM, in
 __device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN, NBUF, GROUPS>& ex,
                                              TwSrc<T, SMEM> tw, T p, T p2) {
   using Sh = NttShape<LOGN>;
-  if constexpr (sizeof(T) == 8) {
+  if constexpr (sizeof(T) == 8 && K != Sh::NPASS - 1) {
+    __trap();  // 64-bit limbs transform whole polynomials (never split)
+  } else if constexpr (sizeof(T) == 8) {
     // 64-bit limbs: FP64 butterflies, inputs < 4p, outputs canonical [0, p)
-    static_assert(K == Sh::NPASS - 1, "64-bit limbs transform whole polynomials");
     const F64Prime P{(double)p, __drcp_rn((double)p)};
     double d[Sh::E];
 #pragma unroll
