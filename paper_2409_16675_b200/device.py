@@ -161,16 +161,20 @@ class RnsContext:
             return
         step = -(-B // max(1, chunks))
         cur = torch.cuda.current_stream()
-        if not hasattr(self, "_pipe"):
-            self._pipe = [torch.cuda.Stream() for _ in range(3)]
-        s_in, s_comp, s_out = self._pipe
+        # streams and staging buffers are per calling thread (contexts are shared by the two
+        # party threads of an in-process session, RnsContext.get)
+        tl = self.__dict__.setdefault("_pipe_tls", threading.local())
+        if not hasattr(tl, "streams"):
+            tl.streams = [torch.cuda.Stream() for _ in range(3)]
+            tl.key = None
+        s_in, s_comp, s_out = tl.streams
         shape_ct = (step,) + tuple(ct_h.shape[1:])
         key = (shape_ct, ct_h.dtype, pt_h.shape[1:], slots)
-        if getattr(self, "_pipe_key", None) != key:
-            self._pipe_buf = [(torch.empty(shape_ct, dtype=ct_h.dtype, device="cuda"),
-                               torch.empty((step,) + tuple(pt_h.shape[1:]), dtype=pt_h.dtype, device="cuda"),
-                               torch.empty(shape_ct, dtype=ct_h.dtype, device="cuda")) for _ in range(slots)]
-            self._pipe_key = key
+        if tl.key != key:
+            tl.buf = [(torch.empty(shape_ct, dtype=ct_h.dtype, device="cuda"),
+                       torch.empty((step,) + tuple(pt_h.shape[1:]), dtype=pt_h.dtype, device="cuda"),
+                       torch.empty(shape_ct, dtype=ct_h.dtype, device="cuda")) for _ in range(slots)]
+            tl.key = key
         ev_in = [torch.cuda.Event() for _ in range(slots)]
         ev_comp = [torch.cuda.Event() for _ in range(slots)]
         ev_out = [None] * slots
@@ -182,7 +186,7 @@ class RnsContext:
             hi = min(B, lo + step)
             n = hi - lo
             k = i % slots
-            ct_d, pt_d, out_d = self._pipe_buf[k]
+            ct_d, pt_d, out_d = tl.buf[k]
             if ev_out[k] is not None:
                 s_in.wait_event(ev_out[k])
             with torch.cuda.stream(s_in):

@@ -97,3 +97,38 @@ def test_eval_addend_is_scaled_forward_ntt():
     ninv = torch.tensor([pow(P.n, -1, q) for q in P.cipher_ring.primes], dtype=torch.int64, device="cuda").view(1, -1, 1)
     expect = (f.to(torch.int64) * ninv) % p
     assert torch.equal(ev.to(torch.int64), expect)
+
+
+def test_cpmul_host_pipeline_matches_device_path_threads():
+    """RnsContext.cpmul_host (pinned host buffers, chunked H2D / CPMul / D2H on 3 streams, the
+    bench's e2e leg) equals ctb_cpmul on device buffers, also from two threads at once."""
+    import threading
+    import torch
+    from paper_2409_16675_b200.device import RnsContext
+    from paper_2409_16675_b200.params import default_he_params
+    P = default_he_params(4096)
+    ctx = RnsContext.get(P.n, P.cipher_ring.primes, P.plain_ring.primes)
+    p = torch.tensor(P.cipher_ring.primes, dtype=torch.int64).view(1, 1, -1, 1)
+    g = torch.Generator().manual_seed(5)
+    results, errors = {}, []
+
+    def run(tag, B, chunks):
+        try:
+            ct = (torch.randint(0, 1 << 62, (B, 2, ctx.L, P.n), generator=g) % p).to(torch.int32)
+            pt = torch.randint(0, P.t, (B, P.n), dtype=torch.int64, generator=g)
+            want = ctx.cpmul(ct.cuda(), pt.cuda()).cpu()
+            out = torch.empty_like(ct).pin_memory()
+            ctx.cpmul_host(ct.pin_memory(), pt.pin_memory(), out, chunks=chunks)
+            torch.cuda.current_stream().synchronize()
+            results[tag] = torch.equal(out, want)
+        except Exception as e:  # pragma: no cover - surfaced below
+            errors.append(e)
+
+    run("single", 37, 5)
+    ts = [threading.Thread(target=run, args=(f"t{i}", 24 + i, 3 + i)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    assert results == {"single": True, "t0": True, "t1": True}
