@@ -281,3 +281,35 @@ def test_ccmul_sum_matches_per_site_and_chunks(p512, rng):
     env = dict(os.environ, CTB_SITE_CHUNK="2")
     res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
     assert res.stdout.strip().endswith("OK"), res.stdout + res.stderr
+
+
+def test_c_abi_fused_entry_errors():
+    """ctb_ccmul_sum / ctb_linear_online reject out-of-range sites and short workspaces."""
+    import ctypes
+    import torch
+    from paper_2409_16675_b200 import _lib
+    from paper_2409_16675_b200.device import RnsContext, _ptr, _stream
+    from paper_2409_16675_b200.params import default_he_params
+    P = default_he_params(4096)
+    ctx = RnsContext.get(P.n, P.cipher_ring.primes, P.plain_ring.primes)
+    lib = _lib.load()
+    ct = torch.zeros((2, 2, ctx.L, P.n), dtype=torch.int32, device="cuda")
+    sites = (ctypes.c_uint32 * 3)(0, 5, 0)   # w index 5 out of range
+    keys = torch.zeros((14, 2, ctx.L, P.n), dtype=torch.int32, device="cuda")
+    out = torch.empty((1, 2, ctx.L, P.n), dtype=torch.int32, device="cuda")
+    wsb = int(lib.ctb_ccmul_sum_workspace_bytes(ctx._h, 2, 2, 1, 1, 1))
+    work = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    rc = lib.ctb_ccmul_sum(ctx._h, _ptr(ct), 2, _ptr(ct), 2, sites, 1, 1, _ptr(keys), _ptr(out), _ptr(work), wsb,
+                           _stream())
+    assert rc == _lib.CTB_ERR_ARG and b"out of range" in lib.ctb_last_error()
+    good = (ctypes.c_uint32 * 3)(0, 1, 0)
+    rc = lib.ctb_ccmul_sum(ctx._h, _ptr(ct), 2, _ptr(ct), 2, good, 1, 1, _ptr(keys), _ptr(out), _ptr(work), 16,
+                           _stream())
+    assert rc == _lib.CTB_ERR_ARG and b"workspace" in lib.ctb_last_error()
+    mx = torch.zeros((2, P.n), dtype=torch.int64, device="cuda")
+    wsl = int(lib.ctb_linear_online_workspace_bytes(ctx._h, 2, 2, 1, 1))
+    work2 = torch.empty(wsl, dtype=torch.uint8, device="cuda")
+    outp = torch.empty((1, P.n), dtype=torch.int64, device="cuda")
+    rc = lib.ctb_linear_online(ctx._h, _ptr(ct), 2, _ptr(ct), 2, _ptr(mx), _ptr(mx), sites, 1, 1, None, 0,
+                               _ptr(out), _ptr(outp), _ptr(work2), _stream())
+    assert rc == _lib.CTB_ERR_ARG and b"out of range" in lib.ctb_last_error()
