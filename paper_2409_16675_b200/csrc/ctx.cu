@@ -77,8 +77,9 @@ static int build_typed(Base& b, uint32_t logn, std::string& err, const uint64_t*
   const uint32_t n = 1u << logn;
   constexpr int W = 8 * sizeof(T);
   std::vector<PrimeTab<T>> tabs(L);
-  const int ent = shape_tw_entries((int)logn);  // pairs per prime (both directions)
-  std::vector<T> tw((size_t)L * 2 * ent);
+  const int ent = shape_tw_entries((int)logn);  // entries per prime (both directions)
+  const int words = tw_words<T>((int)logn);      // u32: (w, w') pairs; u64: one double per entry
+  std::vector<T> tw((size_t)L * words);
   cudaError_t ce = cudaMalloc(&b.d_tw, tw.size() * sizeof(T));
   if (ce != cudaSuccess) { err = std::string("cudaMalloc twiddles: ") + cudaGetErrorString(ce); return -2; }
   ce = cudaMalloc(&b.d_tabs, sizeof(PrimeTab<T>) * (L ? L : 1));
@@ -88,7 +89,7 @@ static int build_typed(Base& b, uint32_t logn, std::string& err, const uint64_t*
     const uint64_t p = b.primes[l];
     uint64_t psi;
     if (!find_psi(p, n, psi)) { err = "no primitive 2N-th root of unity mod " + std::to_string(p); return -1; }
-    T* f = tw.data() + (size_t)l * 2 * ent;
+    T* f = tw.data() + (size_t)l * words;
     // powers in natural order, then scatter by bit reversal
     std::vector<uint64_t> pw(n);
     pw[0] = 1;
@@ -106,12 +107,11 @@ static int build_typed(Base& b, uint32_t logn, std::string& err, const uint64_t*
             const uint64_t w = pw[bitrev(mb, logn)];
             if (sizeof(T) == 4) {
               f[2 * e] = (T)w;  f[2 * e + 1] = shoup_q<T>(w, p);
-            } else {  // 64-bit limbs run the FP64 butterflies (ntt.cuh): (w, w/p) as doubles
-              const double wd = (double)w, wp = (double)w / (double)p;
-              uint64_t bw, bq;
+            } else {  // 64-bit limbs run the FP64 butterflies (ntt.cuh): w as a double
+              const double wd = (double)w;
+              uint64_t bw;
               std::memcpy(&bw, &wd, 8);
-              std::memcpy(&bq, &wp, 8);
-              f[2 * e] = (T)bw;  f[2 * e + 1] = (T)bq;
+              f[e] = (T)bw;
             }
           }
     }
@@ -137,7 +137,7 @@ static int build_typed(Base& b, uint32_t logn, std::string& err, const uint64_t*
     }
     if (tmod) t.tmod = (T)(tmod[l] % p);
     if (delta) { t.delta = (T)(delta[l] % p); t.delta_q = shoup_q<T>(delta[l] % p, p); }
-    t.fwd = d_tw + (size_t)l * 2 * ent;
+    t.fwd = d_tw + (size_t)l * words;
     t.inv = t.fwd;
   }
   ce = cudaMemcpy(b.d_tw, tw.data(), tw.size() * sizeof(T), cudaMemcpyHostToDevice);

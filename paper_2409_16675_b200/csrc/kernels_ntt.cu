@@ -87,7 +87,7 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
   using Sh = NttShape<LOGN>;
   constexpr int GROUPS = cpmul_groups<T, LOGN>();
   using Ex = Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>;
-  constexpr int TW_WORDS = SMEM_TW ? 2 * shape_tw_entries(LOGN) : 0;
+  constexpr int TW_WORDS = SMEM_TW ? tw_words<T>(LOGN) : 0;
   constexpr int GROUP_WORDS = Ex::WORDS + Sh::N;  // exchange image + NTT(pt) strip
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
@@ -178,7 +178,7 @@ struct StreamCfg {
   using Sh = NttShape<LOGN>;
   static constexpr int GROUPS = cpmul_groups<T, LOGN>();
   using Ex = Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>;
-  static constexpr size_t TW_BYTES = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
+  static constexpr size_t TW_BYTES = (size_t)tw_words<T>(LOGN) * sizeof(T);
   // u32: table + images within 200 KB (two CTAs per SM with staging); 64-bit limbs: the
   // (w, w/p) table (140 KB at N=8192) + image fill one CTA's 227 KB
   static constexpr bool SMEM_TW = LOGN >= 9 && TW_BYTES + GROUPS * (size_t)Ex::WORDS * sizeof(T) <=
@@ -200,7 +200,7 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
   using Sh = NttShape<LOGN>;
   constexpr int GROUPS = C::GROUPS;
   constexpr bool PF = C::PF_OK && OP != StreamOp::LiftPrepare && OP != StreamOp::LiftFwd;
-  constexpr int TW_WORDS = SMEM_TW ? 2 * shape_tw_entries(LOGN) : 0;
+  constexpr int TW_WORDS = SMEM_TW ? tw_words<T>(LOGN) : 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
   const int group = (int)(threadIdx.x / Sh::THREADS);
@@ -432,7 +432,7 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
   using Sh = NttShape<LOGN>;
   constexpr int GROUPS = cpmul_groups<T, LOGN>();
   using Ex = Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>;
-  constexpr int TW_WORDS = SMEM_TW ? 2 * shape_tw_entries(LOGN) : 0;
+  constexpr int TW_WORDS = SMEM_TW ? tw_words<T>(LOGN) : 0;
   constexpr int GROUP_WORDS = Ex::WORDS + Sh::N;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
@@ -745,9 +745,9 @@ static cudaError_t launch_cpmul(const Ctx* c, const Base* b, const void* ct, con
   using Sh = NttShape<LOGN>;
   // twiddles in shared memory when the table fits beside the exchange image
   constexpr int GROUPS = cpmul_groups<T, LOGN>();
-  constexpr size_t tw_bytes = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
+  constexpr size_t tw_bytes = (size_t)tw_words<T>(LOGN) * sizeof(T);
   constexpr size_t group_bytes = ((size_t)Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>::WORDS + Sh::N) * sizeof(T);
-  constexpr bool SMEM_TW = sizeof(T) == 4 && LOGN >= 9 && tw_bytes + GROUPS * group_bytes <= 200 * 1024;
+  constexpr bool SMEM_TW = LOGN >= 9 && tw_bytes + GROUPS * group_bytes <= (sizeof(T) == 4 ? 200 : 226) * 1024;
   auto kern = k_cpmul<T, LOGN, SMEM_TW>;
   const size_t smem = GROUPS * group_bytes + (SMEM_TW ? tw_bytes : 0);
   const int L = b->size();
@@ -783,9 +783,9 @@ static cudaError_t launch_encrypt(const Ctx* c, const Base* b, const uint64_t* m
                                   const void* pkprep, void* out, uint64_t batch, cudaStream_t s) {
   using Sh = NttShape<LOGN>;
   constexpr int GROUPS = cpmul_groups<T, LOGN>();
-  constexpr size_t tw_bytes = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
+  constexpr size_t tw_bytes = (size_t)tw_words<T>(LOGN) * sizeof(T);
   constexpr size_t group_bytes = ((size_t)Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>::WORDS + Sh::N) * sizeof(T);
-  constexpr bool SMEM_TW = sizeof(T) == 4 && LOGN >= 9 && tw_bytes + GROUPS * group_bytes <= 200 * 1024;
+  constexpr bool SMEM_TW = LOGN >= 9 && tw_bytes + GROUPS * group_bytes <= (sizeof(T) == 4 ? 200 : 226) * 1024;
   auto kern = k_encrypt<T, LOGN, SMEM_TW>;
   const size_t smem = GROUPS * group_bytes + (SMEM_TW ? tw_bytes : 0);
   const int L = b->size();

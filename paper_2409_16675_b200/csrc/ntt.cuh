@@ -58,6 +58,10 @@ __host__ __device__ constexpr int shape_tw_off(int logn, int k) {
   return off;
 }
 __host__ __device__ constexpr int shape_tw_entries(int logn) { return shape_tw_off(logn, shape_npass(logn)); }
+// Words per prime in the twiddle table: (w, w') pairs for 32-bit limbs; one double w per entry
+// for 64-bit limbs (the FP64 butterflies derive w/p as w * (1/p), see ntt.cuh f64 section).
+template <typename T>
+__host__ __device__ constexpr int tw_words(int logn) { return (sizeof(T) == 4 ? 2 : 1) * shape_tw_entries(logn); }
 
 template <int LOGN>
 struct NttShape {
@@ -359,12 +363,19 @@ __device__ __forceinline__ uint64_t f64_to_canon(double x, const F64Prime& P) { 
   return (uint64_t)__double_as_longlong(__dadd_rn(y, 4503599627370496.0)) & 0x000FFFFFFFFFFFFFull;
 }
 
+// One table word per entry: w as a double; w/p = fl(w * fl(1/p)) (relative error < 2^-52, so
+// |x fl(w/p) - x w / p| < 1/2 for |x| < 2^51 and the product bound |r| < p still holds).
 template <typename T, bool SMEM>
-__device__ __forceinline__ void tw_load_f64(const TwSrc<T, SMEM>& tw, const T* at, double& w, double& wp) {
-  T a, b;
-  tw.load(at, a, b);
+__device__ __forceinline__ void tw_load_f64(const TwSrc<T, SMEM>& tw, const T* at, double pinv, double& w,
+                                            double& wp) {
+  uint64_t a;
+  if constexpr (SMEM) {
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(a) : "r"((uint32_t)__cvta_generic_to_shared(at)));
+  } else {
+    asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(a) : "l"(at));
+  }
   w = __longlong_as_double((long long)a);
-  wp = __longlong_as_double((long long)b);
+  wp = __dmul_rn(w, pinv);
 }
 
 template <typename T, int LOGN, int K, bool SMEM>
@@ -375,14 +386,14 @@ __device__ __forceinline__ void fwd_pass_f64(double (&x)[NttShape<LOGN>::E], TwS
 #pragma unroll
   for (int gg = 0; gg < Sh::E / G; ++gg) {
     const int slot = tw_slot<LOGN, S0, R>(gg);
-    const T* tg = tw.tab + 2 * (Sh::tw_off(K) + slot);
+    const T* tg = tw.tab + (Sh::tw_off(K) + slot);
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const int h = 1 << (R - i - 1);
 #pragma unroll
       for (int jb = 0; jb < (1 << i); ++jb) {
         double w, wp;
-        tw_load_f64(tw, tg + 2 * (((1 << i) - 1 + jb) << S0), w, wp);
+        tw_load_f64(tw, tg + (((1 << i) - 1 + jb) << S0), P.pinv, w, wp);
 #pragma unroll
         for (int jj = 0; jj < h; ++jj) {
           const int a = gg * G + jb * 2 * h + jj;
@@ -404,14 +415,14 @@ __device__ __forceinline__ void inv_pass_f64(double (&x)[NttShape<LOGN>::E], TwS
 #pragma unroll
   for (int gg = 0; gg < Sh::E / G; ++gg) {
     const int slot = (1 << S0) - 1 - tw_slot<LOGN, S0, R>(gg);
-    const T* tg = tw.tab + 2 * (Sh::tw_off(K) + slot);
+    const T* tg = tw.tab + (Sh::tw_off(K) + slot);
 #pragma unroll
     for (int i = R - 1; i >= 0; --i) {
       const int h = 1 << (R - i - 1);
 #pragma unroll
       for (int jb = 0; jb < (1 << i); ++jb) {
         double w, wp;
-        tw_load_f64(tw, tg + 2 * (((1 << i) - 1 + ((1 << i) - 1 - jb)) << S0), w, wp);
+        tw_load_f64(tw, tg + (((1 << i) - 1 + ((1 << i) - 1 - jb)) << S0), P.pinv, w, wp);
 #pragma unroll
         for (int jj = 0; jj < h; ++jj) {
           const int a = gg * G + jb * 2 * h + jj;

@@ -284,7 +284,7 @@ k_tensor_product(const uint32_t* A, const uint32_t* Bt, uint32_t* H, const Prime
                  int K, uint32_t batch) {
   using Sh = NttShape<LOGN>;
   using T = uint32_t;
-  constexpr int TW_WORDS = SMEM_TW ? 2 * shape_tw_entries(LOGN) : 0;
+  constexpr int TW_WORDS = SMEM_TW ? tw_words<T>(LOGN) : 0;
   using Ex = Exchanger<T, LOGN, 1, 1>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
@@ -356,7 +356,7 @@ static cudaError_t launch_tensor_product(const Ctx* c, const uint32_t* a, const 
   using Sh = NttShape<LOGN>;
   const Base& B = c->base[BASE_B];
   using T = uint32_t;
-  constexpr size_t tw_bytes = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
+  constexpr size_t tw_bytes = (size_t)tw_words<T>(LOGN) * sizeof(T);
   constexpr size_t base_bytes = ((size_t)Exchanger<T, LOGN, 1, 1>::WORDS + 3 * (size_t)Sh::N) * sizeof(T);
   constexpr bool SMEM_TW = LOGN >= 9 && tw_bytes + base_bytes <= 200 * 1024;
   auto kern = k_tensor_product<LOGN, SMEM_TW>;
@@ -513,7 +513,7 @@ template <typename T, int LOGN>
 struct RelinCfg {
   using Sh = NttShape<LOGN>;
   using Ex = Exchanger<T, LOGN, 1, 1>;
-  static constexpr size_t TW_BYTES = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
+  static constexpr size_t TW_BYTES = (size_t)tw_words<T>(LOGN) * sizeof(T);
   static constexpr size_t EX_BYTES = ((size_t)Ex::WORDS * sizeof(T) + 15) / 16 * 16;
   static constexpr bool SMEM_TW = sizeof(T) == 4 && LOGN >= 9 && TW_BYTES + EX_BYTES <= 110 * 1024;  // u64: measured slower
   // digits (u32 [N]) staged by TMA one transform ahead: measured slower here (an extra CTA
@@ -530,7 +530,7 @@ k_relin_accum(const T* ct3, int ct_parts, const uint32_t* digits, const T* keypr
   using Sh = NttShape<LOGN>;
   using C = RelinCfg<T, LOGN>;
   constexpr bool PF = C::PF;
-  constexpr int TW_WORDS = SMEM_TW ? 2 * shape_tw_entries(LOGN) : 0;
+  constexpr int TW_WORDS = SMEM_TW ? tw_words<T>(LOGN) : 0;
   using Ex = typename C::Ex;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
@@ -651,7 +651,7 @@ k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict
                uint32_t nsite) {
   using Sh = NttShape<LOGN>;
   using T = uint32_t;
-  constexpr int TW_WORDS = SMEM_TW ? 2 * shape_tw_entries(LOGN) : 0;
+  constexpr int TW_WORDS = SMEM_TW ? tw_words<T>(LOGN) : 0;
   using Ex = Exchanger<T, LOGN, 1, 1>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
@@ -741,7 +741,7 @@ static cudaError_t launch_site_product(const Ctx* c, const uint32_t* ax, const u
   using Sh = NttShape<LOGN>;
   const Base& B = c->base[BASE_B];
   using T = uint32_t;
-  constexpr size_t tw_bytes = 2 * (size_t)shape_tw_entries(LOGN) * sizeof(T);
+  constexpr size_t tw_bytes = (size_t)tw_words<T>(LOGN) * sizeof(T);
   constexpr size_t base_bytes = ((size_t)Exchanger<T, LOGN, 1, 1>::WORDS + (LOGN <= 12 ? 2 : 1) * (size_t)Sh::N) * sizeof(T);
   constexpr bool SMEM_TW = LOGN >= 9 && tw_bytes + base_bytes <= 200 * 1024;
   auto kern = k_site_product<LOGN, SMEM_TW>;
