@@ -14,7 +14,7 @@
 //   LiftPrepare     plain [P][N] -> NTT(lift(m)) N^-1 2^W per limb (k_stream, kernels_ntt.cu)
 //   k_lin_accum     per (slot, limb, 16-byte vector): 2 parts x sum over the slot's sites (eval)
 //   k_stream InvAdd persistent INTT of the slot sums, + mask product (kernels_ntt.cu)
-//   k_lin_plain     CTA per (slot, plain prime): sum of prepared products, INTT
+//   k_lin_accum_plain + k_stream InvAdd: the plain side, same structure over the plain primes
 //   k_plain_crt     plain residues -> uint64 mod t (ring._crt_combine, ring.py:478-485)
 //   k_slot_sum      segmented sum of ciphertexts per slot (offline CCAdd accumulation)
 #include <algorithm>
@@ -106,43 +106,55 @@ k_lin_accum(const T* __restrict__ X, const T* __restrict__ W, const T* __restric
   A4[part4] = o1.u;
 }
 
-// Plain side over the plain primes (u32): MXt canonical eval [n_x][LT][N], MWtp prepared.
-template <int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
-k_lin_plain(const uint32_t* MXt, const uint32_t* MWtp, const int32_t* __restrict__ slot_ptr,
-            const int32_t* __restrict__ site_x, const int32_t* __restrict__ site_w, uint32_t* out,
-            const PrimeTab<uint32_t>* __restrict__ tabs, int LT) {
-  using Sh = NttShape<LOGN>;
-  using T = uint32_t;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Exchanger<T, LOGN> ex{reinterpret_cast<T*>(smem_raw)};
-  const int j = blockIdx.x % LT;
-  const int slot = blockIdx.x / LT;
-  PrimeRegs<T> pr(tabs + j);
-  const size_t N = Sh::N, LN = (size_t)LT * N;
-  using EV = EvalVec<T, LOGN>;
-  T acc[Sh::E];
-#pragma unroll
-  for (int k = 0; k < Sh::E; ++k) acc[k] = 0;
-  const int s0 = slot_ptr[slot], s1 = slot_ptr[slot + 1];
+// Plain side over the plain primes (u32): MXt canonical eval [n_x][LT][N], MWtp prepared;
+// PR [n_out][LT][N] (eval, N^-1 folded) = per slot the sum over its sites of MXt (x) MWtp -- the
+// same memory-level-parallel gather as k_lin_accum, one product per site; k_stream InvAdd
+// (no addend) then transforms the slot sums back in place.
+__global__ void __launch_bounds__(256)
+k_lin_accum_plain(const uint32_t* __restrict__ MXt, const uint32_t* __restrict__ MWtp,
+                  const int32_t* __restrict__ slot_ptr, const int32_t* __restrict__ site_x,
+                  const int32_t* __restrict__ site_w, uint32_t* __restrict__ acc,
+                  const PrimeTab<uint32_t>* __restrict__ tabs, int LT, uint32_t n, uint32_t chunks) {
+  union V { uint4 u; uint32_t t[4]; };
+  uint32_t bid = blockIdx.x;
+  const uint32_t chunk = bid % chunks;
+  bid /= chunks;
+  const int j = (int)(bid % LT);
+  const uint32_t slot = bid / LT;
+  const uint32_t nv = n / 4;
+  const uint32_t v = chunk * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  const uint32_t p = tabs[j].p, p2 = 2 * p, pinv = tabs[j].pinv;
+  const size_t LN4 = (size_t)LT * n / 4;
+  const uint4* X4 = reinterpret_cast<const uint4*>(MXt + (size_t)j * n) + v;
+  const uint4* W4 = reinterpret_cast<const uint4*>(MWtp + (size_t)j * n) + v;
+  uint32_t a[4] = {0, 0, 0, 0};
+  int s = slot_ptr[slot];
+  const int s1 = slot_ptr[slot + 1];
 #pragma unroll 1
-  for (int s = s0; s < s1; ++s) {
-    const T* mx = MXt + (size_t)site_x[s] * LN + j * N;
-    const T* mw = MWtp + (size_t)site_w[s] * LN + j * N;
+  for (; s + 1 < s1; s += 2) {
+    V xa, wa, xb, wb;
+    xa.u = __ldg(X4 + (size_t)site_x[s] * LN4);
+    wa.u = __ldg(W4 + (size_t)site_w[s] * LN4);
+    xb.u = __ldg(X4 + (size_t)site_x[s + 1] * LN4);
+    wb.u = __ldg(W4 + (size_t)site_w[s + 1] * LN4);
 #pragma unroll
-    for (int i = 0; i < EV::CHUNKS; ++i) {
-      T vx[EV::VEC], vw[EV::VEC];
-      EV::load(mx, i, vx);
-      EV::load(mw, i, vw);
-#pragma unroll
-      for (int c = 0; c < EV::VEC; ++c)
-        acc[i * EV::VEC + c] = csub(acc[i * EV::VEC + c] + mont_mul(vx[c], vw[c], pr.p, pr.pinv), pr.p2);
+    for (int c = 0; c < 4; ++c) {
+      a[c] = csub(a[c] + mont_mul(xa.t[c], wa.t[c], p, pinv), p2);
+      a[c] = csub(a[c] + mont_mul(xb.t[c], wb.t[c], p, pinv), p2);
     }
   }
-  ntt_inv_regs<T, LOGN>(acc, ex, pr.inv, pr.p, pr.p2);
-  T* dst = out + ((size_t)slot * LT + j) * N + coef_base<LOGN>();
+  if (s < s1) {
+    V xa, wa;
+    xa.u = __ldg(X4 + (size_t)site_x[s] * LN4);
+    wa.u = __ldg(W4 + (size_t)site_w[s] * LN4);
 #pragma unroll
-  for (int k = 0; k < Sh::E; ++k) dst[coef_off<LOGN>(k)] = csub(acc[k], pr.p);
+    for (int c = 0; c < 4; ++c) a[c] = csub(a[c] + mont_mul(xa.t[c], wa.t[c], p, pinv), p2);
+  }
+  V o;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) o.t[c] = a[c];
+  reinterpret_cast<uint4*>(acc + ((size_t)slot * LT + j) * n)[v] = o.u;
 }
 
 __global__ void k_plain_crt(const uint32_t* res, uint64_t* out, int LT, uint32_t n, uint32_t p0, uint32_t p1,
@@ -293,9 +305,16 @@ extern "C" int ctb_linear_online(const ctb_ctx_t* ctx, const void* ct_x, uint32_
       e = stream_inv_add(c, BASE_Q, out_ct, out_ct, maskprod_eval ? nullptr : maskprod, (uint64_t)n_out * 2, s);
   }
   if (e != cudaSuccess) return cuda_status(e, "ctb_linear_online cipher");
-  CTB_DISPATCH_LOGN(c->logn, e = (launch_ntt_kernel<uint32_t, LOGN>(k_lin_plain<LOGN>, (size_t)n_out * LT, s,
-                                                           (const uint32_t*)MXt, (const uint32_t*)MWt, d_ptr, d_sx,
-                                                           d_sw, PR, (const PrimeTab<uint32_t>*)BT.d_tabs, (int)LT)));
+  {
+    const uint32_t nv = (uint32_t)(N / 4);
+    const uint32_t chunks = (nv + 255) / 256;
+    const uint64_t blocks = (uint64_t)n_out * LT * chunks;
+    k_lin_accum_plain<<<(unsigned)blocks, 256, 0, s>>>(MXt, MWt, d_ptr, d_sx, d_sw, PR,
+                                                        (const PrimeTab<uint32_t>*)BT.d_tabs, (int)LT, (uint32_t)N,
+                                                        chunks);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = stream_inv_add(c, BASE_T, PR, PR, nullptr, (uint64_t)n_out, s);
+  }
   if (e != cudaSuccess) return cuda_status(e, "ctb_linear_online plain");
   const uint64_t total = (uint64_t)n_out * N;
   const uint32_t p0 = (uint32_t)BT.primes[0], p1 = LT > 1 ? (uint32_t)BT.primes[1] : 1u;
