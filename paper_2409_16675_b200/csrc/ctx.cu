@@ -1,3 +1,4 @@
+#include <algorithm>
 // Prime tables: twiddles, Shoup quotients, Montgomery constants.
 #include <cstring>
 #include <mutex>
@@ -24,15 +25,24 @@ void smem_attr_mark(const void* kern) {
 
 static std::mutex g_grid_mu;
 static std::unordered_map<const void*, uint32_t> g_grid;
+uint32_t sm_count() {
+  static const uint32_t n = [] {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return (uint32_t)std::max(sms, 1);
+  }();
+  return n;
+}
+
 uint32_t persistent_grid(const void* kern, int threads, size_t smem) {
   {
     std::lock_guard<std::mutex> g(g_grid_mu);
     auto it = g_grid.find(kern);
     if (it != g_grid.end()) return it->second;
   }
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = (int)sm_count();
+  int per_sm = 1;
   if (!smem_attr_done(kern)) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     smem_attr_mark(kern);

@@ -23,9 +23,6 @@ struct LimbConsts {
   T tm[MAXL];           // plain modulus t mod p (centred lift)
 };
 
-unsigned grid_for(uint64_t total) {
-  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148ull * 16));
-}
 
 template <typename T>
 __device__ __forceinline__ T reduce_word(uint64_t v, const LimbConsts<T>& c, int l) {
@@ -136,11 +133,11 @@ extern "C" int ctb_rns_elementwise(const ctb_ctx_t* ctx, int base, int op, const
   if (!total) return OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (B->word == 4)
-    k_rns_elementwise<uint32_t><<<grid_for(total), 256, 0, s>>>(op, (const uint32_t*)a, (const uint32_t*)b,
+    k_rns_elementwise<uint32_t><<<grid_stride(total, 16), 256, 0, s>>>(op, (const uint32_t*)a, (const uint32_t*)b,
                                                                 (uint32_t*)out, limb_consts<uint32_t>(*B, nullptr, nullptr),
                                                                 B->size(), c->n, total);
   else
-    k_rns_elementwise<uint64_t><<<grid_for(total), 256, 0, s>>>(op, (const uint64_t*)a, (const uint64_t*)b,
+    k_rns_elementwise<uint64_t><<<grid_stride(total, 16), 256, 0, s>>>(op, (const uint64_t*)a, (const uint64_t*)b,
                                                                 (uint64_t*)out, limb_consts<uint64_t>(*B, nullptr, nullptr),
                                                                 B->size(), c->n, total);
   return cuda_status(cudaGetLastError(), "ctb_rns_elementwise");
@@ -157,11 +154,11 @@ extern "C" int ctb_rns_scalar_mul(const ctb_ctx_t* ctx, int base, const void* a,
   if (!total) return OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (B->word == 4)
-    k_rns_elementwise<uint32_t><<<grid_for(total), 256, 0, s>>>(3, (const uint32_t*)a, nullptr, (uint32_t*)out,
+    k_rns_elementwise<uint32_t><<<grid_stride(total, 16), 256, 0, s>>>(3, (const uint32_t*)a, nullptr, (uint32_t*)out,
                                                                 limb_consts<uint32_t>(*B, scalars, nullptr),
                                                                 B->size(), c->n, total);
   else
-    k_rns_elementwise<uint64_t><<<grid_for(total), 256, 0, s>>>(3, (const uint64_t*)a, nullptr, (uint64_t*)out,
+    k_rns_elementwise<uint64_t><<<grid_stride(total, 16), 256, 0, s>>>(3, (const uint64_t*)a, nullptr, (uint64_t*)out,
                                                                 limb_consts<uint64_t>(*B, scalars, nullptr),
                                                                 B->size(), c->n, total);
   return cuda_status(cudaGetLastError(), "ctb_rns_scalar_mul");
@@ -178,10 +175,10 @@ extern "C" int ctb_rns_from_small(const ctb_ctx_t* ctx, int base, const int64_t*
   if (!total) return OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (B->word == 4)
-    k_rns_from_small<uint32_t><<<grid_for(total), 256, 0, s>>>(in, (uint32_t*)out, limb_consts<uint32_t>(*B, nullptr, nullptr),
+    k_rns_from_small<uint32_t><<<grid_stride(total, 16), 256, 0, s>>>(in, (uint32_t*)out, limb_consts<uint32_t>(*B, nullptr, nullptr),
                                                                B->size(), c->n, total);
   else
-    k_rns_from_small<uint64_t><<<grid_for(total), 256, 0, s>>>(in, (uint64_t*)out, limb_consts<uint64_t>(*B, nullptr, nullptr),
+    k_rns_from_small<uint64_t><<<grid_stride(total, 16), 256, 0, s>>>(in, (uint64_t*)out, limb_consts<uint64_t>(*B, nullptr, nullptr),
                                                                B->size(), c->n, total);
   return cuda_status(cudaGetLastError(), "ctb_rns_from_small");
 }
@@ -199,10 +196,10 @@ extern "C" int ctb_lift_plain(const ctb_ctx_t* ctx, const uint64_t* m, const uin
   for (int l = 0; l < B->size(); ++l) tm[l] = c->t % B->primes[l];
   cudaStream_t s = (cudaStream_t)stream;
   if (B->word == 4)
-    k_lift_plain<uint32_t><<<grid_for(total), 256, 0, s>>>(m, (uint32_t*)out, limb_consts<uint32_t>(*B, scale, tm.data()),
+    k_lift_plain<uint32_t><<<grid_stride(total, 16), 256, 0, s>>>(m, (uint32_t*)out, limb_consts<uint32_t>(*B, scale, tm.data()),
                                                            B->size(), c->n, c->t_half, total);
   else
-    k_lift_plain<uint64_t><<<grid_for(total), 256, 0, s>>>(m, (uint64_t*)out, limb_consts<uint64_t>(*B, scale, tm.data()),
+    k_lift_plain<uint64_t><<<grid_stride(total, 16), 256, 0, s>>>(m, (uint64_t*)out, limb_consts<uint64_t>(*B, scale, tm.data()),
                                                            B->size(), c->n, c->t_half, total);
   return cuda_status(cudaGetLastError(), "ctb_lift_plain");
 }
@@ -214,6 +211,6 @@ extern "C" int ctb_plain_elementwise(const ctb_ctx_t* ctx, int op, const uint64_
   if (!c || !c->t || op < 0 || op > 3 || !a || !out || (op < 2 && !b)) { set_error("ctb_plain_elementwise: bad arguments"); return ERR_ARG; }
   const uint64_t total = n_polys * (uint64_t)c->n;
   if (!total) return OK;
-  k_plain_elementwise<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(op, a, b, scalar % c->t, out, c->t, total);
+  k_plain_elementwise<<<grid_stride(total, 16), 256, 0, (cudaStream_t)stream>>>(op, a, b, scalar % c->t, out, c->t, total);
   return cuda_status(cudaGetLastError(), "ctb_plain_elementwise");
 }

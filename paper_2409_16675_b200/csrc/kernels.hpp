@@ -43,6 +43,17 @@ inline cudaError_t launch_ntt_kernel(void (*kern)(KArgs...), size_t nblocks, cud
 // Resident CTAs per SM x SM count for a persistent kernel (cached per kernel).
 uint32_t persistent_grid(const void* kern, int threads, size_t smem);
 
+// Streaming multiprocessors of the current device (cached).
+uint32_t sm_count();
+
+// Grid for a 256-thread grid-stride elementwise kernel over `total` items: enough CTAs for
+// `per_sm` resident per SM, never more than the items need.
+inline unsigned grid_stride(uint64_t total, unsigned per_sm) {
+  const uint64_t cap = (uint64_t)sm_count() * per_sm;
+  const uint64_t need = (total + 255) / 256;
+  return (unsigned)(need < 1 ? 1 : (need < cap ? need : cap));
+}
+
 // Launch with an explicit grid and dynamic shared memory (opt-in handled).
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_kernel_grid(void (*kern)(KArgs...), uint32_t grid, int threads, size_t smem,

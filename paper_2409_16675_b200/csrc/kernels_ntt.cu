@@ -103,9 +103,7 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
   const T tmod = tabs[limb].tmod;
   const T* twp = pr.fwd;
   if constexpr (SMEM_TW) {
-    const uint4* src = reinterpret_cast<const uint4*>(pr.fwd);
-    uint4* dst = reinterpret_cast<uint4*>(tw_sm);
-    for (int i = threadIdx.x; i < TW_WORDS * (int)sizeof(T) / 16; i += Sh::THREADS * GROUPS) dst[i] = __ldg(src + i);
+    stage_twiddles(pr.fwd, tw_sm, TW_WORDS, Sh::THREADS * GROUPS);
     __syncthreads();
     twp = tw_sm;
   }
@@ -216,9 +214,7 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
   PrimeRegs<T> pr(tabs + limb);
   const T* twp = pr.fwd;
   if constexpr (SMEM_TW) {
-    const uint4* src = reinterpret_cast<const uint4*>(pr.fwd);
-    uint4* dst = reinterpret_cast<uint4*>(tw_sm);
-    for (int i = threadIdx.x; i < TW_WORDS * (int)sizeof(T) / 16; i += C::THREADS) dst[i] = __ldg(src + i);
+    stage_twiddles(pr.fwd, tw_sm, TW_WORDS, C::THREADS);
     twp = tw_sm;
   }
   uint32_t b = slot * GROUPS + group;
@@ -448,9 +444,7 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
   const T tmod = tabs[limb].tmod, delta = tabs[limb].delta, delta_q = tabs[limb].delta_q;
   const T* twp = pr.fwd;
   if constexpr (SMEM_TW) {
-    const uint4* src = reinterpret_cast<const uint4*>(pr.fwd);
-    uint4* dst = reinterpret_cast<uint4*>(tw_sm);
-    for (int i = threadIdx.x; i < TW_WORDS * (int)sizeof(T) / 16; i += Sh::THREADS * GROUPS) dst[i] = __ldg(src + i);
+    stage_twiddles(pr.fwd, tw_sm, TW_WORDS, Sh::THREADS * GROUPS);
     __syncthreads();
     twp = tw_sm;
   }

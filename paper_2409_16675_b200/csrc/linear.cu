@@ -192,9 +192,6 @@ using namespace ctb;
 
 namespace {
 const Ctx* cctx(const ctb_ctx_t* ctx) { return reinterpret_cast<const Ctx*>(ctx); }
-unsigned grid_lin(uint64_t total) {
-  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148ull * 16));
-}
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 }  // namespace
 
@@ -320,7 +317,7 @@ extern "C" int ctb_linear_online(const ctb_ctx_t* ctx, const void* ct_x, uint32_
   const uint32_t p0 = (uint32_t)BT.primes[0], p1 = LT > 1 ? (uint32_t)BT.primes[1] : 1u;
   const uint32_t p1_oneq = (uint32_t)((1ull << 32) / p1);
   if (total)
-    k_plain_crt<<<grid_lin(total), 256, 0, s>>>(PR, out_p, (int)LT, (uint32_t)N, p0, p1, c->crt_inv, c->crt_inv_q,
+    k_plain_crt<<<grid_stride(total, 16), 256, 0, s>>>(PR, out_p, (int)LT, (uint32_t)N, p0, p1, c->crt_inv, c->crt_inv_q,
                                                 p1_oneq, total);
   return cuda_status(cudaGetLastError(), "ctb_linear_online crt");
 }
@@ -338,11 +335,11 @@ extern "C" int ctb_slot_sum(const ctb_ctx_t* ctx, int base, const void* in, uint
   if (!total) return OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (B.word == 4)
-    k_slot_sum<uint32_t><<<grid_lin(total), 256, 0, s>>>((const uint32_t*)in, slot_ptr, members, (uint32_t*)out,
+    k_slot_sum<uint32_t><<<grid_stride(total, 16), 256, 0, s>>>((const uint32_t*)in, slot_ptr, members, (uint32_t*)out,
                                                          (const PrimeTab<uint32_t>*)B.d_tabs, B.size(), (int)parts,
                                                          c->n, total);
   else
-    k_slot_sum<uint64_t><<<grid_lin(total), 256, 0, s>>>((const uint64_t*)in, slot_ptr, members, (uint64_t*)out,
+    k_slot_sum<uint64_t><<<grid_stride(total, 16), 256, 0, s>>>((const uint64_t*)in, slot_ptr, members, (uint64_t*)out,
                                                          (const PrimeTab<uint64_t>*)B.d_tabs, B.size(), (int)parts,
                                                          c->n, total);
   return cuda_status(cudaGetLastError(), "ctb_slot_sum");

@@ -169,6 +169,15 @@ __host__ __device__ constexpr int tw_group_slot(int logn, int s, int r, int B) {
   return B;
 }
 
+// Copy one prime's twiddle table (`words` words, 16-byte multiple) into shared memory with
+// `nthreads` cooperating threads (callers synchronise before first use).
+template <typename T>
+__device__ __forceinline__ void stage_twiddles(const T* table, T* smem, int words, int nthreads) {
+  const uint4* src = reinterpret_cast<const uint4*>(table);
+  uint4* dst = reinterpret_cast<uint4*>(smem);
+  for (int i = threadIdx.x; i < words * (int)sizeof(T) / 16; i += nthreads) dst[i] = __ldg(src + i);
+}
+
 template <typename T, bool SMEM>
 struct TwSrc {
   const T* tab;  // generic pointer to pair 0 of this prime's table (global or shared)

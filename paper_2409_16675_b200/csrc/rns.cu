@@ -345,9 +345,6 @@ int rns_words(const RnsConsts* rc) { return rc ? rc->W : 0; }
 
 using namespace ctb;
 
-static unsigned grid_for(uint64_t total) {
-  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148ull * 8));
-}
 
 extern "C" int ctb_decrypt_round(const ctb_ctx_t* ctx, const void* v, uint64_t* out, uint64_t n_polys,
                                  void* stream) {
@@ -359,14 +356,14 @@ extern "C" int ctb_decrypt_round(const ctb_ctx_t* ctx, const void* v, uint64_t* 
   cudaStream_t s = (cudaStream_t)stream;
   if (c->rns->lazy) {
     if (c->rns->dec.L == 7)
-      k_decrypt_round_lazy<7><<<grid_for(total), 256, 0, s>>>((const uint32_t*)v, out, c->rns->dec, c->n, total);
+      k_decrypt_round_lazy<7><<<grid_stride(total, 8), 256, 0, s>>>((const uint32_t*)v, out, c->rns->dec, c->n, total);
     else
-      k_decrypt_round_lazy<0><<<grid_for(total), 256, 0, s>>>((const uint32_t*)v, out, c->rns->dec, c->n, total);
+      k_decrypt_round_lazy<0><<<grid_stride(total, 8), 256, 0, s>>>((const uint32_t*)v, out, c->rns->dec, c->n, total);
   } else if (c->rns->word == 4)
-    k_decrypt_round<uint32_t><<<grid_for(total), 256, 0, s>>>((const uint32_t*)v, out,
+    k_decrypt_round<uint32_t><<<grid_stride(total, 8), 256, 0, s>>>((const uint32_t*)v, out,
                                                               (const QConsts<uint32_t>*)c->rns->d_q, c->n, total);
   else
-    k_decrypt_round<uint64_t><<<grid_for(total), 256, 0, s>>>((const uint64_t*)v, out,
+    k_decrypt_round<uint64_t><<<grid_stride(total, 8), 256, 0, s>>>((const uint64_t*)v, out,
                                                               (const QConsts<uint64_t>*)c->rns->d_q, c->n, total);
   return cuda_status(cudaGetLastError(), "ctb_decrypt_round");
 }
@@ -379,10 +376,10 @@ extern "C" int ctb_rns_to_pos(const ctb_ctx_t* ctx, const void* x, uint64_t* out
   if (!total) return OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (c->rns->word == 4)
-    k_rns_to_pos<uint32_t><<<grid_for(total), 256, 0, s>>>((const uint32_t*)x, out,
+    k_rns_to_pos<uint32_t><<<grid_stride(total, 8), 256, 0, s>>>((const uint32_t*)x, out,
                                                            (const QConsts<uint32_t>*)c->rns->d_q, c->n, total);
   else
-    k_rns_to_pos<uint64_t><<<grid_for(total), 256, 0, s>>>((const uint64_t*)x, out,
+    k_rns_to_pos<uint64_t><<<grid_stride(total, 8), 256, 0, s>>>((const uint64_t*)x, out,
                                                            (const QConsts<uint64_t>*)c->rns->d_q, c->n, total);
   return cuda_status(cudaGetLastError(), "ctb_rns_to_pos");
 }
@@ -395,10 +392,10 @@ extern "C" int ctb_pos_to_rns(const ctb_ctx_t* ctx, const uint64_t* in, void* x,
   if (!total) return OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (c->rns->word == 4)
-    k_pos_to_rns<uint32_t><<<grid_for(total), 256, 0, s>>>(in, (uint32_t*)x, (const QConsts<uint32_t>*)c->rns->d_q,
+    k_pos_to_rns<uint32_t><<<grid_stride(total, 8), 256, 0, s>>>(in, (uint32_t*)x, (const QConsts<uint32_t>*)c->rns->d_q,
                                                            c->n, total);
   else
-    k_pos_to_rns<uint64_t><<<grid_for(total), 256, 0, s>>>(in, (uint64_t*)x, (const QConsts<uint64_t>*)c->rns->d_q,
+    k_pos_to_rns<uint64_t><<<grid_stride(total, 8), 256, 0, s>>>(in, (uint64_t*)x, (const QConsts<uint64_t>*)c->rns->d_q,
                                                            c->n, total);
   return cuda_status(cudaGetLastError(), "ctb_pos_to_rns");
 }

@@ -77,9 +77,6 @@ __global__ void k_draws_layout(const int8_t* in, int8_t* out, uint64_t total) {
 
 using namespace ctb;
 
-static unsigned grid_for(uint64_t total) {
-  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148ull * 16));
-}
 
 extern "C" int ctb_sample_draws(const ctb_ctx_t* ctx, uint64_t seed, uint64_t first_poly, double sigma, int bound,
                                 int8_t* out, uint64_t batch, void* stream) {
@@ -89,7 +86,7 @@ extern "C" int ctb_sample_draws(const ctb_ctx_t* ctx, uint64_t seed, uint64_t fi
   if (bound < 0 || bound > 127 || !(sigma >= 0.0)) { set_error("ctb_sample_draws: bound must be in [0, 127], sigma >= 0"); return ERR_ARG; }
   const uint64_t total = batch * c->n;
   cudaStream_t s = (cudaStream_t)stream;
-  CTB_DISPATCH_LOGN(c->logn, (k_sample_draws<LOGN><<<grid_for(total), 256, 0, s>>>(out, seed, first_poly, total,
+  CTB_DISPATCH_LOGN(c->logn, (k_sample_draws<LOGN><<<grid_stride(total, 16), 256, 0, s>>>(out, seed, first_poly, total,
                                                                                 (float)sigma, bound)));
   return cuda_status(cudaGetLastError(), "ctb_sample_draws");
 }
@@ -101,6 +98,6 @@ extern "C" int ctb_draws_from_natural(const ctb_ctx_t* ctx, const int8_t* in, in
   if (!c || !in || !out || in == out) { set_error("ctb_draws_from_natural: bad context or buffer (no in-place)"); return ERR_ARG; }
   const uint64_t total = batch * 3 * c->n;
   cudaStream_t s = (cudaStream_t)stream;
-  CTB_DISPATCH_LOGN(c->logn, (k_draws_layout<LOGN><<<grid_for(total), 256, 0, s>>>(in, out, total)));
+  CTB_DISPATCH_LOGN(c->logn, (k_draws_layout<LOGN><<<grid_stride(total, 16), 256, 0, s>>>(in, out, total)));
   return cuda_status(cudaGetLastError(), "ctb_draws_from_natural");
 }

@@ -296,9 +296,7 @@ k_tensor_product(const uint32_t* A, const uint32_t* Bt, uint32_t* H, const Prime
   PrimeRegs<T> pr(tabs + k);
   const T* twp = pr.fwd;
   if constexpr (SMEM_TW) {
-    const uint4* src = reinterpret_cast<const uint4*>(pr.fwd);
-    uint4* dst = reinterpret_cast<uint4*>(tw_sm);
-    for (int i = threadIdx.x; i < TW_WORDS * 4 / 16; i += Sh::THREADS) dst[i] = __ldg(src + i);
+    stage_twiddles(pr.fwd, tw_sm, TW_WORDS, Sh::THREADS);
     __syncthreads();
     twp = tw_sm;
   }
@@ -544,9 +542,7 @@ k_relin_accum(const T* ct3, int ct_parts, const uint32_t* digits, const T* keypr
   PrimeRegs<T> pr(tabs + limb);
   const T* twp = pr.fwd;
   if constexpr (SMEM_TW) {
-    const uint4* src = reinterpret_cast<const uint4*>(pr.fwd);
-    uint4* dst = reinterpret_cast<uint4*>(tw_sm);
-    for (int i = threadIdx.x; i < TW_WORDS * (int)sizeof(T) / 16; i += Sh::THREADS) dst[i] = __ldg(src + i);
+    stage_twiddles(pr.fwd, tw_sm, TW_WORDS, Sh::THREADS);
     twp = tw_sm;
   }
   uint32_t phase = 0;
@@ -666,9 +662,7 @@ k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict
   PrimeRegs<T> pr(tabs + k);
   const T* twp = pr.fwd;
   if constexpr (SMEM_TW) {
-    const uint4* src = reinterpret_cast<const uint4*>(pr.fwd);
-    uint4* dst = reinterpret_cast<uint4*>(tw_sm);
-    for (int i = threadIdx.x; i < TW_WORDS * 4 / 16; i += Sh::THREADS) dst[i] = __ldg(src + i);
+    stage_twiddles(pr.fwd, tw_sm, TW_WORDS, Sh::THREADS);
     __syncthreads();
     twp = tw_sm;
   }
@@ -1003,9 +997,6 @@ int tensor_aux_count(const TensorState* t) { return t ? t->K : 0; }
 
 using namespace ctb;
 
-static unsigned grid_pc(uint64_t total) {
-  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148ull * 4));
-}
 
 static int ensure_tensor(const ctb_ctx_t* ctx, const Ctx*& c) {
   c = reinterpret_cast<const Ctx*>(ctx);
@@ -1034,7 +1025,7 @@ extern "C" int ctb_tensor_lift(const ctb_ctx_t* ctx, const void* ct, uint32_t* o
   if (!total) return OK;
   cudaStream_t s = (cudaStream_t)stream;
   const int L = c->tensor->L, K = c->tensor->K;
-  const unsigned grid = grid_pc(total);
+  const unsigned grid = grid_stride(total, 4);
   if (c->base[BASE_Q].word == 4) {
     const auto& tc = *reinterpret_cast<const TensorConsts<uint32_t>*>(c->tensor->host.data());
     if (L == 7 && K == 17) k_tensor_lift<uint32_t, 7, 17><<<grid, 256, 0, s>>>((const uint32_t*)ct, out, tc, c->n, total);
@@ -1070,7 +1061,7 @@ extern "C" int ctb_tensor_round(const ctb_ctx_t* ctx, const uint32_t* h_aux, voi
   if (!total) return OK;
   cudaStream_t s = (cudaStream_t)stream;
   const int L = c->tensor->L, K = c->tensor->K, K2 = c->tensor->K2;
-  const unsigned grid = grid_pc(total);
+  const unsigned grid = grid_stride(total, 4);
   if (c->base[BASE_Q].word == 4) {
     const auto& tc = *reinterpret_cast<const TensorConsts<uint32_t>*>(c->tensor->host.data());
     if (L == 7 && K == 17 && K2 == 10 && c->tensor->q_lead)
@@ -1135,9 +1126,9 @@ extern "C" int ctb_relinearize(const ctb_ctx_t* ctx, const void* ct3, const void
     using T = uint32_t;
     const auto& tc = *reinterpret_cast<const TensorConsts<T>*>(st.host.data());
     if (st.L == 7 && D == 14 && c->relin_base_bits == 16 && tc.lazy_digits)
-      k_relin_digits<T, 7, 14, 16><<<grid_pc(total), 256, 0, s>>>((const T*)ct3, digits_ws, tc, c->n, total);
+      k_relin_digits<T, 7, 14, 16><<<grid_stride(total, 4), 256, 0, s>>>((const T*)ct3, digits_ws, tc, c->n, total);
     else
-      k_relin_digits<T, 0, 0, 0><<<grid_pc(total), 256, 0, s>>>((const T*)ct3, digits_ws, tc, c->n, total);
+      k_relin_digits<T, 0, 0, 0><<<grid_stride(total, 4), 256, 0, s>>>((const T*)ct3, digits_ws, tc, c->n, total);
     e = cudaGetLastError();
     if (e == cudaSuccess)
       CTB_DISPATCH_LOGN(c->logn, e = (launch_relin_accum<T, LOGN>(c, ct3, 3, digits_ws, keyprep, out, batch, D, s)));
@@ -1145,9 +1136,9 @@ extern "C" int ctb_relinearize(const ctb_ctx_t* ctx, const void* ct3, const void
     using T = uint64_t;
     const auto& tc = *reinterpret_cast<const TensorConsts<T>*>(st.host.data());
     if (st.L == 3 && D == 10 && c->relin_base_bits == 16)
-      k_relin_digits<T, 3, 10, 16><<<grid_pc(total), 256, 0, s>>>((const T*)ct3, digits_ws, tc, c->n, total);
+      k_relin_digits<T, 3, 10, 16><<<grid_stride(total, 4), 256, 0, s>>>((const T*)ct3, digits_ws, tc, c->n, total);
     else
-      k_relin_digits<T, 0, 0, 0><<<grid_pc(total), 256, 0, s>>>((const T*)ct3, digits_ws, tc, c->n, total);
+      k_relin_digits<T, 0, 0, 0><<<grid_stride(total, 4), 256, 0, s>>>((const T*)ct3, digits_ws, tc, c->n, total);
     e = cudaGetLastError();
     if (e == cudaSuccess)
       CTB_DISPATCH_LOGN(c->logn, e = (launch_relin_accum<T, LOGN>(c, ct3, 3, digits_ws, keyprep, out, batch, D, s)));
@@ -1282,18 +1273,18 @@ extern "C" int ctb_ccmul_sum(const ctb_ctx_t* ctx, const void* ct_x, uint32_t n_
     if (w == 4) {
       const auto& tc = *reinterpret_cast<const TensorConsts<uint32_t>*>(c->tensor->host.data());
       if (L == 7 && D == 14 && c->relin_base_bits == 16 && tc.lazy_digits)
-        k_slot_digits<uint32_t, 7, 14, 16><<<grid_pc(total), 256, 0, s>>>((const uint32_t*)CT3, d_ptr + o0, s0,
+        k_slot_digits<uint32_t, 7, 14, 16><<<grid_stride(total, 4), 256, 0, s>>>((const uint32_t*)CT3, d_ptr + o0, s0,
                                                                         (uint32_t*)C01, DS, tc, (uint32_t)N, total);
       else
-        k_slot_digits<uint32_t, 0, 0, 0><<<grid_pc(total), 256, 0, s>>>((const uint32_t*)CT3, d_ptr + o0, s0,
+        k_slot_digits<uint32_t, 0, 0, 0><<<grid_stride(total, 4), 256, 0, s>>>((const uint32_t*)CT3, d_ptr + o0, s0,
                                                                        (uint32_t*)C01, DS, tc, (uint32_t)N, total);
     } else {
       const auto& tc = *reinterpret_cast<const TensorConsts<uint64_t>*>(c->tensor->host.data());
       if (L == 3 && D == 10 && c->relin_base_bits == 16)
-        k_slot_digits<uint64_t, 3, 10, 16><<<grid_pc(total), 256, 0, s>>>((const uint64_t*)CT3, d_ptr + o0, s0,
+        k_slot_digits<uint64_t, 3, 10, 16><<<grid_stride(total, 4), 256, 0, s>>>((const uint64_t*)CT3, d_ptr + o0, s0,
                                                                         (uint64_t*)C01, DS, tc, (uint32_t)N, total);
       else
-        k_slot_digits<uint64_t, 0, 0, 0><<<grid_pc(total), 256, 0, s>>>((const uint64_t*)CT3, d_ptr + o0, s0,
+        k_slot_digits<uint64_t, 0, 0, 0><<<grid_stride(total, 4), 256, 0, s>>>((const uint64_t*)CT3, d_ptr + o0, s0,
                                                                        (uint64_t*)C01, DS, tc, (uint32_t)N, total);
     }
     e = cudaGetLastError();
