@@ -67,7 +67,7 @@ def test_ntt_all_degrees_match_oracle(logn, bits):
     assert np.array_equal(back, a.astype(np.uint64))
 
 
-@pytest.mark.parametrize("logn,bits", [(6, 30), (9, 30), (12, 30), (13, 30), (12, 50), (13, 50)])
+@pytest.mark.parametrize("logn,bits", [(6, 30), (9, 30), (12, 30), (13, 30), (12, 50), (13, 50), (12, 36), (10, 44)])
 def test_ring_mul_matches_oracle(logn, bits):
     from paper_2409_16675_b200.device import RnsContext
     n = 1 << logn
