@@ -152,19 +152,28 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------- ours
-def probe_modmul_peak(torch, lib, word: int):
+def probe_modmul_peak(torch, lib, word: int, f64q_of_8=None):
+    """Register-resident modmul/s: Shoup at `word` bytes, or (f64q_of_8 given) the 30-bit mix of
+    Shoup and FP64-quotient products (ctb_probe_modmul_mix)."""
     import ctypes
     sink = torch.zeros(1, dtype=torch.int64, device="cuda")
     stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     n = ctypes.c_uint64()
     iters = 4000 if word == 4 else 1000
+
+    def launch():
+        if f64q_of_8 is None:
+            rc = lib.ctb_probe_modmul(word, iters, ctypes.c_void_p(sink.data_ptr()), ctypes.byref(n), stream)
+        else:
+            rc = lib.ctb_probe_modmul_mix(f64q_of_8, iters, ctypes.c_void_p(sink.data_ptr()), ctypes.byref(n), stream)
+        assert rc == 0, "modmul probe failed"
     for _ in range(2):
-        lib.ctb_probe_modmul(word, iters, ctypes.c_void_p(sink.data_ptr()), ctypes.byref(n), stream)
+        launch()
     best = 0.0
     for _ in range(3):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        lib.ctb_probe_modmul(word, iters, ctypes.c_void_p(sink.data_ptr()), ctypes.byref(n), stream)
+        launch()
         e.record()
         e.synchronize()
         best = max(best, n.value / (s.elapsed_time(e) * 1e-3))
@@ -354,7 +363,12 @@ def run_ours(args):
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     hbm_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
-    modmul_peak = probe_modmul_peak(torch, _lib.load(), 4)  # modmul/s, Shoup u32, register resident
+    # modmul/s of k_cpmul's own butterfly product mix (3/8 FP64-quotient, 5/8 Shoup), register
+    # resident; the pure forms are reported beside it
+    lib = _lib.load()
+    modmul_peak = probe_modmul_peak(torch, lib, 4, f64q_of_8=3)
+    peak_shoup = probe_modmul_peak(torch, lib, 4)
+    peak_f64q = probe_modmul_peak(torch, lib, 4, f64q_of_8=8)
     avg_launch_s = statistics.mean(step_ms) * 1e-3
     modmuls_per = L * (5 * (N // 2) * (N.bit_length() - 1) + 2 * N)   # 3 fwd + 2 inv NTTs + 2 pointwise
     bytes_per = 16 * L * N + 8 * N                                     # read c (u32) + pt (u64), write out
@@ -386,8 +400,11 @@ def run_ours(args):
                 "traffic": _ncu_traffic("k_cpmul<u32,12>", B),
                 "kernel": "k_cpmul<uint32_t,12>",
                 "algorithmic_per_cpmul": {"modmuls": modmuls_per, "bytes": bytes_per},
-                "peak_source": {"int": "measured now: ctb_probe_modmul (Shoup u32, register-resident)",
+                "peak_source": {"int": "measured now: ctb_probe_modmul_mix(3) -- k_cpmul's butterfly product mix "
+                                       "(3/8 FP64-quotient, 5/8 Shoup), u32, register-resident",
                                 "hbm": hbm_src},
+                "int_probes_gmodmul_s": {"mix_3_of_8": modmul_peak / 1e9, "shoup": peak_shoup / 1e9,
+                                         "f64_quotient": peak_f64q / 1e9},
                 "hbm": {"achieved_gbs": achieved_bw, "peak_gbs": hbm_peak, "frac": achieved_bw / hbm_peak},
                 "t_min_ms": 1e3 * max(t_int, t_hbm), "t_measured_ms": 1e3 * avg_launch_s,
             },

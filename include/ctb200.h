@@ -240,6 +240,11 @@ int ctb_slot_sum(const ctb_ctx_t* ctx, int base, const void* in, uint32_t parts,
  * device word that is written only in a never-taken branch. */
 int ctb_probe_modmul(int word_bytes, uint64_t iters, void* sink, uint64_t* modmuls, void* stream);
 
+/* Instrumentation: the 30-bit butterfly product mix of ctb_cpmul -- f64q_of_8 (0, 3 or 8) of
+ * the 8 chains take the FP64-pipe quotient (3 = the share k_cpmul uses), the rest are Shoup
+ * products.  Same launch shape and contract as ctb_probe_modmul; bench.py divides by it. */
+int ctb_probe_modmul_mix(int f64q_of_8, uint64_t iters, void* sink, uint64_t* modmuls, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

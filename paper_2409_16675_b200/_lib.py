@@ -6,10 +6,14 @@ device is visible, every entry point raises.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libctb200.so"
+# development A/B builds (tools/ab_variants.py) point CTB_LIB at an alternative in-tree build
+if os.environ.get("CTB_LIB"):
+    LIB_PATH = Path(os.environ["CTB_LIB"]).resolve()
 
 CTB_OK, CTB_ERR_ARG, CTB_ERR_CUDA, CTB_ERR_UNSUPPORTED = 0, -1, -2, -3
 BASE_Q, BASE_T, BASE_B = 0, 1, 2
@@ -70,6 +74,7 @@ SIGNATURES: dict[str, tuple] = {
                              _c_void_p, _u64, _c_void_p]),
     "ctb_slot_sum": (_int, [_c_void_p, _int, _c_void_p, _u32, _c_void_p, _c_void_p, _u32, _c_void_p, _c_void_p]),
     "ctb_probe_modmul": (_int, [_int, _u64, _c_void_p, ctypes.POINTER(_u64), _c_void_p]),
+    "ctb_probe_modmul_mix": (_int, [_int, _u64, _c_void_p, ctypes.POINTER(_u64), _c_void_p]),
 }
 
 

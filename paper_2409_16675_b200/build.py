@@ -40,12 +40,12 @@ def _deps() -> list[Path]:
     return sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.hpp")) + [INCLUDE / "ctb200.h"]
 
 
-def _compile(src: Path, force: bool, verbose: bool) -> Path:
-    obj = OBJ / (src.stem + ".o")
+def _compile(src: Path, force: bool, verbose: bool, defines=(), objdir: Path = OBJ) -> Path:
+    obj = objdir / (src.stem + ".o")
     newest_dep = max([src.stat().st_mtime] + [d.stat().st_mtime for d in _deps()])
     if not force and obj.exists() and obj.stat().st_mtime >= newest_dep:
         return obj
-    cmd = [nvcc(), *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", str(src), "-o", str(obj)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -56,19 +56,20 @@ def _compile(src: Path, force: bool, verbose: bool) -> Path:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    OBJ.mkdir(parents=True, exist_ok=True)
-    LIB.parent.mkdir(parents=True, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), out: Path = LIB, objdir: Path = OBJ) -> Path:
+    """defines/out/objdir: development variants (tools/ab_variants.py); the product is the default."""
+    objdir.mkdir(parents=True, exist_ok=True)
+    out.parent.mkdir(parents=True, exist_ok=True)
     sources = sorted(CSRC.glob("*.cu"))
     with cf.ThreadPoolExecutor(max_workers=min(8, len(sources))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, force, verbose), sources))
+        objs = list(ex.map(lambda s: _compile(s, force, verbose, defines, objdir), sources))
     newest = max(o.stat().st_mtime for o in objs)
-    if force or not LIB.exists() or LIB.stat().st_mtime < newest:
-        cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+    if force or not out.exists() or out.stat().st_mtime < newest:
+        cmd = [nvcc(), *ARCH, "-shared", "-o", str(out), *map(str, objs), "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stderr[-4000:]}")
-    return LIB
+    return out
 
 
 if __name__ == "__main__":

@@ -1,4 +1,5 @@
 #include <algorithm>
+#include <cmath>
 // Prime tables: twiddles, Shoup quotients, Montgomery constants.
 #include <cstring>
 #include <mutex>
@@ -117,6 +118,13 @@ static int build_typed(Base& b, uint32_t logn, std::string& err, const uint64_t*
             const uint64_t w = pw[bitrev(mb, logn)];
             if (sizeof(T) == 4) {
               f[2 * e] = (T)w;  f[2 * e + 1] = shoup_q<T>(w, p);
+              const int ei = (1 << i) - 1 + jb;
+              if (ei < F64Q_NE) {  // FP64 quotient table (ntt.cuh F64Q_NE): w'/p = round(w 2^52 / p) 2^-52
+                const uint64_t num = (uint64_t)((((unsigned __int128)w << 52) + p / 2) / p);
+                const double wp = std::ldexp((double)num, -52);
+                const size_t qe = (size_t)shape_q_off((int)logn, k) + ((size_t)ei << s) + tw_group_slot((int)logn, s, r, B);
+                std::memcpy(reinterpret_cast<unsigned char*>(f + 2 * ent) + 8 * qe, &wp, 8);
+              }
             } else {  // 64-bit limbs run the FP64 butterflies (ntt.cuh): w as a double
               const double wd = (double)w;
               uint64_t bw;

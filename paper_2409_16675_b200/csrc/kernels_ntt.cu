@@ -72,6 +72,13 @@ __global__ void k_pointwise(const T* a, const T* b, T* out, const PrimeTab<T>* _
 // groups advance through the batch together, so a plaintext read by all 7
 // limbs is an L2 hit after the first.
 constexpr int CPMUL_NBUF = 1;
+// FP64-quotient butterflies (ntt.cuh F64Q_NE) per kernel family: the compute-bound CPMul and
+// encryption kernels gain from moving quotients onto the FP64 pipe; the streaming transforms
+// (latency-bound at their occupancy) do not (A/B: tools/ab_cpmul.py).
+#ifndef CTB_STREAM_QE
+#define CTB_STREAM_QE 0
+#endif
+constexpr int STREAM_QE = CTB_STREAM_QE;
 
 // Groups of THREADS threads per CTA for the persistent CPMul: each group runs
 // its own ciphertext of the CTA's limb, all groups share the CTA's twiddle
@@ -288,9 +295,9 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
         fwd_pass<T, LOGN, 0, SMEM_TW>(x, tw, pr.p, pr.p2);
         ex.template run<Sh::pass_s(0), Sh::pass_r(0), Sh::pass_s(1), Sh::pass_r(1)>(x);
         issue_next();
-        ntt_fwd_regs<T, LOGN, 1, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+        ntt_fwd_regs<T, LOGN, 1, SMEM_TW, CPMUL_NBUF, GROUPS, STREAM_QE>(x, ex, tw, pr.p, pr.p2);
       } else {
-        ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+        ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS, STREAM_QE>(x, ex, tw, pr.p, pr.p2);
         issue_next();
       }
     };
@@ -301,11 +308,11 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
           inv_pass<T, LOGN, K, SMEM_TW>(x, tw, pr.p, pr.p2);
           ex.template run<Sh::pass_s(K), Sh::pass_r(K), Sh::pass_s(K - 1), Sh::pass_r(K - 1)>(x);
           issue_next();
-          ntt_inv_regs<T, LOGN, K - 1, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+          ntt_inv_regs<T, LOGN, K - 1, SMEM_TW, CPMUL_NBUF, GROUPS, STREAM_QE>(x, ex, tw, pr.p, pr.p2);
           return;
         }
       }
-      ntt_inv_regs<T, LOGN, K, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+      ntt_inv_regs<T, LOGN, K, SMEM_TW, CPMUL_NBUF, GROUPS, STREAM_QE>(x, ex, tw, pr.p, pr.p2);
       if (first_in_item) issue_next();
     };
     if constexpr (OP == StreamOp::Inv) {

@@ -58,10 +58,34 @@ __host__ __device__ constexpr int shape_tw_off(int logn, int k) {
   return off;
 }
 __host__ __device__ constexpr int shape_tw_entries(int logn) { return shape_tw_off(logn, shape_npass(logn)); }
-// Words per prime in the twiddle table: (w, w') pairs for 32-bit limbs; one double w per entry
-// for 64-bit limbs (the FP64 butterflies derive w/p as w * (1/p), see ntt.cuh f64 section).
+// FP64-quotient butterflies (32-bit limbs).  The Shoup product a*w mod p costs IMAD.HI + 2 IMAD,
+// all on the fma-heavy pipe (IMAD.HI at half rate), which is what bounds the transforms.  For the
+// twiddle entries e < F64Q_NE of every pass (e = 2^i - 1 + jb: stage 0 and the first block of
+// stage 1, 12 of the 32 butterflies of a radix-16 pass) the quotient comes from the otherwise idle
+// FP64 pipe instead: one DFMA on the exponent-spliced double 2^52 + a gives rint(a * w'/p) with
+// w'/p = round(w 2^52 / p) 2^-52 (|error| < 2^-21 for a < 2^32, so the quotient is floor or ceil of
+// a*w/p), and a*w + p - q*p in (0, 2p) takes 2 IMAD -- the Shoup output range.  Measured register
+// resident on this B200 (tools/probe/imad_probe.cu): Shoup 4.63 T/s, FP64-quotient 6.79 T/s.
+// The quotients live in a second table after the (w, w') pairs: one double w'/p per entry,
+// pass-major, [e][group slot] inside a pass.  -DCTB_F64Q_ENTRIES=0 restores pure Shoup.
+#ifndef CTB_F64Q_ENTRIES
+#define CTB_F64Q_ENTRIES 2
+#endif
+constexpr int F64Q_NE = CTB_F64Q_ENTRIES;
+__host__ __device__ constexpr int shape_q_off(int logn, int k) {
+  int off = 0;
+  for (int q = 0; q < k; ++q) off += F64Q_NE << shape_pass_s(logn, q);
+  return off;
+}
+// doubles in the quotient table, rounded up to a 16-byte multiple
+__host__ __device__ constexpr int shape_q_entries(int logn) { return (shape_q_off(logn, shape_npass(logn)) + 1) & ~1; }
+// Words per prime in the twiddle table: (w, w') pairs (+ the FP64 quotient table) for 32-bit
+// limbs; one double w per entry for 64-bit limbs (the FP64 butterflies derive w/p as w * (1/p),
+// see the f64 section below).
 template <typename T>
-__host__ __device__ constexpr int tw_words(int logn) { return (sizeof(T) == 4 ? 2 : 1) * shape_tw_entries(logn); }
+__host__ __device__ constexpr int tw_words(int logn) {
+  return sizeof(T) == 4 ? 2 * shape_tw_entries(logn) + 2 * shape_q_entries(logn) : shape_tw_entries(logn);
+}
 
 template <int LOGN>
 struct NttShape {
@@ -181,6 +205,14 @@ __device__ __forceinline__ void stage_twiddles(const T* table, T* smem, int word
 template <typename T, bool SMEM>
 struct TwSrc {
   const T* tab;  // generic pointer to pair 0 of this prime's table (global or shared)
+  __device__ __forceinline__ double loadq(const double* at) const {
+    double v;
+    if constexpr (SMEM)
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((uint32_t)__cvta_generic_to_shared(at)));
+    else
+      asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(at));
+    return v;
+  }
   __device__ __forceinline__ void load(const T* at, T& w, T& wq) const {
     if constexpr (SMEM) {
       const uint32_t sa = (uint32_t)__cvta_generic_to_shared(at);
@@ -239,11 +271,31 @@ __device__ __forceinline__ void gs_bfly(T& X, T& Y, T w, T wq, T p, T p2) {
   }
 }
 
-template <typename T, int LOGN, int K, bool SMEM>
+// FP64-quotient product (see F64Q_NE): a < 2^32, w < p < 2^30, wp = w'/p, kq = 1.5 2^52 - 2^52 wp
+// (exact).  fma((2^52 + a), wp, kq) = 1.5 2^52 + a wp exactly before its one rounding, to the
+// nearest integer (ulp 1 there): the low word is rint(a wp) in {floor, ceil}(a w / p).
+__device__ __forceinline__ uint32_t f64q_mul(uint32_t a, uint32_t w, double wp, double kq, uint32_t p, uint32_t pn) {
+  const double qd = __fma_rn(__hiloint2double(0x43300000, (int)a), wp, kq);
+  const uint32_t q = (uint32_t)__double2loint(qd);
+  uint32_t t, r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(a), "r"(w), "r"(p));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(q), "r"(pn), "r"(t));
+  return r;  // a*w + p - q*p in (0, 2p)
+}
+__device__ __forceinline__ double f64q_k(double wp) { return __fma_rn(-4503599627370496.0, wp, 6755399441055744.0); }
+// the FP64 quotient of entry (pass K, e = 0, group slot); entry e is at [e << S0] from it
+template <typename T, int LOGN, int K>
+__device__ __forceinline__ const double* q_group(const T* tab, int slot) {
+  return reinterpret_cast<const double*>(tab + 2 * shape_tw_entries(LOGN)) + shape_q_off(LOGN, K) + slot;
+}
+
+template <typename T, int LOGN, int K, bool SMEM, int QE = F64Q_NE>
 __device__ __forceinline__ void fwd_pass(T (&x)[NttShape<LOGN>::E], TwSrc<T, SMEM> tw, T p, T p2) {
+  static_assert(QE <= F64Q_NE, "FP64 quotient entries beyond the table");
   using Sh = NttShape<LOGN>;
   constexpr int S0 = Sh::pass_s(K), R = Sh::pass_r(K);
   constexpr int G = 1 << R;
+  const T pn = (T)0 - p;
 #pragma unroll
   for (int gg = 0; gg < Sh::E / G; ++gg) {
     const int slot = tw_slot<LOGN, S0, R>(gg);
@@ -253,23 +305,39 @@ __device__ __forceinline__ void fwd_pass(T (&x)[NttShape<LOGN>::E], TwSrc<T, SME
       const int h = 1 << (R - i - 1);
 #pragma unroll
       for (int jb = 0; jb < (1 << i); ++jb) {
+        const int e = (1 << i) - 1 + jb;
         T w, wq;
-        tw.load(tg + 2 * (((1 << i) - 1 + jb) << S0), w, wq);
+        tw.load(tg + 2 * (e << S0), w, wq);
+        if (sizeof(T) == 4 && e < QE) {
+          const double wp = tw.loadq(q_group<T, LOGN, K>(tw.tab, slot) + (e << S0));
+          const double kq = f64q_k(wp);
 #pragma unroll
-        for (int jj = 0; jj < h; ++jj) {
-          const int a = gg * G + jb * 2 * h + jj;
-          ct_bfly(x[a], x[a + h], w, wq, p, p2);
+          for (int jj = 0; jj < h; ++jj) {
+            const int a = gg * G + jb * 2 * h + jj;
+            const T xx = csub(x[a], p2);
+            const T t = (T)f64q_mul((uint32_t)x[a + h], (uint32_t)w, wp, kq, (uint32_t)p, (uint32_t)pn);
+            x[a] = xx + t;
+            x[a + h] = xx - t + p2;
+          }
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < h; ++jj) {
+            const int a = gg * G + jb * 2 * h + jj;
+            ct_bfly(x[a], x[a + h], w, wq, p, p2);
+          }
         }
       }
     }
   }
 }
 
-template <typename T, int LOGN, int K, bool SMEM>
+template <typename T, int LOGN, int K, bool SMEM, int QE = F64Q_NE>
 __device__ __forceinline__ void inv_pass(T (&x)[NttShape<LOGN>::E], TwSrc<T, SMEM> tw, T p, T p2) {
+  static_assert(QE <= F64Q_NE, "FP64 quotient entries beyond the table");
   using Sh = NttShape<LOGN>;
   constexpr int S0 = Sh::pass_s(K), R = Sh::pass_r(K);
   constexpr int G = 1 << R;
+  const T pn = (T)0 - p;
 #pragma unroll
   for (int gg = 0; gg < Sh::E / G; ++gg) {
     const int slot = (1 << S0) - 1 - tw_slot<LOGN, S0, R>(gg);  // mirrored group
@@ -279,12 +347,25 @@ __device__ __forceinline__ void inv_pass(T (&x)[NttShape<LOGN>::E], TwSrc<T, SME
       const int h = 1 << (R - i - 1);
 #pragma unroll
       for (int jb = 0; jb < (1 << i); ++jb) {
+        const int e = (1 << i) - 1 + ((1 << i) - 1 - jb);  // mirrored block
         T w, wq;
-        tw.load(tg + 2 * (((1 << i) - 1 + ((1 << i) - 1 - jb)) << S0), w, wq);
+        tw.load(tg + 2 * (e << S0), w, wq);
+        if (sizeof(T) == 4 && e < QE) {
+          const double wp = tw.loadq(q_group<T, LOGN, K>(tw.tab, slot) + (e << S0));
+          const double kq = f64q_k(wp);
 #pragma unroll
-        for (int jj = 0; jj < h; ++jj) {
-          const int a = gg * G + jb * 2 * h + jj;
-          gs_bfly(x[a], x[a + h], w, wq, p, p2);
+          for (int jj = 0; jj < h; ++jj) {
+            const int a = gg * G + jb * 2 * h + jj;
+            const T X = x[a], Y = x[a + h];
+            x[a] = csub(X + Y, p2);
+            x[a + h] = (T)f64q_mul((uint32_t)(Y - X + p2), (uint32_t)w, wp, kq, (uint32_t)p, (uint32_t)pn);
+          }
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < h; ++jj) {
+            const int a = gg * G + jb * 2 * h + jj;
+            gs_bfly(x[a], x[a + h], w, wq, p, p2);
+          }
         }
       }
     }
@@ -466,7 +547,7 @@ __device__ __forceinline__ void ntt_inv_f64(double (&x)[NttShape<LOGN>::E], Exch
   }
 }
 
-template <typename T, int LOGN, int K = 0, bool SMEM, int NBUF, int GROUPS>
+template <typename T, int LOGN, int K = 0, bool SMEM, int NBUF, int GROUPS, int QE = F64Q_NE>
 __device__ __forceinline__ void ntt_fwd_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN, NBUF, GROUPS>& ex,
                                              TwSrc<T, SMEM> tw, T p, T p2) {
   using Sh = NttShape<LOGN>;
@@ -483,15 +564,15 @@ __device__ __forceinline__ void ntt_fwd_regs(T (&x)[NttShape<LOGN>::E], Exchange
     for (int k = 0; k < Sh::E; ++k) x[k] = f64_to_canon(d[k], P);
   } else {
     constexpr int S = Sh::pass_s(K), R = Sh::pass_r(K);
-    fwd_pass<T, LOGN, K, SMEM>(x, tw, p, p2);
+    fwd_pass<T, LOGN, K, SMEM, QE>(x, tw, p, p2);
     if constexpr (K + 1 < Sh::NPASS) {
       ex.template run<S, R, Sh::pass_s(K + 1), Sh::pass_r(K + 1)>(x);
-      ntt_fwd_regs<T, LOGN, K + 1, SMEM, NBUF, GROUPS>(x, ex, tw, p, p2);
+      ntt_fwd_regs<T, LOGN, K + 1, SMEM, NBUF, GROUPS, QE>(x, ex, tw, p, p2);
     }
   }
 }
 
-template <typename T, int LOGN, int K = NttShape<LOGN>::NPASS - 1, bool SMEM, int NBUF, int GROUPS>
+template <typename T, int LOGN, int K = NttShape<LOGN>::NPASS - 1, bool SMEM, int NBUF, int GROUPS, int QE = F64Q_NE>
 __device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN, NBUF, GROUPS>& ex,
                                              TwSrc<T, SMEM> tw, T p, T p2) {
   using Sh = NttShape<LOGN>;
@@ -508,10 +589,10 @@ __device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchange
     for (int k = 0; k < Sh::E; ++k) x[k] = f64_to_canon(d[k], P);
   } else {
     constexpr int S = Sh::pass_s(K), R = Sh::pass_r(K);
-    inv_pass<T, LOGN, K, SMEM>(x, tw, p, p2);
+    inv_pass<T, LOGN, K, SMEM, QE>(x, tw, p, p2);
     if constexpr (K > 0) {
       ex.template run<S, R, Sh::pass_s(K - 1), Sh::pass_r(K - 1)>(x);
-      ntt_inv_regs<T, LOGN, K - 1, SMEM, NBUF, GROUPS>(x, ex, tw, p, p2);
+      ntt_inv_regs<T, LOGN, K - 1, SMEM, NBUF, GROUPS, QE>(x, ex, tw, p, p2);
     }
   }
 }

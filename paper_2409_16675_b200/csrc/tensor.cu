@@ -39,6 +39,12 @@
 
 namespace ctb {
 
+// FP64-quotient butterflies (ntt.cuh F64Q_NE) in the tensoring / relinearisation transforms.
+#ifndef CTB_TENSOR_QE
+#define CTB_TENSOR_QE 0
+#endif
+constexpr int TENSOR_QE = CTB_TENSOR_QE;
+
 constexpr int MAXA = 20;  // auxiliary primes
 constexpr int MAXQ = 8;   // cipher primes on the tensoring path
 constexpr int MAXDIG = 32;  // relinearisation digits on the lazy path
@@ -312,7 +318,7 @@ k_tensor_product(const uint32_t* A, const uint32_t* Bt, uint32_t* H, const Prime
       const T* p = s < 2 ? src(A, s) : src(Bt, 0);
 #pragma unroll
       for (int j = 0; j < Sh::E; ++j) x[j] = __ldg(p + coef_off<LOGN>(j));
-      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, 1, 1>(x, ex, tw, pr.p, pr.p2);
+      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, 1, 1, TENSOR_QE>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
       for (int j = 0; j < Sh::E; ++j) {
         T v = x[j];
@@ -324,7 +330,7 @@ k_tensor_product(const uint32_t* A, const uint32_t* Bt, uint32_t* H, const Prime
       const T* p = src(Bt, 1);
 #pragma unroll
       for (int j = 0; j < Sh::E; ++j) x[j] = __ldg(p + coef_off<LOGN>(j));
-      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, 1, 1>(x, ex, tw, pr.p, pr.p2);
+      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, 1, 1, TENSOR_QE>(x, ex, tw, pr.p, pr.p2);
     }
     // h2 = a1 b1 ; h1 = a0 b1 + a1 b0 ; h0 = a0 b0
 #pragma unroll 1
@@ -340,7 +346,7 @@ k_tensor_product(const uint32_t* A, const uint32_t* Bt, uint32_t* H, const Prime
         else v = mont_mul(b0, a0, pr.p, pr.pinv);
         y[j] = v;
       }
-      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1>(y, ex, tw, pr.p, pr.p2);
+      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1, TENSOR_QE>(y, ex, tw, pr.p, pr.p2);
       T* dst = H + ((b * 3 + part) * K + k) * N + coef_base<LOGN>();
 #pragma unroll
       for (int j = 0; j < Sh::E; ++j) dst[coef_off<LOGN>(j)] = csub(y[j], pr.p);
@@ -584,7 +590,7 @@ k_relin_accum(const T* ct3, int ct_parts, const uint32_t* digits, const T* keypr
 #pragma unroll
         for (int j = 0; j < Sh::E; ++j) x[j] = pr.reduce_digit(__ldg(src + coef_off<LOGN>(j)));  // any u32 -> [0,p)
       }
-      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, 1, 1>(x, ex, tw, pr.p, pr.p2);
+      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, 1, 1, TENSOR_QE>(x, ex, tw, pr.p, pr.p2);
       const T* kb = keyprep + (((size_t)d * 2 + 0) * L + limb) * N;
       const T* ka = keyprep + (((size_t)d * 2 + 1) * L + limb) * N;
 #pragma unroll
@@ -604,7 +610,7 @@ k_relin_accum(const T* ct3, int ct_parts, const uint32_t* digits, const T* keypr
     for (int part = 0; part < 2; ++part) {
 #pragma unroll
       for (int j = 0; j < Sh::E; ++j) x[j] = part == 0 ? acc0[j] : acc1[j];
-      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1>(x, ex, tw, pr.p, pr.p2);
+      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1, TENSOR_QE>(x, ex, tw, pr.p, pr.p2);
       const size_t off = (((size_t)b * ct_parts + part) * L + limb) * N + cb;
       const size_t oo = ((b * 2 + part) * L + limb) * N + cb;
 #pragma unroll
@@ -704,11 +710,11 @@ k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict
         if constexpr (TWO) strip[(Sh::E + j) * Sh::THREADS] = mont_mul(a0[c], b0[c], pr.p, pr.pinv);
       }
     }
-    ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1>(y, ex, tw, pr.p, pr.p2);
+    ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1, TENSOR_QE>(y, ex, tw, pr.p, pr.p2);
     store(s, 2);
 #pragma unroll
     for (int j = 0; j < Sh::E; ++j) y[j] = strip[j * Sh::THREADS];
-    ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1>(y, ex, tw, pr.p, pr.p2);
+    ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1, TENSOR_QE>(y, ex, tw, pr.p, pr.p2);
     store(s, 1);
     if constexpr (TWO) {
 #pragma unroll
@@ -724,7 +730,7 @@ k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict
         for (int c = 0; c < EV::VEC; ++c) y[i * EV::VEC + c] = mont_mul(a0[c], b0[c], pr.p, pr.pinv);
       }
     }
-    ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1>(y, ex, tw, pr.p, pr.p2);
+    ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1, TENSOR_QE>(y, ex, tw, pr.p, pr.p2);
     store(s, 0);
   }
 }
