@@ -101,7 +101,7 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
   const int group = (int)(threadIdx.x / Sh::THREADS);
   T* gsm = tw_sm + TW_WORDS + group * GROUP_WORDS;
   Ex ex{gsm};
-  T* ysm = gsm + Ex::WORDS + ntt_tid<LOGN>();
+  Strip<T, LOGN> ysm(gsm + Ex::WORDS);  // NTT(pt) N^-1 2^W, this thread's evaluation slots
 
   const int limb = blockIdx.x % L;
   const uint32_t slot = blockIdx.x / L;
@@ -130,7 +130,8 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
       }
       ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
-      for (int k = 0; k < Sh::E; ++k) ysm[k * Sh::THREADS] = shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p);
+      for (int k = 0; k < Sh::E; ++k) x[k] = shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p);
+      ysm.store(x);
     }
 #pragma unroll 1
     for (int part = 0; part < 2; ++part) {
@@ -139,7 +140,15 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
       for (int k = 0; k < Sh::E; ++k) x[k] = ct[off + coef_off<LOGN>(k)];
       ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
-      for (int k = 0; k < Sh::E; ++k) x[k] = mont_mul(x[k], ysm[k * Sh::THREADS], pr.p, pr.pinv);
+      for (int c = 0; c < Strip<T, LOGN>::CHUNKS; ++c) {
+        T y[Strip<T, LOGN>::VEC];
+        ysm.load_chunk(c, y);
+#pragma unroll
+        for (int j = 0; j < Strip<T, LOGN>::VEC; ++j) {
+          const int k = c * Strip<T, LOGN>::VEC + j;
+          x[k] = mont_mul(x[k], y[j], pr.p, pr.pinv);
+        }
+      }
       ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) out[off + coef_off<LOGN>(k)] = csub(x[k], pr.p);
@@ -442,7 +451,7 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
   const int group = (int)(threadIdx.x / Sh::THREADS);
   T* gsm = tw_sm + TW_WORDS + group * GROUP_WORDS;
   Ex ex{gsm};
-  T* usm = gsm + Ex::WORDS + ntt_tid<LOGN>();   // NTT(u), thread-private strip
+  Strip<T, LOGN> usm(gsm + Ex::WORDS);  // NTT(u), this thread's evaluation slots
 
   const int limb = blockIdx.x % L;
   const uint32_t slot = blockIdx.x / L;
@@ -489,19 +498,26 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
       for (int k = 0; k < Sh::E; ++k) x[k] = small(u[k]);
     }
     ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
-#pragma unroll
-    for (int k = 0; k < Sh::E; ++k) usm[k * Sh::THREADS] = x[k];
+    usm.store(x);
 #pragma unroll 1
     for (int part = 0; part < 2; ++part) {
       const T* kp = pkprep + ((size_t)part * L + limb) * Sh::N;
       using EV = EvalVec<T, LOGN>;
+      static_assert(EV::VEC == Strip<T, LOGN>::VEC || EV::VEC == 1, "strip / eval chunking");
 #pragma unroll
       for (int i = 0; i < EV::CHUNKS; ++i) {
         T v[EV::VEC];
         EV::load(kp, i, v);
+        if constexpr (EV::VEC == Strip<T, LOGN>::VEC) {
+          T uu[EV::VEC];
+          usm.load_chunk(i, uu);
 #pragma unroll
-        for (int c = 0; c < EV::VEC; ++c)
-          x[i * EV::VEC + c] = mont_mul(usm[(i * EV::VEC + c) * Sh::THREADS], v[c], pr.p, pr.pinv);
+          for (int c = 0; c < EV::VEC; ++c) x[i * EV::VEC + c] = mont_mul(uu[c], v[c], pr.p, pr.pinv);
+        } else {
+          T uu[Strip<T, LOGN>::VEC];
+          usm.load_chunk(i / Strip<T, LOGN>::VEC, uu);
+          x[i] = mont_mul(uu[i % Strip<T, LOGN>::VEC], v[0], pr.p, pr.pinv);
+        }
       }
       int8_t e[Sh::E];  // issued before the inverse transform, consumed after it
       load_draws(drow + (size_t)(1 + part) * Sh::N, e);

@@ -132,8 +132,49 @@ __host__ __device__ constexpr int phys(int idx) {
 }
 
 template <typename T, int LOGN>
+struct SmemImage;
+
+// Vectorised exchange maps (32-bit words, N = 4096: three radix-16 passes starting at stages 0,
+// 4 and 8).  Each exchange gets its own additive map, chosen so that one side of it moves several
+// consecutive slots per instruction and both sides stay bank-conflict-free
+// (tools/swizzle_check.py --vector proves both):
+//   map 1, passes 0 <-> 1: index bit 8 (pass 0's lowest slot bit) has weight 1, so pass 0 moves
+//          slot pairs with 64-bit accesses; pass 1's lanes (index bits 0-3, 8) cover 32 banks;
+//   map 2, passes 1 <-> 2: index bits 0-3 (pass 2's slots) have weights 1, 2, 4, 8, so pass 2
+//          moves its 16 contiguous slots as four 128-bit accesses; the quarter-warp phases of
+//          pass 2 (index bits 5-7) land on distinct 16-byte bank groups.
+// One exchange then costs 24 (map 1) or 20 (map 2) shared-memory instructions per thread
+// instead of 32.  Map 0 is the generic scalar layout (smem_weight).
+template <typename T, int LOGN, int MAP>
+__host__ __device__ constexpr int phys_map(int idx) {
+  constexpr int M1[12] = {2, 4, 8, 16, 32, 64, 128, 256, 1, 512, 1024, 2048};
+  constexpr int M2[12] = {1, 2, 4, 8, 16, 36, 72, 144, 304, 588, 1176, 2352};
+  if constexpr (MAP == 0) {
+    return phys<T, LOGN>(idx);
+  } else {
+    int r = 0;
+    for (int b = 0; b < LOGN; ++b) r += ((idx >> b) & 1) * (MAP == 1 ? M1[b] : M2[b]);
+    return r;
+  }
+}
+template <typename T, int LOGN>
+__host__ __device__ constexpr bool vec_exchange() { return sizeof(T) == 4 && LOGN == 12; }
+// map of the exchange between the passes starting at stages SA and SB
+template <typename T, int LOGN, int SA, int SB>
+__host__ __device__ constexpr int exchange_map() {
+  if constexpr (!vec_exchange<T, LOGN>()) return 0;
+  else return (SA + SB == 4) ? 1 : (SA + SB == 12 ? 2 : 0);
+}
+// words per access on the side of pass S in map MAP
+template <int MAP, int S>
+__host__ __device__ constexpr int exchange_vec() { return MAP == 1 && S == 0 ? 2 : (MAP == 2 && S == 8 ? 4 : 1); }
+
+template <typename T, int LOGN>
 struct SmemImage {
-  static constexpr int WORDS = phys<T, LOGN>((1 << LOGN) - 1) + 1;
+  static constexpr int RAW = vec_exchange<T, LOGN>() ? (phys_map<T, LOGN, 2>((1 << LOGN) - 1) + 1)  // largest of maps 0-2
+                                                     : phys<T, LOGN>((1 << LOGN) - 1) + 1;
+  // rounded to 16 bytes: whatever follows an image (strips, staging) is vector-accessed
+  static constexpr int WORDS = (RAW + 16 / (int)sizeof(T) - 1) / (16 / (int)sizeof(T)) * (16 / (int)sizeof(T));
 };
 
 // Thread -> group permutation of a pass: the last pass of N >= 1024 rotates the
@@ -400,13 +441,71 @@ struct Exchanger {
     U* b = reinterpret_cast<U*>(buf + cur * SmemImage<T, LOGN>::WORDS);
     if constexpr (NBUF == 2) cur ^= 1;
     else group_sync<LOGN, GROUPS>();
-    U* wa = b + phys<T, LOGN>(pass_index<LOGN, SA, RA>(ntt_tid<LOGN>(), 0));
-    U* wb = b + phys<T, LOGN>(pass_index<LOGN, SB, RB>(ntt_tid<LOGN>(), 0));
+    constexpr int MAP = exchange_map<T, LOGN, SA, SB>();
+    constexpr int VA = exchange_vec<MAP, SA>(), VB = exchange_vec<MAP, SB>();
+    U* wa = b + phys_map<T, LOGN, MAP>(pass_index<LOGN, SA, RA>(ntt_tid<LOGN>(), 0));
+    U* wb = b + phys_map<T, LOGN, MAP>(pass_index<LOGN, SB, RB>(ntt_tid<LOGN>(), 0));
 #pragma unroll
-    for (int k = 0; k < Sh::E; ++k) wa[phys<T, LOGN>(pass_index<LOGN, SA, RA>(0, k))] = x[k];
+    for (int k = 0; k < Sh::E; k += VA) {
+      U* at = wa + phys_map<T, LOGN, MAP>(pass_index<LOGN, SA, RA>(0, k));
+      if constexpr (VA == 4)
+        *reinterpret_cast<uint4*>(at) = make_uint4((uint32_t)x[k], (uint32_t)x[k + 1], (uint32_t)x[k + 2], (uint32_t)x[k + 3]);
+      else if constexpr (VA == 2)
+        *reinterpret_cast<uint2*>(at) = make_uint2((uint32_t)x[k], (uint32_t)x[k + 1]);
+      else
+        *at = x[k];
+    }
     group_sync<LOGN, GROUPS>();
 #pragma unroll
-    for (int k = 0; k < Sh::E; ++k) x[k] = wb[phys<T, LOGN>(pass_index<LOGN, SB, RB>(0, k))];
+    for (int k = 0; k < Sh::E; k += VB) {
+      const U* at = wb + phys_map<T, LOGN, MAP>(pass_index<LOGN, SB, RB>(0, k));
+      if constexpr (VB == 4) {
+        const uint4 v = *reinterpret_cast<const uint4*>(at);
+        x[k] = (U)v.x; x[k + 1] = (U)v.y; x[k + 2] = (U)v.z; x[k + 3] = (U)v.w;
+      } else if constexpr (VB == 2) {
+        const uint2 v = *reinterpret_cast<const uint2*>(at);
+        x[k] = (U)v.x; x[k + 1] = (U)v.y;
+      } else {
+        x[k] = *at;
+      }
+    }
+  }
+};
+
+// Thread-private strip of E words per thread in shared memory (an operand kept in the
+// evaluation layout between transforms: NTT(pt) in k_cpmul, NTT(u) in k_encrypt), stored
+// chunk-major -- 16-byte chunk c of thread t at vector c * THREADS + t -- so it moves with
+// conflict-free 128-bit accesses (E/4 instructions instead of E for 32-bit words).
+// `region` (N words) must be 16-byte aligned.
+template <typename T, int LOGN>
+struct Strip {
+  using Sh = NttShape<LOGN>;
+  static constexpr int VEC = 16 / (int)sizeof(T);
+  static constexpr int CHUNKS = Sh::E / VEC;
+  static_assert(Sh::E % VEC == 0, "strip chunks");
+  uint4* base;
+  __device__ __forceinline__ explicit Strip(T* region) : base(reinterpret_cast<uint4*>(region) + ntt_tid<LOGN>()) {}
+  __device__ __forceinline__ void store_chunk(int c, const T* v) {
+    uint4 w;
+    if constexpr (sizeof(T) == 4) {
+      w = make_uint4((uint32_t)v[0], (uint32_t)v[1], (uint32_t)v[2], (uint32_t)v[3]);
+    } else {
+      w = make_uint4((uint32_t)v[0], (uint32_t)((uint64_t)v[0] >> 32), (uint32_t)v[1], (uint32_t)((uint64_t)v[1] >> 32));
+    }
+    base[c * Sh::THREADS] = w;
+  }
+  __device__ __forceinline__ void load_chunk(int c, T (&v)[VEC]) const {
+    const uint4 w = base[c * Sh::THREADS];
+    if constexpr (sizeof(T) == 4) {
+      v[0] = w.x; v[1] = w.y; v[2] = w.z; v[3] = w.w;
+    } else {
+      v[0] = (T)((uint64_t)w.x | ((uint64_t)w.y << 32));
+      v[1] = (T)((uint64_t)w.z | ((uint64_t)w.w << 32));
+    }
+  }
+  __device__ __forceinline__ void store(const T (&x)[Sh::E]) {
+#pragma unroll
+    for (int c = 0; c < CHUNKS; ++c) store_chunk(c, x + c * VEC);
   }
 };
 

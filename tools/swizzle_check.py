@@ -71,3 +71,38 @@ if __name__ == "__main__":
                 out.append(deg)
             size = phys(N - 1, w) + 1
             print(f"logn={logn:2d} word={word} T={T:4d} passes={passes} conflict={out} smem_words={size}")
+
+    # Vectorised exchange maps of ntt.cuh (32-bit words, N = 4096): map 1 between passes 0 and 1
+    # (pass 0 side 64-bit), map 2 between passes 1 and 2 (pass 2 side 128-bit).  Vector accesses
+    # are modelled per phase (16 lanes x 8 B, 8 lanes x 16 B) and must be contiguous and aligned.
+    MAPS = {1: [2, 4, 8, 16, 32, 64, 128, 256, 1, 512, 1024, 2048],
+            2: [1, 2, 4, 8, 16, 36, 72, 144, 304, 588, 1176, 2352]}
+    logn = 12
+    N, T, E, passes = cfg(logn)
+
+    def vec_degree(w, p, vec):
+        s, r = passes[p]
+        last = p == len(passes) - 1
+        phase = {1: 32, 2: 16, 4: 8}[vec]
+        worst = 1
+        for warp in range(T // 32):
+            for k0 in range(0, E, vec):
+                per_lane = []
+                for lane in range(32):
+                    ad = [phys(pass_idx(logn, N, T, E, s, r, last, warp * 32 + lane, k), w) for k in range(k0, k0 + vec)]
+                    assert ad == list(range(ad[0], ad[0] + vec)) and ad[0] % vec == 0, (p, lane, k0, ad)
+                    per_lane.append(ad)
+                for p0 in range(0, 32, phase):
+                    banks = {}
+                    for ad in per_lane[p0:p0 + phase]:
+                        for a in ad:
+                            banks.setdefault(a % 32, set()).add(a)
+                    worst = max(worst, max(len(v) for v in banks.values()))
+        return worst
+
+    for m, w in MAPS.items():
+        assert len({phys(i, w) for i in range(N)}) == N
+        sides = [(0, 2), (1, 1)] if m == 1 else [(1, 1), (2, 4)]
+        degs = [vec_degree(w, p, v) for p, v in sides]
+        assert degs == [1, 1], (m, degs)
+        print(f"vector map {m}: sides (pass, words) {sides} conflict={degs} smem_words={phys(N - 1, w) + 1}")
