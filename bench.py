@@ -35,7 +35,7 @@ UNIT = "CPMul/s"
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--batch", type=int, default=BATCH)
@@ -81,7 +81,7 @@ class ClockSampler:
                 self.reasons |= self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h) & ~0x1
             except Exception:
                 pass
-            time.sleep(0.02)
+            time.sleep(0.004)
 
     def __enter__(self):
         if self._nv:

@@ -480,27 +480,33 @@ struct Exchanger {
 template <typename T, int LOGN>
 struct Strip {
   using Sh = NttShape<LOGN>;
-  static constexpr int VEC = 16 / (int)sizeof(T);
+  static constexpr int VEC = Sh::E * (int)sizeof(T) >= 16 ? 16 / (int)sizeof(T) : 1;  // scalar for tiny N
   static constexpr int CHUNKS = Sh::E / VEC;
-  static_assert(Sh::E % VEC == 0, "strip chunks");
-  uint4* base;
-  __device__ __forceinline__ explicit Strip(T* region) : base(reinterpret_cast<uint4*>(region) + ntt_tid<LOGN>()) {}
+  T* base;
+  __device__ __forceinline__ explicit Strip(T* region) : base(region + VEC * ntt_tid<LOGN>()) {}
   __device__ __forceinline__ void store_chunk(int c, const T* v) {
-    uint4 w;
-    if constexpr (sizeof(T) == 4) {
-      w = make_uint4((uint32_t)v[0], (uint32_t)v[1], (uint32_t)v[2], (uint32_t)v[3]);
+    T* at = base + (size_t)c * VEC * Sh::THREADS;
+    if constexpr (VEC == 1) {
+      *at = v[0];
+    } else if constexpr (sizeof(T) == 4) {
+      *reinterpret_cast<uint4*>(at) = make_uint4((uint32_t)v[0], (uint32_t)v[1], (uint32_t)v[2], (uint32_t)v[3]);
     } else {
-      w = make_uint4((uint32_t)v[0], (uint32_t)((uint64_t)v[0] >> 32), (uint32_t)v[1], (uint32_t)((uint64_t)v[1] >> 32));
+      *reinterpret_cast<uint4*>(at) =
+          make_uint4((uint32_t)v[0], (uint32_t)((uint64_t)v[0] >> 32), (uint32_t)v[1], (uint32_t)((uint64_t)v[1] >> 32));
     }
-    base[c * Sh::THREADS] = w;
   }
   __device__ __forceinline__ void load_chunk(int c, T (&v)[VEC]) const {
-    const uint4 w = base[c * Sh::THREADS];
-    if constexpr (sizeof(T) == 4) {
-      v[0] = w.x; v[1] = w.y; v[2] = w.z; v[3] = w.w;
+    const T* at = base + (size_t)c * VEC * Sh::THREADS;
+    if constexpr (VEC == 1) {
+      v[0] = *at;
     } else {
-      v[0] = (T)((uint64_t)w.x | ((uint64_t)w.y << 32));
-      v[1] = (T)((uint64_t)w.z | ((uint64_t)w.w << 32));
+      const uint4 w = *reinterpret_cast<const uint4*>(at);
+      if constexpr (sizeof(T) == 4) {
+        v[0] = w.x; v[1] = w.y; v[2] = w.z; v[3] = w.w;
+      } else {
+        v[0] = (T)((uint64_t)w.x | ((uint64_t)w.y << 32));
+        v[1] = (T)((uint64_t)w.z | ((uint64_t)w.w << 32));
+      }
     }
   }
   __device__ __forceinline__ void store(const T (&x)[Sh::E]) {
