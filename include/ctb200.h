@@ -245,6 +245,13 @@ int ctb_probe_modmul(int word_bytes, uint64_t iters, void* sink, uint64_t* modmu
  * products.  Same launch shape and contract as ctb_probe_modmul; bench.py divides by it. */
 int ctb_probe_modmul_mix(int f64q_of_8, uint64_t iters, void* sink, uint64_t* modmuls, void* stream);
 
+/* Self-check (not a reference interface): for every prime of 32-bit base `base` and every entry of
+ * its FP64-quotient twiddle table, the butterfly product a*w mod p with the FP64-pipe quotient must
+ * lie in [0, 2p) and be congruent to a*w for boundary inputs and `samples` pseudo-random 32-bit a
+ * (seeded by `seed`).  Blocking; *bad receives the number of failures (0 expected).  A no-op for
+ * 64-bit bases. */
+int ctb_check_f64q(const ctb_ctx_t* ctx, int base, uint64_t samples, uint64_t seed, uint64_t* bad, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

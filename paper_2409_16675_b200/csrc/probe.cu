@@ -92,3 +92,79 @@ extern "C" int ctb_probe_modmul(int word_bytes, uint64_t iters, void* sink, uint
   if (modmuls) *modmuls = (uint64_t)grid * block * CHAINS * iters;
   return cuda_status(cudaGetLastError(), "ctb_probe_modmul");
 }
+
+// Device self-check of the FP64-quotient tables (ntt.cuh F64Q_NE) of one 32-bit base: for every
+// prime and every quotient-table entry, f64q_mul(a, w, w'/p) must lie in [0, 2p) and equal a*w
+// mod p, for the boundary inputs the butterflies can present (0, 1, p-1, p, 2p-1, 2p, 3p, 4p-1,
+// 2^32-1) and `samples` pseudo-random a in [0, 2^32).  One CTA per (prime, entry).
+namespace {
+__global__ void k_check_f64q(const uint32_t* tw, int words, const uint64_t* primes, int logn, uint64_t samples,
+                             uint64_t seed, unsigned long long* bad) {
+  const int l = blockIdx.y;
+  const uint32_t p = (uint32_t)primes[l];
+  const uint32_t* f = tw + (size_t)l * words;
+  const double* qt = reinterpret_cast<const double*>(f + 2 * shape_tw_entries(logn));
+  // entry blockIdx.x -> (pass k, e, slot)
+  int idx = blockIdx.x, k = 0;
+  for (; k < shape_npass(logn); ++k) {
+    const int n_k = F64Q_NE << shape_pass_s(logn, k);
+    if (idx < n_k) break;
+    idx -= n_k;
+  }
+  if (k == shape_npass(logn)) return;
+  const int s = shape_pass_s(logn, k), r = shape_pass_r(logn, k);
+  const int e = idx >> s, slot = idx & ((1 << s) - 1);
+  if (e >= (1 << r) - 1) return;  // no such stage/block in a short pass: entry unused
+  const uint32_t w = f[2 * (shape_tw_off(logn, k) + (e << s) + slot)];
+  const double wp = qt[shape_q_off(logn, k) + (e << s) + slot];
+  const double kq = f64q_k(wp);
+  const uint32_t pn = 0u - p;
+  unsigned long long nbad = 0;
+  const uint32_t edge[9] = {0u, 1u, p - 1, p, 2 * p - 1, 2 * p, 3 * p, 4 * p - 1, 0xFFFFFFFFu};
+  for (uint64_t i = threadIdx.x; i < samples + 9; i += blockDim.x) {
+    uint32_t a;
+    if (i < 9) {
+      a = edge[i];
+    } else {  // splitmix64
+      uint64_t z = seed + (uint64_t)l * 0x9E3779B97F4A7C15ull + (uint64_t)blockIdx.x * 0xBF58476D1CE4E5B9ull + i * 0x94D049BB133111EBull;
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      a = (uint32_t)(z ^ (z >> 31));
+    }
+    const uint32_t res = f64q_mul(a, w, wp, kq, p, pn);
+    if (res >= 2 * p || res % p != (uint32_t)((uint64_t)a * w % p)) ++nbad;
+  }
+  if (nbad) atomicAdd(bad, nbad);
+}
+}  // namespace
+
+extern "C" int ctb_check_f64q(const ctb_ctx_t* ctx, int base, uint64_t samples, uint64_t seed, uint64_t* bad,
+                              void* stream) {
+  if (!ctx || base < 0 || base >= BASE_COUNT || !bad) { set_error("ctb_check_f64q: bad arguments"); return ERR_ARG; }
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  const Base& b = c->base[base];
+  if (!b.size()) { set_error("ctb_check_f64q: empty base"); return ERR_ARG; }
+  *bad = 0;
+  if (b.word != 4 || F64Q_NE == 0) return OK;  // 64-bit limbs run the FP64 butterflies; nothing to check
+  cudaStream_t s = (cudaStream_t)stream;
+  const int logn = (int)c->logn;
+  unsigned long long* d_bad = nullptr;
+  uint64_t* d_primes = nullptr;
+  cudaError_t e = cudaMallocAsync(&d_bad, sizeof(unsigned long long), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&d_primes, 8 * b.primes.size(), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_primes, b.primes.data(), 8 * b.primes.size(), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) {
+    const dim3 grid((unsigned)shape_q_off(logn, shape_npass(logn)), (unsigned)b.size());
+    k_check_f64q<<<grid, 256, 0, s>>>((const uint32_t*)b.d_tw, tw_words<uint32_t>(logn), d_primes, logn, samples, seed,
+                                      d_bad);
+    e = cudaGetLastError();
+  }
+  unsigned long long h = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d_bad, sizeof(h), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (d_bad) cudaFreeAsync(d_bad, s);
+  if (d_primes) cudaFreeAsync(d_primes, s);
+  *bad = h;
+  return cuda_status(e, "ctb_check_f64q");
+}
