@@ -1,0 +1,69 @@
+"""Full-size BASELINE configs 3-5 end to end on the GPU (client encrypt -> offline CCMul masks ->
+online server step -> client decrypt/extract), decrypted outputs compared exactly with the plain
+convolution / matrix products they encode (float64 on the GPU: every sum here is an integer far
+below 2^53, so the rounded result is the exact integer the reference's protocol decrypts to,
+test_linprot.py:102-127 / test_acceptance.py:103-191).  Seeded synthetic inputs with the configs'
+shapes and value ranges."""
+import pytest
+import torch
+
+from conftest import has_gpu
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
+
+
+@pytest.fixture(scope="module")
+def sess4096():
+    from paper_2409_16675_b200 import workloads as W
+    from paper_2409_16675_b200.params import default_he_params
+    P = default_he_params(4096)
+    return P, W.Session.create(P)
+
+
+def test_cfg3_stride2_conv_batch64(sess4096):
+    from paper_2409_16675_b200 import linprot, packing, workloads as W
+    P, sess = sess4096
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)
+    x = torch.randint(0, 256, (64, 1, 28, 28), generator=g, device="cuda", dtype=torch.int64)
+    w = torch.randint(-128, 128, (5, 1, 5, 5), generator=g, device="cuda", dtype=torch.int64)
+    jobs = {"fwd": [linprot.conv_job(f"c3_{b}", x[b], w, packing.ConvShape(28, 28, 5, 0), P.plain_ring)
+                    for b in range(64)]}
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(11)
+    r = W.run_config(sess, jobs, gen)
+    out = W.signed(r["outputs"]["fwd"], P.t)[:, :, ::2, ::2]          # stride-2 lowering
+    assert out.shape == (64, 5, 12, 12)
+    assert torch.equal(out, W.conv_reference_float(x, w, 0)[:, :, ::2, ::2])
+    assert r["sites"] == 320 and r["ccmul"] == 320
+
+
+def test_cfg4_conv_fwd_bwd_batch32(sess4096):
+    from paper_2409_16675_b200 import workloads as W
+    P, sess = sess4096
+    (x, w, gy), jobs = W.cfg4_jobs(P, 32)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(12)
+    r = W.run_config(sess, jobs, gen)
+    assert r["sites"] == 18432 and r["ccmul"] == 18432
+    assert torch.equal(W.signed(r["outputs"]["fwd"], P.t), W.conv_reference_float(x, w, 1))
+    ref_gw = torch.stack([W.conv_reference_float(x[b][:, None], gy[b][:, None], 1).transpose(0, 1) for b in range(32)])
+    assert torch.equal(W.signed(r["outputs"]["gw"], P.t), ref_gw)
+    wrot = torch.flip(w, dims=(2, 3)).transpose(0, 1).contiguous()
+    assert torch.equal(W.signed(r["outputs"]["gx"], P.t), W.conv_reference_float(gy, wrot, 1))
+
+
+def test_cfg5_training_step_linear_n8192_batch32():
+    from paper_2409_16675_b200 import workloads as W
+    from paper_2409_16675_b200.params import p8192_he_params
+    P8 = p8192_he_params()
+    sess = W.Session.create(P8)
+    T = W.cfg5_tensors(32)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(13)
+    r = W.run_cfg5(sess, T, gen, group=4)
+    ref = W.cfg5_reference_float(T)
+    assert set(r["outputs"]) == set(ref)
+    for fam, v in r["outputs"].items():
+        assert torch.equal(W.signed(v, P8.t), ref[fam]), fam
+    assert sum(r["sites"][k] for k in W.WEIGHT_GRADIENT_FAMILIES) == 137856
