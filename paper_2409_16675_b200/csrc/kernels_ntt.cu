@@ -435,14 +435,20 @@ cudaError_t stream_inv_add(const Ctx* c, int base, const void* in, void* out, co
 // draws [B][3][N] int64 = (u, e1, e2) small signed integers sampled by the
 // caller (the reference's numpy stream, or the device generator).  One forward
 // and two inverse transforms per limb; persistent and limb-stationary like
-// k_cpmul, twiddles in shared memory.
+// k_cpmul, twiddles in shared memory.  At N = 4096 (32-bit limbs) one 1024-thread CTA per SM
+// runs four transform groups on one limb: one shared twiddle table instead of two per SM, and the
+// limb's prepared public key (2 x 16 KB, read by every item) stays resident in the ~78 KB of L1
+// that the smaller shared-memory footprint leaves (two CTAs on different limbs would evict it).
+template <typename T, int LOGN>
+__host__ __device__ constexpr int enc_groups() { return sizeof(T) == 4 && LOGN == 12 ? 4 : cpmul_groups<T, LOGN>(); }
+
 template <typename T, int LOGN, bool SMEM_TW>
-__global__ void __launch_bounds__(NttShape<LOGN>::THREADS * cpmul_groups<T, LOGN>(),
-                                  cpmul_groups<T, LOGN>() == 2 ? 2 : NttShape<LOGN>::MINB)
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS * enc_groups<T, LOGN>(),
+                                  enc_groups<T, LOGN>() == 4 ? 1 : (enc_groups<T, LOGN>() == 2 ? 2 : NttShape<LOGN>::MINB))
 k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, const T* __restrict__ pkprep, T* out,
           const PrimeTab<T>* __restrict__ tabs, int L, uint64_t t_half, uint32_t batch) {
   using Sh = NttShape<LOGN>;
-  constexpr int GROUPS = cpmul_groups<T, LOGN>();
+  constexpr int GROUPS = enc_groups<T, LOGN>();
   using Ex = Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>;
   constexpr int TW_WORDS = SMEM_TW ? tw_words<T>(LOGN) : 0;
   constexpr int GROUP_WORDS = Ex::WORDS + Sh::N;
@@ -799,7 +805,7 @@ template <typename T, int LOGN>
 static cudaError_t launch_encrypt(const Ctx* c, const Base* b, const uint64_t* m, const int8_t* draws,
                                   const void* pkprep, void* out, uint64_t batch, cudaStream_t s) {
   using Sh = NttShape<LOGN>;
-  constexpr int GROUPS = cpmul_groups<T, LOGN>();
+  constexpr int GROUPS = enc_groups<T, LOGN>();
   constexpr size_t tw_bytes = (size_t)tw_words<T>(LOGN) * sizeof(T);
   constexpr size_t group_bytes = ((size_t)Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>::WORDS + Sh::N) * sizeof(T);
   constexpr bool SMEM_TW = LOGN >= 9 && tw_bytes + GROUPS * group_bytes <= (sizeof(T) == 4 ? 200 : 226) * 1024;
