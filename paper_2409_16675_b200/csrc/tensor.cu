@@ -85,6 +85,7 @@ struct TensorConsts {
   float a_rcp[MAXA];
   ShoupC<TQ> a_hat_q[MAXQ][MAXA];     // (M_A/p_k) mod q_l
   TQ a_v_q[MAXQ][MAXA + 1];           // v * M_A mod q_l
+  double q_d[MAXQ], q_dinv[MAXQ];     // q_i and 1/q_i (correctly rounded) as doubles (FP64 paths, 50-bit q)
   int lazy_digits;                    // u32 limbs and D <= MAXDIG: digits by limb dot products
   uint32_t dM[MAXQ][MAXDIG];          // dM[i][j] = j-th w-bit limb of M_i
 };
@@ -222,12 +223,13 @@ __device__ __forceinline__ void crt_extend(const TensorConsts<TQ>& c, int n_rt, 
     } else {
       // 50-bit q_l: FP64 products (ntt.cuh f64_mulmod; constants as (c, c/q) doubles), each in
       // (-q, q), the running sum re-centred every 4 terms
-      const F64Prime P{(double)q, __drcp_rn((double)q)};
+      // (q, 1/q precomputed on the host; xi converted by exponent splicing, not I2F)
+      const F64Prime P{c.q_d[l], c.q_dinv[l]};
       double acc = 0.0;
 #pragma unroll
       for (int k = 0; k < (NC ? NC : MAXA); ++k) {
         if (!NC && k >= n) break;
-        acc = __dadd_rn(acc, f64_mulmod((double)xi[k], __longlong_as_double((long long)hat_q[l][k].w),
+        acc = __dadd_rn(acc, f64_mulmod(f64_from_u64(xi[k]), __longlong_as_double((long long)hat_q[l][k].w),
                                         __longlong_as_double((long long)hat_q[l][k].wq), P.p));
         if ((k & 3) == 3) acc = f64_center(acc, P);
       }
@@ -376,7 +378,10 @@ static cudaError_t launch_tensor_product(const Ctx* c, const uint32_t* a, const 
 // ----------------------------------------------------------------------------- 3 round
 // H: [B][3][K][N] -> out [B][3][L][N] (TQ): round(h t / Q) mod Q.
 template <typename TQ, int LC, int KC, int K2C>
-__global__ void __launch_bounds__(256, 3) k_tensor_round(const uint32_t* H, TQ* out,
+#ifndef CTB_ROUND64_MINB
+#define CTB_ROUND64_MINB 4
+#endif
+__global__ void __launch_bounds__(256, sizeof(TQ) == 8 ? CTB_ROUND64_MINB : 3) k_tensor_round(const uint32_t* H, TQ* out,
                                                       const __grid_constant__ TensorConsts<TQ> c, uint32_t n,
                                                       uint64_t total) {
   const int L = LC ? LC : c.L, K = KC ? KC : c.K, K2 = K2C ? K2C : c.K2;
@@ -421,7 +426,9 @@ __global__ void __launch_bounds__(256, 3) k_tensor_round(const uint32_t* H, TQ* 
 #pragma unroll
     for (int k = 0; k < (K2C ? K2C : MAXA); ++k) {
       if (!K2C && k >= K2) break;
-      const int ai = (KC && LC && sizeof(TQ) == 4) ? LC + k : c.p2_idx[k];
+      // P2 primes are the leading non-Q auxiliary primes (build_tensor; the launcher checks it
+      // before picking the compile-time form), so the index stays static and h[] in registers
+      const int ai = (KC && LC) ? (sizeof(TQ) == 4 ? LC + k : k) : c.p2_idx[k];
       const uint32_t p = c.ap[ai];
       p2p[k] = p;
       const uint32_t zk = add_mod(csub(shoup_mul<uint32_t>(h[ai], c.t_aux[ai].w, c.t_aux[ai].wq, p), p), c.hQ_aux[ai], p);
@@ -909,6 +916,8 @@ static int build_tensor(Ctx* c, std::string& err) {
     h->hQ_aux[k] = (uint32_t)hQ.mod_small(p);
   }
   for (int l = 0; l < L; ++l) {
+    h->q_d[l] = (double)q[l];
+    h->q_dinv[l] = 1.0 / (double)q[l];  // IEEE division: the same value __drcp_rn gives on the device
     h->t_q[l] = spair<TQ>(c->t % q[l], q[l]);
     h->hQ_q[l] = (TQ)hQ.mod_small(q[l]);
   }
@@ -1075,7 +1084,9 @@ extern "C" int ctb_tensor_round(const ctb_ctx_t* ctx, const uint32_t* h_aux, voi
     else k_tensor_round<uint32_t, 0, 0, 0><<<grid, 256, 0, s>>>(h_aux, (uint32_t*)out, tc, c->n, total);
   } else {
     const auto& tc = *reinterpret_cast<const TensorConsts<uint64_t>*>(c->tensor->host.data());
-    if (L == 3 && K == 11 && K2 == 7)
+    bool p2_lead = true;  // P2 = aux primes 0..K2-1 (64-bit limbs: no cipher prime is an aux prime)
+    for (int k = 0; k < K2; ++k) p2_lead = p2_lead && tc.p2_idx[k] == k;
+    if (L == 3 && K == 11 && K2 == 7 && p2_lead)
       k_tensor_round<uint64_t, 3, 11, 7><<<grid, 256, 0, s>>>(h_aux, (uint64_t*)out, tc, c->n, total);
     else k_tensor_round<uint64_t, 0, 0, 0><<<grid, 256, 0, s>>>(h_aux, (uint64_t*)out, tc, c->n, total);
   }
