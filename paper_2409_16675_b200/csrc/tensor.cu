@@ -270,7 +270,9 @@ __global__ void __launch_bounds__(256, 3) k_tensor_lift(const TQ* in, uint32_t* 
       if (!KC && k >= K) break;
       uint32_t v;
       const int qi = c.aux_is_q[k];
-      if (qi >= 0) {
+      // 64-bit limbs: no cipher prime is an aux prime (build_tensor), so r[] is never indexed by a
+      // runtime value there (it would live in local memory)
+      if (sizeof(TQ) == 4 && qi >= 0) {
         v = (uint32_t)r[KC && LC && sizeof(TQ) == 4 && k < LC ? k : qi];  // x == centred value (mod q_i)
       } else {
         if constexpr (sizeof(TQ) == 4) v = digits_to_aux<TQ, LC>(c, L, k, a);
@@ -479,6 +481,42 @@ __device__ __forceinline__ void value_digits(const TensorConsts<TQ>& c, const TQ
       }
       return;
     }
+  }
+  if constexpr (sizeof(TQ) == 8 && LC > 0 && DC > 0 && WC > 0) {
+    // 64-bit limbs with compile-time shape: mixed-radix digits, then X = sum a_k prod_{i<k} q_i in
+    // 2 LC + 1 32-bit words with fully unrolled loops (registers, no local memory)
+    TQ a[LC];
+    mrc_digits<TQ, LC>(c.mrcQ, r, a);
+    constexpr int NW = 2 * LC + 1;
+    uint32_t X[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) X[w] = 0;
+    X[0] = (uint32_t)a[LC - 1];
+    X[1] = (uint32_t)((uint64_t)a[LC - 1] >> 32);
+#pragma unroll
+    for (int k = LC - 2; k >= 0; --k) {
+      const uint64_t qk = (uint64_t)c.mrcQ.q[k];
+      const uint32_t q0 = (uint32_t)qk, q1 = (uint32_t)(qk >> 32);
+      // X = X * qk + a_k, word by word with a 64-bit carry (q_k < 2^50: two 32-bit halves)
+      uint64_t carry = (uint64_t)a[k];
+      uint32_t prev = 0;  // X[w-1], the word multiplied by the high half q1
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const uint32_t xw = X[w];
+        const unsigned __int128 t = (unsigned __int128)xw * q0 + (unsigned __int128)prev * q1 + carry;
+        X[w] = (uint32_t)t;
+        carry = (uint64_t)(t >> 32);
+        prev = xw;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < DC; ++j) {
+      const int bit = j * WC, wi = bit >> 5, sh = bit & 31;
+      uint64_t v = (uint64_t)X[wi] >> sh;
+      if (sh + WC > 32 && wi + 1 < NW) v |= (uint64_t)X[wi + 1] << (32 - sh);
+      if (ACC) dig[j] += (uint32_t)v & mask; else dig[j] = (uint32_t)v & mask;
+    }
+    return;
   }
   TQ a[MAXQ];
   mrc_digits<TQ>(c.mrcQ, r, a);
