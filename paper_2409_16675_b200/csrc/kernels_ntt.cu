@@ -458,6 +458,14 @@ cudaError_t stream_inv_add(const Ctx* c, int base, const void* in, void* out, co
 // that the smaller shared-memory footprint leaves (two CTAs on different limbs would evict it).
 template <typename T, int LOGN>
 __host__ __device__ constexpr int enc_groups() { return sizeof(T) == 4 && LOGN == 12 ? 4 : cpmul_groups<T, LOGN>(); }
+// The limb's prepared public key (b^, a^: 2 x N words) staged once per CTA in shared memory, in the
+// chunk-major Strip layout (conflict-free 128-bit reads), instead of re-reading it from L1/L2 for every
+// item: at N = 4096 (four groups) twiddles + images + strips + key = 200 KB.
+#ifndef CTB_ENC_PKSM
+#define CTB_ENC_PKSM 1
+#endif
+template <typename T, int LOGN>
+__host__ __device__ constexpr bool enc_pk_smem() { return CTB_ENC_PKSM && sizeof(T) == 4 && LOGN == 12; }
 
 template <typename T, int LOGN, bool SMEM_TW>
 __global__ void __launch_bounds__(NttShape<LOGN>::THREADS * enc_groups<T, LOGN>(),
@@ -469,12 +477,16 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
   using Ex = Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>;
   constexpr int TW_WORDS = SMEM_TW ? tw_words<T>(LOGN) : 0;
   constexpr int GROUP_WORDS = Ex::WORDS + Sh::N;
+  constexpr bool PKSM = enc_pk_smem<T, LOGN>() && SMEM_TW;
+  using EV = EvalVec<T, LOGN>;
+  static_assert(!PKSM || (EV::VEC == Strip<T, LOGN>::VEC && GROUPS >= 2), "key strips need contiguous eval chunks");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
   const int group = (int)(threadIdx.x / Sh::THREADS);
   T* gsm = tw_sm + TW_WORDS + group * GROUP_WORDS;
   Ex ex{gsm};
   Strip<T, LOGN> usm(gsm + Ex::WORDS);  // NTT(u), this thread's evaluation slots
+  T* pk_sm = tw_sm + TW_WORDS + GROUPS * GROUP_WORDS;  // PKSM: [part][N] key strips
 
   const int limb = blockIdx.x % L;
   const uint32_t slot = blockIdx.x / L;
@@ -482,6 +494,18 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
   PrimeRegs<T> pr(tabs + limb);
   const T tmod = tabs[limb].tmod, delta = tabs[limb].delta, delta_q = tabs[limb].delta_q;
   const T* twp = pr.fwd;
+  if constexpr (PKSM) {
+    if (group < 2) {  // group g stages part g of this limb's key
+      const T* kp = pkprep + ((size_t)group * L + limb) * Sh::N;
+      Strip<T, LOGN> ks(pk_sm + (size_t)group * Sh::N);
+#pragma unroll
+      for (int i = 0; i < EV::CHUNKS; ++i) {
+        T v[EV::VEC];
+        EV::load(kp, i, v);
+        ks.store_chunk(i, v);
+      }
+    }
+  }
   if constexpr (SMEM_TW) {
     stage_twiddles(pr.fwd, tw_sm, TW_WORDS, Sh::THREADS * GROUPS);
     __syncthreads();
@@ -525,12 +549,13 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
 #pragma unroll 1
     for (int part = 0; part < 2; ++part) {
       const T* kp = pkprep + ((size_t)part * L + limb) * Sh::N;
-      using EV = EvalVec<T, LOGN>;
       static_assert(EV::VEC == Strip<T, LOGN>::VEC || EV::VEC == 1, "strip / eval chunking");
+      const Strip<T, LOGN> ks(pk_sm + (size_t)part * Sh::N);
 #pragma unroll
       for (int i = 0; i < EV::CHUNKS; ++i) {
         T v[EV::VEC];
-        EV::load(kp, i, v);
+        if constexpr (PKSM) ks.load_chunk(i, v);
+        else EV::load(kp, i, v);
         if constexpr (EV::VEC == Strip<T, LOGN>::VEC) {
           T uu[EV::VEC];
           usm.load_chunk(i, uu);
@@ -826,8 +851,10 @@ static cudaError_t launch_encrypt(const Ctx* c, const Base* b, const uint64_t* m
   constexpr size_t tw_bytes = (size_t)tw_words<T>(LOGN) * sizeof(T);
   constexpr size_t group_bytes = ((size_t)Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>::WORDS + Sh::N) * sizeof(T);
   constexpr bool SMEM_TW = LOGN >= 9 && tw_bytes + GROUPS * group_bytes <= (sizeof(T) == 4 ? 200 : 226) * 1024;
+  constexpr size_t pk_bytes = enc_pk_smem<T, LOGN>() && SMEM_TW ? 2 * (size_t)Sh::N * sizeof(T) : 0;
+  static_assert((SMEM_TW ? tw_bytes : 0) + GROUPS * group_bytes + pk_bytes <= 227 * 1024, "k_encrypt shared memory");
   auto kern = k_encrypt<T, LOGN, SMEM_TW>;
-  const size_t smem = GROUPS * group_bytes + (SMEM_TW ? tw_bytes : 0);
+  const size_t smem = GROUPS * group_bytes + (SMEM_TW ? tw_bytes : 0) + pk_bytes;
   const int L = b->size();
   if (batch == 0) return cudaSuccess;
   const int threads = Sh::THREADS * GROUPS;
