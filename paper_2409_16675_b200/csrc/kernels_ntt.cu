@@ -206,8 +206,17 @@ struct StreamCfg {
   // transform groups per CTA: at N = 4096 four (one 1024-thread CTA per SM, one twiddle table
   // per SM, ~78 KB of L1 left for the epilogue operands; measured 4-6% faster than two 512-thread
   // CTAs on different limbs)
-  static constexpr int GROUPS = (CTB_STREAM_GROUPS4 && sizeof(T) == 4 && LOGN == 12) ? 4 : cpmul_groups<T, LOGN>();
-  static constexpr int CTAS_PER_SM = GROUPS == 4 ? 1 : 2;
+  // at N = 8192 (32-bit limbs: the auxiliary base of the 50-bit tensoring) two per 1024-thread CTA:
+  // one twiddle table per SM and room for the TMA staging buffers (one 512-thread CTA per SM
+  // otherwise) -- measured 24.8 -> 22.0 ms forward transforms per 4 cfg5 images (-11%)
+#ifndef CTB_STREAM_G2_13
+#define CTB_STREAM_G2_13 1
+#endif
+  static constexpr bool WIDE = (CTB_STREAM_GROUPS4 && sizeof(T) == 4 && LOGN == 12) ||
+                               (CTB_STREAM_G2_13 && sizeof(T) == 4 && LOGN == 13);
+  static constexpr int GROUPS = (CTB_STREAM_GROUPS4 && sizeof(T) == 4 && LOGN == 12) ? 4
+                                : (CTB_STREAM_G2_13 && sizeof(T) == 4 && LOGN == 13) ? 2 : cpmul_groups<T, LOGN>();
+  static constexpr int CTAS_PER_SM = WIDE ? 1 : 2;
   using Ex = Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>;
   static constexpr size_t TW_BYTES = (size_t)tw_words<T>(LOGN) * sizeof(T);
   // u32: table + images within 200 KB (two CTAs per SM with staging); 64-bit limbs: the
@@ -221,7 +230,7 @@ struct StreamCfg {
   static constexpr int GW = EXW + (PF_OK ? Sh::N : 0);  // words per group
   static constexpr size_t SMEM = (SMEM_TW ? TW_BYTES : 0) + GROUPS * (size_t)GW * sizeof(T) + (PF_OK ? 64 : 0);
   static constexpr int THREADS = Sh::THREADS * GROUPS;
-  static constexpr int MINB = GROUPS == 4 ? 1 : (GROUPS == 2 ? 2 : Sh::MINB);
+  static constexpr int MINB = WIDE ? 1 : (GROUPS == 2 ? 2 : Sh::MINB);
 };
 
 template <typename T, int LOGN, bool SMEM_TW, StreamOp OP>

@@ -691,29 +691,50 @@ static cudaError_t launch_relin_accum(const Ctx* c, const void* ct3, int ct_part
 //    (k_slot_digits) and relinearised once per SLOT (k_relin_accum).
 
 // AX [*][2][K][N] prepared eval, AW [*][2][K][N] canonical eval (aux base) -> H [nsite][3][K][N].
+// -DCTB_SITE_G2=1: at N = 8192 two sites per 1024-thread CTA (one transform group each, named
+// barriers) sharing the prime's twiddle table, 32 instead of 16 resident warps per SM -- measured
+// 27% SLOWER (57.4 -> 72.7 ms per 4 cfg5 images): the 64-register cap of a 1024-thread CTA spills
+// 128 B per thread, and the spills miss the ~20 KB of L1 the shared memory leaves.
+#ifndef CTB_SITE_G2
+#define CTB_SITE_G2 0
+#endif
+template <int LOGN>
+__host__ __device__ constexpr int site_groups() { return CTB_SITE_G2 && LOGN == 13 ? 2 : 1; }
+template <int LOGN>
+__host__ __device__ constexpr int site_strips() { return LOGN <= 12 ? 2 : 1; }
+// 32-bit words per site group (exchange image + strips), rounded to 16 bytes
+template <int LOGN, int GROUPS>
+__host__ __device__ constexpr int site_group_words() {
+  return (Exchanger<uint32_t, LOGN, 1, GROUPS>::WORDS + site_strips<LOGN>() * (1 << LOGN) + 3) / 4 * 4;
+}
+
 template <int LOGN, bool SMEM_TW>
-__global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS * site_groups<LOGN>(), site_groups<LOGN>() == 2 ? 1 : NttShape<LOGN>::MINB)
 k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict__ sx,
                const int32_t* __restrict__ sw, uint32_t* H, const PrimeTab<uint32_t>* __restrict__ tabs, int K,
                uint32_t nsite) {
   using Sh = NttShape<LOGN>;
   using T = uint32_t;
+  constexpr int GROUPS = site_groups<LOGN>();
   constexpr int TW_WORDS = SMEM_TW ? tw_words<T>(LOGN) : 0;
-  using Ex = Exchanger<T, LOGN, 1, 1>;
+  using Ex = Exchanger<T, LOGN, 1, GROUPS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
-  Ex ex{tw_sm + TW_WORDS};
+  const int group = (int)(threadIdx.x / Sh::THREADS);
+  T* gsm = tw_sm + TW_WORDS + group * site_group_words<LOGN, GROUPS>();
+  Ex ex{gsm};
   // thread-private strips: h1 (and h0 when two strips: N <= 4096; at N = 8192 h0 is
   // recomputed from re-read operands, which measured faster than a second strip)
-  constexpr bool TWO = LOGN <= 12;
-  T* strip = tw_sm + TW_WORDS + Ex::WORDS + threadIdx.x;
+  constexpr bool TWO = site_strips<LOGN>() == 2;
+  T* strip = gsm + Ex::WORDS + ntt_tid<LOGN>();
   const int k = blockIdx.x % K;
   const uint32_t slot = blockIdx.x / K;
   const uint32_t nslots = (gridDim.x - k + K - 1) / K;
+  const uint32_t step = nslots * GROUPS;
   PrimeRegs<T> pr(tabs + k);
   const T* twp = pr.fwd;
   if constexpr (SMEM_TW) {
-    stage_twiddles(pr.fwd, tw_sm, TW_WORDS, Sh::THREADS);
+    stage_twiddles(pr.fwd, tw_sm, TW_WORDS, Sh::THREADS * GROUPS);
     __syncthreads();
     twp = tw_sm;
   }
@@ -727,12 +748,12 @@ k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict
     for (int j = 0; j < Sh::E; ++j) dst[coef_off<LOGN>(j)] = csub(y[j], pr.p);
   };
 #pragma unroll 1
-  for (uint32_t s = slot; s < nsite; s += nslots) {
+  for (uint32_t s = slot * GROUPS + group; s < nsite; s += step) {
     const T* a0p = AX + (size_t)sx[s] * 2 * KN + k * N;
     const T* b0p = AW + (size_t)sw[s] * 2 * KN + k * N;
-    if (threadIdx.x == 0 && s + nslots < nsite) {  // next item's operands towards L2
-      const T* na = AX + (size_t)sx[s + nslots] * 2 * KN + k * N;
-      const T* nb = AW + (size_t)sw[s + nslots] * 2 * KN + k * N;
+    if (ntt_tid<LOGN>() == 0 && s + step < nsite) {  // next item's operands towards L2
+      const T* na = AX + (size_t)sx[s + step] * 2 * KN + k * N;
+      const T* nb = AW + (size_t)sw[s + step] * 2 * KN + k * N;
       bulk_prefetch_l2(na, (uint32_t)(N * 4));
       bulk_prefetch_l2(na + KN, (uint32_t)(N * 4));
       bulk_prefetch_l2(nb, (uint32_t)(N * 4));
@@ -755,11 +776,11 @@ k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict
         if constexpr (TWO) strip[(Sh::E + j) * Sh::THREADS] = mont_mul(a0[c], b0[c], pr.p, pr.pinv);
       }
     }
-    ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1, TENSOR_QE>(y, ex, tw, pr.p, pr.p2);
+    ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, GROUPS, TENSOR_QE>(y, ex, tw, pr.p, pr.p2);
     store(s, 2);
 #pragma unroll
     for (int j = 0; j < Sh::E; ++j) y[j] = strip[j * Sh::THREADS];
-    ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1, TENSOR_QE>(y, ex, tw, pr.p, pr.p2);
+    ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, GROUPS, TENSOR_QE>(y, ex, tw, pr.p, pr.p2);
     store(s, 1);
     if constexpr (TWO) {
 #pragma unroll
@@ -775,7 +796,7 @@ k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict
         for (int c = 0; c < EV::VEC; ++c) y[i * EV::VEC + c] = mont_mul(a0[c], b0[c], pr.p, pr.pinv);
       }
     }
-    ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1, TENSOR_QE>(y, ex, tw, pr.p, pr.p2);
+    ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, GROUPS, TENSOR_QE>(y, ex, tw, pr.p, pr.p2);
     store(s, 0);
   }
 }
@@ -787,15 +808,19 @@ static cudaError_t launch_site_product(const Ctx* c, const uint32_t* ax, const u
   const Base& B = c->base[BASE_B];
   using T = uint32_t;
   constexpr size_t tw_bytes = (size_t)tw_words<T>(LOGN) * sizeof(T);
-  constexpr size_t base_bytes = ((size_t)Exchanger<T, LOGN, 1, 1>::WORDS + (LOGN <= 12 ? 2 : 1) * (size_t)Sh::N) * sizeof(T);
-  constexpr bool SMEM_TW = LOGN >= 9 && tw_bytes + base_bytes <= 200 * 1024;
+  constexpr int GROUPS = site_groups<LOGN>();
+  constexpr size_t base_bytes = (size_t)site_group_words<LOGN, GROUPS>() * sizeof(T);
+  constexpr bool SMEM_TW = LOGN >= 9 && tw_bytes + GROUPS * base_bytes <= (GROUPS == 2 ? 224 : 200) * 1024;
+  static_assert(GROUPS == 1 || SMEM_TW, "two site groups need the shared twiddle table");
   auto kern = k_site_product<LOGN, SMEM_TW>;
-  const size_t smem = base_bytes + (SMEM_TW ? tw_bytes : 0);
+  const size_t smem = GROUPS * base_bytes + (SMEM_TW ? tw_bytes : 0);
   const int K = B.size();
   if (nsite == 0) return cudaSuccess;
-  uint32_t grid = persistent_grid((const void*)kern, Sh::THREADS, smem);
-  grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(grid / K * K, (uint64_t)K), nsite * (uint64_t)K);
-  return launch_kernel_grid(kern, grid, Sh::THREADS, smem, s, ax, aw, sx, sw, h, (const PrimeTab<T>*)B.d_tabs, K,
+  const int threads = Sh::THREADS * GROUPS;
+  uint32_t grid = persistent_grid((const void*)kern, threads, smem);
+  grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(grid / K * K, (uint64_t)K),
+                                      (nsite + GROUPS - 1) / GROUPS * (uint64_t)K);
+  return launch_kernel_grid(kern, grid, threads, smem, s, ax, aw, sx, sw, h, (const PrimeTab<T>*)B.d_tabs, K,
                             (uint32_t)nsite);
 }
 
