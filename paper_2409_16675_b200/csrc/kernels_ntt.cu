@@ -88,22 +88,35 @@ __host__ __device__ constexpr int cpmul_groups() { return sizeof(T) == 4 && (LOG
 // k_cpmul at N = 4096: one 1024-thread CTA per SM running four transform groups on one limb (one
 // twiddle table per SM instead of two, 64 registers, 32 warps) -- measured 6% faster than two
 // 512-thread CTAs per SM (1.263 vs 1.344 ms per 4096 CPMul).
-#ifndef CTB_CPMUL_GROUPS4
-#define CTB_CPMUL_GROUPS4 1
+// CTB_CPMUL_GROUPS / CTB_CPMUL_NBUF (N = 4096, 32-bit limbs): transform groups per CTA and
+// exchange buffers per group (2 = double-buffered, one barrier per exchange instead of two).
+#ifndef CTB_CPMUL_GROUPS
+#define CTB_CPMUL_GROUPS 4
+#endif
+#ifndef CTB_CPMUL_NBUF
+#define CTB_CPMUL_NBUF 1
 #endif
 template <typename T, int LOGN>
 __host__ __device__ constexpr int cpmul_kernel_groups() {
-  return (CTB_CPMUL_GROUPS4 && sizeof(T) == 4 && LOGN == 12) ? 4 : cpmul_groups<T, LOGN>();
+  return (sizeof(T) == 4 && LOGN == 12) ? CTB_CPMUL_GROUPS : cpmul_groups<T, LOGN>();
+}
+template <typename T, int LOGN>
+__host__ __device__ constexpr int cpmul_kernel_nbuf() {
+  return (sizeof(T) == 4 && LOGN == 12) ? CTB_CPMUL_NBUF : CPMUL_NBUF;
+}
+template <typename T, int LOGN>
+__host__ __device__ constexpr int cpmul_kernel_minb() {
+  return cpmul_kernel_groups<T, LOGN>() >= 3 ? 1 : (cpmul_kernel_groups<T, LOGN>() == 2 ? 2 : NttShape<LOGN>::MINB);
 }
 
 template <typename T, int LOGN, bool SMEM_TW>
-__global__ void __launch_bounds__(NttShape<LOGN>::THREADS * cpmul_kernel_groups<T, LOGN>(),
-                                  cpmul_kernel_groups<T, LOGN>() == 4 ? 1 : (cpmul_kernel_groups<T, LOGN>() == 2 ? 2 : NttShape<LOGN>::MINB))
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS * cpmul_kernel_groups<T, LOGN>(), cpmul_kernel_minb<T, LOGN>())
 k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>* __restrict__ tabs,
         int L, uint64_t t_half, uint32_t batch, bool plain_fast) {
   using Sh = NttShape<LOGN>;
   constexpr int GROUPS = cpmul_kernel_groups<T, LOGN>();
-  using Ex = Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>;
+  constexpr int NB = cpmul_kernel_nbuf<T, LOGN>();
+  using Ex = Exchanger<T, LOGN, NB, GROUPS>;
   constexpr int TW_WORDS = SMEM_TW ? tw_words<T>(LOGN) : 0;
   constexpr int GROUP_WORDS = Ex::WORDS + Sh::N;  // exchange image + NTT(pt) strip
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -138,7 +151,7 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
         if (v > t_half) r = sub_mod(r, tmod, pr.p);         // centred lift: v - t
         x[k] = r;
       }
-      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, NB, GROUPS>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) x[k] = shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p);
       ysm.store(x);
@@ -148,7 +161,7 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
       const size_t off = (((size_t)b * 2 + part) * L + limb) * (size_t)Sh::N + coef_base<LOGN>();
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) x[k] = ct[off + coef_off<LOGN>(k)];
-      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, NB, GROUPS>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
       for (int c = 0; c < Strip<T, LOGN>::CHUNKS; ++c) {
         T y[Strip<T, LOGN>::VEC];
@@ -159,7 +172,7 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
           x[k] = mont_mul(x[k], y[j], pr.p, pr.pinv);
         }
       }
-      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, NB, GROUPS>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) out[off + coef_off<LOGN>(k)] = csub(x[k], pr.p);
     }
@@ -820,7 +833,7 @@ static cudaError_t launch_cpmul(const Ctx* c, const Base* b, const void* ct, con
   // twiddles in shared memory when the table fits beside the exchange image
   constexpr int GROUPS = cpmul_kernel_groups<T, LOGN>();
   constexpr size_t tw_bytes = (size_t)tw_words<T>(LOGN) * sizeof(T);
-  constexpr size_t group_bytes = ((size_t)Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>::WORDS + Sh::N) * sizeof(T);
+  constexpr size_t group_bytes = ((size_t)Exchanger<T, LOGN, cpmul_kernel_nbuf<T, LOGN>(), GROUPS>::WORDS + Sh::N) * sizeof(T);
   constexpr bool SMEM_TW = LOGN >= 9 && tw_bytes + GROUPS * group_bytes <= (sizeof(T) == 4 ? 200 : 226) * 1024;
   auto kern = k_cpmul<T, LOGN, SMEM_TW>;
   const size_t smem = GROUPS * group_bytes + (SMEM_TW ? tw_bytes : 0);
