@@ -487,7 +487,12 @@ __host__ __device__ constexpr int enc_groups() { return sizeof(T) == 4 && LOGN =
 #define CTB_ENC_PKSM 1
 #endif
 template <typename T, int LOGN>
-__host__ __device__ constexpr bool enc_pk_smem() { return CTB_ENC_PKSM && sizeof(T) == 4 && LOGN == 12; }
+__host__ __device__ constexpr bool enc_pk_smem() {
+  return CTB_ENC_PKSM && sizeof(T) == 4 && LOGN == 12 &&
+         (size_t)tw_words<T>(LOGN) * sizeof(T) +
+                 enc_groups<T, LOGN>() * ((size_t)Exchanger<T, LOGN, CPMUL_NBUF, enc_groups<T, LOGN>()>::WORDS + (1 << LOGN)) * sizeof(T) +
+                 2 * (size_t)(1 << LOGN) * sizeof(T) <= 227 * 1024;
+}
 
 template <typename T, int LOGN, bool SMEM_TW>
 __global__ void __launch_bounds__(NttShape<LOGN>::THREADS * enc_groups<T, LOGN>(),
@@ -834,7 +839,7 @@ static cudaError_t launch_cpmul(const Ctx* c, const Base* b, const void* ct, con
   constexpr int GROUPS = cpmul_kernel_groups<T, LOGN>();
   constexpr size_t tw_bytes = (size_t)tw_words<T>(LOGN) * sizeof(T);
   constexpr size_t group_bytes = ((size_t)Exchanger<T, LOGN, cpmul_kernel_nbuf<T, LOGN>(), GROUPS>::WORDS + Sh::N) * sizeof(T);
-  constexpr bool SMEM_TW = LOGN >= 9 && tw_bytes + GROUPS * group_bytes <= (sizeof(T) == 4 ? 200 : 226) * 1024;
+  constexpr bool SMEM_TW = LOGN >= 9 && tw_bytes + GROUPS * group_bytes <= (sizeof(T) == 4 ? 224 : 226) * 1024;
   auto kern = k_cpmul<T, LOGN, SMEM_TW>;
   const size_t smem = GROUPS * group_bytes + (SMEM_TW ? tw_bytes : 0);
   const int L = b->size();
