@@ -231,6 +231,11 @@ struct StreamCfg {
                                 : (CTB_STREAM_G2_13 && sizeof(T) == 4 && LOGN == 13) ? 2 : cpmul_groups<T, LOGN>();
   static constexpr int CTAS_PER_SM = WIDE ? 1 : 2;
   using Ex = Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>;
+  // eval-layout outputs stored through the exchange image (ntt.cuh store_eval_xpose)
+#ifndef CTB_EVAL_XPOSE
+#define CTB_EVAL_XPOSE 1
+#endif
+  static constexpr bool XPOSE = CTB_EVAL_XPOSE && eval_xpose_ok<T, LOGN>(Ex::WORDS);
   static constexpr size_t TW_BYTES = (size_t)tw_words<T>(LOGN) * sizeof(T);
   // u32: table + images within 200 KB (two CTAs per SM with staging); 64-bit limbs: the
   // (w, w/p) table (140 KB at N=8192) + image fill one CTA's 227 KB
@@ -349,6 +354,10 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
         issue_next();
       }
     };
+    auto store_out = [&](const T (&v)[Sh::E]) {
+      if constexpr (C::XPOSE) store_eval_xpose<T, LOGN, GROUPS>(a.out + off, v, gsm);
+      else store_eval<T, LOGN>(a.out + off, v);
+    };
     auto xform_inv = [&](bool first_in_item) {
       constexpr int K = Sh::NPASS - 1;
       if constexpr (SPLIT) {
@@ -382,15 +391,15 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
       if constexpr (OP == StreamOp::Fwd || OP == StreamOp::LiftFwd) {
 #pragma unroll
         for (int k = 0; k < Sh::E; ++k) x[k] = pr.canon_fwd(x[k]);
-        store_eval<T, LOGN>(a.out + off, x);
+        store_out(x);
       } else if constexpr (OP == StreamOp::FwdNinv) {
 #pragma unroll
         for (int k = 0; k < Sh::E; ++k) x[k] = csub(shoup_mul(x[k], pr.ninv, pr.ninv_q, pr.p), pr.p);
-        store_eval<T, LOGN>(a.out + off, x);
+        store_out(x);
       } else if constexpr (OP == StreamOp::Prepare || OP == StreamOp::LiftPrepare) {
 #pragma unroll
         for (int k = 0; k < Sh::E; ++k) x[k] = csub(shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p), pr.p);
-        store_eval<T, LOGN>(a.out + off, x);
+        store_out(x);
       } else {
         const T* pb = a.bprep + ((size_t)b * a.b_stride * L + limb) * (size_t)Sh::N;
         using EV = EvalVec<T, LOGN>;

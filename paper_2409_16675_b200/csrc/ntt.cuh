@@ -834,6 +834,59 @@ __device__ __forceinline__ void store_eval(T* base, const T (&x)[NttShape<LOGN>:
   }
 }
 
+// store_eval through the group's (free) exchange image: the last pass leaves thread t with the
+// E-word block f(t) (pass_thread rotates the low thread bits, so a warp's blocks are 2 apart and
+// every 16-byte store of store_eval lands in a different 128-byte line).  Transposed through
+// shared memory, each warp instruction stores 512 contiguous bytes instead.  Chunk c of block B
+// sits at 16-byte slot 4B + c + B/2 (u32: the pad makes both the block-strided writes and the
+// contiguous reads conflict-free) or 8B + (c ^ (B/2 mod 8)) (u64).  Two group barriers: the
+// image may still be read by the last exchange (WAR), and the reads need every write (RAW).
+template <typename T, int LOGN>
+__host__ __device__ constexpr int eval_xpose_chunks() {
+  using Sh = NttShape<LOGN>;
+  constexpr int CH = Sh::E * (int)sizeof(T) / 16;
+  constexpr int NB = Sh::N / Sh::E;
+  return CH == 4 ? 4 * NB + NB / 2 : (CH == 8 ? 8 * NB : 0);
+}
+template <typename T, int LOGN>
+__host__ __device__ constexpr bool eval_xpose_ok(int image_words) {
+  using Sh = NttShape<LOGN>;
+  return Sh::pass_r(Sh::NPASS - 1) == Sh::LOGE && Sh::E * sizeof(T) % 16 == 0 && eval_xpose_chunks<T, LOGN>() > 0 &&
+         (size_t)eval_xpose_chunks<T, LOGN>() * 16 <= (size_t)image_words * sizeof(T);
+}
+__device__ __forceinline__ int eval_xpose_slot4(int B, int c) { return 4 * B + c + (B >> 1); }
+__device__ __forceinline__ int eval_xpose_slot8(int B, int c) { return 8 * B + (c ^ ((B >> 1) & 7)); }
+
+template <typename T, int LOGN, int GROUPS>
+__device__ __forceinline__ void store_eval_xpose(T* base, const T (&x)[NttShape<LOGN>::E], T* img) {
+  using Sh = NttShape<LOGN>;
+  constexpr int CH = Sh::E * (int)sizeof(T) / 16;
+  static_assert(CH == 4 || CH == 8, "eval transpose: 4 or 8 chunks per thread");
+  uint4* img4 = reinterpret_cast<uint4*>(img);
+  const int blk = eval_base<LOGN>() / Sh::E;
+  group_sync<LOGN, GROUPS>();
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    uint4 w;
+    if constexpr (sizeof(T) == 4) {
+      w = make_uint4((uint32_t)x[4 * c], (uint32_t)x[4 * c + 1], (uint32_t)x[4 * c + 2], (uint32_t)x[4 * c + 3]);
+    } else {
+      w = make_uint4((uint32_t)x[2 * c], (uint32_t)((uint64_t)x[2 * c] >> 32), (uint32_t)x[2 * c + 1],
+                     (uint32_t)((uint64_t)x[2 * c + 1] >> 32));
+    }
+    img4[CH == 4 ? eval_xpose_slot4(blk, c) : eval_xpose_slot8(blk, c)] = w;
+  }
+  group_sync<LOGN, GROUPS>();
+  uint4* out4 = reinterpret_cast<uint4*>(base);
+  const int t = ntt_tid<LOGN>();
+#pragma unroll
+  for (int j = 0; j < CH; ++j) {
+    const int G = j * Sh::THREADS + t;
+    const int B = G / CH, c = G % CH;
+    out4[G] = img4[CH == 4 ? eval_xpose_slot4(B, c) : eval_xpose_slot8(B, c)];
+  }
+}
+
 // Load a PrimeTab into registers (uniform across the CTA).
 template <typename T>
 struct PrimeRegs {
