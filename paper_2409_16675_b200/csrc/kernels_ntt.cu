@@ -80,6 +80,7 @@ constexpr int CPMUL_NBUF = 1;
 #endif
 constexpr int STREAM_QE = CTB_STREAM_QE;
 
+
 // Groups of THREADS threads per CTA for the persistent CPMul: each group runs
 // its own ciphertext of the CTA's limb, all groups share the CTA's twiddle
 // table (2 groups at N >= 2048: 512-thread CTAs, 2 per SM, 32 warps).
@@ -231,11 +232,11 @@ struct StreamCfg {
                                 : (CTB_STREAM_G2_13 && sizeof(T) == 4 && LOGN == 13) ? 2 : cpmul_groups<T, LOGN>();
   static constexpr int CTAS_PER_SM = WIDE ? 1 : 2;
   using Ex = Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>;
-  // eval-layout outputs stored through the exchange image (ntt.cuh store_eval_xpose)
-#ifndef CTB_EVAL_XPOSE
-#define CTB_EVAL_XPOSE 1
-#endif
+  // eval-layout loads / stores through the exchange image (ntt.cuh eval_xpose_*)
   static constexpr bool XPOSE = CTB_EVAL_XPOSE && eval_xpose_ok<T, LOGN>(Ex::WORDS);
+  // loads too for 32-bit words (u64 loads measured neutral to 6% slower in cfg5's InvAdd /
+  // MulPrepared: the 64-bit path stages chunk by chunk without a prefetch across the barrier)
+  static constexpr bool XPOSE_LD = XPOSE && sizeof(T) == 4;
   static constexpr size_t TW_BYTES = (size_t)tw_words<T>(LOGN) * sizeof(T);
   // u32: table + images within 200 KB (two CTAs per SM with staging); 64-bit limbs: the
   // (w, w/p) table (140 KB at N=8192) + image fill one CTA's 227 KB
@@ -300,7 +301,14 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
       mbar_wait(bar, phase);
       phase ^= 1;
       if constexpr (EVAL_IN) {
-        load_eval_smem<T, LOGN>(stg, x);
+        if constexpr (C::XPOSE_LD) {
+          eval_xpose_apply<T, LOGN, GROUPS, true>(stg, gsm, [&](int c, const T* v) {
+#pragma unroll
+            for (int i = 0; i < 16 / (int)sizeof(T); ++i) x[c * (16 / (int)sizeof(T)) + i] = v[i];
+          });
+        } else {
+          load_eval_smem<T, LOGN>(stg, x);
+        }
       } else {
 #pragma unroll
         for (int k = 0; k < Sh::E; ++k) x[k] = stg[cb + coef_off<LOGN>(k)];
@@ -319,7 +327,14 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
         x[k] = r;
       }
     } else if constexpr (EVAL_IN) {
-      load_eval<T, LOGN>(a.in + ioff, x);
+      if constexpr (C::XPOSE_LD) {
+        eval_xpose_apply<T, LOGN, GROUPS>(a.in + ioff, gsm, [&](int c, const T* v) {
+#pragma unroll
+          for (int i = 0; i < 16 / (int)sizeof(T); ++i) x[c * (16 / (int)sizeof(T)) + i] = v[i];
+        });
+      } else {
+        load_eval<T, LOGN>(a.in + ioff, x);
+      }
     } else {
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) x[k] = a.in[ioff + cb + coef_off<LOGN>(k)];
@@ -403,12 +418,19 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
       } else {
         const T* pb = a.bprep + ((size_t)b * a.b_stride * L + limb) * (size_t)Sh::N;
         using EV = EvalVec<T, LOGN>;
+        if constexpr (C::XPOSE_LD) {
+          eval_xpose_apply<T, LOGN, GROUPS>(pb, gsm, [&](int i, const T* v) {
 #pragma unroll
-        for (int i = 0; i < EV::CHUNKS; ++i) {
-          T v[EV::VEC];
-          EV::load(pb, i, v);
+            for (int c = 0; c < EV::VEC; ++c) x[i * EV::VEC + c] = mont_mul(x[i * EV::VEC + c], v[c], pr.p, pr.pinv);
+          });
+        } else {
 #pragma unroll
-          for (int c = 0; c < EV::VEC; ++c) x[i * EV::VEC + c] = mont_mul(x[i * EV::VEC + c], v[c], pr.p, pr.pinv);
+          for (int i = 0; i < EV::CHUNKS; ++i) {
+            T v[EV::VEC];
+            EV::load(pb, i, v);
+#pragma unroll
+            for (int c = 0; c < EV::VEC; ++c) x[i * EV::VEC + c] = mont_mul(x[i * EV::VEC + c], v[c], pr.p, pr.pinv);
+          }
         }
         xform_inv(false);
 #pragma unroll
@@ -515,6 +537,8 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
   constexpr int GROUP_WORDS = Ex::WORDS + Sh::N;
   constexpr bool PKSM = enc_pk_smem<T, LOGN>() && SMEM_TW;
   using EV = EvalVec<T, LOGN>;
+  constexpr bool ENC_XPOSE = !PKSM && sizeof(T) == 4 && CTB_EVAL_XPOSE && EV::VEC == Strip<T, LOGN>::VEC &&
+                             eval_xpose_ok<T, LOGN>(Ex::WORDS);
   static_assert(!PKSM || (EV::VEC == Strip<T, LOGN>::VEC && GROUPS >= 2), "key strips need contiguous eval chunks");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
@@ -587,6 +611,15 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
       const T* kp = pkprep + ((size_t)part * L + limb) * Sh::N;
       static_assert(EV::VEC == Strip<T, LOGN>::VEC || EV::VEC == 1, "strip / eval chunking");
       const Strip<T, LOGN> ks(pk_sm + (size_t)part * Sh::N);
+      if constexpr (ENC_XPOSE) {
+        // key read with contiguous 16-byte accesses through the exchange image (ntt.cuh)
+        eval_xpose_apply<T, LOGN, GROUPS>(kp, gsm, [&](int i, const T* v) {
+          T uu[EV::VEC];
+          usm.load_chunk(i, uu);
+#pragma unroll
+          for (int c = 0; c < EV::VEC; ++c) x[i * EV::VEC + c] = mont_mul(uu[c], v[c], pr.p, pr.pinv);
+        });
+      } else {
 #pragma unroll
       for (int i = 0; i < EV::CHUNKS; ++i) {
         T v[EV::VEC];
@@ -602,6 +635,7 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
           usm.load_chunk(i / Strip<T, LOGN>::VEC, uu);
           x[i] = mont_mul(uu[i % Strip<T, LOGN>::VEC], v[0], pr.p, pr.pinv);
         }
+      }
       }
       int8_t e[Sh::E];  // issued before the inverse transform, consumed after it
       load_draws(drow + (size_t)(1 + part) * Sh::N, e);

@@ -834,56 +834,116 @@ __device__ __forceinline__ void store_eval(T* base, const T (&x)[NttShape<LOGN>:
   }
 }
 
-// store_eval through the group's (free) exchange image: the last pass leaves thread t with the
-// E-word block f(t) (pass_thread rotates the low thread bits, so a warp's blocks are 2 apart and
-// every 16-byte store of store_eval lands in a different 128-byte line).  Transposed through
-// shared memory, each warp instruction stores 512 contiguous bytes instead.  Chunk c of block B
-// sits at 16-byte slot 4B + c + B/2 (u32: the pad makes both the block-strided writes and the
-// contiguous reads conflict-free) or 8B + (c ^ (B/2 mod 8)) (u64).  Two group barriers: the
-// image may still be read by the last exchange (WAR), and the reads need every write (RAW).
-template <typename T, int LOGN>
-__host__ __device__ constexpr int eval_xpose_chunks() {
-  using Sh = NttShape<LOGN>;
-  constexpr int CH = Sh::E * (int)sizeof(T) / 16;
-  constexpr int NB = Sh::N / Sh::E;
-  return CH == 4 ? 4 * NB + NB / 2 : (CH == 8 ? 8 * NB : 0);
-}
+// Eval-layout global traffic through the group's (free) exchange image.  The last pass leaves
+// thread t with the E-word block f(t) (pass_thread rotates the low thread bits, so a warp's blocks
+// are 2 apart and each 16-byte access of store_eval / EvalVec lands in a different 128-byte line,
+// and the natural-order TMA staging buffer read that way is an 8-way bank conflict).  Transposed
+// through shared memory, each warp instruction moves 512 contiguous bytes instead.  16-byte chunk
+// c of block B sits at slot
+//   u32 (4 chunks per block): 8 (B/2) + 4 ((B ^ B/2) & 1) + (c ^ (B/4 mod 4))
+//   u64 (8 chunks per block): 8 B + (c ^ (B/2 mod 8))
+// so that both the block-wise side (a quarter warp holds blocks 2u + e for 8 consecutive u) and
+// the contiguous side (a quarter warp holds 8 consecutive chunks) hit 8 distinct 16-byte bank
+// groups, in exactly N words.  Barriers: the image may still be read by the last exchange (WAR),
+// and the second side needs every write of the first (RAW); every later use of the image (an
+// exchange, or the next transposition) starts with a group barrier.
+// -DCTB_EVAL_XPOSE=0 restores the direct (line-per-lane) eval-layout accesses.
+#ifndef CTB_EVAL_XPOSE
+#define CTB_EVAL_XPOSE 1
+#endif
 template <typename T, int LOGN>
 __host__ __device__ constexpr bool eval_xpose_ok(int image_words) {
   using Sh = NttShape<LOGN>;
-  return Sh::pass_r(Sh::NPASS - 1) == Sh::LOGE && Sh::E * sizeof(T) % 16 == 0 && eval_xpose_chunks<T, LOGN>() > 0 &&
-         (size_t)eval_xpose_chunks<T, LOGN>() * 16 <= (size_t)image_words * sizeof(T);
+  constexpr int CH = Sh::E * (int)sizeof(T) / 16;
+  return Sh::pass_r(Sh::NPASS - 1) == Sh::LOGE && Sh::E * sizeof(T) % 16 == 0 && (CH == 4 || CH == 8) &&
+         Sh::THREADS % 8 == 0 && image_words >= Sh::N;
 }
-__device__ __forceinline__ int eval_xpose_slot4(int B, int c) { return 4 * B + c + (B >> 1); }
-__device__ __forceinline__ int eval_xpose_slot8(int B, int c) { return 8 * B + (c ^ ((B >> 1) & 7)); }
+template <int CH>
+__device__ __forceinline__ int eval_xpose_slot(int B, int c) {
+  if constexpr (CH == 4) return 8 * (B >> 1) + 4 * ((B ^ (B >> 1)) & 1) + (c ^ ((B >> 2) & 3));
+  else return 8 * B + (c ^ ((B >> 1) & 7));
+}
+template <typename T>
+__device__ __forceinline__ uint4 pack_chunk(const T* v) {
+  if constexpr (sizeof(T) == 4) return make_uint4((uint32_t)v[0], (uint32_t)v[1], (uint32_t)v[2], (uint32_t)v[3]);
+  else return make_uint4((uint32_t)v[0], (uint32_t)((uint64_t)v[0] >> 32), (uint32_t)v[1], (uint32_t)((uint64_t)v[1] >> 32));
+}
+template <typename T>
+__device__ __forceinline__ void unpack_chunk(const uint4& w, T* v) {
+  if constexpr (sizeof(T) == 4) {
+    v[0] = w.x; v[1] = w.y; v[2] = w.z; v[3] = w.w;
+  } else {
+    v[0] = (T)((uint64_t)w.x | ((uint64_t)w.y << 32));
+    v[1] = (T)((uint64_t)w.z | ((uint64_t)w.w << 32));
+  }
+}
 
 template <typename T, int LOGN, int GROUPS>
 __device__ __forceinline__ void store_eval_xpose(T* base, const T (&x)[NttShape<LOGN>::E], T* img) {
   using Sh = NttShape<LOGN>;
-  constexpr int CH = Sh::E * (int)sizeof(T) / 16;
-  static_assert(CH == 4 || CH == 8, "eval transpose: 4 or 8 chunks per thread");
+  constexpr int CH = Sh::E * (int)sizeof(T) / 16, VEC = 16 / (int)sizeof(T);
   uint4* img4 = reinterpret_cast<uint4*>(img);
   const int blk = eval_base<LOGN>() / Sh::E;
   group_sync<LOGN, GROUPS>();
 #pragma unroll
-  for (int c = 0; c < CH; ++c) {
-    uint4 w;
-    if constexpr (sizeof(T) == 4) {
-      w = make_uint4((uint32_t)x[4 * c], (uint32_t)x[4 * c + 1], (uint32_t)x[4 * c + 2], (uint32_t)x[4 * c + 3]);
-    } else {
-      w = make_uint4((uint32_t)x[2 * c], (uint32_t)((uint64_t)x[2 * c] >> 32), (uint32_t)x[2 * c + 1],
-                     (uint32_t)((uint64_t)x[2 * c + 1] >> 32));
-    }
-    img4[CH == 4 ? eval_xpose_slot4(blk, c) : eval_xpose_slot8(blk, c)] = w;
-  }
+  for (int c = 0; c < CH; ++c) img4[eval_xpose_slot<CH>(blk, c)] = pack_chunk<T>(x + c * VEC);
   group_sync<LOGN, GROUPS>();
   uint4* out4 = reinterpret_cast<uint4*>(base);
   const int t = ntt_tid<LOGN>();
 #pragma unroll
   for (int j = 0; j < CH; ++j) {
     const int G = j * Sh::THREADS + t;
-    const int B = G / CH, c = G % CH;
-    out4[G] = img4[CH == 4 ? eval_xpose_slot4(B, c) : eval_xpose_slot8(B, c)];
+    out4[G] = img4[eval_xpose_slot<CH>(G / CH, G % CH)];
+  }
+}
+
+// The converse: an eval-layout polynomial at src (global, read-only; or shared memory in natural
+// order) is staged into the image with contiguous 16-byte accesses (eval_xpose_stage), then each
+// thread reads chunk c (VEC words) of its own block (eval_xpose_chunk) -- consumed chunk by chunk
+// so only VEC extra registers are live.
+template <typename T, int LOGN, int GROUPS, bool SRC_SMEM = false>
+__device__ __forceinline__ void eval_xpose_stage(const T* src, T* img) {
+  using Sh = NttShape<LOGN>;
+  constexpr int CH = Sh::E * (int)sizeof(T) / 16;
+  uint4* img4 = reinterpret_cast<uint4*>(img);
+  const uint4* src4 = reinterpret_cast<const uint4*>(src);
+  const int t = ntt_tid<LOGN>();
+  if constexpr (CH == 4) {  // 16 registers: the loads fly across the WAR barrier
+    uint4 w[CH];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) w[j] = SRC_SMEM ? src4[j * Sh::THREADS + t] : __ldg(src4 + j * Sh::THREADS + t);
+    group_sync<LOGN, GROUPS>();
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      const int G = j * Sh::THREADS + t;
+      img4[eval_xpose_slot<CH>(G / CH, G % CH)] = w[j];
+    }
+  } else {  // 64-bit words (register-heavy kernels): load and place one chunk at a time
+    group_sync<LOGN, GROUPS>();
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      const int G = j * Sh::THREADS + t;
+      img4[eval_xpose_slot<CH>(G / CH, G % CH)] = SRC_SMEM ? src4[G] : __ldg(src4 + G);
+    }
+  }
+  group_sync<LOGN, GROUPS>();
+}
+template <typename T, int LOGN>
+__device__ __forceinline__ void eval_xpose_chunk(const T* img, int c, T* v) {
+  using Sh = NttShape<LOGN>;
+  constexpr int CH = Sh::E * (int)sizeof(T) / 16;
+  unpack_chunk<T>(reinterpret_cast<const uint4*>(img)[eval_xpose_slot<CH>(eval_base<LOGN>() / Sh::E, c)], v);
+}
+template <typename T, int LOGN, int GROUPS, bool SRC_SMEM = false, typename F>
+__device__ __forceinline__ void eval_xpose_apply(const T* src, T* img, F&& f) {
+  using Sh = NttShape<LOGN>;
+  constexpr int CH = Sh::E * (int)sizeof(T) / 16, VEC = 16 / (int)sizeof(T);
+  eval_xpose_stage<T, LOGN, GROUPS, SRC_SMEM>(src, img);
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    T v[VEC];
+    eval_xpose_chunk<T, LOGN>(img, c, v);
+    f(c, v);
   }
 }
 

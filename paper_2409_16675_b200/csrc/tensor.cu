@@ -558,6 +558,11 @@ __global__ void __launch_bounds__(256) k_relin_digits(const TQ* ct3, uint32_t* d
 // out [B][2][L][N] = (c0, c1) + sum_j NTT^-1(NTT(d_j) * keyprep[j][0|1]).  Persistent and
 // limb-stationary (CTA k serves limb k % L), the limb's twiddle table staged in shared
 // memory; both accumulators stay in registers across the D digit transforms.
+// Relinearisation keys through the exchange image (ntt.cuh eval_xpose_*): off by default -- with
+// the digit transform and both accumulators live it spills (232 B per thread at 64-bit limbs).
+#ifndef CTB_RELIN_XPOSE
+#define CTB_RELIN_XPOSE 0
+#endif
 template <typename T, int LOGN>
 struct RelinCfg {
   using Sh = NttShape<LOGN>;
@@ -638,6 +643,31 @@ k_relin_accum(const T* ct3, int ct_parts, const uint32_t* digits, const T* keypr
       ntt_fwd_regs<T, LOGN, 0, SMEM_TW, 1, 1, TENSOR_QE>(x, ex, tw, pr.p, pr.p2);
       const T* kb = keyprep + (((size_t)d * 2 + 0) * L + limb) * N;
       const T* ka = keyprep + (((size_t)d * 2 + 1) * L + limb) * N;
+      if constexpr (CTB_RELIN_XPOSE && eval_xpose_ok<T, LOGN>(Ex::WORDS)) {
+        // keys read with contiguous 16-byte accesses through the exchange image (ntt.cuh)
+        eval_xpose_stage<T, LOGN, 1>(kb, ex.buf);
+#pragma unroll
+        for (int i = 0; i < EV::CHUNKS; ++i) {
+          T v[EV::VEC];
+          eval_xpose_chunk<T, LOGN>(ex.buf, i, v);
+#pragma unroll
+          for (int c = 0; c < EV::VEC; ++c) {
+            const int j = i * EV::VEC + c;
+            acc0[j] = csub(acc0[j] + mont_mul(x[j], v[c], pr.p, pr.pinv), pr.p2);
+          }
+        }
+        eval_xpose_stage<T, LOGN, 1>(ka, ex.buf);
+#pragma unroll
+        for (int i = 0; i < EV::CHUNKS; ++i) {
+          T v[EV::VEC];
+          eval_xpose_chunk<T, LOGN>(ex.buf, i, v);
+#pragma unroll
+          for (int c = 0; c < EV::VEC; ++c) {
+            const int j = i * EV::VEC + c;
+            acc1[j] = csub(acc1[j] + mont_mul(x[j], v[c], pr.p, pr.pinv), pr.p2);
+          }
+        }
+      } else
 #pragma unroll
       for (int i = 0; i < EV::CHUNKS; ++i) {
         T vb[EV::VEC], va[EV::VEC];
