@@ -577,7 +577,7 @@ struct RelinCfg {
   static constexpr int MINB = (Sh::THREADS == 256 && sizeof(T) == 4) ? 3 : Sh::MINB;
 };
 
-template <typename T, int LOGN, bool SMEM_TW>
+template <typename T, int LOGN, bool SMEM_TW, bool KSTRIP = false>
 __global__ void __launch_bounds__(NttShape<LOGN>::THREADS, RelinCfg<T, LOGN>::MINB)
 k_relin_accum(const T* ct3, int ct_parts, const uint32_t* digits, const T* keyprep, T* out,
               const PrimeTab<T>* __restrict__ tabs, int L, int D, uint32_t batch) {
@@ -671,8 +671,13 @@ k_relin_accum(const T* ct3, int ct_parts, const uint32_t* digits, const T* keypr
 #pragma unroll
       for (int i = 0; i < EV::CHUNKS; ++i) {
         T vb[EV::VEC], va[EV::VEC];
-        EV::load(kb, i, vb);
-        EV::load(ka, i, va);
+        if constexpr (KSTRIP) {  // thread-major chunk layout (k_eval_to_strip): contiguous warp loads
+          unpack_chunk<T>(__ldg(reinterpret_cast<const uint4*>(kb) + i * Sh::THREADS + threadIdx.x), vb);
+          unpack_chunk<T>(__ldg(reinterpret_cast<const uint4*>(ka) + i * Sh::THREADS + threadIdx.x), va);
+        } else {
+          EV::load(kb, i, vb);
+          EV::load(ka, i, va);
+        }
 #pragma unroll
         for (int c = 0; c < EV::VEC; ++c) {
           const int j = i * EV::VEC + c;
@@ -694,19 +699,59 @@ k_relin_accum(const T* ct3, int ct_parts, const uint32_t* digits, const T* keypr
   }
 }
 
+// Prepared keys (eval layout, [npoly][N]) -> thread-major chunk layout: chunk c of transform
+// thread t at 16-byte index c * THREADS + t.  The eval layout gives thread t the block f(t)
+// (ntt.cuh eval_xpose_*), so direct eval-layout key loads put every lane of a warp in its own
+// 128-byte line; in this layout each warp load is 512 contiguous bytes.  One block per polynomial.
+template <typename T, int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS) k_eval_to_strip(const T* __restrict__ in, T* __restrict__ out) {
+  using Sh = NttShape<LOGN>;
+  using EV = EvalVec<T, LOGN>;
+  const T* src = in + (size_t)blockIdx.x * Sh::N;
+  uint4* dst = reinterpret_cast<uint4*>(out + (size_t)blockIdx.x * Sh::N);
+#pragma unroll
+  for (int i = 0; i < EV::CHUNKS; ++i) {
+    T v[EV::VEC];
+    EV::load(src, i, v);
+    dst[i * Sh::THREADS + threadIdx.x] = pack_chunk<T>(v);
+  }
+}
+// Relinearisation keys in the thread-major layout (per call: a stream-ordered temporary, D x 2 x L
+// polynomials, negligible beside the D x L digit transforms per slot).  -DCTB_RELIN_KSTRIP=0: direct.
+#ifndef CTB_RELIN_KSTRIP
+#define CTB_RELIN_KSTRIP 1
+#endif
+
 template <typename T, int LOGN>
 static cudaError_t launch_relin_accum(const Ctx* c, const void* ct3, int ct_parts, const uint32_t* digits,
                                       const void* keyprep, void* out, uint64_t batch, int D, cudaStream_t s) {
   using Sh = NttShape<LOGN>;
   using C = RelinCfg<T, LOGN>;
+  using EV = EvalVec<T, LOGN>;
+  constexpr bool KS = CTB_RELIN_KSTRIP && EV::CONTIG && EV::VEC * (int)sizeof(T) == 16 && !C::PF;
   const Base& B = c->base[BASE_Q];
-  auto kern = k_relin_accum<T, LOGN, C::SMEM_TW>;
+  auto kern = k_relin_accum<T, LOGN, C::SMEM_TW, KS>;
   const int L = B.size();
   if (batch == 0) return cudaSuccess;
+  const void* keys = keyprep;
+  void* tmp = nullptr;
+  if constexpr (KS) {
+    const size_t npoly = (size_t)D * 2 * L;
+    cudaError_t e = cudaMallocAsync(&tmp, npoly * Sh::N * sizeof(T), s);
+    if (e != cudaSuccess) return e;
+    k_eval_to_strip<T, LOGN><<<(unsigned)npoly, Sh::THREADS, 0, s>>>((const T*)keyprep, (T*)tmp);
+    if ((e = cudaGetLastError()) != cudaSuccess) { cudaFreeAsync(tmp, s); return e; }
+    keys = tmp;
+  }
   uint32_t grid = persistent_grid((const void*)kern, Sh::THREADS, C::SMEM);
   grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(grid / L * L, (uint64_t)L), batch * (uint64_t)L);
-  return launch_kernel_grid(kern, grid, Sh::THREADS, C::SMEM, s, (const T*)ct3, ct_parts, digits, (const T*)keyprep,
-                            (T*)out, (const PrimeTab<T>*)B.d_tabs, L, D, (uint32_t)batch);
+  cudaError_t e = launch_kernel_grid(kern, grid, Sh::THREADS, C::SMEM, s, (const T*)ct3, ct_parts, digits, (const T*)keys,
+                                     (T*)out, (const PrimeTab<T>*)B.d_tabs, L, D, (uint32_t)batch);
+  if (tmp) {
+    const cudaError_t f = cudaFreeAsync(tmp, s);
+    if (e == cudaSuccess) e = f;
+  }
+  return e;
 }
 
 // ----------------------------------------------------------------------------- 6 fused site sums
