@@ -9,6 +9,7 @@ using namespace ctb;
 
 namespace ctb {
 Ctx::~Ctx() {
+  if (pool) cudaMemPoolDestroy(pool);
   free_tensor_consts(tensor);
   free_rns_consts(rns);
   for (auto& b : base) free_base(b);
@@ -33,6 +34,17 @@ extern "C" int ctb_ctx_create(ctb_ctx_t** out, uint32_t n, const uint64_t* q_pri
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     c->wave_chunk = 2u * (uint32_t)(sms > 0 ? sms : 148);
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if (cudaMemPoolCreate(&c->pool, &props) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    } else {
+      c->pool = nullptr;
+      cudaGetLastError();
+    }
     if (const char* env = std::getenv("CTB_WAVE_CHUNK")) {  // tuning knob
       const long v = std::strtol(env, nullptr, 10);
       if (v > 0) c->wave_chunk = (uint32_t)v;

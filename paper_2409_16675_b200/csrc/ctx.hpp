@@ -38,6 +38,10 @@ struct Ctx {
   uint32_t wave_chunk = 296;    // items per limb-major chunk (= 2 x SM count, set at creation)
   RnsConsts* rns = nullptr;
   TensorState* tensor = nullptr;  // built lazily on first CCMul (tensor.cu)
+  // stream-ordered scratch (per-call temporaries, e.g. relinearisation keys in the thread-major
+  // layout); its own pool keeps freed memory mapped across synchronisations (release threshold
+  // max) and is safe for concurrent calls from the party threads sharing the context
+  cudaMemPool_t pool = nullptr;
   ~Ctx();
 };
 

@@ -120,8 +120,9 @@ cudaError_t stream_inv_add(const Ctx* c, int base, const void* in, void* out, co
 
 // Persistent forward NTT of [npoly][L][N] over base `base`: canonical eval, or prepared
 // (N^-1 2^W Montgomery operand) when `prepare` (k_stream Fwd / Prepare).  In place allowed.
+// strip_out: thread-major chunk layout instead of the eval layout (internal operands only).
 cudaError_t stream_forward(const Ctx* c, int base, bool prepare, const void* in, void* out, uint64_t npoly,
-                           cudaStream_t s);
+                           cudaStream_t s, bool strip_out = false);
 
 // NTT of the lift of plain [npoly][N] (centred for the cipher base) per limb of `base`:
 // prepared (N^-1 2^W, k_stream LiftPrepare) or canonical eval (LiftFwd).

@@ -209,6 +209,9 @@ struct StreamArgs {
   const uint64_t* plain;   // LiftPrepare: [npoly][N] values in [0, t)
   uint64_t in_stride, b_stride, add_stride, t_half;
   bool plain_fast;
+  bool strip_out;          // Fwd / Prepare: thread-major chunk layout (chunk c of transform thread t at
+                           // 16-byte index c * THREADS + t) for internal operands whose consumer reads
+                           // them the same way (k_site_product); contiguous warp stores, no transposition
 };
 
 template <typename T, int LOGN>
@@ -370,6 +373,15 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
       }
     };
     auto store_out = [&](const T (&v)[Sh::E]) {
+      if constexpr (EvalVec<T, LOGN>::CONTIG && EvalVec<T, LOGN>::VEC * sizeof(T) == 16) {
+        if (a.strip_out) {
+          uint4* o4 = reinterpret_cast<uint4*>(a.out + off);
+#pragma unroll
+          for (int c = 0; c < EvalVec<T, LOGN>::CHUNKS; ++c)
+            o4[c * Sh::THREADS + ntt_tid<LOGN>()] = pack_chunk<T>(v + c * EvalVec<T, LOGN>::VEC);
+          return;
+        }
+      }
       if constexpr (C::XPOSE) store_eval_xpose<T, LOGN, GROUPS>(a.out + off, v, gsm);
       else store_eval<T, LOGN>(a.out + off, v);
     };
@@ -474,15 +486,19 @@ static StreamArgs<T> sargs(const void* in, void* out, const void* bprep = nullpt
 }
 
 cudaError_t stream_forward(const Ctx* c, int base, bool prepare, const void* in, void* out, uint64_t npoly,
-                           cudaStream_t s) {
+                           cudaStream_t s, bool strip_out) {
   const Base* b = &c->base[base];
   cudaError_t e = cudaSuccess;
   if (b->word == 4) {
-    if (prepare) CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::Prepare>(b, sargs<uint32_t>(in, out), npoly, s)))
-    else CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::Fwd>(b, sargs<uint32_t>(in, out), npoly, s)))
+    auto a = sargs<uint32_t>(in, out);
+    a.strip_out = strip_out;
+    if (prepare) CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::Prepare>(b, a, npoly, s)))
+    else CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::Fwd>(b, a, npoly, s)))
   } else {
-    if (prepare) CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::Prepare>(b, sargs<uint64_t>(in, out), npoly, s)))
-    else CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::Fwd>(b, sargs<uint64_t>(in, out), npoly, s)))
+    auto a = sargs<uint64_t>(in, out);
+    a.strip_out = strip_out;
+    if (prepare) CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::Prepare>(b, a, npoly, s)))
+    else CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::Fwd>(b, a, npoly, s)))
   }
   return e;
 }

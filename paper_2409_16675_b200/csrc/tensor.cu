@@ -737,7 +737,8 @@ static cudaError_t launch_relin_accum(const Ctx* c, const void* ct3, int ct_part
   void* tmp = nullptr;
   if constexpr (KS) {
     const size_t npoly = (size_t)D * 2 * L;
-    cudaError_t e = cudaMallocAsync(&tmp, npoly * Sh::N * sizeof(T), s);
+    cudaError_t e = c->pool ? cudaMallocFromPoolAsync(&tmp, npoly * Sh::N * sizeof(T), c->pool, s)
+                            : cudaMallocAsync(&tmp, npoly * Sh::N * sizeof(T), s);
     if (e != cudaSuccess) return e;
     k_eval_to_strip<T, LOGN><<<(unsigned)npoly, Sh::THREADS, 0, s>>>((const T*)keyprep, (T*)tmp);
     if ((e = cudaGetLastError()) != cudaSuccess) { cudaFreeAsync(tmp, s); return e; }
@@ -783,6 +784,16 @@ __host__ __device__ constexpr int site_group_words() {
   return (Exchanger<uint32_t, LOGN, 1, GROUPS>::WORDS + site_strips<LOGN>() * (1 << LOGN) + 3) / 4 * 4;
 }
 
+// SITE_STRIP: AX / AW in the thread-major chunk layout (stream_forward strip_out): contiguous warp
+// loads instead of one 128-byte line per lane.  -DCTB_SITE_STRIP=0: eval layout.
+#ifndef CTB_SITE_STRIP
+#define CTB_SITE_STRIP 1
+#endif
+template <int LOGN>
+__host__ __device__ constexpr bool site_strip() {
+  return CTB_SITE_STRIP && EvalVec<uint32_t, LOGN>::CONTIG && EvalVec<uint32_t, LOGN>::VEC == 4;
+}
+
 template <int LOGN, bool SMEM_TW>
 __global__ void __launch_bounds__(NttShape<LOGN>::THREADS * site_groups<LOGN>(), site_groups<LOGN>() == 2 ? 1 : NttShape<LOGN>::MINB)
 k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict__ sx,
@@ -816,6 +827,10 @@ k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict
   const TwSrc<T, SMEM_TW> tw{twp};
   const size_t N = Sh::N, KN = (size_t)K * N;
   using EV = EvalVec<T, LOGN>;
+  auto ld = [&](const T* base, int i, T (&v)[EV::VEC]) {
+    if constexpr (site_strip<LOGN>()) unpack_chunk<T>(__ldg(reinterpret_cast<const uint4*>(base) + i * Sh::THREADS + ntt_tid<LOGN>()), v);
+    else EV::load(base, i, v);
+  };
   T y[Sh::E];
   auto store = [&](uint32_t s, int part) {
     T* dst = H + ((size_t)s * 3 + part) * KN + k * N + coef_base<LOGN>();
@@ -838,10 +853,10 @@ k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict
 #pragma unroll
     for (int i = 0; i < EV::CHUNKS; ++i) {
       T a0[EV::VEC], a1[EV::VEC], b0[EV::VEC], b1[EV::VEC];
-      EV::load(a0p, i, a0);
-      EV::load(a0p + KN, i, a1);
-      EV::load(b0p, i, b0);
-      EV::load(b0p + KN, i, b1);
+      ld(a0p, i, a0);
+      ld(a0p + KN, i, a1);
+      ld(b0p, i, b0);
+      ld(b0p + KN, i, b1);
 #pragma unroll
       for (int c = 0; c < EV::VEC; ++c) {
         const int j = i * EV::VEC + c;
@@ -865,8 +880,8 @@ k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict
 #pragma unroll
       for (int i = 0; i < EV::CHUNKS; ++i) {
         T a0[EV::VEC], b0[EV::VEC];
-        EV::load(a0p, i, a0);
-        EV::load(b0p, i, b0);
+        ld(a0p, i, a0);
+        ld(b0p, i, b0);
 #pragma unroll
         for (int c = 0; c < EV::VEC; ++c) y[i * EV::VEC + c] = mont_mul(a0[c], b0[c], pr.p, pr.pinv);
       }
@@ -1410,8 +1425,13 @@ extern "C" int ctb_ccmul_sum(const ctb_ctx_t* ctx, const void* ct_x, uint32_t n_
   // every distinct ciphertext: centred lift to the aux base, forward transform once
   if ((rc = ctb_tensor_lift(ctx, ct_x, AX, n_x, stream))) return rc;
   if ((rc = ctb_tensor_lift(ctx, ct_w, AW, n_w, stream))) return rc;
-  if ((e = stream_forward(c, BASE_B, true, AX, AX, (uint64_t)n_x * 2, s)) != cudaSuccess) return cuda_status(e, "ctb_ccmul_sum ntt");
-  if ((e = stream_forward(c, BASE_B, false, AW, AW, (uint64_t)n_w * 2, s)) != cudaSuccess) return cuda_status(e, "ctb_ccmul_sum ntt");
+  // AX / AW are consumed only by k_site_product: thread-major chunk layout when it reads them so
+  {
+    bool strip = false;
+    CTB_DISPATCH_LOGN(c->logn, strip = site_strip<LOGN>());
+    if ((e = stream_forward(c, BASE_B, true, AX, AX, (uint64_t)n_x * 2, s, strip)) != cudaSuccess) return cuda_status(e, "ctb_ccmul_sum ntt");
+    if ((e = stream_forward(c, BASE_B, false, AW, AW, (uint64_t)n_w * 2, s, strip)) != cudaSuccess) return cuda_status(e, "ctb_ccmul_sum ntt");
+  }
   // chunks of whole slots
   uint32_t o0 = 0;
   while (o0 < n_out) {
