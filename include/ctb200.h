@@ -83,6 +83,12 @@ int ctb_ring_mul(const ctb_ctx_t* ctx, int base, const void* a, uint64_t a_strid
  * (ctb_linear_online maskprod_eval = 1).  In place allowed. */
 int ctb_eval_addend(const ctb_ctx_t* ctx, int base, const void* in, void* out, uint64_t n_polys, void* stream);
 
+/* The same values (NTT(in) * N^-1, canonical) in ctb_linear_online's internal evaluation layout
+ * (16-byte chunk c of transform thread t at chunk index c * (N/16) + t): the form its
+ * maskprod_eval = 1 argument takes.  Replaces the server's per-slot mask-product addition of
+ * precompute_online_server (linprot.py:482-484), moved offline.  In place allowed. */
+int ctb_linear_addend(const ctb_ctx_t* ctx, int base, const void* in, void* out, uint64_t n_polys, void* stream);
+
 /* Prepared operand for repeated products: out = NTT(in) scaled into the
  * Montgomery domain with N^-1 folded (layout [poly][L][N], evaluation order).
  * Keys (public, secret, relinearisation) are prepared once per session. */
@@ -214,7 +220,7 @@ int ctb_lift_prepare(const ctb_ctx_t* ctx, const uint64_t* m, void* out, uint64_
  * masked plaintexts (x - r_x, w - r_w); sites_host: HOST array of n_sites
  * (x index, w index, out slot) triples (linprot.JobShape.sites); maskprod
  * [n_out][2][L][N] or NULL, as ciphertexts (maskprod_eval = 0) or in the
- * ctb_eval_addend form (maskprod_eval = 1: the server transformed its mask products
+ * ctb_linear_addend form (maskprod_eval = 1: the server transformed its mask products
  * offline, so the online step adds them in the evaluation domain);
  * out_ct [n_out][2][L][N]; out_p [n_out][N].
  * workspace: ctb_linear_online_workspace_bytes() bytes of device memory.

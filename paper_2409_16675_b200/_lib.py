@@ -69,6 +69,7 @@ SIGNATURES: dict[str, tuple] = {
                                  ctypes.POINTER(_u32), _u32, _u32, _c_void_p, _int, _c_void_p, _c_void_p, _c_void_p,
                                  _c_void_p]),
     "ctb_eval_addend": (_int, [_c_void_p, _int, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_linear_addend": (_int, [_c_void_p, _int, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_ccmul_sum_workspace_bytes": (_u64, [_c_void_p, _u32, _u32, _u32, _u32, _u32]),
     "ctb_ccmul_sum": (_int, [_c_void_p, _c_void_p, _u32, _c_void_p, _u32, _c_void_p, _u32, _u32, _c_void_p, _c_void_p,
                              _c_void_p, _u64, _c_void_p]),

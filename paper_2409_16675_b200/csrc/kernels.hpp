@@ -115,8 +115,9 @@ inline cudaError_t launch_kernel_grid(void (*kern)(KArgs...), uint32_t grid, int
 
 // Unscaled inverse NTT of eval-domain [npoly][L][N] (+ coefficient addend), persistent
 // (kernels_ntt.cu k_stream InvAdd).  In place allowed.
+// strip_in: input in the thread-major chunk layout (stream_forward strip_out).
 cudaError_t stream_inv_add(const Ctx* c, int base, const void* in, void* out, const void* addend, uint64_t npoly,
-                           cudaStream_t s);
+                           cudaStream_t s, bool strip_in = false);
 
 // Persistent forward NTT of [npoly][L][N] over base `base`: canonical eval, or prepared
 // (N^-1 2^W Montgomery operand) when `prepare` (k_stream Fwd / Prepare).  In place allowed.
@@ -127,6 +128,6 @@ cudaError_t stream_forward(const Ctx* c, int base, bool prepare, const void* in,
 // NTT of the lift of plain [npoly][N] (centred for the cipher base) per limb of `base`:
 // prepared (N^-1 2^W, k_stream LiftPrepare) or canonical eval (LiftFwd).
 cudaError_t stream_lift(const Ctx* c, int base, bool prepare, const uint64_t* m, void* out, uint64_t npoly,
-                        cudaStream_t s);
+                        cudaStream_t s, bool strip_out = false);
 
 }  // namespace ctb

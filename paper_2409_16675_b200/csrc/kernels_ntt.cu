@@ -209,6 +209,7 @@ struct StreamArgs {
   const uint64_t* plain;   // LiftPrepare: [npoly][N] values in [0, t)
   uint64_t in_stride, b_stride, add_stride, t_half;
   bool plain_fast;
+  bool strip_in;           // Inv / InvAdd: input in the thread-major chunk layout (see strip_out)
   bool strip_out;          // Fwd / Prepare: thread-major chunk layout (chunk c of transform thread t at
                            // 16-byte index c * THREADS + t) for internal operands whose consumer reads
                            // them the same way (k_site_product); contiguous warp stores, no transposition
@@ -304,7 +305,13 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
       mbar_wait(bar, phase);
       phase ^= 1;
       if constexpr (EVAL_IN) {
-        if constexpr (C::XPOSE_LD) {
+        constexpr bool SI = EvalVec<T, LOGN>::CONTIG && EvalVec<T, LOGN>::VEC * sizeof(T) == 16;
+        if (SI && a.strip_in) {  // thread-major chunks: contiguous, conflict-free staging reads
+          const uint4* s4 = reinterpret_cast<const uint4*>(stg);
+#pragma unroll
+          for (int c = 0; c < Sh::E * (int)sizeof(T) / 16; ++c)
+            unpack_chunk<T>(s4[c * Sh::THREADS + ntt_tid<LOGN>()], x + c * (16 / (int)sizeof(T)));
+        } else if constexpr (C::XPOSE_LD) {
           eval_xpose_apply<T, LOGN, GROUPS, true>(stg, gsm, [&](int c, const T* v) {
 #pragma unroll
             for (int i = 0; i < 16 / (int)sizeof(T); ++i) x[c * (16 / (int)sizeof(T)) + i] = v[i];
@@ -330,7 +337,13 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
         x[k] = r;
       }
     } else if constexpr (EVAL_IN) {
-      if constexpr (C::XPOSE_LD) {
+      constexpr bool SI = EvalVec<T, LOGN>::CONTIG && EvalVec<T, LOGN>::VEC * sizeof(T) == 16;
+      if (SI && a.strip_in) {
+        const uint4* s4 = reinterpret_cast<const uint4*>(a.in + ioff);
+#pragma unroll
+        for (int c = 0; c < Sh::E * (int)sizeof(T) / 16; ++c)
+          unpack_chunk<T>(__ldg(s4 + c * Sh::THREADS + ntt_tid<LOGN>()), x + c * (16 / (int)sizeof(T)));
+      } else if constexpr (C::XPOSE_LD) {
         eval_xpose_apply<T, LOGN, GROUPS>(a.in + ioff, gsm, [&](int c, const T* v) {
 #pragma unroll
           for (int i = 0; i < 16 / (int)sizeof(T); ++i) x[c * (16 / (int)sizeof(T)) + i] = v[i];
@@ -504,13 +517,17 @@ cudaError_t stream_forward(const Ctx* c, int base, bool prepare, const void* in,
 }
 
 cudaError_t stream_inv_add(const Ctx* c, int base, const void* in, void* out, const void* addend, uint64_t npoly,
-                           cudaStream_t s) {
+                           cudaStream_t s, bool strip_in) {
   const Base* b = &c->base[base];
   cudaError_t e = cudaSuccess;
   if (b->word == 4) {
-    CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::InvAdd>(b, sargs<uint32_t>(in, out, nullptr, 0, addend), npoly, s)));
+    auto a = sargs<uint32_t>(in, out, nullptr, 0, addend);
+    a.strip_in = strip_in;
+    CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::InvAdd>(b, a, npoly, s)));
   } else {
-    CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::InvAdd>(b, sargs<uint64_t>(in, out, nullptr, 0, addend), npoly, s)));
+    auto a = sargs<uint64_t>(in, out, nullptr, 0, addend);
+    a.strip_in = strip_in;
+    CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::InvAdd>(b, a, npoly, s)));
   }
   return e;
 }
@@ -786,6 +803,26 @@ extern "C" int ctb_eval_addend(const ctb_ctx_t* ctx, int base, const void* in, v
   return cuda_status(e, "ctb_eval_addend");
 }
 
+extern "C" int ctb_linear_addend(const ctb_ctx_t* ctx, int base, const void* in, void* out, uint64_t n_polys,
+                                 void* stream) {
+  if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
+  const Base* b = base_of(ctx, base);
+  if (!b || !in || !out) { set_error("ctb_linear_addend: bad context, base or buffer"); return ERR_ARG; }
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  if (b->word == 4) {
+    auto a = sargs<uint32_t>(in, out);
+    a.strip_out = true;
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::FwdNinv>(b, a, n_polys, s)));
+  } else {
+    auto a = sargs<uint64_t>(in, out);
+    a.strip_out = true;
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::FwdNinv>(b, a, n_polys, s)));
+  }
+  return cuda_status(e, "ctb_linear_addend");
+}
+
 extern "C" int ctb_prepare_operand(const ctb_ctx_t* ctx, int base, const void* in, void* out, uint64_t n_polys,
                                    void* stream) {
   if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
@@ -828,7 +865,7 @@ extern "C" int ctb_mul_prepared(const ctb_ctx_t* ctx, int base, const void* a, c
 }
 
 cudaError_t ctb::stream_lift(const Ctx* c, int base, bool prepare, const uint64_t* m, void* out, uint64_t npoly,
-                             cudaStream_t s) {
+                             cudaStream_t s, bool strip_out) {
   const Base* b = &c->base[base];
   // the plain base needs no centring: t = 0 mod t_j
   const uint64_t t_half = base == BASE_Q ? c->t_half : ~0ull;
@@ -836,12 +873,12 @@ cudaError_t ctb::stream_lift(const Ctx* c, int base, bool prepare, const uint64_
   cudaError_t e = cudaSuccess;
   if (b->word == 4) {
     StreamArgs<uint32_t> a = sargs<uint32_t>(nullptr, out);
-    a.plain = m; a.t_half = t_half; a.plain_fast = fast;
+    a.plain = m; a.t_half = t_half; a.plain_fast = fast; a.strip_out = strip_out;
     if (prepare) CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::LiftPrepare>(b, a, npoly, s)))
     else CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::LiftFwd>(b, a, npoly, s)))
   } else {
     StreamArgs<uint64_t> a = sargs<uint64_t>(nullptr, out);
-    a.plain = m; a.t_half = t_half; a.plain_fast = fast;
+    a.plain = m; a.t_half = t_half; a.plain_fast = fast; a.strip_out = strip_out;
     if (prepare) CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::LiftPrepare>(b, a, npoly, s)))
     else CTB_DISPATCH_LOGN_E(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::LiftFwd>(b, a, npoly, s)))
   }

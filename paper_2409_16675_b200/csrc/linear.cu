@@ -273,14 +273,18 @@ extern "C" int ctb_linear_online(const ctb_ctx_t* ctx, const void* ct_x, uint32_
   const int32_t* d_sx = csr + n_out + 1;
   const int32_t* d_sw = d_sx + n_sites;
   int rc;
+  // Every eval-domain operand of this call is internal (and the eval-form mask product comes from
+  // ctb_linear_addend), so they all use the thread-major chunk layout (k_stream strip_out /
+  // strip_in): contiguous warp stores in the forward transforms and conflict-free staging reads in
+  // the inverse ones, no transposition; the slot sums below are elementwise, layout-agnostic.
   // forward transforms of every ciphertext part, lifted+prepared masked plaintexts
-  if ((rc = ctb_ntt_forward(ctx, CTB_BASE_Q, ct_x, X, (uint64_t)n_x * 2, stream))) return rc;
-  if ((rc = ctb_ntt_forward(ctx, CTB_BASE_Q, ct_w, W, (uint64_t)n_w * 2, stream))) return rc;
-  if ((rc = ctb_lift_prepare(ctx, mx, MX, n_x, stream))) return rc;
-  if ((rc = ctb_lift_prepare(ctx, mw, MW, n_w, stream))) return rc;
+  if ((e = stream_forward(c, BASE_Q, false, ct_x, X, (uint64_t)n_x * 2, s, true)) != cudaSuccess) return cuda_status(e, "ctb_linear_online ntt");
+  if ((e = stream_forward(c, BASE_Q, false, ct_w, W, (uint64_t)n_w * 2, s, true)) != cudaSuccess) return cuda_status(e, "ctb_linear_online ntt");
+  if ((e = stream_lift(c, BASE_Q, true, mx, MX, n_x, s, true)) != cudaSuccess) return cuda_status(e, "ctb_linear_online lift");
+  if ((e = stream_lift(c, BASE_Q, true, mw, MW, n_w, s, true)) != cudaSuccess) return cuda_status(e, "ctb_linear_online lift");
   // plain side: residues mod t_j of mx (eval) and mw (prepared)
-  if ((e = stream_lift(c, BASE_T, false, mx, MXt, n_x, s)) != cudaSuccess) return cuda_status(e, "ctb_linear_online lift");
-  if ((e = stream_lift(c, BASE_T, true, mw, MWt, n_w, s)) != cudaSuccess) return cuda_status(e, "ctb_linear_online lift");
+  if ((e = stream_lift(c, BASE_T, false, mx, MXt, n_x, s, true)) != cudaSuccess) return cuda_status(e, "ctb_linear_online lift");
+  if ((e = stream_lift(c, BASE_T, true, mw, MWt, n_w, s, true)) != cudaSuccess) return cuda_status(e, "ctb_linear_online lift");
   {
     // cipher side: gather-accumulate into out_ct (eval domain), then INTT in place + mask product
     const uint32_t nv = (uint32_t)(N * w / 16);
@@ -299,7 +303,7 @@ extern "C" int ctb_linear_online(const ctb_ctx_t* ctx, const void* ct_x, uint32_
           (const PrimeTab<uint64_t>*)B.d_tabs, (int)L, (uint32_t)N, chunks);
     e = cudaGetLastError();
     if (e == cudaSuccess)
-      e = stream_inv_add(c, BASE_Q, out_ct, out_ct, maskprod_eval ? nullptr : maskprod, (uint64_t)n_out * 2, s);
+      e = stream_inv_add(c, BASE_Q, out_ct, out_ct, maskprod_eval ? nullptr : maskprod, (uint64_t)n_out * 2, s, true);
   }
   if (e != cudaSuccess) return cuda_status(e, "ctb_linear_online cipher");
   {
@@ -310,7 +314,7 @@ extern "C" int ctb_linear_online(const ctb_ctx_t* ctx, const void* ct_x, uint32_
                                                         (const PrimeTab<uint32_t>*)BT.d_tabs, (int)LT, (uint32_t)N,
                                                         chunks);
     e = cudaGetLastError();
-    if (e == cudaSuccess) e = stream_inv_add(c, BASE_T, PR, PR, nullptr, (uint64_t)n_out, s);
+    if (e == cudaSuccess) e = stream_inv_add(c, BASE_T, PR, PR, nullptr, (uint64_t)n_out, s, true);
   }
   if (e != cudaSuccess) return cuda_status(e, "ctb_linear_online plain");
   const uint64_t total = (uint64_t)n_out * N;

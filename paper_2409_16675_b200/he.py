@@ -144,7 +144,7 @@ class CiphertextBatch:
 
     def __init__(self, data: torch.Tensor, noise, backend_tag: str, cipher: RingParams):
         self.data = data
-        self.eval_form = None   # optional ctb_eval_addend form of `data` (server-side mask products)
+        self.eval_form = None   # optional ctb_linear_addend form of `data` (server-side mask products)
         self._nu = int(noise) if isinstance(noise, int) else [int(v) for v in noise]
         self.backend_tag = backend_tag
         self._cipher = cipher

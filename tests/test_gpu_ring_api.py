@@ -99,6 +99,30 @@ def test_eval_addend_is_scaled_forward_ntt():
     assert torch.equal(ev.to(torch.int64), expect)
 
 
+def test_linear_addend_is_eval_addend_in_thread_major_layout():
+    """ctb_linear_addend = ctb_eval_addend permuted into ctb_linear_online's internal layout: 16-byte
+    chunk c of transform thread t at chunk c * (N/16) + t, where thread t holds the 16-word eval
+    block f(t) (f rotates the low 6 thread bits: ntt.cuh pass_thread)."""
+    import torch
+    from paper_2409_16675_b200 import _lib
+    from paper_2409_16675_b200.device import RnsContext, _ptr, _stream
+    from paper_2409_16675_b200.params import default_he_params
+    P = default_he_params(4096)
+    ctx = RnsContext.get(P.n, P.cipher_ring.primes, P.plain_ring.primes)
+    p = torch.tensor(P.cipher_ring.primes, dtype=torch.int64, device="cuda").view(1, -1, 1)
+    x = (torch.randint(0, 1 << 62, (3, ctx.L, P.n), device="cuda") % p).to(torch.int32)
+    ev, lin = torch.empty_like(x), torch.empty_like(x)
+    _lib.check(ctx._lib.ctb_eval_addend(ctx._h, 0, _ptr(x), _ptr(ev), 3, _stream()), "ctb_eval_addend")
+    _lib.check(ctx._lib.ctb_linear_addend(ctx._h, 0, _ptr(x), _ptr(lin), 3, _stream()), "ctb_linear_addend")
+    threads = P.n // 16
+    t = torch.arange(threads)
+    f = (t & ~63) | ((t << 1) & 62) | ((t >> 5) & 1)
+    c = torch.arange(4)
+    src = (4 * f[None, :] + c[:, None]).reshape(-1)           # eval chunk of strip chunk c*threads + t
+    want = ev.view(3, ctx.L, P.n // 4, 4)[:, :, src.cuda()].reshape(3, ctx.L, P.n)
+    assert torch.equal(lin, want)
+
+
 def test_cpmul_host_pipeline_matches_device_path_threads():
     """RnsContext.cpmul_host (pinned host buffers, chunked H2D / CPMul / D2H on 3 streams, the
     bench's e2e leg) equals ctb_cpmul on device buffers, also from two threads at once."""
