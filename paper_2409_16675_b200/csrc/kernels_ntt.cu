@@ -558,6 +558,16 @@ __host__ __device__ constexpr bool enc_pk_smem() {
                  2 * (size_t)(1 << LOGN) * sizeof(T) <= 227 * 1024;
 }
 
+// Public key in the thread-major chunk layout (converted per call into a pool temporary) when it
+// is not staged in shared memory (64-bit limbs): contiguous warp loads.  -DCTB_ENC_PKSTRIP=0: direct.
+#ifndef CTB_ENC_PKSTRIP
+#define CTB_ENC_PKSTRIP 1
+#endif
+template <typename T, int LOGN>
+__host__ __device__ constexpr bool enc_pk_strip() {
+  return CTB_ENC_PKSTRIP && !enc_pk_smem<T, LOGN>() && EvalVec<T, LOGN>::CONTIG && EvalVec<T, LOGN>::VEC * sizeof(T) == 16;
+}
+
 template <typename T, int LOGN, bool SMEM_TW>
 __global__ void __launch_bounds__(NttShape<LOGN>::THREADS * enc_groups<T, LOGN>(),
                                   enc_groups<T, LOGN>() == 4 ? 1 : (enc_groups<T, LOGN>() == 2 ? 2 : NttShape<LOGN>::MINB))
@@ -570,8 +580,8 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
   constexpr int GROUP_WORDS = Ex::WORDS + Sh::N;
   constexpr bool PKSM = enc_pk_smem<T, LOGN>() && SMEM_TW;
   using EV = EvalVec<T, LOGN>;
-  constexpr bool ENC_XPOSE = !PKSM && sizeof(T) == 4 && CTB_EVAL_XPOSE && EV::VEC == Strip<T, LOGN>::VEC &&
-                             eval_xpose_ok<T, LOGN>(Ex::WORDS);
+  constexpr bool ENC_XPOSE = !PKSM && !enc_pk_strip<T, LOGN>() && sizeof(T) == 4 && CTB_EVAL_XPOSE &&
+                             EV::VEC == Strip<T, LOGN>::VEC && eval_xpose_ok<T, LOGN>(Ex::WORDS);
   static_assert(!PKSM || (EV::VEC == Strip<T, LOGN>::VEC && GROUPS >= 2), "key strips need contiguous eval chunks");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
@@ -657,6 +667,8 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
       for (int i = 0; i < EV::CHUNKS; ++i) {
         T v[EV::VEC];
         if constexpr (PKSM) ks.load_chunk(i, v);
+        else if constexpr (enc_pk_strip<T, LOGN>())
+          unpack_chunk<T>(__ldg(reinterpret_cast<const uint4*>(kp) + i * Sh::THREADS + ntt_tid<LOGN>()), v);
         else EV::load(kp, i, v);
         if constexpr (EV::VEC == Strip<T, LOGN>::VEC) {
           T uu[EV::VEC];
@@ -981,11 +993,26 @@ static cudaError_t launch_encrypt(const Ctx* c, const Base* b, const uint64_t* m
   const int L = b->size();
   if (batch == 0) return cudaSuccess;
   const int threads = Sh::THREADS * GROUPS;
+  const void* pk = pkprep;
+  void* tmp = nullptr;
+  if constexpr (enc_pk_strip<T, LOGN>()) {
+    cudaError_t e = c->pool ? cudaMallocFromPoolAsync(&tmp, 2 * (size_t)L * Sh::N * sizeof(T), c->pool, s)
+                            : cudaMallocAsync(&tmp, 2 * (size_t)L * Sh::N * sizeof(T), s);
+    if (e != cudaSuccess) return e;
+    k_eval_to_strip<T, LOGN><<<(unsigned)(2 * L), Sh::THREADS, 0, s>>>((const T*)pkprep, (T*)tmp);
+    if ((e = cudaGetLastError()) != cudaSuccess) { cudaFreeAsync(tmp, s); return e; }
+    pk = tmp;
+  }
   uint32_t grid = persistent_grid((const void*)kern, threads, smem);
   const uint64_t max_grid = (batch + GROUPS - 1) / GROUPS * (uint64_t)L;
   grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(grid / L * L, (uint64_t)L), max_grid);
-  return launch_kernel_grid(kern, grid, threads, smem, s, m, draws, (const T*)pkprep, (T*)out,
-                            (const PrimeTab<T>*)b->d_tabs, L, c->t_half, (uint32_t)batch);
+  cudaError_t e = launch_kernel_grid(kern, grid, threads, smem, s, m, draws, (const T*)pk, (T*)out,
+                                     (const PrimeTab<T>*)b->d_tabs, L, c->t_half, (uint32_t)batch);
+  if (tmp) {
+    const cudaError_t f = cudaFreeAsync(tmp, s);
+    if (e == cudaSuccess) e = f;
+  }
+  return e;
 }
 
 extern "C" int ctb_encrypt(const ctb_ctx_t* ctx, const uint64_t* m, const int8_t* draws, const void* pkprep,

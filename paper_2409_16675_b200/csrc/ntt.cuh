@@ -947,6 +947,23 @@ __device__ __forceinline__ void eval_xpose_apply(const T* src, T* img, F&& f) {
   }
 }
 
+// Eval layout ([npoly][N], e.g. prepared keys) -> thread-major chunk layout: chunk c of transform
+// thread t at 16-byte index c * THREADS + t.  The eval layout gives thread t the block f(t)
+// (ntt.cuh eval_xpose_*), so direct eval-layout key loads put every lane of a warp in its own
+// 128-byte line; in this layout each warp load is 512 contiguous bytes.  One block per polynomial.
+template <typename T, int LOGN>
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS) k_eval_to_strip(const T* __restrict__ in, T* __restrict__ out) {
+  using Sh = NttShape<LOGN>;
+  using EV = EvalVec<T, LOGN>;
+  const T* src = in + (size_t)blockIdx.x * Sh::N;
+  uint4* dst = reinterpret_cast<uint4*>(out + (size_t)blockIdx.x * Sh::N);
+#pragma unroll
+  for (int i = 0; i < EV::CHUNKS; ++i) {
+    T v[EV::VEC];
+    EV::load(src, i, v);
+    dst[i * Sh::THREADS + threadIdx.x] = pack_chunk<T>(v);
+  }
+}
 // Load a PrimeTab into registers (uniform across the CTA).
 template <typename T>
 struct PrimeRegs {

@@ -699,23 +699,6 @@ k_relin_accum(const T* ct3, int ct_parts, const uint32_t* digits, const T* keypr
   }
 }
 
-// Prepared keys (eval layout, [npoly][N]) -> thread-major chunk layout: chunk c of transform
-// thread t at 16-byte index c * THREADS + t.  The eval layout gives thread t the block f(t)
-// (ntt.cuh eval_xpose_*), so direct eval-layout key loads put every lane of a warp in its own
-// 128-byte line; in this layout each warp load is 512 contiguous bytes.  One block per polynomial.
-template <typename T, int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::THREADS) k_eval_to_strip(const T* __restrict__ in, T* __restrict__ out) {
-  using Sh = NttShape<LOGN>;
-  using EV = EvalVec<T, LOGN>;
-  const T* src = in + (size_t)blockIdx.x * Sh::N;
-  uint4* dst = reinterpret_cast<uint4*>(out + (size_t)blockIdx.x * Sh::N);
-#pragma unroll
-  for (int i = 0; i < EV::CHUNKS; ++i) {
-    T v[EV::VEC];
-    EV::load(src, i, v);
-    dst[i * Sh::THREADS + threadIdx.x] = pack_chunk<T>(v);
-  }
-}
 // Relinearisation keys in the thread-major layout (per call: a stream-ordered temporary, D x 2 x L
 // polynomials, negligible beside the D x L digit transforms per slot).  -DCTB_RELIN_KSTRIP=0: direct.
 #ifndef CTB_RELIN_KSTRIP
