@@ -210,6 +210,7 @@ struct StreamArgs {
   uint64_t in_stride, b_stride, add_stride, t_half;
   bool plain_fast;
   bool strip_in;           // Inv / InvAdd: input in the thread-major chunk layout (see strip_out)
+  bool bprep_strip;        // MulPrepared: the prepared operand in the thread-major chunk layout
   bool strip_out;          // Fwd / Prepare: thread-major chunk layout (chunk c of transform thread t at
                            // 16-byte index c * THREADS + t) for internal operands whose consumer reads
                            // them the same way (k_site_product); contiguous warp stores, no transposition
@@ -443,7 +444,16 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
       } else {
         const T* pb = a.bprep + ((size_t)b * a.b_stride * L + limb) * (size_t)Sh::N;
         using EV = EvalVec<T, LOGN>;
-        if constexpr (C::XPOSE_LD) {
+        constexpr bool SB = EV::CONTIG && EV::VEC * sizeof(T) == 16;
+        if (SB && a.bprep_strip) {
+#pragma unroll
+          for (int i = 0; i < EV::CHUNKS; ++i) {
+            T v[EV::VEC];
+            unpack_chunk<T>(__ldg(reinterpret_cast<const uint4*>(pb) + i * Sh::THREADS + ntt_tid<LOGN>()), v);
+#pragma unroll
+            for (int c = 0; c < EV::VEC; ++c) x[i * EV::VEC + c] = mont_mul(x[i * EV::VEC + c], v[c], pr.p, pr.pinv);
+          }
+        } else if constexpr (C::XPOSE_LD) {
           eval_xpose_apply<T, LOGN, GROUPS>(pb, gsm, [&](int i, const T* v) {
 #pragma unroll
             for (int c = 0; c < EV::VEC; ++c) x[i * EV::VEC + c] = mont_mul(x[i * EV::VEC + c], v[c], pr.p, pr.pinv);
@@ -851,6 +861,33 @@ extern "C" int ctb_prepare_operand(const ctb_ctx_t* ctx, int base, const void* i
   return cuda_status(e, "ctb_prepare_operand");
 }
 
+// MulPrepared; a broadcast prepared operand (b_stride 0: a key multiplying every item, e.g. the
+// secret key of decryption) is first converted into the thread-major chunk layout (pool temporary,
+// L polynomials) so every item reads it with contiguous warp loads.
+template <typename T, int LOGN>
+static cudaError_t launch_mul_prepared(const Ctx* c, const Base* b, StreamArgs<T> a, uint64_t npoly, cudaStream_t s) {
+  using Sh = NttShape<LOGN>;
+  using EV = EvalVec<T, LOGN>;
+  void* tmp = nullptr;
+  if constexpr (EV::CONTIG && EV::VEC * sizeof(T) == 16 && CTB_EVAL_XPOSE) {
+    if (a.b_stride == 0 && npoly > 1) {
+      const size_t bytes = (size_t)b->size() * Sh::N * sizeof(T);
+      cudaError_t e = c->pool ? cudaMallocFromPoolAsync(&tmp, bytes, c->pool, s) : cudaMallocAsync(&tmp, bytes, s);
+      if (e != cudaSuccess) return e;
+      k_eval_to_strip<T, LOGN><<<(unsigned)b->size(), Sh::THREADS, 0, s>>>(a.bprep, (T*)tmp);
+      if ((e = cudaGetLastError()) != cudaSuccess) { cudaFreeAsync(tmp, s); return e; }
+      a.bprep = (const T*)tmp;
+      a.bprep_strip = true;
+    }
+  }
+  cudaError_t e = launch_stream<T, LOGN, StreamOp::MulPrepared>(b, a, npoly, s);
+  if (tmp) {
+    const cudaError_t f = cudaFreeAsync(tmp, s);
+    if (e == cudaSuccess) e = f;
+  }
+  return e;
+}
+
 extern "C" int ctb_mul_prepared_strided(const ctb_ctx_t* ctx, int base, const void* a, uint64_t a_stride,
                                         const void* bprep, uint64_t b_stride, const void* addend,
                                         uint64_t add_stride, void* out, uint64_t n_polys, void* stream) {
@@ -864,9 +901,9 @@ extern "C" int ctb_mul_prepared_strided(const ctb_ctx_t* ctx, int base, const vo
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
   if (b->word == 4) {
-    CTB_DISPATCH_LOGN(c->logn, e = (launch_stream<uint32_t, LOGN, StreamOp::MulPrepared>(b, sargs<uint32_t>(a, out, bprep, b_stride, addend, a_stride, add_stride), n_polys, s)));
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_mul_prepared<uint32_t, LOGN>(c, b, sargs<uint32_t>(a, out, bprep, b_stride, addend, a_stride, add_stride), n_polys, s)));
   } else {
-    CTB_DISPATCH_LOGN(c->logn, e = (launch_stream<uint64_t, LOGN, StreamOp::MulPrepared>(b, sargs<uint64_t>(a, out, bprep, b_stride, addend, a_stride, add_stride), n_polys, s)));
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_mul_prepared<uint64_t, LOGN>(c, b, sargs<uint64_t>(a, out, bprep, b_stride, addend, a_stride, add_stride), n_polys, s)));
   }
   return cuda_status(e, "ctb_mul_prepared");
 }
