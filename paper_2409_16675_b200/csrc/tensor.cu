@@ -563,6 +563,10 @@ __global__ void __launch_bounds__(256) k_relin_digits(const TQ* ct3, uint32_t* d
 #ifndef CTB_RELIN_XPOSE
 #define CTB_RELIN_XPOSE 0
 #endif
+// L2 prefetch of the next digit polynomial while the current one transforms
+#ifndef CTB_RELIN_L2PF
+#define CTB_RELIN_L2PF 1
+#endif
 template <typename T, int LOGN>
 struct RelinCfg {
   using Sh = NttShape<LOGN>;
@@ -637,6 +641,13 @@ k_relin_accum(const T* ct3, int ct_parts, const uint32_t* digits, const T* keypr
         }
       } else {
         const uint32_t* src = digits + ((size_t)b * D + d) * N + cb;
+        // the next digit (or the next item's first) towards L2: 32-bit limbs -3.5% (13.49 -> 13.01 ms per
+        // cfg4 batch); neutral-to-slower at 64-bit limbs
+        if (CTB_RELIN_L2PF && sizeof(T) == 4 && threadIdx.x == 0) {
+          const uint32_t nb = d + 1 < D ? b : b + nslots;
+          const int nd = d + 1 < D ? d + 1 : 0;
+          if (nb < batch) bulk_prefetch_l2(digits + ((size_t)nb * D + nd) * N, (uint32_t)(N * 4));
+        }
 #pragma unroll
         for (int j = 0; j < Sh::E; ++j) x[j] = pr.reduce_digit(__ldg(src + coef_off<LOGN>(j)));  // any u32 -> [0,p)
       }
@@ -757,10 +768,21 @@ static cudaError_t launch_relin_accum(const Ctx* c, const void* ct3, int ct_part
 #ifndef CTB_SITE_G2
 #define CTB_SITE_G2 0
 #endif
+// site products keep h0 in a second strip up to this ring degree (above it, h0 is recomputed from
+// re-read operands -- cheap since the operands are read in the thread-major layout)
+#ifndef CTB_SITE_TWO_MAXLOGN
+#define CTB_SITE_TWO_MAXLOGN 11  // N = 4096: one strip, 3 CTAs per SM (-3.3% vs two strips, 2 CTAs)
+#endif
 template <int LOGN>
 __host__ __device__ constexpr int site_groups() { return CTB_SITE_G2 && LOGN == 13 ? 2 : 1; }
 template <int LOGN>
-__host__ __device__ constexpr int site_strips() { return LOGN <= 12 ? 2 : 1; }
+__host__ __device__ constexpr int site_strips() { return LOGN <= CTB_SITE_TWO_MAXLOGN ? 2 : 1; }
+// resident CTAs per SM the site-product registers are capped for (one strip: 3 CTAs of 256 threads fit
+// the shared memory at N = 4096)
+template <int LOGN>
+__host__ __device__ constexpr int site_minb() {
+  return site_groups<LOGN>() == 2 ? 1 : (site_strips<LOGN>() == 1 && NttShape<LOGN>::THREADS == 256 ? 3 : NttShape<LOGN>::MINB);
+}
 // 32-bit words per site group (exchange image + strips), rounded to 16 bytes
 template <int LOGN, int GROUPS>
 __host__ __device__ constexpr int site_group_words() {
@@ -778,7 +800,7 @@ __host__ __device__ constexpr bool site_strip() {
 }
 
 template <int LOGN, bool SMEM_TW>
-__global__ void __launch_bounds__(NttShape<LOGN>::THREADS * site_groups<LOGN>(), site_groups<LOGN>() == 2 ? 1 : NttShape<LOGN>::MINB)
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS * site_groups<LOGN>(), site_minb<LOGN>())
 k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict__ sx,
                const int32_t* __restrict__ sw, uint32_t* H, const PrimeTab<uint32_t>* __restrict__ tabs, int K,
                uint32_t nsite) {
