@@ -31,22 +31,30 @@ namespace ctb {
 // one thread per 16-byte vector of one (slot, limb), sites two at a time so a thread
 // has 12 independent 16-byte loads in flight -- this phase is a gather over HBM/L2 and
 // lives on memory-level parallelism, while the transforms run in k_stream (InvAdd).
+// resident k_lin_accum blocks per SM of the grid-stride launch
+#ifndef CTB_LIN_BLOCKS_PER_SM
+#define CTB_LIN_BLOCKS_PER_SM 4
+#endif
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_lin_accum(const T* __restrict__ X, const T* __restrict__ W, const T* __restrict__ MXp, const T* __restrict__ MWp,
             const int32_t* __restrict__ slot_ptr, const int32_t* __restrict__ site_x,
             const int32_t* __restrict__ site_w, const T* __restrict__ init, T* __restrict__ acc,
-            const PrimeTab<T>* __restrict__ tabs, int L, uint32_t n, uint32_t chunks) {
+            const PrimeTab<T>* __restrict__ tabs, int L, uint32_t n, uint32_t chunks, uint64_t units) {
   constexpr int VEC = 16 / sizeof(T);
   union V { uint4 u; T t[VEC]; };
-  uint32_t bid = blockIdx.x;
+  // grid-stride over (slot, limb, chunk) units: a few resident blocks per SM instead of one short
+  // block per unit (the gather is latency-bound; block turnover costs issue slots)
+#pragma unroll 1
+  for (uint64_t unit = blockIdx.x; unit < units; unit += gridDim.x) {
+  uint32_t bid = (uint32_t)unit;
   const uint32_t chunk = bid % chunks;
   bid /= chunks;
   const int limb = (int)(bid % L);
   const uint32_t slot = bid / L;
   const uint32_t nv = n / VEC;
   const uint32_t v = chunk * blockDim.x + threadIdx.x;
-  if (v >= nv) return;
+  if (v >= nv) continue;
   const T p = tabs[limb].p, p2 = 2 * p, pinv = tabs[limb].pinv;
   const size_t LN = (size_t)L * n;
   const uint4* X4 = reinterpret_cast<const uint4*>(X + (size_t)limb * n) + v;
@@ -104,6 +112,7 @@ k_lin_accum(const T* __restrict__ X, const T* __restrict__ W, const T* __restric
   for (int c = 0; c < VEC; ++c) { o0.t[c] = a0[c]; o1.t[c] = a1[c]; }
   A4[0] = o0.u;
   A4[part4] = o1.u;
+  }
 }
 
 // Plain side over the plain primes (u32): MXt canonical eval [n_x][LT][N], MWtp prepared;
@@ -291,16 +300,17 @@ extern "C" int ctb_linear_online(const ctb_ctx_t* ctx, const void* ct_x, uint32_
     const uint32_t chunks = (nv + 255) / 256;
     const uint64_t blocks = (uint64_t)n_out * L * chunks;
     if (blocks >= (1ull << 31)) { set_error("ctb_linear_online: job too large"); return ERR_ARG; }
+    const unsigned grid = (unsigned)std::min<uint64_t>(blocks, (uint64_t)grid_stride(blocks * 256, CTB_LIN_BLOCKS_PER_SM));
     if (B.word == 4)
-      k_lin_accum<uint32_t><<<(unsigned)blocks, 256, 0, s>>>((const uint32_t*)X, (const uint32_t*)W,
+      k_lin_accum<uint32_t><<<grid, 256, 0, s>>>((const uint32_t*)X, (const uint32_t*)W,
           (const uint32_t*)MX, (const uint32_t*)MW, d_ptr, d_sx, d_sw,
           maskprod_eval ? (const uint32_t*)maskprod : nullptr, (uint32_t*)out_ct,
-          (const PrimeTab<uint32_t>*)B.d_tabs, (int)L, (uint32_t)N, chunks);
+          (const PrimeTab<uint32_t>*)B.d_tabs, (int)L, (uint32_t)N, chunks, blocks);
     else
-      k_lin_accum<uint64_t><<<(unsigned)blocks, 256, 0, s>>>((const uint64_t*)X, (const uint64_t*)W,
+      k_lin_accum<uint64_t><<<grid, 256, 0, s>>>((const uint64_t*)X, (const uint64_t*)W,
           (const uint64_t*)MX, (const uint64_t*)MW, d_ptr, d_sx, d_sw,
           maskprod_eval ? (const uint64_t*)maskprod : nullptr, (uint64_t*)out_ct,
-          (const PrimeTab<uint64_t>*)B.d_tabs, (int)L, (uint32_t)N, chunks);
+          (const PrimeTab<uint64_t>*)B.d_tabs, (int)L, (uint32_t)N, chunks, blocks);
     e = cudaGetLastError();
     if (e == cudaSuccess)
       e = stream_inv_add(c, BASE_Q, out_ct, out_ct, maskprod_eval ? nullptr : maskprod, (uint64_t)n_out * 2, s, true);
