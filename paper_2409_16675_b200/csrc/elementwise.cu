@@ -40,7 +40,7 @@ template <typename T>
 __global__ void k_rns_elementwise(int op, const T* a, const T* b, T* out, LimbConsts<T> c, int L, uint32_t n,
                                   uint64_t total) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
-    const int l = (int)((i / n) % L);
+    const int l = (int)((i >> pow2_shift(n)) % L);
     const T p = c.p[l];
     T r;
     if (op == 0) r = add_mod(a[i], b[i], p);
@@ -56,8 +56,8 @@ __global__ void k_rns_from_small(const int64_t* in, T* out, LimbConsts<T> c, int
   // total = n_polys * L * N; output [poly][L][N]
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t poly = i / ((uint64_t)L * n);
-    const int l = (int)((i / n) % L);
-    const int64_t v = in[poly * n + i % n];
+    const int l = (int)((i >> pow2_shift(n)) % L);
+    const int64_t v = in[poly * n + (i & (n - 1))];
     const uint64_t mag = v < 0 ? (uint64_t)(-(v + 1)) + 1 : (uint64_t)v;
     T r = reduce_word<T>(mag, c, l);
     if (v < 0) r = sub_mod((T)0, r, c.p[l]);
@@ -70,9 +70,9 @@ __global__ void k_lift_plain(const uint64_t* m, T* out, LimbConsts<T> c, int L, 
                              uint64_t total) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t poly = i / ((uint64_t)L * n);
-    const int l = (int)((i / n) % L);
+    const int l = (int)((i >> pow2_shift(n)) % L);
     const T p = c.p[l];
-    const uint64_t v = m[poly * n + i % n];
+    const uint64_t v = m[poly * n + (i & (n - 1))];
     T r = reduce_word<T>(v, c, l);
     if (v > t_half) r = sub_mod(r, c.tm[l], p);
     out[i] = csub(shoup_mul<T>(r, c.s[l], c.sq[l], p), p);

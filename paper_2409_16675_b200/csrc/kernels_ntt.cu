@@ -50,7 +50,7 @@ __global__ void k_pointwise(const T* a, const T* b, T* out, const PrimeTab<T>* _
                             int L, uint32_t n, uint64_t total) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    const int limb = (int)((i / n) % L);
+    const int limb = (int)((i >> pow2_shift(n)) % L);
     const PrimeTab<T>* t = tabs + limb;
     const T p = t->p, pinv = t->pinv;
     T v = mont_mul(a[i], b[i], p, pinv);       // a b R^-1

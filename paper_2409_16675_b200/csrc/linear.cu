@@ -169,7 +169,7 @@ k_lin_accum_plain(const uint32_t* __restrict__ MXt, const uint32_t* __restrict__
 __global__ void k_plain_crt(const uint32_t* res, uint64_t* out, int LT, uint32_t n, uint32_t p0, uint32_t p1,
                             uint32_t cinv, uint32_t cinv_q, uint32_t p1_oneq, uint64_t total) {
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t poly = g / n, i = g % n;
+    const uint64_t poly = g >> pow2_shift(n), i = g & (n - 1);
     const uint32_t r0 = res[(poly * LT) * n + i];
     if (LT == 1) { out[g] = r0; continue; }
     const uint32_t r1 = res[(poly * LT + 1) * n + i];
@@ -187,7 +187,7 @@ __global__ void k_slot_sum(const T* in, const int32_t* __restrict__ slot_ptr, co
   const uint64_t per = (uint64_t)parts * L * n;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t o = g / per, r = g % per;
-    const int limb = (int)((r / n) % L);
+    const int limb = (int)((r >> pow2_shift(n)) % L);
     const T p = tabs[limb].p;
     T acc = 0;
     for (int s = slot_ptr[o]; s < slot_ptr[o + 1]; ++s) acc = add_mod(acc, in[(uint64_t)idx[s] * per + r], p);

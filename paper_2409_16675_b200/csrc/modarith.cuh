@@ -36,6 +36,10 @@ __device__ __forceinline__ T csub(T x, T y) {
   return min(x - y, x);  // IMNMX
 }
 
+// log2 of a power of two (the ring degree): index splits by shift and mask instead of a 64-bit
+// division by a runtime value
+__device__ __forceinline__ int pow2_shift(uint64_t n) { return __ffsll((long long)n) - 1; }
+
 // Shoup: a * w mod p, lazily in [0, 2p), for any a < 2^W.
 template <typename T>
 __device__ __forceinline__ T shoup_mul(T a, T w, T wq, T p) {

@@ -105,7 +105,7 @@ __global__ void k_decrypt_round(const T* v, uint64_t* out, const QConsts<T>* __r
   const int L = c.mrc.L;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
        g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t b = g / n, i = g % n;
+    const uint64_t b = g >> pow2_shift(n), i = g & (n - 1);  // n = ring degree (power of two)
     T r[MAX_MRC], a[MAX_MRC];
     for (int l = 0; l < L; ++l) {
       const T q = c.mrc.q[l];
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(256) k_decrypt_round_lazy(const uint32_t* v, u
   const int L = LC ? LC : c.L;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
        g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t b = g / n, i = g % n;
+    const uint64_t b = g >> pow2_shift(n), i = g & (n - 1);  // n = ring degree (power of two)
     uint32_t a[DEC_MAXQ];
 #pragma unroll
     for (int j = 0; j < (LC ? LC : DEC_MAXQ); ++j) {
@@ -197,7 +197,7 @@ __global__ void k_rns_to_pos(const T* x, uint64_t* out, const QConsts<T>* __rest
   const int L = m.L;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
        g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t b = g / n, i = g % n;
+    const uint64_t b = g >> pow2_shift(n), i = g & (n - 1);  // n = ring degree (power of two)
     T r[MAX_MRC], a[MAX_MRC];
     for (int l = 0; l < L; ++l) r[l] = x[(b * L + l) * n + i];
     mrc_digits(m, r, a);
@@ -220,7 +220,7 @@ __global__ void k_pos_to_rns(const uint64_t* in, T* x, const QConsts<T>* __restr
   const int L = c.mrc.L, W = c.W;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
        g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t b = g / n, i = g % n;
+    const uint64_t b = g >> pow2_shift(n), i = g & (n - 1);  // n = ring degree (power of two)
     uint64_t words[8];
     for (int w = 0; w < W; ++w) words[w] = in[g * W + w];
     for (int l = 0; l < L; ++l) {

@@ -42,8 +42,8 @@ __global__ void k_sample_draws(int8_t* out, uint64_t seed, uint64_t first_poly, 
   constexpr uint32_t n = 1u << LOGN;
   const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t poly = g / n;
-    const uint32_t pos = (uint32_t)(g % n);
+    const uint64_t poly = g >> pow2_shift(n);
+    const uint32_t pos = (uint32_t)(g & (n - 1));
     const uint32_t i = (uint32_t)draw_coef<LOGN>((int)pos);
     const uint64_t gp = first_poly + poly;
     const uint4 r = Philox4x32::run(make_uint4(i, (uint32_t)gp, (uint32_t)(gp >> 32), 0x43544232u), key);
@@ -67,8 +67,8 @@ template <int LOGN>
 __global__ void k_draws_layout(const int8_t* in, int8_t* out, uint64_t total) {
   constexpr uint32_t n = 1u << LOGN;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t row = g / n;   // poly * 3 + kind
-    const uint32_t pos = (uint32_t)(g % n);
+    const uint64_t row = g >> pow2_shift(n);   // poly * 3 + kind
+    const uint32_t pos = (uint32_t)(g & (n - 1));
     out[g] = in[row * n + (uint32_t)draw_coef<LOGN>((int)pos)];
   }
 }
