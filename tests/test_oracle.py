@@ -104,6 +104,30 @@ def test_ccmul_relin_512_matches_reference(golden):
     assert digest(H.decrypt(P, rel, keys["s"])) == g["dec"]
 
 
+def test_known_answer_products_512():
+    """Reference tests/test_he.py:78-87 (Enc(3)*Enc(5) decrypts to 15) and the CPMul
+    negacyclic wrap: Enc(x^(n-1)) * x = -1, i.e. t-1 in coefficient 0."""
+    P = H.default_params(512, plain_bits=17)
+    keys = H.keygen(P, 7)
+    rng = np.random.default_rng(8)
+
+    def mono(v, deg):
+        m = np.zeros(P.n, dtype=np.uint64)
+        m[deg] = v
+        return m
+
+    three = H.encrypt(P, mono(3, 0), keys["pk"], rng)
+    five = H.encrypt(P, mono(5, 0), keys["pk"], rng)
+    out = H.decrypt(P, H.cc_mul(P, three, five, keys["relin"]), keys["s"])
+    assert int(out[0]) == 15 and not out[1:].any()
+    top = H.encrypt(P, mono(1, P.n - 1), keys["pk"], rng)
+    out = H.decrypt(P, H.cp_mul(P, top, mono(1, 1)), keys["s"])
+    assert int(out[0]) == P.t - 1 and not out[1:].any()
+    # CCAdd of the two fresh ciphertexts decrypts to the plain sum
+    out = H.decrypt(P, H._add(P, three, five), keys["s"])
+    assert int(out[0]) == 8 and not out[1:].any()
+
+
 @pytest.mark.slow
 def test_ccmul_4096_matches_reference(golden):
     P = H.default_params(4096)
