@@ -178,3 +178,26 @@ def test_fp64_butterflies_extreme_inputs(logn):
     assert np.array_equal(back, a)
     got = _np(ctx.ring_mul(_t(a, ctx.dtype()), _t(a[::-1].copy(), ctx.dtype())))
     assert np.array_equal(got, R.ring_mul_rns(a, a[::-1].copy(), primes))
+
+
+@pytest.mark.parametrize("which", ["p4096", "p8192"])
+def test_cpmul_empty_and_maximum_inputs(which):
+    """Edge cases: an empty batch is a no-op (reference cp_mul is per-object, so the batched
+    boundary's B=0 must not launch or fault), and every residue at q_i - 1 with every plaintext
+    coefficient at t - 1 (largest operands of each modular product) matches the oracle."""
+    import torch
+    from paper_2409_16675_b200.device import RnsContext
+    P = H.default_params(4096) if which == "p4096" else H.p8192_params()
+    ctx = RnsContext.get(P.n, P.q_primes, P.t_primes)
+    L = len(P.q_primes)
+    empty = torch.empty((0, 2, L, P.n), dtype=ctx.dtype(), device="cuda")
+    out = ctx.cpmul(empty, torch.empty((0, P.n), dtype=torch.int64, device="cuda"))
+    assert out.shape == (0, 2, L, P.n)
+    ct = np.stack([np.stack([np.full(P.n, q - 1, dtype=np.uint64) for q in P.q_primes])] * 2)[None]
+    pts = [np.full(P.n, P.t - 1, dtype=np.uint64), np.full(P.n, P.t // 2 + 1, dtype=np.uint64)]
+    for pt in pts:
+        got = _np(ctx.cpmul(_t(ct, ctx.dtype()), _t(pt[None], torch.int64)))
+        assert np.array_equal(got[0], H.cp_mul(P, ct[0], pt))
+        fa = ctx.ntt_forward(_t(ct[:, 0], ctx.dtype()))
+        back = _np(ctx.ntt_inverse(fa))
+        assert np.array_equal(back, ct[:, 0])
