@@ -113,3 +113,27 @@ def test_trainer_fixture_matches_plain_oracle():
                 exp = a * int(b)
             assert np.array_equal(exp, out), (tag, ci, m)
     assert seen == {"conv_forward", "conv_pairwise", "fc", "outer", "affine"}
+
+
+def test_packing_error_behaviour():
+    """Reference tests/test_packing.py:99-103 (wrap detection) and :192-196 (infeasible
+    budget): the same exception classes surface from the device-path packer."""
+    import torch
+    from paper_2409_16675_b200.params import RingParams
+    h = 4
+    tiny = h * (2 * h - 1) + h - 1
+    with pytest.raises(packing.InfeasibleWindowError):
+        packing.choose_tiles(packing.ConvShape(8, 8, h, 0), tiny)
+    with pytest.raises(packing.PackingError):
+        shape = packing.ConvShape(7, 7, 3, 2)
+        plan = packing.plan_correlated(shape, 256, window=(7, 7))
+        ring64 = RingParams(64, 17)
+        packing.pack_input_batch(torch.ones((1, 7, 7), dtype=torch.int64), plan, ring64)
+    P = default_he_params(4096)
+    plan = packing.plan_correlated(packing.ConvShape(8, 8, 3, 1), 4096)
+    with pytest.raises(packing.PackingError):  # wrong input extent
+        packing.pack_input_batch(torch.ones((1, 9, 8), dtype=torch.int64), plan, P.plain_ring)
+    with pytest.raises(packing.PackingError):  # wrong kernel extent
+        packing.pack_kernel_batch(torch.ones((1, 2, 2), dtype=torch.int64), plan, P.plain_ring)
+    with pytest.raises(packing.PackingError):  # fc input wider than the ring (packing.py:557-558)
+        packing.pack_fc_input_batch(torch.ones((1, 4097), dtype=torch.int64), P.plain_ring)
