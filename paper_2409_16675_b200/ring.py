@@ -230,23 +230,59 @@ class RingElem:
 
 # --------------------------------------------------------------------------- arithmetic
 
+def _values_to_rns(ctx: RnsContext, values: torch.Tensor) -> torch.Tensor:
+    """[N] canonical values of a modulus < 2^63 -> [1, L, N] residues (exact positional conversion)."""
+    wc = ctx._lib.ctb_ctx_pos_words(ctx._h)
+    words = values.view(-1, 1)
+    if wc != 1:
+        words = torch.cat([words, torch.zeros((values.numel(), wc - 1), dtype=torch.int64, device=values.device)], 1)
+    out = torch.empty((1, ctx.L, values.numel()), dtype=ctx.dtype(), device="cuda")
+    _lib.check(ctx._lib.ctb_pos_to_rns(ctx._h, _ptr(words.contiguous()), _ptr(out), 1, _stream()), "ctb_pos_to_rns")
+    return out
+
+
+def _rns_to_values(ctx: RnsContext, res: torch.Tensor) -> torch.Tensor:
+    wc = ctx._lib.ctb_ctx_pos_words(ctx._h)
+    n = res.shape[-1]
+    words = torch.empty((n, wc), dtype=torch.int64, device="cuda")
+    _lib.check(ctx._lib.ctb_rns_to_pos(ctx._h, _ptr(res.contiguous()), _ptr(words), 1, _stream()), "ctb_rns_to_pos")
+    return words[:, 0].contiguous()
+
+
+def _as_residues(ctx: RnsContext, a: RingElem) -> torch.Tensor:
+    """Value tensor of a ring with modulus < 2^63 viewed as [1, L, N] residues: a single prime
+    (>= 2^30, so the context's words are 64-bit) is its own residue; several primes go through
+    the exact positional conversion."""
+    if ctx.L == 1:
+        return a.data.view(1, 1, -1).to(ctx.dtype())
+    return _values_to_rns(ctx, a.data)
+
+
+def _from_residues(ctx: RnsContext, res: torch.Tensor) -> torch.Tensor:
+    if ctx.L == 1:
+        return res.reshape(-1).to(torch.int64)
+    return _rns_to_values(ctx, res)
+
+
 def _small_op(a: RingElem, b: RingElem | None, op: int, scalar: int = 0) -> RingElem:
     ctx = context_of(a.params)
-    out = torch.empty_like(a.data)
     if ctx.t:  # plain-ring kernel (t = modulus)
+        out = torch.empty_like(a.data)
         _lib.check(ctx._lib.ctb_plain_elementwise(ctx._h, op, _ptr(a.data), _ptr(b.data) if b is not None else None,
                                                   scalar, _ptr(out), 1, _stream()), "ctb_plain_elementwise")
         return RingElem(a.params, out, a.domain)
-    # single large prime (>= 2^30): the residue is the value; use the RNS kernels on [1, N]
-    x = a.data.view(1, 1, -1)
+    # modulus < 2^63 whose factorisation is not a plain context (a prime >= 2^30, or 3+ primes):
+    # run the RNS kernels on the residues and convert back
+    x = _as_residues(ctx, a)
+    out = torch.empty_like(x)
     if op == 3:
-        _lib.check(ctx._lib.ctb_rns_scalar_mul(ctx._h, BASE_Q, _ptr(x), _lib.u64_array([scalar % a.params.modulus]),
+        _lib.check(ctx._lib.ctb_rns_scalar_mul(ctx._h, BASE_Q, _ptr(x), _lib.u64_array([scalar % p for p in ctx.q_primes]),
                                                _ptr(out), 1, _stream()), "ctb_rns_scalar_mul")
     else:
-        y = b.data.view(1, 1, -1) if b is not None else None
+        y = _as_residues(ctx, b) if b is not None else None
         _lib.check(ctx._lib.ctb_rns_elementwise(ctx._h, BASE_Q, op, _ptr(x), _ptr(y) if y is not None else None,
                                                 _ptr(out), 1, _stream()), "ctb_rns_elementwise")
-    return RingElem(a.params, out, a.domain)
+    return RingElem(a.params, _from_residues(ctx, out), a.domain)
 
 
 def _rns_op(a: RingElem, b: RingElem | None, op: int) -> RingElem:
@@ -294,9 +330,7 @@ def ring_mul(a: RingElem, b: RingElem) -> RingElem:
         if ctx.t:
             out = ctx.pp_mul(a.data.view(1, -1), b.data.view(1, -1)).view(-1)
             return RingElem(a.params, out)
-        x = a.data.view(1, 1, -1).to(ctx.dtype())
-        y = b.data.view(1, 1, -1).to(ctx.dtype())
-        return RingElem(a.params, ctx.ring_mul(x, y).view(-1).to(torch.int64))
+        return RingElem(a.params, _from_residues(ctx, ctx.ring_mul(_as_residues(ctx, a), _as_residues(ctx, b))))
     out = ctx.ring_mul(a.data.unsqueeze(0), b.data.unsqueeze(0))
     return RingElem(a.params, out.squeeze(0))
 

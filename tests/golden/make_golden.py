@@ -39,6 +39,33 @@ def plain_vals(elem: RingElem) -> np.ndarray:
     return np.array([int(c) for c in elem.coeffs], dtype=np.uint64)
 
 
+def protocol_case(params, job, keygen_seed=3, offline_seed=2, online_seed=4, timeout=60.0):
+    cli, srv = he.He(params, he.BACKEND_RLWE), he.He(params, he.BACKEND_RLWE)
+    keys = cli.keygen(keygen_seed)
+    cpool, spool = linprot.TriplePool(), linprot.TriplePool()
+
+    def client(end):
+        linprot.setup_client(end, cli, keys)
+        linprot.precompute_offline_client(end, cli, keys, np.random.default_rng(offline_seed), job.shape, 1, cpool)
+        return linprot.precompute_online_client(end, cli, keys, np.random.default_rng(online_seed), job, cpool)
+
+    def server(end):
+        pks = linprot.setup_server(end, srv)
+        linprot.precompute_offline_server(end, srv, pks, spool)
+        linprot.precompute_online_server(end, srv, pks, spool)
+
+    ce, se = transport.inproc_pair(capture=True, timeout=timeout)
+    res, _ = transport.run_pair(client, server, ce, se)
+    tr = ce.stats.transcript
+    signed = np.asarray(packing.to_signed_matrix(np.asarray(res.tensor), params.t), dtype=np.int64)
+    return {"c2s": hashlib.sha256(bytes(tr[transport.CLIENT])).hexdigest(),
+            "s2c": hashlib.sha256(bytes(tr[transport.SERVER])).hexdigest(),
+            "c2s_len": len(tr[transport.CLIENT]), "s2c_len": len(tr[transport.SERVER]),
+            "tensor": digest(signed.astype(np.uint64)), "tensor_shape": list(signed.shape),
+            "server_counts": srv.meter.snapshot()["counts"]}
+
+
+
 def main():
     out: dict = {}
     # ------------------------------------------------------------ parameters
@@ -155,31 +182,6 @@ def main():
                    "cfg4_fwd_sites_digest": hashlib.sha256(json.dumps(js.sites).encode()).hexdigest()}
 
     # ------------------------------------------------------------ two-party precompute protocol transcripts
-    def protocol_case(params, job, keygen_seed=3, offline_seed=2, online_seed=4):
-        cli, srv = he.He(params, he.BACKEND_RLWE), he.He(params, he.BACKEND_RLWE)
-        keys = cli.keygen(keygen_seed)
-        cpool, spool = linprot.TriplePool(), linprot.TriplePool()
-
-        def client(end):
-            linprot.setup_client(end, cli, keys)
-            linprot.precompute_offline_client(end, cli, keys, np.random.default_rng(offline_seed), job.shape, 1, cpool)
-            return linprot.precompute_online_client(end, cli, keys, np.random.default_rng(online_seed), job, cpool)
-
-        def server(end):
-            pks = linprot.setup_server(end, srv)
-            linprot.precompute_offline_server(end, srv, pks, spool)
-            linprot.precompute_online_server(end, srv, pks, spool)
-
-        ce, se = transport.inproc_pair(capture=True)
-        res, _ = transport.run_pair(client, server, ce, se)
-        tr = ce.stats.transcript
-        signed = np.asarray(packing.to_signed_matrix(np.asarray(res.tensor), params.t), dtype=np.int64)
-        return {"c2s": hashlib.sha256(bytes(tr[transport.CLIENT])).hexdigest(),
-                "s2c": hashlib.sha256(bytes(tr[transport.SERVER])).hexdigest(),
-                "c2s_len": len(tr[transport.CLIENT]), "s2c_len": len(tr[transport.SERVER]),
-                "tensor": digest(signed.astype(np.uint64)), "tensor_shape": list(signed.shape),
-                "server_counts": srv.meter.snapshot()["counts"]}
-
     rng = np.random.default_rng(21)
     x = rng.integers(-40, 40, size=(2, 8, 8))
     w = rng.integers(-9, 9, size=(2, 2, 3, 3))

@@ -150,9 +150,9 @@ def test_pool_discipline_and_mask_product(p512, rng, tmp_path):
     channel.run_pair(c, s, ce, se)
     # persistence round trip
     linprot.save_server_pool(spool, srv, str(tmp_path / "s.pool"))
-    linprot.save_client_pool(cpool, str(tmp_path / "c.pool"), cli)
+    linprot.save_client_pool(cpool, str(tmp_path / "c.pool"))   # reference signature (linprot.py:550)
     spool2 = linprot.load_server_pool(srv, str(tmp_path / "s.pool"))
-    cpool2 = linprot.load_client_pool(cli, str(tmp_path / "c.pool"))
+    cpool2 = linprot.load_client_pool(p512.plain_ring, str(tmp_path / "c.pool"))   # linprot.py:565
     assert spool2.available("L") == 2 and cpool2.available("L") == 2
     b1, b2 = cpool.take("L"), cpool2.take("L")
     assert np.array_equal(b1.r_x.cpu().numpy(), b2.r_x.cpu().numpy())
@@ -313,3 +313,29 @@ def test_c_abi_fused_entry_errors():
     rc = lib.ctb_linear_online(ctx._h, _ptr(ct), 2, _ptr(ct), 2, _ptr(mx), _ptr(mx), sites, 1, 1, None, 0,
                                _ptr(out), _ptr(outp), _ptr(work2), _stream())
     assert rc == _lib.CTB_ERR_ARG and b"out of range" in lib.ctb_last_error()
+
+
+def test_server_rejects_inconsistent_jobs(p512):
+    """The server validates the declared JobShape against what arrived: too few blobs,
+    out-of-range sites or a pool entry with the wrong slot count raise LinProtError before any
+    device buffer is sized from the header."""
+    import torch
+    from paper_2409_16675_b200 import linprot
+    cli, srv, keys = evaluators(p512)
+    pks = srv.public_keys_from_bytes(cli.public_keys_to_bytes(keys))
+    pool = linprot.TriplePool()
+    js = linprot.JobShape("L", 2, 1, 1, ((0, 0, 0), (1, 0, 0)))
+    with pytest.raises(linprot.LinProtError):
+        linprot.precompute_online_server(None, srv, pks, pool, blobs=[b"pre", js.to_bytes(), b"", b""])
+    with pytest.raises(linprot.LinProtError):
+        linprot.linear_b_server(None, srv, pks, blobs=[b"b", js.to_bytes(), b""])
+    bad = linprot.JobShape("L", 1, 1, 1, ((0, 0, 3),))
+    with pytest.raises(linprot.LinProtError):
+        linprot.linear_b_server(None, srv, pks, blobs=[b"b", bad.to_bytes(), b"", b""])
+    # a pool entry whose slot count differs from the job's
+    cts = cli.encrypt_many(torch.zeros((2, p512.n), dtype=torch.int64, device="cuda"), keys, np.random.default_rng(1))
+    pool.add(linprot.MaskProduct("L", cts))
+    blobs = [b"pre", js.to_bytes()] + cli.batch_to_bytes(cts) + cli.batch_to_bytes(cts)[:1] \
+        + cli.plain_to_bytes(torch.zeros((3, p512.n), dtype=torch.int64, device="cuda"))
+    with pytest.raises(linprot.LinProtError):
+        linprot.precompute_online_server(None, srv, pks, pool, blobs=blobs)

@@ -156,3 +156,30 @@ def test_cpmul_host_pipeline_matches_device_path_threads():
         t.join()
     assert not errors, errors
     assert results == {"single": True, "t0": True, "t1": True}
+
+
+@pytest.mark.parametrize("bits,count", [(31, 2), (20, 3), (31, 1)])
+def test_small_moduli_outside_the_plain_context(bits, count):
+    """Moduli < 2^63 whose factorisation is not a 1-2 prime (< 2^30) plain context: two primes below
+    2^31 (ntt_primes(n, 31, 2), allowed by the reference's cap), three 20-bit primes, one 31-bit prime.
+    Elementwise ops and products go through the residues and back (ring.py _small_op)."""
+    from paper_2409_16675_b200 import ring
+    from paper_2409_16675_b200.ring import RingElem, RingParams
+    n = 256
+    primes = R.ntt_primes(n, bits, count)
+    m = 1
+    for p in primes:
+        m *= p
+    P = RingParams(n, m, tuple(primes))
+    rng = np.random.default_rng(bits * 10 + count)
+    a = RingElem.random(P, rng)
+    b = RingElem.random(P, rng)
+    ai = [int(v) for v in a.coeffs]
+    bi = [int(v) for v in b.coeffs]
+    assert ring.ring_add(a, b).to_ints() == [(x + y) % m for x, y in zip(ai, bi)]
+    assert ring.ring_sub(a, b).to_ints() == [(x - y) % m for x, y in zip(ai, bi)]
+    assert ring.ring_neg(a).to_ints() == [(-x) % m for x in ai]
+    c = 987654321987
+    assert ring.ring_scalar_mul(a, c).to_ints() == [x * c % m for x in ai]
+    want = R.crt_combine(R.ring_mul_rns(R.to_rns(ai, primes), R.to_rns(bi, primes), primes), primes)
+    assert ring.ring_mul(a, b).to_ints() == [int(v) for v in want]

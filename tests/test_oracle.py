@@ -155,3 +155,52 @@ def test_serialization_matches_reference(golden):
     assert hashlib.sha256(blob).hexdigest() == golden["serial"]["c0_bytes"]
     back = R.ring_from_bytes(blob, P.n, P.q)
     assert all(int(a) == int(b) for a, b in zip(back, c0))
+
+
+# ---------------------------------------------------------------- the protocol restatement (oracle/linprot_ref.py)
+
+def _proto_check(case, p, job_id, job):
+    import hashlib
+    from oracle import linprot_ref as LP
+    from oracle import packing_ref as PR
+    res = LP.run_protocol(p, job_id, job)
+    assert len(res["c2s"]) == case["c2s_len"] and len(res["s2c"]) == case["s2c_len"]
+    assert hashlib.sha256(res["c2s"]).hexdigest() == case["c2s"]
+    assert hashlib.sha256(res["s2c"]).hexdigest() == case["s2c"]
+    signed = PR.centered(job["extract"](res["out"]), p.t)
+    assert list(signed.shape) == case["tensor_shape"]
+    assert digest(signed.astype(np.uint64)) == case["tensor"]
+    return signed
+
+
+def test_protocol_restatement_matches_reference_transcripts(golden):
+    """oracle.linprot_ref + oracle.packing_ref reproduce the reference's two-party precompute-protocol
+    transcripts (both directions, every ciphertext byte) for conv, grad-w and FC jobs."""
+    from oracle import packing_ref as PR
+    from oracle.plainconv import conv2d_multi
+    Ps = H.default_params(512, plain_bits=17)
+    g = golden["protocol"]["small_conv"]
+    x, w = np.array(g["x"]), np.array(g["w"])
+    out = _proto_check(g, Ps, "c", PR.conv_job(x, w, 8, 8, 3, 1, 512, Ps.t))
+    assert np.array_equal(out, conv2d_multi(x, w, 1))
+    g = golden["protocol"]["small_gradw"]
+    _proto_check(g, Ps, "g", PR.conv_grad_w_job(np.array(g["x"]), np.array(g["gy"]), 6, 6, 4, 1, 512, Ps.t))
+    g = golden["protocol"]["small_fc"]
+    x, w = np.array(g["x"]), np.array(g["w"])
+    out = _proto_check(g, Ps, "fc", PR.fc_job(x, w, 512, Ps.t))
+    assert np.array_equal(out, w @ x)
+
+
+def test_packing_restatement_plans(golden):
+    from oracle import packing_ref as PR
+    g = golden["packing"]
+    assert list(PR.choose_tiles(64, 64, 5, 4096)) == g["choose_tiles_64_64_5_4_4096"]
+    assert PR.plan(28, 28, 5, 0, 4096)["O"] == g["cfg3_plan"]
+    assert PR.plan(32, 32, 3, 1, 4096)["O"] == g["cfg4_plan"]
+    pl = PR.plan(32, 32, 32, 1, 4096)
+    assert [pl["O"], len(pl["tiles"])] == g["cfg4_gw_plan"]
+    # reference tests/test_packing.py toy degrees: 2x2 input -> {0,1,3,4}, 2x2 kernel -> {4,3,1,0}
+    pl = PR.plan(2, 2, 2, 0, 16)
+    assert sorted(np.nonzero(PR.pack_input(np.array([[1, 2], [3, 4]]), pl, 97)[0])[0].tolist()) == [0, 1, 3, 4]
+    k = PR.pack_kernel(np.array([[1, 2], [3, 4]]), pl, 97)
+    assert [int(k[d]) for d in (4, 3, 1, 0)] == [1, 2, 3, 4]
