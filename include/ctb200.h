@@ -162,6 +162,39 @@ int ctb_plain_elementwise(const ctb_ctx_t* ctx, int op, const uint64_t* a, const
 /* Decrypt's exact scale-and-round: v [n][L][N] residues of c0 + c1 s (+ c2 s^2)
  * -> out [n][N] = floor((v t + floor(q/2)) / q) mod t   (He.decrypt, he.py:347-349). */
 int ctb_decrypt_round(const ctb_ctx_t* ctx, const void* v, uint64_t* out, uint64_t n_polys, void* stream);
+/* ctb_decrypt_round fused with the client's unmasking and extraction (precompute_online_client,
+ * linprot.py:444-452: decrypt(c) - p, then job.extract = packing.extract_output / to_signed_matrix,
+ * packing.py:476-522, or the FC / outer extractions :577-605): for polynomial b and coefficient d
+ * with m = maps[kind[b]][d] >= 0 and base[b] + m < dst_len,
+ *   out[base[b] + m] = (round(v[b])[d] - sub[b][d]) mod t   (sub may be NULL),
+ * centred into (-t/2, t/2] when `centered` (to_signed_matrix).  maps [n_maps][N] int32, kind [n]
+ * int32, base [n] int64, out int64 -- all device.  Coefficients without a destination are not
+ * rounded at all. */
+int ctb_decrypt_round_extract(const ctb_ctx_t* ctx, const void* v, const uint64_t* sub, const int32_t* maps,
+                              uint32_t n_maps, const int32_t* kind, const int64_t* base, uint64_t dst_len,
+                              int centered, int64_t* out, uint64_t n_polys, void* stream);
+
+/* Encode side of the correlated linear layer as one gather (packing.pack_input_correlated /
+ * pack_kernel_correlated, packing.py:407-445; pack_fc_input / pack_fc_matrix / pack_outer_left,
+ * packing.py:545-597; affine_job's packing, linprot.py:243-257):
+ *   out_plain[p][d] = m >= 0 && base[p] + m < src_len ? src[base[p] + m] mod t : 0,
+ *   m = maps[kind[p]][d]
+ * src int64 signed values (reduced like RingElem.from_ints); maps [n_maps][N] int32 (-1 = empty
+ * degree), kind [n_polys] int32, base [n_polys] int64 -- all device.  When r != NULL also
+ * out_masked[p][d] = (out_plain[p][d] - r[p][d]) mod t, the client's masking x - r_x / w - r_w of
+ * precompute_online_client (linprot.py:438-441), fused; out_plain may then be NULL. */
+int ctb_pack_gather(const ctb_ctx_t* ctx, const int64_t* src, uint64_t src_len, const int32_t* maps, uint32_t n_maps,
+                    const int32_t* kind, const int64_t* base, const uint64_t* r, uint64_t* out_plain,
+                    uint64_t* out_masked, uint64_t n_polys, void* stream);
+
+/* Decode side as one scatter (packing.extract_output packing.py:476-509 + to_signed_matrix :512-522,
+ * extract_fc_output / extract_outer :577-605) from plain values in [n_slots][N] uint64:
+ *   out[base[s] + m] = (in[s][d] - sub[s][d]) mod t (sub may be NULL), centred if `centered`,
+ * for m = maps[kind[s]][d] >= 0 and base[s] + m < dst_len. */
+int ctb_plain_scatter(const ctb_ctx_t* ctx, const uint64_t* in, const uint64_t* sub, const int32_t* maps,
+                      uint32_t n_maps, const int32_t* kind, const int64_t* base, uint64_t dst_len, int centered,
+                      int64_t* out, uint64_t n_slots, void* stream);
+
 /* Wire format: residues [n][L][N] <-> positional little-endian 64-bit words
  * [n][N][W], W = ctb_ctx_pos_words = ring.RingParams.limb_count (ring.py:147,
  * ring_to_bytes / ring_from_bytes ring.py:592-615; input words reduced mod q). */
@@ -201,7 +234,8 @@ int ctb_relinearize(const ctb_ctx_t* ctx, const void* ct3, const void* keyprep, 
  * the per-site computation.  Each distinct ciphertext is lifted and transformed once and
  * relinearisation runs once per slot (digit sums; a slot may hold at most
  * (2^32 - 1) / (2^w - 1) sites).  workspace: ctb_ccmul_sum_workspace_bytes(..., largest
- * slot's site count).  Synchronises `stream` once (site table upload). */
+ * slot's site count).  The host site table is copied stream-ordered through a pinned staging
+ * buffer: the call does not synchronise `stream` and sites_host may be freed on return. */
 uint64_t ctb_ccmul_sum_workspace_bytes(const ctb_ctx_t* ctx, uint32_t n_x, uint32_t n_w, uint32_t n_out,
                                        uint32_t n_sites, uint32_t max_slot_sites);
 int ctb_ccmul_sum(const ctb_ctx_t* ctx, const void* ct_x, uint32_t n_x, const void* ct_w, uint32_t n_w,
@@ -225,7 +259,8 @@ int ctb_lift_prepare(const ctb_ctx_t* ctx, const uint64_t* m, void* out, uint64_
  * out_ct [n_out][2][L][N]; out_p [n_out][N].
  * workspace: ctb_linear_online_workspace_bytes() bytes of device memory.
  * Every ciphertext part and masked plaintext is NTT'd once; each slot is
- * accumulated in the evaluation domain and inverse-transformed once. */
+ * accumulated in the evaluation domain and inverse-transformed once.  Like ctb_ccmul_sum the
+ * call returns without synchronising `stream` (sites_host may be freed on return). */
 uint64_t ctb_linear_online_workspace_bytes(const ctb_ctx_t* ctx, uint32_t n_x, uint32_t n_w, uint32_t n_out,
                                            uint32_t n_sites);
 int ctb_linear_online(const ctb_ctx_t* ctx, const void* ct_x, uint32_t n_x, const void* ct_w, uint32_t n_w,

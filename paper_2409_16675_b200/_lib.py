@@ -52,6 +52,12 @@ SIGNATURES: dict[str, tuple] = {
     "ctb_lift_plain": (_int, [_c_void_p, _c_void_p, ctypes.POINTER(_u64), _c_void_p, _u64, _c_void_p]),
     "ctb_plain_elementwise": (_int, [_c_void_p, _int, _c_void_p, _c_void_p, _u64, _c_void_p, _u64, _c_void_p]),
     "ctb_decrypt_round": (_int, [_c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_decrypt_round_extract": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _u32, _c_void_p, _c_void_p, _u64,
+                                          _int, _c_void_p, _u64, _c_void_p]),
+    "ctb_pack_gather": (_int, [_c_void_p, _c_void_p, _u64, _c_void_p, _u32, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
+                               _c_void_p, _u64, _c_void_p]),
+    "ctb_plain_scatter": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _u32, _c_void_p, _c_void_p, _u64, _int,
+                                 _c_void_p, _u64, _c_void_p]),
     "ctb_ctx_pos_words": (_int, [_c_void_p]),
     "ctb_rns_to_pos": (_int, [_c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_pos_to_rns": (_int, [_c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),

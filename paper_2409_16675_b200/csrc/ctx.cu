@@ -13,6 +13,68 @@ static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 const char* get_error() { return g_err.c_str(); }
 
+// ------------------------------------------------------------------ staged host->device uploads
+// Small per-call host tables (site CSRs) are copied through a thread-local pinned ring buffer: the
+// copy is stream-ordered and the call returns without synchronising; a ring region is rewritten only
+// after the event recorded behind its previous copy has completed (rare: only when the ring wraps onto
+// a copy still queued).  Thread-local, so the two party threads never share a region.
+namespace {
+struct Staging {
+  char* buf = nullptr;
+  size_t cap = 0, head = 0;
+  struct Inflight { size_t lo, hi; cudaEvent_t ev; };
+  std::vector<Inflight> inflight;
+  cudaError_t drain(size_t lo, size_t hi) {  // wait for copies overlapping [lo, hi)
+    cudaError_t e = cudaSuccess;
+    std::vector<Inflight> keep;
+    for (auto& f : inflight) {
+      if (f.lo < hi && lo < f.hi) {
+        if (e == cudaSuccess) e = cudaEventSynchronize(f.ev);
+        cudaEventDestroy(f.ev);
+      } else {
+        keep.push_back(f);
+      }
+    }
+    inflight.swap(keep);
+    return e;
+  }
+  ~Staging() {
+    drain(0, (size_t)-1);
+    if (buf) cudaFreeHost(buf);  // may fail harmlessly at process teardown
+  }
+};
+thread_local Staging g_stage;
+}  // namespace
+
+cudaError_t stage_upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (!bytes) return cudaSuccess;
+  Staging& st = g_stage;
+  const size_t need = (bytes + 255) & ~(size_t)255;
+  cudaError_t e;
+  if (need > st.cap) {
+    if ((e = st.drain(0, (size_t)-1)) != cudaSuccess) return e;
+    if (st.buf) cudaFreeHost(st.buf);
+    st.cap = std::max<size_t>(need, (size_t)4 << 20);
+    st.head = 0;
+    if ((e = cudaHostAlloc((void**)&st.buf, st.cap, cudaHostAllocDefault)) != cudaSuccess) {
+      st.buf = nullptr;
+      st.cap = 0;
+      return e;
+    }
+  }
+  if (st.head + need > st.cap) st.head = 0;
+  const size_t lo = st.head, hi = lo + need;
+  if ((e = st.drain(lo, hi)) != cudaSuccess) return e;
+  std::memcpy(st.buf + lo, src, bytes);
+  if ((e = cudaMemcpyAsync(dst, st.buf + lo, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
+  cudaEvent_t ev;
+  if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+  if ((e = cudaEventRecord(ev, s)) != cudaSuccess) { cudaEventDestroy(ev); return e; }
+  st.inflight.push_back({lo, hi, ev});
+  st.head = hi;
+  return cudaSuccess;
+}
+
 static std::mutex g_attr_mu;
 static std::unordered_set<const void*> g_attr_set;
 bool smem_attr_done(const void* kern) {

@@ -49,6 +49,10 @@ struct Ctx {
 void set_error(const std::string& msg);
 const char* get_error();
 
+// stream-ordered copy of a small host table through a thread-local pinned ring buffer (ctx.cu):
+// returns without synchronising the stream; the host source may be freed right after the call
+cudaError_t stage_upload(void* dst, const void* src, size_t bytes, cudaStream_t s);
+
 // exact host arithmetic
 inline uint64_t mulmod(uint64_t a, uint64_t b, uint64_t m) {
   return (uint64_t)((unsigned __int128)a * b % m);

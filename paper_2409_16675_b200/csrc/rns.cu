@@ -1,6 +1,7 @@
 // Exact conversions between the cipher base's residues and integers.
 //
 //   ctb_decrypt_round  he.py:347-349  out = floor((v t + floor(q/2)) / q) mod t
+//   ctb_decrypt_round_extract  the same, fused with the client's c - p and job.extract (linprot.py:444-452)
 //   ctb_rns_to_pos     ring.py:592-599 positional little-endian 64-bit words (wire format)
 //   ctb_pos_to_rns     ring.py:602-615 the inverse (from_ints: value mod q)
 //
@@ -55,6 +56,41 @@ struct DecLazy {
   ShoupC<uint32_t> qinv_t[2], crt;
 };
 
+// Optional epilogue of the decrypt rounding kernels (ctb_decrypt_round_extract): the client's
+// unmasking c - p (linprot.py:444-450) and the job's extraction (packing.extract_output +
+// to_signed_matrix, packing.py:476-522) as a scatter through per-kind degree maps.  With maps set,
+// coefficients that are not outputs are skipped before any rounding work.
+struct DecEpi {
+  const uint64_t* sub = nullptr;   // [n][N] plain values subtracted mod t (may be null)
+  const int32_t* maps = nullptr;   // [n_maps][N] destination offsets (-1: not an output); null: identity
+  const int32_t* kind = nullptr;   // [n] map row per polynomial
+  const int64_t* base = nullptr;   // [n] destination base per polynomial
+  uint32_t n_maps = 0;
+  int centered = 0;                // store (-t/2, t/2] signed values
+  uint64_t dst_len = 0;
+  uint64_t t = 0;
+};
+
+// destination of coefficient i of polynomial b, or -1 when the epilogue drops it
+__device__ __forceinline__ int64_t epi_dst(const DecEpi& e, uint64_t b, uint64_t i, uint32_t n, uint64_t g) {
+  if (!e.maps) return (int64_t)g;
+  const uint32_t k = (uint32_t)e.kind[b];
+  if (k >= e.n_maps) return -1;
+  const int32_t m = e.maps[(uint64_t)k * n + i];
+  if (m < 0) return -1;
+  const uint64_t dst = (uint64_t)e.base[b] + (uint64_t)m;
+  return dst < e.dst_len ? (int64_t)dst : -1;
+}
+
+__device__ __forceinline__ void epi_store(const DecEpi& e, uint64_t* out, int64_t dst, uint64_t g, uint64_t v) {
+  if (e.sub) {
+    const uint64_t b = e.sub[g];
+    v = v >= b ? v - b : v + e.t - b;
+  }
+  if (e.centered && v > e.t / 2) v -= e.t;  // two's complement int64 view
+  out[dst] = v;
+}
+
 struct RnsConsts {
   void* d_q = nullptr;  // QConsts<T> for the cipher base
   int word = 4;
@@ -94,7 +130,7 @@ __device__ __forceinline__ uint32_t eval_mod_plain(int L, const T* a, const Plai
 
 template <typename T>
 __global__ void k_decrypt_round(const T* v, uint64_t* out, const QConsts<T>* __restrict__ cq, uint32_t n,
-                                uint64_t total) {
+                                uint64_t total, const DecEpi epi) {
   __shared__ QConsts<T> c;
   {
     const uint32_t* src = reinterpret_cast<const uint32_t*>(cq);
@@ -106,6 +142,8 @@ __global__ void k_decrypt_round(const T* v, uint64_t* out, const QConsts<T>* __r
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
        g += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t b = g >> pow2_shift(n), i = g & (n - 1);  // n = ring degree (power of two)
+    const int64_t dst = epi_dst(epi, b, i, n, g);
+    if (dst < 0) continue;
     T r[MAX_MRC], a[MAX_MRC];
     for (int l = 0; l < L; ++l) {
       const T q = c.mrc.q[l];
@@ -127,18 +165,20 @@ __global__ void k_decrypt_round(const T* v, uint64_t* out, const QConsts<T>* __r
       const uint32_t d = csub(shoup_mul<uint32_t>(sub_mod(w[1], w0m, m1), c.pe.crt.w, c.pe.crt.wq, m1), m1);
       res = (uint64_t)w[0] + (uint64_t)c.pe.tp[0] * d;
     }
-    out[g] = res;
+    epi_store(epi, out, dst, g, res);
   }
 }
 
 template <int LC>
 __global__ void __launch_bounds__(256) k_decrypt_round_lazy(const uint32_t* v, uint64_t* out,
                                                             const __grid_constant__ DecLazy c, uint32_t n,
-                                                            uint64_t total) {
+                                                            uint64_t total, const __grid_constant__ DecEpi epi) {
   const int L = LC ? LC : c.L;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
        g += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t b = g >> pow2_shift(n), i = g & (n - 1);  // n = ring degree (power of two)
+    const int64_t dst = epi_dst(epi, b, i, n, g);
+    if (dst < 0) continue;
     uint32_t a[DEC_MAXQ];
 #pragma unroll
     for (int j = 0; j < (LC ? LC : DEC_MAXQ); ++j) {
@@ -178,7 +218,7 @@ __global__ void __launch_bounds__(256) k_decrypt_round_lazy(const uint32_t* v, u
       const uint32_t d = csub(shoup_mul<uint32_t>(sub_mod(w[1], w0m, m1), c.crt.w, c.crt.wq, m1), m1);
       res = (uint64_t)w[0] + (uint64_t)c.tp[0] * d;
     }
-    out[g] = res;
+    epi_store(epi, out, dst, g, res);
   }
 }
 
@@ -346,26 +386,56 @@ int rns_words(const RnsConsts* rc) { return rc ? rc->W : 0; }
 using namespace ctb;
 
 
+namespace {
+int launch_decrypt_round(const Ctx* c, const void* v, uint64_t* out, uint64_t n_polys, const DecEpi& epi,
+                         cudaStream_t s) {
+  const uint64_t total = n_polys * c->n;
+  if (!total) return OK;
+  if (c->rns->lazy) {
+    if (c->rns->dec.L == 7)
+      k_decrypt_round_lazy<7><<<grid_stride(total, 8), 256, 0, s>>>((const uint32_t*)v, out, c->rns->dec, c->n, total,
+                                                                    epi);
+    else
+      k_decrypt_round_lazy<0><<<grid_stride(total, 8), 256, 0, s>>>((const uint32_t*)v, out, c->rns->dec, c->n, total,
+                                                                    epi);
+  } else if (c->rns->word == 4)
+    k_decrypt_round<uint32_t><<<grid_stride(total, 8), 256, 0, s>>>((const uint32_t*)v, out,
+                                                              (const QConsts<uint32_t>*)c->rns->d_q, c->n, total, epi);
+  else
+    k_decrypt_round<uint64_t><<<grid_stride(total, 8), 256, 0, s>>>((const uint64_t*)v, out,
+                                                              (const QConsts<uint64_t>*)c->rns->d_q, c->n, total, epi);
+  return cuda_status(cudaGetLastError(), "ctb_decrypt_round");
+}
+}  // namespace
+
 extern "C" int ctb_decrypt_round(const ctb_ctx_t* ctx, const void* v, uint64_t* out, uint64_t n_polys,
                                  void* stream) {
   if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
   if (!c || !c->rns || !c->t || !v || !out) { set_error("ctb_decrypt_round: context lacks plain ring or bad buffer"); return ERR_ARG; }
-  const uint64_t total = n_polys * c->n;
-  if (!total) return OK;
-  cudaStream_t s = (cudaStream_t)stream;
-  if (c->rns->lazy) {
-    if (c->rns->dec.L == 7)
-      k_decrypt_round_lazy<7><<<grid_stride(total, 8), 256, 0, s>>>((const uint32_t*)v, out, c->rns->dec, c->n, total);
-    else
-      k_decrypt_round_lazy<0><<<grid_stride(total, 8), 256, 0, s>>>((const uint32_t*)v, out, c->rns->dec, c->n, total);
-  } else if (c->rns->word == 4)
-    k_decrypt_round<uint32_t><<<grid_stride(total, 8), 256, 0, s>>>((const uint32_t*)v, out,
-                                                              (const QConsts<uint32_t>*)c->rns->d_q, c->n, total);
-  else
-    k_decrypt_round<uint64_t><<<grid_stride(total, 8), 256, 0, s>>>((const uint64_t*)v, out,
-                                                              (const QConsts<uint64_t>*)c->rns->d_q, c->n, total);
-  return cuda_status(cudaGetLastError(), "ctb_decrypt_round");
+  return launch_decrypt_round(c, v, out, n_polys, DecEpi{}, (cudaStream_t)stream);
+}
+
+extern "C" int ctb_decrypt_round_extract(const ctb_ctx_t* ctx, const void* v, const uint64_t* sub,
+                                         const int32_t* maps, uint32_t n_maps, const int32_t* kind,
+                                         const int64_t* base, uint64_t dst_len, int centered, int64_t* out,
+                                         uint64_t n_polys, void* stream) {
+  if (n_polys == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (!c || !c->rns || !c->t || !v || !maps || !kind || !base || (dst_len && !out)) {
+    set_error("ctb_decrypt_round_extract: context lacks plain ring or bad buffer");
+    return ERR_ARG;
+  }
+  DecEpi e;
+  e.sub = sub;
+  e.maps = maps;
+  e.kind = kind;
+  e.base = base;
+  e.n_maps = n_maps;
+  e.centered = centered;
+  e.dst_len = dst_len;
+  e.t = c->t;
+  return launch_decrypt_round(c, v, reinterpret_cast<uint64_t*>(out), n_polys, e, (cudaStream_t)stream);
 }
 
 extern "C" int ctb_rns_to_pos(const ctb_ctx_t* ctx, const void* x, uint64_t* out, uint64_t n_polys, void* stream) {

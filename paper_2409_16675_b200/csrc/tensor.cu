@@ -1430,8 +1430,7 @@ extern "C" int ctb_ccmul_sum(const ctb_ctx_t* ctx, const void* ct_x, uint32_t n_
   std::copy(ptr.begin(), ptr.end(), packed.begin());
   std::copy(sx.begin(), sx.end(), packed.begin() + n_out + 1);
   std::copy(sw.begin(), sw.end(), packed.begin() + n_out + 1 + n_sites);
-  cudaError_t e = cudaMemcpyAsync(csr, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // the host vector dies at return
+  cudaError_t e = stage_upload(csr, packed.data(), packed.size() * 4, s);  // no stream sync
   if (e != cudaSuccess) return cuda_status(e, "ctb_ccmul_sum csr");
   const int32_t* d_ptr = csr;
   const int32_t* d_sx = csr + n_out + 1;

@@ -18,10 +18,14 @@ exact ring arithmetic.  Both parties run co-resident on one GPU
 (`ctb_linear_online`) and client decryption exchange device buffers instead
 of wire bytes; the byte-level two-party path is `linprot`'s channel functions.
 
-The non-linear primitives run the reference's OT protocol (mpc.py) in the
-reference; that protocol is outside this repository's scope, so
-the engine returns their exact values (max(x, 0) and the window max), which is
-what the OT protocol reconstructs.
+The non-linear primitives are NOT computed here: `relu` / `maxpool4` hand the
+values, as 2^bits residues (mpc.from_signed), to an injected non-linear protocol
+with the signature of the reference's `SecureSession.nonlinear(op, values, bits)`
+(session.py:78-84 -> mpc.client_nonlinear, the OT protocol of mpc.py), and map its
+reconstruction back with mpc.to_signed -- exactly SecureEngine.relu / maxpool4
+(train.py:278-290).  The OT protocol stays in the reference; an
+engine without one refuses to run a non-linear layer.  `cleartext_nonlinear` is
+an explicitly named TEST DOUBLE returning what the OT protocol reconstructs.
 
 Beyond the reference (the trainer lowerings BASELINE configs 3 and 5 need,
 SURVEY.md Appendix A): `conv_forward_strided` (stride-1 job + subsample) and
@@ -133,22 +137,39 @@ class DeviceSession:
             raise linprot.LinProtError(f"pool entry for {js.job_id!r} has a different job shape")
         return bundle, prod
 
-    def linear_polys(self, job: LinearJob) -> torch.Tensor:
-        """[n_out, N] mod-t output polynomials of one job."""
+    def _online(self, job: LinearJob, decode: bool, centered: bool) -> torch.Tensor:
         t0 = time.perf_counter()
         if self.protocol == PROTOCOL_B:
             out = self._linear_b(job)
+            if decode and job.extract is not None:
+                out = job.extract(out)
+                if centered:
+                    out = packing.to_signed_tensor(out, self.params.t)
         else:
             bundle, prod = self._take(job.shape)
-            out = workloads.online(self.parties, job, bundle, prod, self.gen)
+            out = workloads.online(self.parties, job, bundle, prod, self.gen, decode=decode, centered=centered)
         _sync()
         self.online_seconds += time.perf_counter() - t0
         self.jobs_run += 1
         return out
 
+    def linear_polys(self, job: LinearJob) -> torch.Tensor:
+        """[n_out, N] mod-t output polynomials of one job."""
+        return self._online(job, decode=False, centered=False)
+
     def linear(self, job: LinearJob) -> torch.Tensor:
-        out = self.linear_polys(job)
-        return job.extract(out) if job.extract else out
+        """The job's extracted tensor, residues mod t (session.py:67-76 -> job.extract)."""
+        if job.out is None:
+            out = self.linear_polys(job)
+            return job.extract(out) if job.extract else out
+        return self._online(job, decode=True, centered=False)
+
+    def linear_signed(self, job: LinearJob) -> torch.Tensor:
+        """The job's extracted tensor centred into (-t/2, t/2] (to_signed_matrix), decoded in the
+        decrypt epilogue."""
+        if job.out is None:
+            return packing.to_signed_tensor(self.linear(job), self.params.t)
+        return self._online(job, decode=True, centered=True)
 
     def _linear_b(self, job: LinearJob) -> torch.Tensor:
         js, cli, srv = job.shape, self.client, self.server
@@ -167,14 +188,49 @@ class DeviceSession:
                 "jobs": self.jobs_run}
 
 
+def _umod(arr, bits: int) -> np.ndarray:
+    return np.asarray(arr, dtype=np.int64).astype(np.uint64) & np.uint64((1 << bits) - 1)
+
+
+def from_signed(x, bits: int) -> np.ndarray:
+    """mpc.from_signed (mpc.py:114-115): signed values -> residues mod 2^bits."""
+    return _umod(x, bits)
+
+
+def to_signed(x, bits: int) -> np.ndarray:
+    """mpc.to_signed (mpc.py:108-111)."""
+    v = (np.asarray(x, dtype=np.uint64) & np.uint64((1 << bits) - 1)).astype(np.int64)
+    half = 1 << (bits - 1)
+    return np.where(v >= half, v - (1 << bits), v)
+
+
+def cleartext_nonlinear(op: str, values: np.ndarray, bits: int) -> np.ndarray:
+    """TEST DOUBLE for the OT non-linear protocol: returns, in the clear, what mpc.client_nonlinear
+    reconstructs (relu: max(x, 0); maxpool: the max over the 4 window rows), as 2^bits residues.
+    Never use it where the secure protocol is required -- pass SecureSession.nonlinear instead."""
+    x = to_signed(values, bits)
+    if op == "relu":
+        out = np.maximum(x, 0)
+    elif op == "maxpool":
+        out = x.max(axis=0)
+    else:
+        raise TrainError(f"unknown nonlinear op {op!r}")
+    return from_signed(out, bits)
+
+
 class DeviceSecureEngine:
-    """SecureEngine-compatible primitives on the device path (train.py:232-290)."""
+    """SecureEngine-compatible primitives on the device path (train.py:232-290).
+
+    `nonlinear(op, values, bits) -> values` is the secure non-linear protocol, e.g. the bound
+    method `SecureSession.nonlinear` of a reference session (session.py:78-84), which runs the
+    OT protocol of mpc.py against the reference server loop."""
 
     name = "secure"
 
     def __init__(self, session: DeviceSession, plain_ring=None, bits: int = 32,
-                 scheme: str = packing.SCHEME_CORRELATED):
+                 scheme: str = packing.SCHEME_CORRELATED, nonlinear=None):
         self.session = session
+        self.nonlinear = nonlinear
         self.ring = plain_ring if plain_ring is not None else session.params.plain_ring
         self.bits = bits
         self.scheme = scheme
@@ -190,7 +246,9 @@ class DeviceSecureEngine:
         return check_range(signed, 2 * self.bits)
 
     def _run(self, job: LinearJob) -> np.ndarray:
-        return self._signed(self.session.linear(job))
+        # train.py:251-254: session.linear -> to_signed_matrix -> check_range; the centring runs
+        # in the decrypt epilogue here
+        return check_range(self.session.linear_signed(job).cpu().numpy().astype(np.int64), 2 * self.bits)
 
     # -- the reference primitives ----------------------------------------------------------
 
@@ -211,18 +269,35 @@ class DeviceSecureEngine:
     def affine(self, x, gamma: int, job_id: str = "bn") -> np.ndarray:
         return self._run(linprot.affine_job(self._jid(job_id), x, int(gamma), self.ring))
 
+    def _nl(self):
+        if self.nonlinear is None:
+            raise TrainError("no non-linear protocol attached: construct the engine with "
+                             "nonlinear=SecureSession.nonlinear (the reference OT path, session.py:78-84)")
+        return self.nonlinear
+
     def relu(self, x: np.ndarray) -> np.ndarray:
-        return np.maximum(np.asarray(x, dtype=np.int64), 0)
+        """train.py:278-283: from_signed -> session.nonlinear("relu") -> to_signed."""
+        x = np.asarray(x)
+        flat = from_signed(x.ravel(), self.bits)
+        out = self._nl()("relu", flat, self.bits)
+        return to_signed(out, self.bits).reshape(x.shape)
 
     def maxpool4(self, windows: np.ndarray) -> np.ndarray:
-        return np.asarray(windows, dtype=np.int64).max(axis=0)
+        """train.py:285-290: the 4 window rows go to session.nonlinear("maxpool")."""
+        vals = from_signed(np.asarray(windows), self.bits)
+        out = self._nl()("maxpool", vals, self.bits)
+        return to_signed(out, self.bits)
 
     # -- lowerings the BASELINE configs need (not in the reference) ----------------------
 
     def conv_forward_strided(self, x, w, shape: packing.ConvShape, stride: int,
                              job_id: str = "conv") -> np.ndarray:
-        """Stride-s convolution as the stride-1 job subsampled (SPEC.md:544 lowering)."""
-        return self.conv_forward(x, w, shape, job_id)[:, ::stride, ::stride]
+        """Stride-s convolution as the stride-1 job subsampled (SPEC.md:544 lowering); the
+        subsampling is the job's extraction map, so only the kept outputs are decrypted."""
+        self.scheme_counts[self.scheme] += 1
+        x = np.asarray(x) if not isinstance(x, torch.Tensor) else x
+        xb = x[None] if x.ndim == 3 else x[None, None]
+        return self._run(linprot.conv_job_batch(self._jid(job_id), xb, w, shape, self.ring, stride=stride))[0]
 
     def fc_chunked(self, w, x, job_id: str = "fc") -> np.ndarray:
         """y = W x for in_dim > N: one fc job per N-column chunk, summed client-side."""
@@ -249,25 +324,15 @@ class DeviceSecureEngine:
 
     def conv_forward_batch(self, xs, w, shape: packing.ConvShape, job_id: str = "conv") -> np.ndarray:
         """conv_forward for a batch of images [B, cin, H, W] in one fused job."""
-        jobs = [linprot.conv_job(f"{job_id}.b{b}", xs[b], w, shape, self.ring, self.scheme) for b in range(len(xs))]
-        return self._run_batch(jobs, job_id)
+        self.scheme_counts[self.scheme] += len(xs)
+        return self._run(linprot.conv_job_batch(job_id, xs, w, shape, self.ring))
 
     def conv_pairwise_batch(self, xs, gys, shape: packing.ConvShape, job_id: str = "convgw") -> np.ndarray:
-        jobs = [linprot.conv_grad_w_job(f"{job_id}.b{b}", xs[b], gys[b], shape, self.ring) for b in range(len(xs))]
-        return self._run_batch(jobs, job_id)
-
-    def _run_batch(self, jobs: list[LinearJob], job_id: str) -> np.ndarray:
-        self.scheme_counts[self.scheme] += len(jobs)
-        big, shapes = workloads.concat_jobs(jobs, job_id)
-        out = self.session.linear_polys(big)
-        outs, o = [], 0
-        for j, s in zip(jobs, shapes):
-            outs.append(self._signed(j.extract(out[o:o + s.n_out])))
-            o += s.n_out
-        return np.stack(outs)
+        self.scheme_counts[packing.SCHEME_CORRELATED] += len(xs)
+        return self._run(linprot.conv_grad_w_job_batch(job_id, xs, gys, shape, self.ring))
 
     def batch_shape(self, jobs_or_shapes, job_id: str) -> JobShape:
-        """The concatenated JobShape `_run_batch` consumes (for ensure_offline)."""
+        """The block-diagonal JobShape the *_batch primitives consume (for ensure_offline)."""
         shapes = [j.shape if isinstance(j, LinearJob) else j for j in jobs_or_shapes]
         sites, xo, wo, oo = [], 0, 0, 0
         for s in shapes:

@@ -397,9 +397,8 @@ class He:
         out = self.decrypt_values(cts, keys)
         return [RingElem(self.params.plain_ring, out[i]) for i in range(out.shape[0])]
 
-    def decrypt_values(self, cts, keys: KeySet) -> torch.Tensor:
-        """decrypt_many as one int64 tensor [B, N] of plain values (no per-poly objects)."""
-        t0 = self._t0()
+    def _dec_acc(self, cts, keys: KeySet) -> tuple[CiphertextBatch, torch.Tensor]:
+        """Noise gate (he.py:336-340) and v = c0 + c1 s (+ c2 s^2) residues [B, L, N]."""
         if isinstance(cts, CiphertextBatch):
             batch = cts
         else:
@@ -424,11 +423,37 @@ class He:
             _lib.check(self.ctx._lib.ctb_mul_prepared_strided(self.ctx._h, BASE_Q, _ptr(d[:, 2]), P,
                                                               _ptr(self._s_prep(keys, 2)), 0, _ptr(acc), 1,
                                                               _ptr(acc), B, _stream()), "ctb_mul_prepared_strided")
+        return batch, acc
+
+    def decrypt_values(self, cts, keys: KeySet) -> torch.Tensor:
+        """decrypt_many as one int64 tensor [B, N] of plain values (no per-poly objects)."""
+        t0 = self._t0()
+        batch, acc = self._dec_acc(cts, keys)
         out = torch.empty((len(batch), self.params.n), dtype=torch.int64, device="cuda")
         _lib.check(self.ctx._lib.ctb_decrypt_round(self.ctx._h, _ptr(acc), _ptr(out), len(batch), _stream()),
                    "ctb_decrypt_round")
         self.meter.tick("Dec", self._elapsed(t0), count=len(batch))
         return out
+
+    def decrypt_extract(self, cts, keys: KeySet, out, sub: torch.Tensor | None = None,
+                        centered: bool = True) -> torch.Tensor:
+        """The client's tail of an online job in one epilogue: decrypt each slot, subtract the
+        server's plain share p (linprot.py:444-450), extract the job's output tensor
+        (packing.extract_output and friends) and centre it (to_signed_matrix) -- `out` is the job's
+        packing.Scatter.  Only extracted coefficients are rounded (ctb_decrypt_round_extract)."""
+        t0 = self._t0()
+        batch, acc = self._dec_acc(cts, keys)
+        if int(out.kind.shape[0]) != len(batch):
+            raise HeError(f"extraction expects {int(out.kind.shape[0])} slots, got {len(batch)}")
+        if sub is not None and tuple(sub.shape) != (len(batch), self.params.n):
+            raise HeError("plain share shape does not match the slots")
+        res = torch.empty(out.shape, dtype=torch.int64, device="cuda")   # the extraction covers every element
+        _lib.check(self.ctx._lib.ctb_decrypt_round_extract(
+            self.ctx._h, _ptr(acc), _ptr(sub.contiguous()) if sub is not None else None, _ptr(out.maps),
+            out.maps.shape[0], _ptr(out.kind), _ptr(out.base), out.numel, int(centered), _ptr(res), len(batch),
+            _stream()), "ctb_decrypt_round_extract")
+        self.meter.tick("Dec", self._elapsed(t0), count=len(batch))
+        return res
 
     # -- homomorphic ops --------------------------------------------------------
     def cc_add(self, a: Ciphertext, b: Ciphertext) -> Ciphertext:

@@ -31,13 +31,16 @@ from .ring import RingParams
 
 
 def concat_jobs(jobs: list[LinearJob], job_id: str) -> tuple[LinearJob, list[JobShape]]:
-    """Block-diagonal union of per-image jobs (site indices offset per image)."""
+    """Block-diagonal union of per-image jobs given as packed polynomials (site indices offset per
+    image).  The batched builders (linprot.conv_job_batch & co.) build such unions directly from
+    the raw tensors; this is for arbitrary job lists."""
     sites, xo, wo, oo = [], 0, 0, 0
     for j in jobs:
+        arr = j.shape.sites_array().astype(np.int64)
+        sites.append(arr + np.array([xo, wo, oo], dtype=np.int64))
         s = j.shape
-        sites.extend((x + xo, w + wo, o + oo) for x, w, o in s.sites)
         xo, wo, oo = xo + s.n_x, wo + s.n_w, oo + s.n_out
-    js = JobShape(job_id, xo, wo, oo, tuple(sites))
+    js = JobShape(job_id, xo, wo, oo, np.concatenate(sites) if sites else np.zeros((0, 3)))
     x = torch.cat([j.x_plain for j in jobs])
     w = torch.cat([j.w_plain for j in jobs])
     return LinearJob(js, x, w, None, jobs[0].plain_ring), [j.shape for j in jobs]
@@ -77,15 +80,27 @@ def offline(sess: Session, job: LinearJob, gen) -> tuple[linprot.MaskBundle, Cip
     return linprot.MaskBundle(js.job_id, r[:js.n_x], r[js.n_x:]), prod
 
 
-def online(sess: Session, job: LinearJob, bundle: linprot.MaskBundle, maskprod: CiphertextBatch, gen) -> torch.Tensor:
-    """Client encrypt + mask, server fused linear step, client decrypt - p.  Returns [n_out, N] mod t."""
+def online(sess: Session, job: LinearJob, bundle: linprot.MaskBundle, maskprod: CiphertextBatch, gen,
+           decode: bool = True, centered: bool = True) -> torch.Tensor:
+    """One online job, client and server co-resident (linprot.py:430-485):
+
+      client  pack + mask      ctb_pack_gather (x, x - r_x and w, w - r_w in one kernel per side)
+              encrypt          ctb_encrypt (device draws)
+      server  linear step      ctb_linear_online
+      client  decrypt + decode ctb_mul_prepared_strided + ctb_decrypt_round_extract (c - p,
+                               extraction and centring in the rounding kernel's epilogue)
+
+    decode=True returns the job's centred output tensor; decode=False (or a job without a decode
+    descriptor) returns the [n_out, N] mod-t polynomials decrypt(c) - p.  centered=False decodes to
+    residues in [0, t) (the reference's job.extract) instead of to_signed_matrix values."""
     js = job.shape
     cli, srv = sess.client, sess.server
+    mx, mw = job.masked(cli.ctx, bundle.r_x, bundle.r_w)
     cx = cli.encrypt_many(job.x_plain, sess.keys, gen)
     cw = cli.encrypt_many(job.w_plain, sess.keys, gen)
-    mx = linprot._plain_sub(cli, job.x_plain, bundle.r_x)
-    mw = linprot._plain_sub(cli, job.w_plain, bundle.r_w)
     c_slots, p_slots = linprot.linear_online(srv, cx, cw, mx, mw, js, maskprod)
+    if decode and job.out is not None:
+        return cli.decrypt_extract(c_slots, sess.keys, job.out, sub=p_slots, centered=centered)
     c = cli.decrypt_values(c_slots, sess.keys)
     return linprot._plain_sub(cli, c, p_slots)
 
@@ -94,51 +109,92 @@ def _sync():
     torch.cuda.synchronize()
 
 
-# ---------------------------------------------------------------------------------------- cfg4
+# ---------------------------------------------------------------------------------------- cfg3 / cfg4
 
-def cfg4_jobs(params, images: int = 32, seed: int = 4):
+def cfg3_tensors(images: int = 64, seed: int = 3):
+    """x in [0,2^8) (B,1,28,28), w in [-2^7,2^7) (5,1,5,5)."""
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    x = torch.randint(0, 256, (images, 1, 28, 28), generator=g, device="cuda", dtype=torch.int64)
+    w = torch.randint(-128, 128, (5, 1, 5, 5), generator=g, device="cuda", dtype=torch.int64)
+    return x, w
+
+
+def cfg3_builders(params, x, w):
+    """conv 1x28x28, 5 filters 5x5, stride 2: the stride-1 job with a stride-2 extraction."""
+    pr = params.plain_ring
+    return {"fwd": lambda: linprot.conv_job_batch("cfg3", x, w, packing.ConvShape(28, 28, 5, 0), pr, stride=2)}
+
+
+def cfg4_tensors(images: int = 32, seed: int = 4):
     """x in [0,2^8) (B,3,32,32), w in [-2^7,2^7) (64,3,3,3), gy in [-2^7,2^7) (B,64,32,32)."""
     g = torch.Generator(device="cuda")
     g.manual_seed(seed)
     x = torch.randint(0, 256, (images, 3, 32, 32), generator=g, device="cuda", dtype=torch.int64)
     w = torch.randint(-128, 128, (64, 3, 3, 3), generator=g, device="cuda", dtype=torch.int64)
     gy = torch.randint(-128, 128, (images, 64, 32, 32), generator=g, device="cuda", dtype=torch.int64)
+    return x, w, gy
+
+
+def cfg4_builders(params, x, w, gy):
+    """The trainer's lowering of one conv layer's forward and backward (train.py:478-494), batched:
+    fwd conv(x, w), grad-w conv_grad_w(x, gy) with the 32x32 gradient as the kernel, grad-x
+    conv(gy, rot180(w)^T)."""
     pr = params.plain_ring
     wrot = torch.flip(w, dims=(2, 3)).transpose(0, 1).contiguous()          # train.py:487
-    fwd = [linprot.conv_job(f"fwd{b}", x[b], w, packing.ConvShape(32, 32, 3, 1), pr) for b in range(images)]
-    gw = [linprot.conv_grad_w_job(f"gw{b}", x[b], gy[b], packing.ConvShape(32, 32, 32, 1), pr) for b in range(images)]
-    gx = [linprot.conv_job(f"gx{b}", gy[b], wrot, packing.ConvShape(32, 32, 3, 1), pr) for b in range(images)]
-    return (x, w, gy), {"fwd": fwd, "gw": gw, "gx": gx}
+    return {
+        "fwd": lambda: linprot.conv_job_batch("fwd", x, w, packing.ConvShape(32, 32, 3, 1), pr),
+        "gw": lambda: linprot.conv_grad_w_job_batch("gw", x, gy, packing.ConvShape(32, 32, 32, 1), pr),
+        "gx": lambda: linprot.conv_job_batch("gx", gy, wrot, packing.ConvShape(32, 32, 3, 1), pr),
+    }
 
 
-def run_config(sess: Session, per_image: dict, gen, check=None) -> dict:
-    """Offline then online for every job family; returns timings (ms) and outputs."""
-    res = {"offline_ms": 0.0, "online_ms": 0.0, "outputs": {}, "sites": 0, "ccmul": 0}
-    batched = {k: concat_jobs(v, k) for k, v in per_image.items()}
+def run_config(sess: Session, builders: dict, gen) -> dict:
+    """Offline, then the online phase twice over every job family:
+
+      online_ms        the whole client + server step from the raw tensors: job build (cached
+                       descriptors), pack + mask, encrypt, server step, decrypt + extract + centre
+      online_core_ms   the same without encode / decode: operands packed and masked before the
+                       timer, the result left as [n_out, N] mod-t polynomials (decrypt(c) - p)
+    Returns timings (ms, host-timed around device-synchronised regions) and the decoded outputs."""
+    res = {"offline_ms": 0.0, "online_ms": 0.0, "online_core_ms": 0.0, "outputs": {}, "sites": 0, "ccmul": 0}
+    shapes = {k: b() for k, b in builders.items()}
     prepared = {}
     _sync()
     t0 = time.perf_counter()
-    for k, (job, _) in batched.items():
+    for k, job in shapes.items():
         prepared[k] = offline(sess, job, gen)
-        res["ccmul"] += len(job.shape.sites)
+        res["ccmul"] += len(job.shape)
     _sync()
     res["offline_ms"] = 1e3 * (time.perf_counter() - t0)
+    # online, encode/decode included
     _sync()
     t0 = time.perf_counter()
-    outs = {}
-    for k, (job, _) in batched.items():
+    for k, build in builders.items():
+        job = build()
         bundle, mp = prepared[k]
-        outs[k] = online(sess, job, bundle, mp, gen)
-        res["sites"] += len(job.shape.sites)
+        res["outputs"][k] = online(sess, job, bundle, mp, gen)
+        res["sites"] += len(job.shape)
     _sync()
     res["online_ms"] = 1e3 * (time.perf_counter() - t0)
-    # split back per image and extract (client-side decode, outside the timed region)
-    for k, (job, shapes) in batched.items():
-        o, parts = 0, []
-        for img_job, s in zip(per_image[k], shapes):
-            parts.append(img_job.extract(outs[k][o:o + s.n_out]))
-            o += s.n_out
-        res["outputs"][k] = torch.stack(parts)
+    # online core: pre-packed, pre-masked operands; no extraction (reuses the masks above: timing
+    # only, the outputs are discarded)
+    pre = {}
+    for k, build in builders.items():
+        job = build()
+        bundle, _ = prepared[k]
+        mx, mw = job.masked(sess.client.ctx, bundle.r_x, bundle.r_w)
+        pre[k] = (job, mx, mw)
+    _sync()
+    t0 = time.perf_counter()
+    for k, (job, mx, mw) in pre.items():
+        cli, srv = sess.client, sess.server
+        cx = cli.encrypt_many(job.x_plain, sess.keys, gen)
+        cw = cli.encrypt_many(job.w_plain, sess.keys, gen)
+        c_slots, p_slots = linprot.linear_online(srv, cx, cw, mx, mw, job.shape, prepared[k][1])
+        linprot._plain_sub(cli, cli.decrypt_values(c_slots, sess.keys), p_slots)
+    _sync()
+    res["online_core_ms"] = 1e3 * (time.perf_counter() - t0)
     return res
 
 
@@ -146,10 +202,6 @@ def conv_reference_float(x, w, pad):
     """Plain convolution on the GPU in float64 (exact at these magnitudes) -- a sanity check."""
     import torch.nn.functional as F
     return F.conv2d(x.double(), w.double(), padding=pad).round().to(torch.int64)
-
-
-def signed(t: torch.Tensor, modulus: int) -> torch.Tensor:
-    return packing.to_signed_tensor(t, modulus)
 
 
 # ---------------------------------------------------------------------------------------- cfg5
@@ -175,27 +227,29 @@ def cfg5_tensors(images: int = 32, seed: int = 5):
     }
 
 
-def cfg5_image_jobs(params, T: dict, b: int, n_chunk: int) -> dict:
-    """Per image: the trainer's linear jobs (train.py:353-494 lowering) plus the stride-2 and
-    FC-chunk lowerings the reference lacks; 12,733 sites at N=8192."""
+def cfg5_builders(params, T: dict, lo: int, hi: int, n_chunk: int) -> dict:
+    """Images lo..hi-1 of the trainer's linear jobs (train.py:353-494 lowering) batched per family,
+    plus the stride-2 and FC-chunk lowerings the reference lacks; 12,733 sites per
+    image at N=8192.  conv2's stride-2 forward keeps only the strided outputs in its extraction."""
     pr = params.plain_ring
     CS = packing.ConvShape
+    sl = slice(lo, hi)
     w2rot = torch.flip(T["w2"], dims=(2, 3)).transpose(0, 1).contiguous()
-    gy2u = upsample2(T["gy2"][b], 32)
-    xfc = T["a2"][b].reshape(-1)
-    jobs = {
-        "conv1_fwd": linprot.conv_job(f"c1f{b}", T["x"][b], T["w1"], CS(32, 32, 3, 1), pr),
-        "conv1_gw": linprot.conv_grad_w_job(f"c1w{b}", T["x"][b], T["gy1"][b], CS(32, 32, 32, 1), pr),
-        "conv2_fwd": linprot.conv_job(f"c2f{b}", T["a1"][b], T["w2"], CS(32, 32, 3, 1), pr),
-        "conv2_gx": linprot.conv_job(f"c2x{b}", gy2u, w2rot, CS(32, 32, 3, 1), pr),
-        "conv2_gw": linprot.conv_grad_w_job(f"c2w{b}", T["a1"][b], gy2u, CS(32, 32, 32, 1), pr),
-        "fc_gx": linprot.fc_job(f"fcx{b}", T["gfc"][b], T["wfc"].t().contiguous(), pr),
+    gy2u = upsample2(T["gy2"][sl], 32)
+    xfc = T["a2"][sl].reshape(hi - lo, -1)
+    b = {
+        "conv1_fwd": lambda: linprot.conv_job_batch("c1f", T["x"][sl], T["w1"], CS(32, 32, 3, 1), pr),
+        "conv1_gw": lambda: linprot.conv_grad_w_job_batch("c1w", T["x"][sl], T["gy1"][sl], CS(32, 32, 32, 1), pr),
+        "conv2_fwd": lambda: linprot.conv_job_batch("c2f", T["a1"][sl], T["w2"], CS(32, 32, 3, 1), pr, stride=2),
+        "conv2_gx": lambda: linprot.conv_job_batch("c2x", gy2u, w2rot, CS(32, 32, 3, 1), pr),
+        "conv2_gw": lambda: linprot.conv_grad_w_job_batch("c2w", T["a1"][sl], gy2u, CS(32, 32, 32, 1), pr),
+        "fc_gx": lambda: linprot.fc_job_batch("fcx", T["gfc"][sl], T["wfc"].t().contiguous(), pr),
     }
-    for c, lo in enumerate(range(0, xfc.numel(), n_chunk)):
-        hi = lo + n_chunk
-        jobs[f"fc_fwd{c}"] = linprot.fc_job(f"fcf{b}_{c}", xfc[lo:hi], T["wfc"][:, lo:hi], pr)
-        jobs[f"fc_gw{c}"] = linprot.outer_job(f"fcw{b}_{c}", T["gfc"][b], xfc[lo:hi], pr)
-    return jobs
+    for c, c0 in enumerate(range(0, xfc.shape[1], n_chunk)):
+        xs = xfc[:, c0:c0 + n_chunk].contiguous()
+        b[f"fc_fwd{c}"] = (lambda xs=xs, c0=c0: linprot.fc_job_batch("fcf", xs, T["wfc"][:, c0:c0 + n_chunk], pr))
+        b[f"fc_gw{c}"] = (lambda xs=xs: linprot.outer_job_batch("fcw", T["gfc"][sl], xs, pr))
+    return b
 
 
 WEIGHT_GRADIENT_FAMILIES = ("conv1_gw", "conv2_gw", "fc_gw0", "fc_gw1")
@@ -203,34 +257,30 @@ WEIGHT_GRADIENT_FAMILIES = ("conv1_gw", "conv2_gw", "fc_gw0", "fc_gw1")
 
 def run_cfg5(sess: Session, T: dict, gen, group: int = 4, families=None) -> dict:
     """Offline + online for every image (processed in groups of `group` images to bound HBM),
-    outputs decoded per family; timings in ms (device-synchronised)."""
+    outputs decoded per family (centred); timings in ms (device-synchronised).  The online
+    time includes encode (pack + mask) and decode (extraction in the decrypt epilogue)."""
     P = sess.client.params
     images = T["x"].shape[0]
     res = {"offline_ms": {}, "online_ms": {}, "sites": {}, "outputs": {}}
     for g0 in range(0, images, group):
-        per_image = [cfg5_image_jobs(P, T, b, P.n) for b in range(g0, min(images, g0 + group))]
-        fams = families or list(per_image[0])
+        builders = cfg5_builders(P, T, g0, min(images, g0 + group), P.n)
+        fams = families or list(builders)
         for fam in fams:
-            jobs = [pi[fam] for pi in per_image]
-            job, shapes = concat_jobs(jobs, fam)
+            shape_job = builders[fam]()
             _sync()
             t0 = time.perf_counter()
-            bundle, mp = offline(sess, job, gen)
+            bundle, mp = offline(sess, shape_job, gen)
             _sync()
             t1 = time.perf_counter()
-            out = online(sess, job, bundle, mp, gen)
+            out = online(sess, builders[fam](), bundle, mp, gen)
             _sync()
             t2 = time.perf_counter()
             res["offline_ms"][fam] = res["offline_ms"].get(fam, 0.0) + 1e3 * (t1 - t0)
             res["online_ms"][fam] = res["online_ms"].get(fam, 0.0) + 1e3 * (t2 - t1)
-            res["sites"][fam] = res["sites"].get(fam, 0) + len(job.shape.sites)
-            o, parts = 0, []
-            for img_job, s in zip(jobs, shapes):
-                parts.append(img_job.extract(out[o:o + s.n_out]))
-                o += s.n_out
-            res["outputs"].setdefault(fam, []).extend(parts)
-            del bundle, mp, out
-    res["outputs"] = {k: torch.stack(v) for k, v in res["outputs"].items()}
+            res["sites"][fam] = res["sites"].get(fam, 0) + len(shape_job.shape)
+            res["outputs"].setdefault(fam, []).append(out)
+            del bundle, mp, out, shape_job
+    res["outputs"] = {k: torch.cat(v) for k, v in res["outputs"].items()}
     return res
 
 
@@ -244,7 +294,7 @@ def cfg5_reference_float(T: dict) -> dict:
     ref = {
         "conv1_fwd": conv(x, w1, 1),
         "conv1_gw": torch.stack([conv(x[b][:, None], gy1[b][:, None], 1).transpose(0, 1) for b in range(B)]),
-        "conv2_fwd": conv(a1, w2, 1),
+        "conv2_fwd": conv(a1, w2, 1)[:, :, ::2, ::2],
         "conv2_gx": conv(gy2u, w2rot, 1),
         "conv2_gw": torch.stack([conv(a1[b][:, None], gy2u[b][:, None], 1).transpose(0, 1) for b in range(B)]),
         "fc_gx": (gfc.double() @ wfc.double()).round().to(torch.int64),

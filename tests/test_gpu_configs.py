@@ -21,18 +21,14 @@ def sess4096():
 
 
 def test_cfg3_stride2_conv_batch64(sess4096):
-    from paper_2409_16675_b200 import linprot, packing, workloads as W
+    """Stride 2 as the stride-1 job whose extraction keeps every other output row / column."""
+    from paper_2409_16675_b200 import workloads as W
     P, sess = sess4096
-    g = torch.Generator(device="cuda")
-    g.manual_seed(3)
-    x = torch.randint(0, 256, (64, 1, 28, 28), generator=g, device="cuda", dtype=torch.int64)
-    w = torch.randint(-128, 128, (5, 1, 5, 5), generator=g, device="cuda", dtype=torch.int64)
-    jobs = {"fwd": [linprot.conv_job(f"c3_{b}", x[b], w, packing.ConvShape(28, 28, 5, 0), P.plain_ring)
-                    for b in range(64)]}
+    x, w = W.cfg3_tensors(64)
     gen = torch.Generator(device="cuda")
     gen.manual_seed(11)
-    r = W.run_config(sess, jobs, gen)
-    out = W.signed(r["outputs"]["fwd"], P.t)[:, :, ::2, ::2]          # stride-2 lowering
+    r = W.run_config(sess, W.cfg3_builders(P, x, w), gen)
+    out = r["outputs"]["fwd"]
     assert out.shape == (64, 5, 12, 12)
     assert torch.equal(out, W.conv_reference_float(x, w, 0)[:, :, ::2, ::2])
     assert r["sites"] == 320 and r["ccmul"] == 320
@@ -41,16 +37,16 @@ def test_cfg3_stride2_conv_batch64(sess4096):
 def test_cfg4_conv_fwd_bwd_batch32(sess4096):
     from paper_2409_16675_b200 import workloads as W
     P, sess = sess4096
-    (x, w, gy), jobs = W.cfg4_jobs(P, 32)
+    x, w, gy = W.cfg4_tensors(32)
     gen = torch.Generator(device="cuda")
     gen.manual_seed(12)
-    r = W.run_config(sess, jobs, gen)
+    r = W.run_config(sess, W.cfg4_builders(P, x, w, gy), gen)
     assert r["sites"] == 18432 and r["ccmul"] == 18432
-    assert torch.equal(W.signed(r["outputs"]["fwd"], P.t), W.conv_reference_float(x, w, 1))
+    assert torch.equal(r["outputs"]["fwd"], W.conv_reference_float(x, w, 1))
     ref_gw = torch.stack([W.conv_reference_float(x[b][:, None], gy[b][:, None], 1).transpose(0, 1) for b in range(32)])
-    assert torch.equal(W.signed(r["outputs"]["gw"], P.t), ref_gw)
+    assert torch.equal(r["outputs"]["gw"], ref_gw)
     wrot = torch.flip(w, dims=(2, 3)).transpose(0, 1).contiguous()
-    assert torch.equal(W.signed(r["outputs"]["gx"], P.t), W.conv_reference_float(gy, wrot, 1))
+    assert torch.equal(r["outputs"]["gx"], W.conv_reference_float(gy, wrot, 1))
 
 
 def test_cfg5_training_step_linear_n8192_batch32():
@@ -65,5 +61,5 @@ def test_cfg5_training_step_linear_n8192_batch32():
     ref = W.cfg5_reference_float(T)
     assert set(r["outputs"]) == set(ref)
     for fam, v in r["outputs"].items():
-        assert torch.equal(W.signed(v, P8.t), ref[fam]), fam
+        assert torch.equal(v, ref[fam]), fam
     assert sum(r["sites"][k] for k in W.WEIGHT_GRADIENT_FAMILIES) == 137856
