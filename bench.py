@@ -212,30 +212,115 @@ def _time_cpmul(torch, ctx, B, qs, t, steps, warm):
     return ms
 
 
+def _probe_f64(torch, lib, fn: str = "ctb_probe_bfly_f64"):
+    """Register-resident 50-bit FP64 butterflies/s (ctb_probe_bfly_f64) or bare products/s
+    (ctb_probe_modmul_f64)."""
+    import ctypes
+    sink = torch.zeros(1, dtype=torch.float64, device="cuda")
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    n = ctypes.c_uint64()
+    f = getattr(lib, fn)
+
+    def launch():
+        assert f(1000, ctypes.c_void_p(sink.data_ptr()), ctypes.byref(n), stream) == 0
+    for _ in range(2):
+        launch()
+    best = 0.0
+    for _ in range(3):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        launch()
+        e.record()
+        e.synchronize()
+        best = max(best, n.value / (s.elapsed_time(e) * 1e-3))
+    return best
+
+
+def _roof(modmuls: float, ms: float, peak: float, peak_name: str) -> dict:
+    achieved = modmuls / (ms * 1e-3)
+    return {"bound": "int", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gmodmul/s",
+            "frac": achieved / peak, "algorithmic_modmuls": int(modmuls), "t_min_ms": 1e3 * modmuls / peak,
+            "t_measured_ms": ms, "peak_source": peak_name,
+            "counted": "transform butterflies + slotwise products (paper_2409_16675_b200/workcount.py); "
+                       "exact rounding / CRT / lift arithmetic not counted, so frac is a lower bound"}
+
+
+def _cpu_protocol(secs: dict, cores: int, wall: float, shapes: dict, phase: str, reps: dict, label: str) -> dict:
+    from oracle import cpu_ops
+    ms = 1e3 * sum(cpu_ops.extrapolate(cpu_ops.job_counts(*dims)[phase], secs, cores) for dims in shapes.values())
+    return {"value": ms, "unit": "ms", "cores": cores, "kind": "port",
+            "sample": f"{label}: per-operation seconds of the oracle restatement (oracle/cpu_ops.py) measured on "
+                      f"{cores} processes at once ({', '.join(f'{k} x{v}' for k, v in reps.items())} per process, "
+                      f"{wall:.1f} s wall) x the reference meters' {phase} operation counts of the batch, spread over "
+                      f"{cores} cores (extrapolated, not a full run)",
+            "per_op_ms": {k: round(1e3 * v, 3) for k, v in secs.items()}}
+
+
 def run_extras(torch, steps):
-    """cfg2b (N=8192, 3 x 50-bit), cfg3 (64 images), cfg4 (32 images: fwd + grad-w + grad-x)."""
-    from paper_2409_16675_b200 import workloads as W
+    """cfg2b (N=8192, 3 x 50-bit), cfg3 (64 images), cfg4 (32 images: fwd + grad-w + grad-x), cfg5,
+    each with a roofline fraction and the reference's CPU path timed here on the host cores."""
+    from oracle import cpu_ops
+    from paper_2409_16675_b200 import _lib, workcount as WC, workloads as W
     from paper_2409_16675_b200.device import RnsContext
     from paper_2409_16675_b200.params import default_he_params, p8192_he_params
-    extras = {}
+    lib = _lib.load()
+    peak32 = probe_modmul_peak(torch, lib, 4, f64q_of_8=3)
+    peak64 = _probe_f64(torch, lib)
+    peak64_product = _probe_f64(torch, lib, "ctb_probe_modmul_f64")
+    src32 = "measured now: ctb_probe_modmul_mix(3), u32 (k_cpmul's product mix)"
+    src64 = ("measured now: ctb_probe_bfly_f64, the 64-bit-limb FP64 butterfly (product + add + sub + its share "
+             "of the lazy reduction, all on the FP64 pipe) register-resident; the bare-product probe "
+             "(ctb_probe_modmul_f64) is reported beside it")
+    # the reference's per-operation CPU costs, all host cores at once (bounded sample)
+    reps4 = {"Enc": 3, "Dec": 3, "CPMul": 3, "CCAdd": 10, "PPMul": 5, "CCMul": 1}
+    reps8 = {"Enc": 1, "Dec": 1, "CPMul": 2, "CCAdd": 5, "PPMul": 2, "CCMul": 1}
+    sec4, cores, wall4 = cpu_ops.op_seconds("p4096", reps4)
+    sec8, _, wall8 = cpu_ops.op_seconds("p8192", reps8)
+    extras = {"cpu_reference_ops": {"p4096_ms": {k: round(1e3 * v, 3) for k, v in sec4.items()},
+                                    "p8192_ms": {k: round(1e3 * v, 3) for k, v in sec8.items()},
+                                    "cores": cores, "kind": "port"}}
     P8 = p8192_he_params()
     ctx8 = RnsContext.get(P8.n, P8.cipher_ring.primes, P8.plain_ring.primes)
     ms = _time_cpmul(torch, ctx8, 4096, P8.cipher_ring.primes, P8.t, max(3, steps // 4), 2)
-    extras["cfg2b_p8192_cpmul"] = {"value": 4096 / (ms * 1e-3), "unit": UNIT, "ms_per_batch": ms,
-                                   "workload": "4096 CPMul, N=8192, q=3x50-bit (u64 residues), t=163841*147457"}
+    extras["cfg2b_p8192_cpmul"] = {
+        "value": 4096 / (ms * 1e-3), "unit": UNIT, "ms_per_batch": ms,
+        "workload": "4096 CPMul, N=8192, q=3x50-bit (u64 residues), t=163841*147457",
+        "roofline": dict(_roof(WC.cpmul(8192, 3) * 4096, ms, peak64, src64),
+                         frac_vs_bare_product_probe=WC.cpmul(8192, 3) * 4096 / (ms * 1e-3) / peak64_product,
+                         probes_g_per_s={"f64_butterfly": peak64 / 1e9, "f64_product": peak64_product / 1e9}),
+        "cpu_baseline": {"value": cores / sec8["CPMul"], "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"oracle he_ref.cp_mul at N=8192 / 3 x 50-bit (per-limb products + CRT), "
+                                   f"{reps8['CPMul']} CPMuls on each of {cores} processes at once"},
+    }
     P = default_he_params(4096)
+    L4, LT4 = len(P.cipher_ring.primes), len(P.plain_ring.primes)
     sess = W.Session.create(P)
+    K4 = int(sess.server.ctx._lib.ctb_tensor_aux_size(sess.server.ctx._h) or 17)
+    D4 = P.relin_digits
     gen = torch.Generator(device="cuda")
     gen.manual_seed(11)
+
+    def work(shapes, n, L, LT, K, D):
+        on = sum(WC.online_job(n, L, LT, *d) for d in shapes.values())
+        off = sum(WC.offline_job(n, L, K, D, *d) for d in shapes.values())
+        return on, off
+
     # cfg3: 64 images, 1x28x28, 5 filters 5x5, stride 2 (stride-1 job, stride-2 extraction)
     x3, w3 = W.cfg3_tensors(64)
     b3 = W.cfg3_builders(P, x3, w3)
     W.run_config(sess, b3, gen)  # warm
     r3 = W.run_config(sess, b3, gen)
     ok3 = bool(torch.equal(r3["outputs"]["fwd"], W.conv_reference_float(x3, w3, 0)[:, :, ::2, ::2]))
-    extras["cfg3_conv_stride2_b64"] = {"online_ms": r3["online_ms"], "online_core_ms": r3["online_core_ms"],
-                                       "offline_ms": r3["offline_ms"], "sites": r3["sites"],
-                                       "exact_vs_float64_conv": ok3}
+    on3, off3 = work(r3["shapes"], 4096, L4, LT4, K4, D4)
+    extras["cfg3_conv_stride2_b64"] = {
+        "online_ms": r3["online_ms"], "online_core_ms": r3["online_core_ms"], "offline_ms": r3["offline_ms"],
+        "sites": r3["sites"], "exact_vs_float64_conv": ok3,
+        "roofline": _roof(on3, r3["online_ms"], peak32, src32),
+        "roofline_offline": _roof(off3, r3["offline_ms"], peak32, src32),
+        "cpu_baseline": _cpu_protocol(sec4, cores, wall4, r3["shapes"], "online", reps4, "online phase, batch 64"),
+        "cpu_baseline_offline": _cpu_protocol(sec4, cores, wall4, r3["shapes"], "offline", reps4,
+                                              "offline phase, batch 64"),
+    }
     # cfg4: 32 images fwd + gw + gx
     x, w, gy = W.cfg4_tensors(32)
     b4 = W.cfg4_builders(P, x, w, gy)
@@ -248,6 +333,7 @@ def run_extras(torch, steps):
     ok4 = (bool(torch.equal(r4["outputs"]["fwd"], W.conv_reference_float(x, w, 1)))
            and bool(torch.equal(r4["outputs"]["gw"], ref_gw))
            and bool(torch.equal(r4["outputs"]["gx"], W.conv_reference_float(gy, wrot, 1))))
+    on4, off4 = work(r4["shapes"], 4096, L4, LT4, K4, D4)
     extras["cfg4_he_conv_fwd_bwd_ms"] = {
         "value": r4["online_ms"], "unit": "ms", "higher_is_better": False,
         "online_ms_runs": [round(r["online_ms"], 2) for r in runs],
@@ -255,6 +341,11 @@ def run_extras(torch, steps):
         "offline_ms": r4["offline_ms"], "offline_ccmul": r4["ccmul"],
         "offline_ccmul_per_s": r4["ccmul"] / (r4["offline_ms"] * 1e-3),
         "sites": r4["sites"], "exact_vs_float64_conv_fwd_gw_gx": ok4,
+        "roofline": _roof(on4, r4["online_ms"], peak32, src32),
+        "roofline_offline": _roof(off4, r4["offline_ms"], peak32, src32),
+        "cpu_baseline": _cpu_protocol(sec4, cores, wall4, r4["shapes"], "online", reps4, "online phase, batch 32"),
+        "cpu_baseline_offline": _cpu_protocol(sec4, cores, wall4, r4["shapes"], "offline", reps4,
+                                              "offline phase, batch 32"),
         "workload": "batch 32: conv 3->64 3x3 pad 1 fwd + grad-w + grad-x (train.py:478-494 lowering), "
                     "precompute protocol, client+server co-resident, device RNG sampling; value = online phase "
                     "from the raw tensors incl. pack + mask and decrypt + extract",
@@ -270,8 +361,18 @@ def run_extras(torch, steps):
     ref5 = W.cfg5_reference_float(T5)
     ok5 = all(bool(torch.equal(v, ref5[k])) for k, v in r5["outputs"].items())
     wg = W.WEIGHT_GRADIENT_FAMILIES
+    K8 = int(sess8.server.ctx._lib.ctb_tensor_aux_size(sess8.server.ctx._h) or 11)
+    L8, LT8, D8 = len(P8.cipher_ring.primes), len(P8.plain_ring.primes), P8.relin_digits
+    on5 = sum(WC.online_job(8192, L8, LT8, *d) for d in r5["shapes"].values())
+    off5 = sum(WC.offline_job(8192, L8, K8, D8, *d) for d in r5["shapes"].values())
+    on5_ms, off5_ms = sum(r5["online_ms"].values()), sum(r5["offline_ms"].values())
     extras["cfg5_train_step_linear_n8192"] = {
-        "online_ms": sum(r5["online_ms"].values()), "offline_ms": sum(r5["offline_ms"].values()),
+        "online_ms": on5_ms, "offline_ms": off5_ms,
+        "roofline": _roof(on5, on5_ms, peak64, src64),
+        "roofline_offline": _roof(off5, off5_ms, peak64, src64),
+        "cpu_baseline": _cpu_protocol(sec8, cores, wall8, r5["shapes"], "online", reps8, "online phase, batch 32"),
+        "cpu_baseline_offline": _cpu_protocol(sec8, cores, wall8, r5["shapes"], "offline", reps8,
+                                              "offline phase, batch 32"),
         "offline_ms_weight_gradient_jobs": sum(r5["offline_ms"][k] for k in wg),
         "ccmul_weight_gradient_jobs": sum(r5["sites"][k] for k in wg),
         "sites_total": sum(r5["sites"].values()), "exact_vs_float64": ok5,

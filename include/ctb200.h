@@ -286,6 +286,16 @@ int ctb_probe_modmul(int word_bytes, uint64_t iters, void* sink, uint64_t* modmu
  * products.  Same launch shape and contract as ctb_probe_modmul; bench.py divides by it. */
 int ctb_probe_modmul_mix(int f64q_of_8, uint64_t iters, void* sink, uint64_t* modmuls, void* stream);
 
+/* Instrumentation: the 50-bit product of the FP64 butterflies (64-bit limbs: exact integers in
+ * doubles, 6 FP64 operations per product, ntt.cuh f64_mulmod).  Same launch shape and contract as
+ * ctb_probe_modmul; bench.py divides the 50-bit configurations by it. */
+int ctb_probe_modmul_f64(uint64_t iters, void* sink, uint64_t* modmuls, void* stream);
+
+/* Instrumentation: the forward butterfly of the 64-bit-limb transforms (product + add + sub + its share
+ * of the once-per-pass reduction, ntt.cuh fwd_pass_f64), one modmul counted per butterfly: the FP64
+ * pipe's ceiling for the transforms' own arithmetic. */
+int ctb_probe_bfly_f64(uint64_t iters, void* sink, uint64_t* modmuls, void* stream);
+
 /* Self-check (not a reference interface): for every prime of 32-bit base `base` and every entry of
  * its FP64-quotient twiddle table, the butterfly product a*w mod p with the FP64-pipe quotient must
  * lie in [0, 2p) and be congruent to a*w for boundary inputs and `samples` pseudo-random 32-bit a

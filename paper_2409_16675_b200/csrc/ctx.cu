@@ -187,8 +187,8 @@ static int build_typed(Base& b, uint32_t logn, std::string& err, const uint64_t*
                 const size_t qe = (size_t)shape_q_off((int)logn, k) + ((size_t)ei << s) + tw_group_slot((int)logn, s, r, B);
                 std::memcpy(reinterpret_cast<unsigned char*>(f + 2 * ent) + 8 * qe, &wp, 8);
               }
-            } else {  // 64-bit limbs run the FP64 butterflies (ntt.cuh): w as a double
-              const double wd = (double)w;
+            } else {  // 64-bit limbs run the FP64 butterflies (ntt.cuh): w CENTRED, as a double
+              const double wd = w > p / 2 ? -(double)(p - w) : (double)w;
               uint64_t bw;
               std::memcpy(&bw, &wd, 8);
               f[e] = (T)bw;

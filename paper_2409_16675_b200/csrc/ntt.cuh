@@ -516,16 +516,22 @@ struct Strip {
 };
 
 // ---- FP64 butterflies for 64-bit limbs (primes < 2^50) --------------------------------
-// Residues are held as exact integers in doubles, signed and lazily reduced.  For |x| < 2^51:
-//   mulmod(x, w): hi = fl(x w), lo = x w - hi (exact, fma), q = rint(x * fl(w/p)) is within 1
-//   of x w / p (relative error < 2^-52 on a value < 2^51), r = (hi - q p) + lo is exact and
-//   |r| < p;
-//   center(x) = x - p rint(x / p) in [-p/2, p/2] (tiny slack) for |x| < 2^51.
-// rint uses the 1.5 * 2^52 magic constant (exact for |y| < 2^51).  Forward (CT) invariant:
-// inputs in (-2p, 2p) -> outputs in (-1.5p, 1.5p); inverse (GS): (-p, p) -> (-p, p).
-// The integer Shoup product costs ~4x its 32-bit form; on B200's full-rate FP64 pipe this
-// costs ~11 FP64 operations per butterfly (2x the integer modmul throughput, measured by
-// tools/probe/f64_modmul.cu).
+// Residues are held as exact integers in doubles, signed and lazily reduced.  Twiddles are stored
+// CENTRED, w in (-p/2, p/2] (ctx.cu), so |w/p| <= 1/2.  For |x w / p| < 2^51:
+//   mulmod(x, w): hi = fl(x w), lo = x w - hi (exact, fma), q = rint(x * wp) with wp = fl(w fl(1/p))
+//   (|wp - w/p| <= 2^-53 because |w/p| <= 1/2), so |q - x w / p| <= 1/2 + |x| 2^-53, and
+//   r = (hi - q p) + lo is exact with |r| <= (1/2 + |x| 2^-53) p  (< 0.95 p for |x| <= 3.5 p);
+//   center(x) = x - p rint(x / p) in [-p/2, p/2] (tiny slack), exact for |x| < 2^52.
+// rint uses the 1.5 * 2^52 magic constant (exact for |y| < 2^51); sums stay exact below 2^53.
+// Reduction schedule (bounds in units of p; p < 2^50, so 2^51 / p > 2):
+//   forward CT  X' = X + t, Y' = X - t, t = mulmod(Y): a pass starts from centred values (0.5) and
+//               runs its <= 4 stages WITHOUT reducing X: 0.5 -> 1.5 -> 2.5 -> 3.5 -> 4.5, the
+//               multiplied operand never exceeds 3.5 (|Y wp| <= 1.75 p < 2^51); all 16 values are
+//               centred once at the next pass boundary (3 ops per value per pass instead of 3 per
+//               butterfly per stage).
+//   inverse GS  X' = X + Y, Y' = mulmod(Y - X): X' is centred on every second stage (odd stages
+//               see inputs <= 1.5, even ones <= 1.5 + 1.5 = 3 for the difference, |.| wp <= 1.5 p).
+// About 9.5 FP64 operations per butterfly instead of 11 with full reduction every stage.
 struct F64Prime {
   double p, pinv;
 };
@@ -552,7 +558,7 @@ __device__ __forceinline__ double f64_center(double x, const F64Prime& P) {
 __device__ __forceinline__ double f64_from_u64(uint64_t x) {
   return __dadd_rn(__longlong_as_double((long long)(x | 0x4330000000000000ull)), -4503599627370496.0);
 }
-__device__ __forceinline__ uint64_t f64_to_canon(double x, const F64Prime& P) {  // x in (-2p, 2p)
+__device__ __forceinline__ uint64_t f64_to_canon(double x, const F64Prime& P) {  // |x| < 2^52
   double y = f64_center(x, P);                   // [-p/2 - e, p/2 + e]
   y = y < 0.0 ? __dadd_rn(y, P.p) : y;           // [0, p)
   return (uint64_t)__double_as_longlong(__dadd_rn(y, 4503599627370496.0)) & 0x000FFFFFFFFFFFFFull;
@@ -578,6 +584,11 @@ __device__ __forceinline__ void fwd_pass_f64(double (&x)[NttShape<LOGN>::E], TwS
   using Sh = NttShape<LOGN>;
   constexpr int S0 = Sh::pass_s(K), R = Sh::pass_r(K);
   constexpr int G = 1 << R;
+  static_assert(R <= 4, "the lazy forward schedule assumes at most 4 stages per pass");
+  if constexpr (K > 0) {
+#pragma unroll
+    for (int k = 0; k < Sh::E; ++k) x[k] = f64_center(x[k], P);  // <= 4.5 p -> 0.5 p
+  }
 #pragma unroll
   for (int gg = 0; gg < Sh::E / G; ++gg) {
     const int slot = tw_slot<LOGN, S0, R>(gg);
@@ -592,7 +603,7 @@ __device__ __forceinline__ void fwd_pass_f64(double (&x)[NttShape<LOGN>::E], TwS
 #pragma unroll
         for (int jj = 0; jj < h; ++jj) {
           const int a = gg * G + jb * 2 * h + jj;
-          const double X = f64_center(x[a], P);
+          const double X = x[a];
           const double t = f64_mulmod(x[a + h], w, wp, P.p);
           x[a] = __dadd_rn(X, t);
           x[a + h] = __dadd_rn(X, -t);
@@ -607,6 +618,7 @@ __device__ __forceinline__ void inv_pass_f64(double (&x)[NttShape<LOGN>::E], TwS
   using Sh = NttShape<LOGN>;
   constexpr int S0 = Sh::pass_s(K), R = Sh::pass_r(K);
   constexpr int G = 1 << R;
+  constexpr int DONE = LOGN - S0 - R;  // inverse stages run before this pass
 #pragma unroll
   for (int gg = 0; gg < Sh::E / G; ++gg) {
     const int slot = (1 << S0) - 1 - tw_slot<LOGN, S0, R>(gg);
@@ -614,6 +626,7 @@ __device__ __forceinline__ void inv_pass_f64(double (&x)[NttShape<LOGN>::E], TwS
 #pragma unroll
     for (int i = R - 1; i >= 0; --i) {
       const int h = 1 << (R - i - 1);
+      const bool reduce = ((DONE + (R - 1 - i)) & 1) == 1;  // every second global stage
 #pragma unroll
       for (int jb = 0; jb < (1 << i); ++jb) {
         double w, wp;
@@ -622,7 +635,8 @@ __device__ __forceinline__ void inv_pass_f64(double (&x)[NttShape<LOGN>::E], TwS
         for (int jj = 0; jj < h; ++jj) {
           const int a = gg * G + jb * 2 * h + jj;
           const double X = x[a], Y = x[a + h];
-          x[a] = f64_center(__dadd_rn(X, Y), P);
+          const double sum = __dadd_rn(X, Y);
+          x[a] = reduce ? f64_center(sum, P) : sum;
           x[a + h] = f64_mulmod(__dadd_rn(Y, -X), w, wp, P.p);
         }
       }
@@ -659,7 +673,8 @@ __device__ __forceinline__ void ntt_fwd_regs(T (&x)[NttShape<LOGN>::E], Exchange
   if constexpr (sizeof(T) == 8 && K != 0) {
     __trap();  // 64-bit limbs transform whole polynomials (never split)
   } else if constexpr (sizeof(T) == 8) {
-    // 64-bit limbs: FP64 butterflies, inputs < 4p (< 2^52), outputs canonical [0, p)
+    // 64-bit limbs: FP64 butterflies, inputs < 4p (< 2^52), outputs canonical [0, p) (the lazy
+    // schedule leaves |d| <= 4.5 p, which f64_to_canon reduces exactly)
     const F64Prime P{(double)p, __drcp_rn((double)p)};
     double d[Sh::E];
 #pragma unroll

@@ -46,7 +46,77 @@ __global__ void __launch_bounds__(256) k_probe_mix(uint32_t* sink, uint64_t iter
   for (int j = 0; j < CHAINS; ++j) acc ^= a[j];
   if (acc == 0x5eedu) sink[0] = acc;
 }
+// The 50-bit product of the FP64 butterflies (ntt.cuh f64_mulmod): exact integers in doubles,
+// centred twiddle, x w = hi + lo, q = rint(x w/p), r = (hi - q p) + lo -- 6 FP64 operations.
+__global__ void __launch_bounds__(256) k_probe_f64(double* sink, uint64_t iters, double p, double w, double wp) {
+  double a[CHAINS];
+#pragma unroll
+  for (int j = 0; j < CHAINS; ++j) a[j] = (double)((threadIdx.x * 131 + blockIdx.x * 7 + j) % 1000003);
+  for (uint64_t i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < CHAINS; ++j) a[j] = f64_mulmod(a[j], w, wp, p);
+  }
+  double acc = 0;
+#pragma unroll
+  for (int j = 0; j < CHAINS; ++j) acc += a[j];
+  if (acc == 12345.0) sink[0] = acc;
+}
+// The forward butterfly of the 64-bit-limb transforms as the kernels run it (ntt.cuh fwd_pass_f64):
+// t = mulmod(Y, w), X' = X + t, Y' = X - t, every value centred once per 4 stages.  On the FP64
+// pipe the butterfly's additions and its share of the lazy reduction cost as much as products, so
+// this -- not the bare product -- is the ceiling of the transforms' own arithmetic; one modmul
+// counted per butterfly.
+__global__ void __launch_bounds__(256) k_probe_f64_bfly(double* sink, uint64_t iters, double p, double w,
+                                                        double wp) {
+  constexpr int PAIRS = CHAINS / 2;
+  const F64Prime P{p, 1.0 / p};
+  double x[CHAINS];
+#pragma unroll
+  for (int j = 0; j < CHAINS; ++j) x[j] = (double)((threadIdx.x * 131 + blockIdx.x * 7 + j) % 1000003);
+  for (uint64_t i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int st = 0; st < 4; ++st) {
+#pragma unroll
+      for (int j = 0; j < PAIRS; ++j) {
+        const double X = x[2 * j];
+        const double t = f64_mulmod(x[2 * j + 1], w, wp, p);
+        x[2 * j] = __dadd_rn(X, t);
+        x[2 * j + 1] = __dadd_rn(X, -t);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < CHAINS; ++j) x[j] = f64_center(x[j], P);
+  }
+  double acc = 0;
+#pragma unroll
+  for (int j = 0; j < CHAINS; ++j) acc += x[j];
+  if (acc == 12345.0) sink[0] = acc;
+}
 }  // namespace
+
+extern "C" int ctb_probe_bfly_f64(uint64_t iters, void* sink, uint64_t* modmuls, void* stream) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)sms * 8, block = 256;
+  const uint64_t p = 1125899906826241ull;
+  const double w = -(double)(p / 3);
+  k_probe_f64_bfly<<<grid, block, 0, (cudaStream_t)stream>>>((double*)sink, iters, (double)p, w, w * (1.0 / (double)p));
+  if (modmuls) *modmuls = (uint64_t)grid * block * (CHAINS / 2) * 4 * iters;
+  return cuda_status(cudaGetLastError(), "ctb_probe_bfly_f64");
+}
+
+extern "C" int ctb_probe_modmul_f64(uint64_t iters, void* sink, uint64_t* modmuls, void* stream) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)sms * 8, block = 256;
+  const uint64_t p = 1125899906826241ull;  // ntt_primes(8192, 50, 3)[0]
+  const double w = -(double)(p / 3);        // a centred twiddle
+  k_probe_f64<<<grid, block, 0, (cudaStream_t)stream>>>((double*)sink, iters, (double)p, w, w * (1.0 / (double)p));
+  if (modmuls) *modmuls = (uint64_t)grid * block * CHAINS * iters;
+  return cuda_status(cudaGetLastError(), "ctb_probe_modmul_f64");
+}
 
 extern "C" int ctb_probe_modmul_mix(int f64q_of_8, uint64_t iters, void* sink, uint64_t* modmuls, void* stream) {
   int dev = 0, sms = 0;

@@ -240,6 +240,7 @@ class He:
         self.L = self.ctx.L
         self._delta_res = [params.delta % p for p in self.ctx.q_primes]
         self._zero_plain = None
+        self._draws = None
 
     # -- helpers --------------------------------------------------------------
     def _t0(self) -> float:
@@ -373,7 +374,7 @@ class He:
     def _device_draws(self, B: int, gen: torch.Generator) -> torch.Tensor:
         """int8 draws [B*3, N] from ctb_sample_draws, keyed by the generator's seed and
         Philox offset (advanced by B, so successive calls draw fresh values)."""
-        out = torch.empty((B * 3, self.params.n), dtype=torch.int8, device="cuda")
+        out = self._draw_scratch(B * 3 * self.params.n).view(B * 3, self.params.n)
         seed = gen.initial_seed() & ((1 << 64) - 1)
         first = gen.get_offset()
         gen.set_offset(first + 4 * B)   # CUDA Philox offsets move in multiples of 4
@@ -381,6 +382,17 @@ class He:
                                                   int(self.params.error_bound), _ptr(out), B, _stream()),
                    "ctb_sample_draws")
         return out
+
+    def _draw_scratch(self, nbytes: int) -> torch.Tensor:
+        """Per-evaluator int8 scratch for device draws, grown geometrically and reused (stream-ordered:
+        every consumer of the draws is queued before the next encryption overwrites them).  A fresh
+        sub-megabyte allocation per call occasionally cost tens of ms in the caching allocator's
+        small-block pool (cudaMalloc of a new segment) inside cfg5's online phase."""
+        buf = self._draws
+        if buf is None or buf.numel() < nbytes:
+            size = 1 << max(20, (nbytes - 1).bit_length())
+            buf = self._draws = torch.empty(size, dtype=torch.int8, device="cuda")
+        return buf[:nbytes]
 
     def _s_prep(self, keys, power: int) -> torch.Tensor:
         s = keys.secret.data

@@ -149,6 +149,11 @@ def cfg4_builders(params, x, w, gy):
     }
 
 
+def job_dims(js: JobShape) -> tuple[int, int, int, int]:
+    """(n_x, n_w, n_out, sites) of a job: what the roofline work counts (workcount.py) need."""
+    return js.n_x, js.n_w, js.n_out, len(js)
+
+
 def run_config(sess: Session, builders: dict, gen) -> dict:
     """Offline, then the online phase twice over every job family:
 
@@ -159,6 +164,7 @@ def run_config(sess: Session, builders: dict, gen) -> dict:
     Returns timings (ms, host-timed around device-synchronised regions) and the decoded outputs."""
     res = {"offline_ms": 0.0, "online_ms": 0.0, "online_core_ms": 0.0, "outputs": {}, "sites": 0, "ccmul": 0}
     shapes = {k: b() for k, b in builders.items()}
+    res["shapes"] = {k: job_dims(j.shape) for k, j in shapes.items()}
     prepared = {}
     _sync()
     t0 = time.perf_counter()
@@ -261,7 +267,7 @@ def run_cfg5(sess: Session, T: dict, gen, group: int = 4, families=None) -> dict
     time includes encode (pack + mask) and decode (extraction in the decrypt epilogue)."""
     P = sess.client.params
     images = T["x"].shape[0]
-    res = {"offline_ms": {}, "online_ms": {}, "sites": {}, "outputs": {}}
+    res = {"offline_ms": {}, "online_ms": {}, "sites": {}, "outputs": {}, "shapes": {}}
     for g0 in range(0, images, group):
         builders = cfg5_builders(P, T, g0, min(images, g0 + group), P.n)
         fams = families or list(builders)
@@ -277,7 +283,10 @@ def run_cfg5(sess: Session, T: dict, gen, group: int = 4, families=None) -> dict
             t2 = time.perf_counter()
             res["offline_ms"][fam] = res["offline_ms"].get(fam, 0.0) + 1e3 * (t1 - t0)
             res["online_ms"][fam] = res["online_ms"].get(fam, 0.0) + 1e3 * (t2 - t1)
+            res.setdefault("online_ms_calls", {}).setdefault(fam, []).append(round(1e3 * (t2 - t1), 2))
             res["sites"][fam] = res["sites"].get(fam, 0) + len(shape_job.shape)
+            prev = res["shapes"].get(fam, (0, 0, 0, 0))
+            res["shapes"][fam] = tuple(a + b for a, b in zip(prev, job_dims(shape_job.shape)))
             res["outputs"].setdefault(fam, []).append(out)
             del bundle, mp, out, shape_job
     res["outputs"] = {k: torch.cat(v) for k, v in res["outputs"].items()}
