@@ -195,6 +195,17 @@ int ctb_plain_scatter(const ctb_ctx_t* ctx, const uint64_t* in, const uint64_t* 
                       uint32_t n_maps, const int32_t* kind, const int64_t* base, uint64_t dst_len, int centered,
                       int64_t* out, uint64_t n_slots, void* stream);
 
+/* Dense bit-packed transfer format (not a reference format: the end-to-end path's PCIe leg).
+ * `count` values of `bits` bits (uint32 values for word_bytes 4, uint64 for 8; values must be
+ * < 2^bits) form one little-endian bitstream, value j at bits [j*bits, (j+1)*bits), in
+ * ctb_bits_words(bits, count) uint32 words -- e.g. 30-bit residues at 3.75 B instead of 4 B and
+ * 50-bit plaintexts at 6.25 B instead of 8 B.  Device buffers, stream-ordered. */
+uint64_t ctb_bits_words(uint32_t bits, uint64_t count);
+int ctb_bits_pack(const ctb_ctx_t* ctx, int word_bytes, const void* in, uint32_t bits, uint32_t* out, uint64_t count,
+                  void* stream);
+int ctb_bits_unpack(const ctb_ctx_t* ctx, int word_bytes, const uint32_t* in, uint32_t bits, void* out, uint64_t count,
+                    void* stream);
+
 /* Wire format: residues [n][L][N] <-> positional little-endian 64-bit words
  * [n][N][W], W = ctb_ctx_pos_words = ring.RingParams.limb_count (ring.py:147,
  * ring_to_bytes / ring_from_bytes ring.py:592-615; input words reduced mod q). */

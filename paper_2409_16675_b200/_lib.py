@@ -58,6 +58,9 @@ SIGNATURES: dict[str, tuple] = {
                                _c_void_p, _u64, _c_void_p]),
     "ctb_plain_scatter": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _u32, _c_void_p, _c_void_p, _u64, _int,
                                  _c_void_p, _u64, _c_void_p]),
+    "ctb_bits_words": (_u64, [_u32, _u64]),
+    "ctb_bits_pack": (_int, [_c_void_p, _int, _c_void_p, _u32, _c_void_p, _u64, _c_void_p]),
+    "ctb_bits_unpack": (_int, [_c_void_p, _int, _c_void_p, _u32, _c_void_p, _u64, _c_void_p]),
     "ctb_ctx_pos_words": (_int, [_c_void_p]),
     "ctb_rns_to_pos": (_int, [_c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_pos_to_rns": (_int, [_c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),

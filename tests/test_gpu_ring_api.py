@@ -183,3 +183,63 @@ def test_small_moduli_outside_the_plain_context(bits, count):
     assert ring.ring_scalar_mul(a, c).to_ints() == [x * c % m for x in ai]
     want = R.crt_combine(R.ring_mul_rns(R.to_rns(ai, primes), R.to_rns(bi, primes), primes), primes)
     assert ring.ring_mul(a, b).to_ints() == [int(v) for v in want]
+
+
+def _pack_ref(vals, bits):
+    """Host reference of the dense packed format: value j at bits [j*bits, (j+1)*bits), LE words."""
+    acc, nb, out = 0, 0, []
+    for v in vals:
+        acc |= int(v) << nb
+        nb += bits
+        while nb >= 32:
+            out.append(acc & 0xFFFFFFFF)
+            acc >>= 32
+            nb -= 32
+    if nb:
+        out.append(acc & 0xFFFFFFFF)
+    return np.array(out, dtype=np.uint64).astype(np.uint32)
+
+
+@pytest.mark.parametrize("bits,word", [(30, 4), (17, 4), (32, 4), (50, 8), (35, 8), (64, 8), (1, 4)])
+def test_bits_pack_roundtrip_matches_host_reference(bits, word):
+    import torch
+    from paper_2409_16675_b200.device import RnsContext
+    from paper_2409_16675_b200.params import default_he_params
+    P = default_he_params(4096)
+    ctx = RnsContext.get(P.n, P.cipher_ring.primes, P.plain_ring.primes)
+    rng = np.random.default_rng(bits)
+    count = 4096 * 3 + 32
+    hi = 1 << bits
+    vals = rng.integers(0, hi, size=count, dtype=np.uint64) if bits < 64 else rng.integers(0, 1 << 63, size=count, dtype=np.uint64) * 2 + 1
+    vals[:3] = [0, hi - 1, hi >> 1] if bits < 64 else [0, (1 << 64) - 1, 1 << 63]
+    dt = torch.int32 if word == 4 else torch.int64
+    x = torch.from_numpy(vals.astype(np.uint32 if word == 4 else np.uint64).view(np.int32 if word == 4 else np.int64)).cuda()
+    packed = ctx.pack_bits(x, bits)
+    assert np.array_equal(packed.cpu().numpy().view(np.uint32), _pack_ref(vals.tolist(), bits))
+    back = ctx.unpack_bits(packed, bits, (count,), dt)
+    assert torch.equal(back, x)
+
+
+def test_cpmul_host_packed_equals_device_path():
+    import torch
+    from paper_2409_16675_b200.device import RnsContext
+    from paper_2409_16675_b200.params import default_he_params
+    P = default_he_params(4096)
+    qs = P.cipher_ring.primes
+    ctx = RnsContext.get(P.n, qs, P.plain_ring.primes)
+    B = 37
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    ct = torch.empty((B, 2, len(qs), P.n), dtype=torch.int32, device="cuda")
+    for i, q in enumerate(qs):
+        ct[:, :, i] = torch.randint(0, q, (B, 2, P.n), generator=g, device="cuda").to(torch.int32)
+    pt = torch.randint(0, P.t, (B, P.n), generator=g, device="cuda")
+    want = ctx.cpmul(ct, pt)
+    ctp = ctx.pack_bits(ct, ctx.q_bits).cpu().pin_memory()
+    ptp = ctx.pack_bits(pt, ctx.t_bits).cpu().pin_memory()
+    outp = torch.empty_like(ctp).pin_memory()
+    assert ctx.q_bits == 30 and ctx.t_bits == 50
+    assert ctp.numel() * 4 == B * 2 * len(qs) * P.n * 30 // 8
+    ctx.cpmul_host_packed(ctp, ptp, outp, B, chunks=4)
+    torch.cuda.synchronize()
+    assert torch.equal(ctx.unpack_bits(outp.cuda(), 30, tuple(want.shape), torch.int32), want)
