@@ -396,13 +396,35 @@ __global__ void __launch_bounds__(256, sizeof(TQ) == 8 ? CTB_ROUND64_MINB : 3) k
                                                       const __grid_constant__ TensorConsts<TQ> c, uint32_t n,
                                                       uint64_t total) {
   const int L = LC ? LC : c.L, K = KC ? KC : c.K, K2 = K2C ? K2C : c.K2;
-  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
+  // The K aux residues of the NEXT grid-stride item are copied into this thread's slots of a
+  // double-buffered shared tile (cp.async) while the current item computes: the 11-17 strided
+  // loads per coefficient were the kernel's top stall (long scoreboard) at its register-capped
+  // occupancy.  Each thread reads only what it copied, so no block barrier is needed.
+  extern __shared__ uint32_t hbuf[];   // [2][K][blockDim.x]
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  auto issue = [&](uint64_t gg, int slot) {
+    if (gg < total) {
+      const uint64_t poly = gg >> pow2_shift(n), i = gg & (n - 1);
+#pragma unroll
+      for (int k = 0; k < (KC ? KC : MAXA); ++k) {
+        if (!KC && k >= K) break;
+        cp_async4(hbuf + ((size_t)slot * K + k) * blockDim.x + threadIdx.x, H + (poly * K + k) * n + i);
+      }
+    }
+    cp_async_commit();
+  };
+  uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  issue(g, 0);
+  int slot = 0;
+  for (; g < total; g += stride, slot ^= 1) {
+    issue(g + stride, slot ^ 1);
+    cp_async_wait<1>();
     const uint64_t poly = g >> pow2_shift(n), i = g & (n - 1);   // poly = b * 3 + part
     uint32_t h[MAXA];
 #pragma unroll
     for (int k = 0; k < (KC ? KC : MAXA); ++k) {
       if (!KC && k >= K) break;
-      h[k] = H[(poly * K + k) * n + i];
+      h[k] = hbuf[((size_t)slot * K + k) * blockDim.x + threadIdx.x];
     }
     // h mod q_i
     TQ hq[MAXQ];
@@ -1244,18 +1266,22 @@ extern "C" int ctb_tensor_round(const ctb_ctx_t* ctx, const uint32_t* h_aux, voi
   cudaStream_t s = (cudaStream_t)stream;
   const int L = c->tensor->L, K = c->tensor->K, K2 = c->tensor->K2;
   const unsigned grid = grid_stride(total, 4);
+  // double-buffered aux residues: at most 2 x MAXA x 256 words = 40 KB, below the 48 KB default
+  const size_t smem = 2 * (size_t)K * 256 * sizeof(uint32_t);
   if (c->base[BASE_Q].word == 4) {
     const auto& tc = *reinterpret_cast<const TensorConsts<uint32_t>*>(c->tensor->host.data());
     if (L == 7 && K == 17 && K2 == 10 && c->tensor->q_lead)
-      k_tensor_round<uint32_t, 7, 17, 10><<<grid, 256, 0, s>>>(h_aux, (uint32_t*)out, tc, c->n, total);
-    else k_tensor_round<uint32_t, 0, 0, 0><<<grid, 256, 0, s>>>(h_aux, (uint32_t*)out, tc, c->n, total);
+      k_tensor_round<uint32_t, 7, 17, 10><<<grid, 256, smem, s>>>(h_aux, (uint32_t*)out, tc, c->n, total);
+    else
+      k_tensor_round<uint32_t, 0, 0, 0><<<grid, 256, smem, s>>>(h_aux, (uint32_t*)out, tc, c->n, total);
   } else {
     const auto& tc = *reinterpret_cast<const TensorConsts<uint64_t>*>(c->tensor->host.data());
     bool p2_lead = true;  // P2 = aux primes 0..K2-1 (64-bit limbs: no cipher prime is an aux prime)
     for (int k = 0; k < K2; ++k) p2_lead = p2_lead && tc.p2_idx[k] == k;
     if (L == 3 && K == 11 && K2 == 7 && p2_lead)
-      k_tensor_round<uint64_t, 3, 11, 7><<<grid, 256, 0, s>>>(h_aux, (uint64_t*)out, tc, c->n, total);
-    else k_tensor_round<uint64_t, 0, 0, 0><<<grid, 256, 0, s>>>(h_aux, (uint64_t*)out, tc, c->n, total);
+      k_tensor_round<uint64_t, 3, 11, 7><<<grid, 256, smem, s>>>(h_aux, (uint64_t*)out, tc, c->n, total);
+    else
+      k_tensor_round<uint64_t, 0, 0, 0><<<grid, 256, smem, s>>>(h_aux, (uint64_t*)out, tc, c->n, total);
   }
   return cuda_status(cudaGetLastError(), "ctb_tensor_round");
 }

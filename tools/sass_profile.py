@@ -13,6 +13,9 @@ path = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
 txt = (gzip.open(path, "rt") if path.endswith(".gz") else open(path)).read()
 rows = list(csv.reader(io.StringIO(txt)))
+# several launches may be concatenated (one "Kernel Name" block each): keep the first
+starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] + [len(rows)]
+rows = rows[starts[0]:starts[1]]
 hdr = rows[1]
 ix = {h: i for i, h in enumerate(hdr)}
 ex = collections.Counter()
