@@ -973,7 +973,7 @@ extern "C" int ctb_pointwise_mul(const ctb_ctx_t* ctx, int base, const void* a, 
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
   const uint64_t total = n_polys * b->size() * (uint64_t)c->n;
   if (!total) return OK;
-  const unsigned grid = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
+  const unsigned grid = grid_stride(total, 16);  // SM count of the current device x 16 CTAs
   cudaStream_t s = (cudaStream_t)stream;
   if (b->word == 4)
     k_pointwise<uint32_t><<<grid, 256, 0, s>>>((const uint32_t*)a, (const uint32_t*)bb, (uint32_t*)out,

@@ -849,18 +849,12 @@ k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict
   // recomputed from re-read operands, which measured faster than a second strip)
   constexpr bool TWO = site_strips<LOGN>() == 2;
   T* strip = gsm + Ex::WORDS + ntt_tid<LOGN>();
-  const int k = blockIdx.x % K;
-  const uint32_t slot = blockIdx.x / K;
-  const uint32_t nslots = (gridDim.x - k + K - 1) / K;
-  const uint32_t step = nslots * GROUPS;
-  PrimeRegs<T> pr(tabs + k);
-  const T* twp = pr.fwd;
-  if constexpr (SMEM_TW) {
-    stage_twiddles(pr.fwd, tw_sm, TW_WORDS, Sh::THREADS * GROUPS);
-    __syncthreads();
-    twp = tw_sm;
-  }
-  const TwSrc<T, SMEM_TW> tw{twp};
+  // Work units are (aux prime, site) pairs in prime-major order; CTA b takes the contiguous range
+  // [b U / G, (b + 1) U / G) of the U = K * nsite units, so every SM gets the same number of
+  // products whatever gcd(K, SM count) is (K = 17 on 148 SMs left 12 SMs idle with one CTA per
+  // prime), and a CTA switches prime -- restaging its twiddle table -- at most a few times.
+  const uint64_t U = (uint64_t)K * nsite;
+  const uint64_t u0 = U * blockIdx.x / gridDim.x, u1 = U * (blockIdx.x + 1) / gridDim.x;
   const size_t N = Sh::N, KN = (size_t)K * N;
   using EV = EvalVec<T, LOGN>;
   auto ld = [&](const T* base, int i, T (&v)[EV::VEC]) {
@@ -868,62 +862,79 @@ k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict
     else EV::load(base, i, v);
   };
   T y[Sh::E];
-  auto store = [&](uint32_t s, int part) {
-    T* dst = H + ((size_t)s * 3 + part) * KN + k * N + coef_base<LOGN>();
-#pragma unroll
-    for (int j = 0; j < Sh::E; ++j) dst[coef_off<LOGN>(j)] = csub(y[j], pr.p);
-  };
 #pragma unroll 1
-  for (uint32_t s = slot * GROUPS + group; s < nsite; s += step) {
-    const T* a0p = AX + (size_t)sx[s] * 2 * KN + k * N;
-    const T* b0p = AW + (size_t)sw[s] * 2 * KN + k * N;
-    if (ntt_tid<LOGN>() == 0 && s + step < nsite) {  // next item's operands towards L2
-      const T* na = AX + (size_t)sx[s + step] * 2 * KN + k * N;
-      const T* nb = AW + (size_t)sw[s + step] * 2 * KN + k * N;
-      bulk_prefetch_l2(na, (uint32_t)(N * 4));
-      bulk_prefetch_l2(na + KN, (uint32_t)(N * 4));
-      bulk_prefetch_l2(nb, (uint32_t)(N * 4));
-      bulk_prefetch_l2(nb + KN, (uint32_t)(N * 4));
+  for (uint64_t seg = u0; seg < u1;) {
+    const int k = (int)(seg / nsite);
+    const uint32_t s_lo = (uint32_t)(seg - (uint64_t)k * nsite);
+    const uint32_t s_hi = (uint32_t)(std::min<uint64_t>(u1, (uint64_t)(k + 1) * nsite) - (uint64_t)k * nsite);
+    seg = (uint64_t)k * nsite + s_hi;
+    PrimeRegs<T> pr(tabs + k);
+    const T* twp = pr.fwd;
+    if constexpr (SMEM_TW) {
+      __syncthreads();  // every group is done with the previous prime's table
+      stage_twiddles(pr.fwd, tw_sm, TW_WORDS, Sh::THREADS * GROUPS);
+      __syncthreads();
+      twp = tw_sm;
     }
-    // h2 = a1 b1 (registers), h1 = a0 b1 + a1 b0 (strip)
+    const TwSrc<T, SMEM_TW> tw{twp};
+    auto store = [&](uint32_t s, int part) {
+      T* dst = H + ((size_t)s * 3 + part) * KN + k * N + coef_base<LOGN>();
 #pragma unroll
-    for (int i = 0; i < EV::CHUNKS; ++i) {
-      T a0[EV::VEC], a1[EV::VEC], b0[EV::VEC], b1[EV::VEC];
-      ld(a0p, i, a0);
-      ld(a0p + KN, i, a1);
-      ld(b0p, i, b0);
-      ld(b0p + KN, i, b1);
-#pragma unroll
-      for (int c = 0; c < EV::VEC; ++c) {
-        const int j = i * EV::VEC + c;
-        y[j] = mont_mul(a1[c], b1[c], pr.p, pr.pinv);
-        strip[j * Sh::THREADS] =
-            csub(mont_mul(a0[c], b1[c], pr.p, pr.pinv) + mont_mul(a1[c], b0[c], pr.p, pr.pinv), pr.p2);
-        if constexpr (TWO) strip[(Sh::E + j) * Sh::THREADS] = mont_mul(a0[c], b0[c], pr.p, pr.pinv);
+      for (int j = 0; j < Sh::E; ++j) dst[coef_off<LOGN>(j)] = csub(y[j], pr.p);
+    };
+    constexpr uint32_t step = GROUPS;
+#pragma unroll 1
+    for (uint32_t s = s_lo + group; s < s_hi; s += step) {
+      const T* a0p = AX + (size_t)sx[s] * 2 * KN + k * N;
+      const T* b0p = AW + (size_t)sw[s] * 2 * KN + k * N;
+      if (ntt_tid<LOGN>() == 0 && s + step < s_hi) {  // next item's operands towards L2
+        const T* na = AX + (size_t)sx[s + step] * 2 * KN + k * N;
+        const T* nb = AW + (size_t)sw[s + step] * 2 * KN + k * N;
+        bulk_prefetch_l2(na, (uint32_t)(N * 4));
+        bulk_prefetch_l2(na + KN, (uint32_t)(N * 4));
+        bulk_prefetch_l2(nb, (uint32_t)(N * 4));
+        bulk_prefetch_l2(nb + KN, (uint32_t)(N * 4));
       }
-    }
-    ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, GROUPS, TENSOR_QE>(y, ex, tw, pr.p, pr.p2);
-    store(s, 2);
-#pragma unroll
-    for (int j = 0; j < Sh::E; ++j) y[j] = strip[j * Sh::THREADS];
-    ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, GROUPS, TENSOR_QE>(y, ex, tw, pr.p, pr.p2);
-    store(s, 1);
-    if constexpr (TWO) {
-#pragma unroll
-      for (int j = 0; j < Sh::E; ++j) y[j] = strip[(Sh::E + j) * Sh::THREADS];
-    } else {
-      // h0 = a0 b0 (operands re-read: L1/L2 hits)
+      // h2 = a1 b1 (registers), h1 = a0 b1 + a1 b0 (strip)
 #pragma unroll
       for (int i = 0; i < EV::CHUNKS; ++i) {
-        T a0[EV::VEC], b0[EV::VEC];
+        T a0[EV::VEC], a1[EV::VEC], b0[EV::VEC], b1[EV::VEC];
         ld(a0p, i, a0);
+        ld(a0p + KN, i, a1);
         ld(b0p, i, b0);
+        ld(b0p + KN, i, b1);
 #pragma unroll
-        for (int c = 0; c < EV::VEC; ++c) y[i * EV::VEC + c] = mont_mul(a0[c], b0[c], pr.p, pr.pinv);
+        for (int c = 0; c < EV::VEC; ++c) {
+          const int j = i * EV::VEC + c;
+          y[j] = mont_mul(a1[c], b1[c], pr.p, pr.pinv);
+          strip[j * Sh::THREADS] =
+              csub(mont_mul(a0[c], b1[c], pr.p, pr.pinv) + mont_mul(a1[c], b0[c], pr.p, pr.pinv), pr.p2);
+          if constexpr (TWO) strip[(Sh::E + j) * Sh::THREADS] = mont_mul(a0[c], b0[c], pr.p, pr.pinv);
+        }
       }
+      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, GROUPS, TENSOR_QE>(y, ex, tw, pr.p, pr.p2);
+      store(s, 2);
+#pragma unroll
+      for (int j = 0; j < Sh::E; ++j) y[j] = strip[j * Sh::THREADS];
+      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, GROUPS, TENSOR_QE>(y, ex, tw, pr.p, pr.p2);
+      store(s, 1);
+      if constexpr (TWO) {
+#pragma unroll
+        for (int j = 0; j < Sh::E; ++j) y[j] = strip[(Sh::E + j) * Sh::THREADS];
+      } else {
+        // h0 = a0 b0 (operands re-read: L1/L2 hits)
+#pragma unroll
+        for (int i = 0; i < EV::CHUNKS; ++i) {
+          T a0[EV::VEC], b0[EV::VEC];
+          ld(a0p, i, a0);
+          ld(b0p, i, b0);
+#pragma unroll
+          for (int c = 0; c < EV::VEC; ++c) y[i * EV::VEC + c] = mont_mul(a0[c], b0[c], pr.p, pr.pinv);
+        }
+      }
+      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, GROUPS, TENSOR_QE>(y, ex, tw, pr.p, pr.p2);
+      store(s, 0);
     }
-    ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, GROUPS, TENSOR_QE>(y, ex, tw, pr.p, pr.p2);
-    store(s, 0);
   }
 }
 
@@ -943,9 +954,8 @@ static cudaError_t launch_site_product(const Ctx* c, const uint32_t* ax, const u
   const int K = B.size();
   if (nsite == 0) return cudaSuccess;
   const int threads = Sh::THREADS * GROUPS;
-  uint32_t grid = persistent_grid((const void*)kern, threads, smem);
-  grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(grid / K * K, (uint64_t)K),
-                                      (nsite + GROUPS - 1) / GROUPS * (uint64_t)K);
+  uint32_t grid = persistent_grid((const void*)kern, threads, smem);   // all SMs (units balance per CTA)
+  grid = (uint32_t)std::min<uint64_t>(grid, (nsite + GROUPS - 1) / GROUPS * (uint64_t)K);
   return launch_kernel_grid(kern, grid, threads, smem, s, ax, aw, sx, sw, h, (const PrimeTab<T>*)B.d_tabs, K,
                             (uint32_t)nsite);
 }

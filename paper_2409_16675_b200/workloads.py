@@ -252,8 +252,9 @@ def cfg5_builders(params, T: dict, lo: int, hi: int, n_chunk: int) -> dict:
         "fc_gx": lambda: linprot.fc_job_batch("fcx", T["gfc"][sl], T["wfc"].t().contiguous(), pr),
     }
     for c, c0 in enumerate(range(0, xfc.shape[1], n_chunk)):
-        xs = xfc[:, c0:c0 + n_chunk].contiguous()
-        b[f"fc_fwd{c}"] = (lambda xs=xs, c0=c0: linprot.fc_job_batch("fcf", xs, T["wfc"][:, c0:c0 + n_chunk], pr))
+        xs = xfc[:, c0:c0 + n_chunk].contiguous()       # the client's inputs, chunked once
+        ws = T["wfc"][:, c0:c0 + n_chunk].contiguous()
+        b[f"fc_fwd{c}"] = (lambda xs=xs, ws=ws: linprot.fc_job_batch("fcf", xs, ws, pr))
         b[f"fc_gw{c}"] = (lambda xs=xs: linprot.outer_job_batch("fcw", T["gfc"][sl], xs, pr))
     return b
 
