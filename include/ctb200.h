@@ -122,6 +122,14 @@ int ctb_cpmul(const ctb_ctx_t* ctx, const void* ct, const uint64_t* pt, void* ou
 int ctb_encrypt(const ctb_ctx_t* ctx, const uint64_t* m, const int8_t* draws, const void* pkprep, void* out,
                 uint64_t batch, void* stream);
 
+/* ctb_encrypt with the plaintexts given by their packing descriptor (the arguments of
+ * ctb_pack_gather) instead of packed values: the correlated / FC packing fused into the encryption
+ * (packing.py:407-445, 545-597 then he.py:307-323), so packed plaintexts are never written out.
+ * Identical ciphertexts to ctb_pack_gather followed by ctb_encrypt. */
+int ctb_encrypt_gather(const ctb_ctx_t* ctx, const int64_t* src, uint64_t src_len, const int32_t* maps, uint32_t n_maps,
+                       const int32_t* kind, const int64_t* base, const int8_t* draws, const void* pkprep, void* out,
+                       uint64_t batch, void* stream);
+
 /* Device sampler for ctb_encrypt's draws (He._ternary / He._error, he.py:292-303):
  * Philox4x32-10 keyed by `seed`, counter = (first_poly + k, coefficient), so the
  * stream is launch-shape independent; u uniform over {-1,0,1}, e1/e2 = clip(rint(

@@ -43,6 +43,8 @@ SIGNATURES: dict[str, tuple] = {
                                          _c_void_p]),
     "ctb_cpmul": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_encrypt": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
+    "ctb_encrypt_gather": (_int, [_c_void_p, _c_void_p, _u64, _c_void_p, _u32, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
+                                   _c_void_p, _u64, _c_void_p]),
     "ctb_sample_draws": (_int, [_c_void_p, _u64, _u64, ctypes.c_double, _int, _c_void_p, _u64, _c_void_p]),
     "ctb_draws_from_natural": (_int, [_c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),
     "ctb_pp_mul": (_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _u64, _c_void_p]),

@@ -43,6 +43,41 @@ inline cudaError_t launch_ntt_kernel(void (*kern)(KArgs...), size_t nblocks, cud
 // Resident CTAs per SM x SM count for a persistent kernel (cached per kernel).
 uint32_t persistent_grid(const void* kern, int threads, size_t smem);
 
+// x mod t for a signed 64-bit value (RingElem.from_ints semantics), t < 2^63.
+__device__ __forceinline__ uint64_t mod_signed(int64_t v, uint64_t t) {
+  if (v >= 0) return (uint64_t)v < t ? (uint64_t)v : (uint64_t)v % t;
+  const uint64_t a = (uint64_t)(-(v + 1)) + 1;  // |v| without overflow at INT64_MIN
+  const uint64_t r = a < t ? a : a % t;
+  return r ? t - r : 0;
+}
+
+// A packed plaintext given by its packing descriptor instead of its values (ctb_pack_gather's
+// arguments): coefficient i of polynomial p is src[base[p] + maps[kind[p]][i]] mod t, 0 where the
+// map is -1.  Kernels that consume plaintexts (encryption) read them through this directly, so the
+// packed polynomial is never written out; `maps == nullptr` means "not used".
+struct PlainGather {
+  const int64_t* src = nullptr;
+  uint64_t src_len = 0;
+  const int32_t* maps = nullptr;
+  uint32_t n_maps = 0;
+  const int32_t* kind = nullptr;
+  const int64_t* base = nullptr;
+  uint64_t t = 0;
+  // (kind, base) of one polynomial, loaded once per item
+  __device__ __forceinline__ void row(uint64_t poly, uint32_t n, const int32_t*& mrow, int64_t& b) const {
+    const uint32_t k = (uint32_t)__ldg(kind + poly);
+    mrow = k < n_maps ? maps + (size_t)k * n : nullptr;
+    b = __ldg(base + poly);
+  }
+  __device__ __forceinline__ uint64_t value(const int32_t* mrow, int64_t b, uint32_t i) const {
+    if (!mrow) return 0;
+    const int32_t m = __ldg(mrow + i);
+    if (m < 0) return 0;
+    const uint64_t at = (uint64_t)b + (uint64_t)m;
+    return at < src_len ? mod_signed(__ldg(src + at), t) : 0;
+  }
+};
+
 // Streaming multiprocessors of the current device (cached).
 uint32_t sm_count();
 

@@ -581,11 +581,12 @@ __host__ __device__ constexpr bool enc_pk_strip() {
   return CTB_ENC_PKSTRIP && !enc_pk_smem<T, LOGN>() && EvalVec<T, LOGN>::CONTIG && EvalVec<T, LOGN>::VEC * sizeof(T) == 16;
 }
 
-template <typename T, int LOGN, bool SMEM_TW>
+template <typename T, int LOGN, bool SMEM_TW, bool GATHER = false>
 __global__ void __launch_bounds__(NttShape<LOGN>::THREADS * enc_groups<T, LOGN>(),
                                   enc_groups<T, LOGN>() == 4 ? 1 : (enc_groups<T, LOGN>() == 2 ? 2 : NttShape<LOGN>::MINB))
 k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, const T* __restrict__ pkprep, T* out,
-          const PrimeTab<T>* __restrict__ tabs, int L, uint64_t t_half, uint32_t batch) {
+          const PrimeTab<T>* __restrict__ tabs, int L, uint64_t t_half, uint32_t batch,
+          const __grid_constant__ PlainGather g) {
   using Sh = NttShape<LOGN>;
   constexpr int GROUPS = enc_groups<T, LOGN>();
   using Ex = Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>;
@@ -654,9 +655,19 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
     const int8_t* drow = draws + (size_t)b * 3 * Sh::N;
     if (ntt_tid<LOGN>() == 0 && b + nslots * GROUPS < batch) {  // next item's inputs towards L2
       const uint32_t nb = b + nslots * GROUPS;
-      bulk_prefetch_l2(m + (size_t)nb * Sh::N, (uint32_t)(Sh::N * 8));
+      if (!GATHER) bulk_prefetch_l2(m + (size_t)nb * Sh::N, (uint32_t)(Sh::N * 8));
       bulk_prefetch_l2(draws + (size_t)nb * 3 * Sh::N, (uint32_t)(Sh::N * 3));
     }
+    // the plaintext: packed values, or read through the packing descriptor (pack fused into the
+    // encryption: the map row is shared by every polynomial of its kind and stays in L1/L2, and a
+    // sparse polynomial -- one 3 x 3 kernel in 4096 degrees -- loads almost no source values)
+    const int32_t* grow = nullptr;
+    int64_t gbase = 0;
+    if constexpr (GATHER) g.row(b, Sh::N, grow, gbase);
+    auto m_at = [&](int k) -> uint64_t {
+      if constexpr (GATHER) return g.value(grow, gbase, (uint32_t)(cb + coef_off<LOGN>(k)));
+      else return __ldg(m + (size_t)b * Sh::N + cb + coef_off<LOGN>(k));
+    };
     {
       int8_t u[Sh::E];
       load_draws(drow, u);
@@ -668,14 +679,13 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
     // MSTRIP: part 1 first; part 0's plaintext reads are issued before its slotwise product and
     // Delta * lift(m) is parked in the NTT(u) strip (dead after that product) across the inverse
     // transform, instead of reading m after the transform with the whole L2 latency exposed.
-    const uint64_t* mm = m + (size_t)b * Sh::N + cb;
 #pragma unroll 1
     for (int pi = 0; pi < 2; ++pi) {
       const int part = MSTRIP ? 1 - pi : pi;
       uint64_t mv[MSTRIP ? Sh::E : 1];
       if (MSTRIP && part == 0) {
 #pragma unroll
-        for (int k = 0; k < Sh::E; ++k) mv[k] = __ldg(mm + coef_off<LOGN>(k));
+        for (int k = 0; k < Sh::E; ++k) mv[k] = m_at(k);
       }
       const T* kp = pkprep + ((size_t)part * L + limb) * Sh::N;
       static_assert(EV::VEC == Strip<T, LOGN>::VEC || EV::VEC == 1, "strip / eval chunking");
@@ -735,7 +745,7 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
         for (int j = 0; j < Strip<T, LOGN>::VEC; ++j) {
           const int k = c * Strip<T, LOGN>::VEC + j;
           T v = add_mod(csub(x[k], pr.p), small(e[k]), pr.p);
-          if (part == 0) v = add_mod(v, MSTRIP ? d[j] : delta_m(__ldg(mm + coef_off<LOGN>(k))), pr.p);
+          if (part == 0) v = add_mod(v, MSTRIP ? d[j] : delta_m(m_at(k)), pr.p);
           o[coef_off<LOGN>(k)] = v;
         }
       }
@@ -1048,7 +1058,8 @@ extern "C" int ctb_cpmul(const ctb_ctx_t* ctx, const void* ct, const uint64_t* p
 
 template <typename T, int LOGN>
 static cudaError_t launch_encrypt(const Ctx* c, const Base* b, const uint64_t* m, const int8_t* draws,
-                                  const void* pkprep, void* out, uint64_t batch, cudaStream_t s) {
+                                  const void* pkprep, void* out, uint64_t batch, cudaStream_t s,
+                                  const PlainGather& g) {
   using Sh = NttShape<LOGN>;
   constexpr int GROUPS = enc_groups<T, LOGN>();
   constexpr size_t tw_bytes = (size_t)tw_words<T>(LOGN) * sizeof(T);
@@ -1056,7 +1067,7 @@ static cudaError_t launch_encrypt(const Ctx* c, const Base* b, const uint64_t* m
   constexpr bool SMEM_TW = LOGN >= 9 && tw_bytes + GROUPS * group_bytes <= (sizeof(T) == 4 ? 200 : 226) * 1024;
   constexpr size_t pk_bytes = enc_pk_smem<T, LOGN>() && SMEM_TW ? 2 * (size_t)Sh::N * sizeof(T) : 0;
   static_assert((SMEM_TW ? tw_bytes : 0) + GROUPS * group_bytes + pk_bytes <= 227 * 1024, "k_encrypt shared memory");
-  auto kern = k_encrypt<T, LOGN, SMEM_TW>;
+  auto kern = g.maps ? k_encrypt<T, LOGN, SMEM_TW, true> : k_encrypt<T, LOGN, SMEM_TW, false>;
   const size_t smem = GROUPS * group_bytes + (SMEM_TW ? tw_bytes : 0) + pk_bytes;
   const int L = b->size();
   if (batch == 0) return cudaSuccess;
@@ -1075,7 +1086,7 @@ static cudaError_t launch_encrypt(const Ctx* c, const Base* b, const uint64_t* m
   const uint64_t max_grid = (batch + GROUPS - 1) / GROUPS * (uint64_t)L;
   grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(grid / L * L, (uint64_t)L), max_grid);
   cudaError_t e = launch_kernel_grid(kern, grid, threads, smem, s, m, draws, (const T*)pk, (T*)out,
-                                     (const PrimeTab<T>*)b->d_tabs, L, c->t_half, (uint32_t)batch);
+                                     (const PrimeTab<T>*)b->d_tabs, L, c->t_half, (uint32_t)batch, g);
   if (tmp) {
     const cudaError_t f = cudaFreeAsync(tmp, s);
     if (e == cudaSuccess) e = f;
@@ -1092,12 +1103,42 @@ extern "C" int ctb_encrypt(const ctb_ctx_t* ctx, const uint64_t* m, const int8_t
   if (batch >= (1ull << 32)) { set_error("ctb_encrypt: batch too large"); return ERR_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
+  const PlainGather g{};
   if (b->word == 4) {
-    CTB_DISPATCH_LOGN(c->logn, e = (launch_encrypt<uint32_t, LOGN>(c, b, m, draws, pkprep, out, batch, s)));
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_encrypt<uint32_t, LOGN>(c, b, m, draws, pkprep, out, batch, s, g)));
   } else {
-    CTB_DISPATCH_LOGN(c->logn, e = (launch_encrypt<uint64_t, LOGN>(c, b, m, draws, pkprep, out, batch, s)));
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_encrypt<uint64_t, LOGN>(c, b, m, draws, pkprep, out, batch, s, g)));
   }
   return cuda_status(e, "ctb_encrypt");
+}
+
+extern "C" int ctb_encrypt_gather(const ctb_ctx_t* ctx, const int64_t* src, uint64_t src_len, const int32_t* maps,
+                                  uint32_t n_maps, const int32_t* kind, const int64_t* base, const int8_t* draws,
+                                  const void* pkprep, void* out, uint64_t batch, void* stream) {
+  if (batch == 0 && ctx) return OK;  // empty batch: no-op, buffers may be null
+  const Base* b = base_of(ctx, BASE_Q);
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (!b || !c->t || (src_len && !src) || !maps || !kind || !base || !draws || !pkprep || !out) {
+    set_error("ctb_encrypt_gather: bad context (needs plain ring) or buffer");
+    return ERR_ARG;
+  }
+  if (batch >= (1ull << 32)) { set_error("ctb_encrypt_gather: batch too large"); return ERR_ARG; }
+  PlainGather g;
+  g.src = src;
+  g.src_len = src_len;
+  g.maps = maps;
+  g.n_maps = n_maps;
+  g.kind = kind;
+  g.base = base;
+  g.t = c->t;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  if (b->word == 4) {
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_encrypt<uint32_t, LOGN>(c, b, nullptr, draws, pkprep, out, batch, s, g)));
+  } else {
+    CTB_DISPATCH_LOGN(c->logn, e = (launch_encrypt<uint64_t, LOGN>(c, b, nullptr, draws, pkprep, out, batch, s, g)));
+  }
+  return cuda_status(e, "ctb_encrypt_gather");
 }
 
 extern "C" int ctb_pp_mul(const ctb_ctx_t* ctx, const uint64_t* a, const uint64_t* bb, uint64_t* out,

@@ -23,38 +23,50 @@ using namespace ctb;
 
 namespace {
 
-__device__ __forceinline__ uint64_t mod_signed(int64_t v, uint64_t t) {
-  if (v >= 0) return (uint64_t)v < t ? (uint64_t)v : (uint64_t)v % t;
-  const uint64_t a = (uint64_t)(-(v + 1)) + 1;  // |v| without overflow at INT64_MIN
-  const uint64_t r = a < t ? a : a % t;
-  return r ? t - r : 0;
-}
-
+// Four consecutive degrees per thread: one 16-byte map load, four independent source loads and
+// 16-byte mask loads / stores, so each thread keeps several memory requests in flight (the kernel is
+// latency-bound on the dependent map -> source loads with one degree per thread).
 __global__ void __launch_bounds__(256) k_pack_gather(const int64_t* __restrict__ src, uint64_t src_len,
                                                      const int32_t* __restrict__ maps, uint32_t n_maps,
                                                      const int32_t* __restrict__ kind,
                                                      const int64_t* __restrict__ base,
                                                      const uint64_t* __restrict__ r, uint64_t* out_plain,
                                                      uint64_t* out_masked, uint64_t t, uint32_t logn,
-                                                     uint64_t total) {
+                                                     uint64_t total4) {
   const uint32_t n = 1u << logn;
-  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
-       g += (uint64_t)gridDim.x * blockDim.x) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < total4;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t g = q * 4;
     const uint64_t p = g >> logn;
     const uint32_t d = (uint32_t)g & (n - 1);
-    const uint32_t k = (uint32_t)kind[p];
-    uint64_t v = 0;
+    const uint32_t k = (uint32_t)__ldg(kind + p);
+    uint64_t v[4] = {0, 0, 0, 0};
     if (k < n_maps) {
-      const int32_t m = maps[(uint64_t)k * n + d];
-      if (m >= 0) {
-        const uint64_t at = (uint64_t)base[p] + (uint64_t)m;
-        if (at < src_len) v = mod_signed(src[at], t);
+      const int4 m = __ldg(reinterpret_cast<const int4*>(maps + (uint64_t)k * n + d));
+      const uint64_t b = (uint64_t)__ldg(base + p);
+      const int mm[4] = {m.x, m.y, m.z, m.w};
+      int64_t sv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t at = b + (uint64_t)mm[j];
+        sv[j] = (mm[j] >= 0 && at < src_len) ? __ldg(src + at) : 0;
       }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = mod_signed(sv[j], t);
     }
-    if (out_plain) out_plain[g] = v;
+    if (out_plain) {
+      reinterpret_cast<ulonglong2*>(out_plain + g)[0] = make_ulonglong2(v[0], v[1]);
+      reinterpret_cast<ulonglong2*>(out_plain + g)[1] = make_ulonglong2(v[2], v[3]);
+    }
     if (out_masked) {
-      const uint64_t rv = r[g];
-      out_masked[g] = v >= rv ? v - rv : v + t - rv;
+      const ulonglong2 r01 = __ldg(reinterpret_cast<const ulonglong2*>(r + g));
+      const ulonglong2 r23 = __ldg(reinterpret_cast<const ulonglong2*>(r + g) + 1);
+      const uint64_t rv[4] = {r01.x, r01.y, r23.x, r23.y};
+      uint64_t o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[j] = v[j] >= rv[j] ? v[j] - rv[j] : v[j] + t - rv[j];
+      reinterpret_cast<ulonglong2*>(out_masked + g)[0] = make_ulonglong2(o[0], o[1]);
+      reinterpret_cast<ulonglong2*>(out_masked + g)[1] = make_ulonglong2(o[2], o[3]);
     }
   }
 }
@@ -98,9 +110,9 @@ extern "C" int ctb_pack_gather(const ctb_ctx_t* ctx, const int64_t* src, uint64_
     set_error("ctb_pack_gather: context lacks a plain ring or bad buffer");
     return ERR_ARG;
   }
-  const uint64_t total = n_polys * (uint64_t)c->n;
-  k_pack_gather<<<grid_stride(total, 8), 256, 0, (cudaStream_t)stream>>>(src, src_len, maps, n_maps, kind, base, r,
-                                                                         out_plain, out_masked, c->t, c->logn, total);
+  const uint64_t total4 = n_polys * (uint64_t)c->n / 4;   // ring degree >= 4, a multiple of 4
+  k_pack_gather<<<grid_stride(total4, 8), 256, 0, (cudaStream_t)stream>>>(src, src_len, maps, n_maps, kind, base, r,
+                                                                          out_plain, out_masked, c->t, c->logn, total4);
   return cuda_status(cudaGetLastError(), "ctb_pack_gather");
 }
 

@@ -175,8 +175,7 @@ class DeviceSession:
         js, cli, srv = job.shape, self.client, self.server
         keys = self.parties.keys
         fresh = srv.params.fresh_noise
-        cx = cli.encrypt_many(job.x_plain, keys, self.gen)
-        cw = cli.encrypt_many(job.w_plain, keys, self.gen)
+        cx, cw = job.encrypt_operands(cli, keys, self.gen)
         xs = CiphertextBatch(cx.data, fresh, cx.backend_tag, cx._cipher)
         ws = CiphertextBatch(cw.data, fresh, cw.backend_tag, cw._cipher)
         slots = linprot._sites_ccmul_sum(srv, self.parties.pks, xs, ws, js)

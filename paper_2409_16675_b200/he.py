@@ -332,7 +332,8 @@ class He:
         return self.encrypt_many([m], keys, rng)[0]
 
     def encrypt_many(self, ms, keys, rng) -> CiphertextBatch:
-        """Encrypt plain polys (list of RingElem or an int64 tensor [B, N] of values in [0, t)).
+        """Encrypt plain polys (list of RingElem, an int64 tensor [B, N] of values in [0, t), or a
+        packing.Gather descriptor: the packing fused into the encryption, ctb_encrypt_gather).
 
         With a numpy Generator the draws are the reference's, in the reference's
         order (identical to calling encrypt() B times).  With a torch.Generator
@@ -341,15 +342,19 @@ class He:
         drawn by the device Philox stream -- the production mode, which does not
         reproduce numpy's stream.
         """
+        from . import packing
         t0 = self._t0()
-        if isinstance(ms, torch.Tensor):
+        gather = ms if isinstance(ms, packing.Gather) else None
+        if gather is not None:
+            mt = None           # plaintexts read through the packing descriptor (ctb_encrypt_gather)
+        elif isinstance(ms, torch.Tensor):
             mt = ms.contiguous()
         else:
             for m in ms:
                 if not m.params.compatible(self.params.plain_ring):
                     raise HeError("payload must live in the plain ring")
             mt = self._plain_tensor(ms)
-        B, n = mt.shape[0], self.params.n
+        B, n = (gather.n_polys if gather is not None else mt.shape[0]), self.params.n
         if self.params.error_bound > 127:
             raise HeError("the device encryptor takes int8 draws: error bound must be <= 127")
         if isinstance(rng, torch.Generator):
@@ -366,8 +371,15 @@ class He:
                        "ctb_draws_from_natural")
         pk = self._pk_prep(keys)
         out = torch.empty((B, 2, self.L, n), dtype=self.ctx.dtype(), device="cuda")
-        _lib.check(self.ctx._lib.ctb_encrypt(self.ctx._h, _ptr(mt), _ptr(draws.contiguous()), _ptr(pk), _ptr(out), B,
-                                             _stream()), "ctb_encrypt")
+        if gather is not None:
+            src = gather.src.contiguous()
+            _lib.check(self.ctx._lib.ctb_encrypt_gather(
+                self.ctx._h, _ptr(src) if src.numel() else None, src.numel(), _ptr(gather.maps), gather.maps.shape[0],
+                _ptr(gather.kind), _ptr(gather.base), _ptr(draws.contiguous()), _ptr(pk), _ptr(out), B, _stream()),
+                "ctb_encrypt_gather")
+        else:
+            _lib.check(self.ctx._lib.ctb_encrypt(self.ctx._h, _ptr(mt), _ptr(draws.contiguous()), _ptr(pk), _ptr(out),
+                                                 B, _stream()), "ctb_encrypt")
         self.meter.tick("Enc", self._elapsed(t0), count=B)
         return CiphertextBatch(out, self.params.fresh_noise, self.backend, self.params.cipher_ring)
 

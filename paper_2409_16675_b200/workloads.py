@@ -85,7 +85,7 @@ def online(sess: Session, job: LinearJob, bundle: linprot.MaskBundle, maskprod: 
     """One online job, client and server co-resident (linprot.py:430-485):
 
       client  pack + mask      ctb_pack_gather (x, x - r_x and w, w - r_w in one kernel per side)
-              encrypt          ctb_encrypt (device draws)
+              encrypt          ctb_encrypt (device draws) of the packed values
       server  linear step      ctb_linear_online
       client  decrypt + decode ctb_mul_prepared_strided + ctb_decrypt_round_extract (c - p,
                                extraction and centring in the rounding kernel's epilogue)
@@ -96,8 +96,7 @@ def online(sess: Session, job: LinearJob, bundle: linprot.MaskBundle, maskprod: 
     js = job.shape
     cli, srv = sess.client, sess.server
     mx, mw = job.masked(cli.ctx, bundle.r_x, bundle.r_w)
-    cx = cli.encrypt_many(job.x_plain, sess.keys, gen)
-    cw = cli.encrypt_many(job.w_plain, sess.keys, gen)
+    cx, cw = job.encrypt_operands(cli, sess.keys, gen)
     c_slots, p_slots = linprot.linear_online(srv, cx, cw, mx, mw, js, maskprod)
     if decode and job.out is not None:
         return cli.decrypt_extract(c_slots, sess.keys, job.out, sub=p_slots, centered=centered)

@@ -191,3 +191,28 @@ def test_empty_and_malformed(plain4096):
     assert lib.ctb_pack_gather(ctx._h, None, 0, None, 0, None, None, None, None, None, 1, None) == -1
     assert lib.ctb_plain_scatter(ctx._h, None, None, None, 0, None, None, 0, 0, None, 1, None) == -1
     assert lib.ctb_pack_gather(ctx._h, None, 0, None, 0, None, None, None, None, None, 0, None) == 0
+
+
+@pytest.mark.parametrize("params_name", ["p4096", "p8192"])
+def test_encrypt_gather_equals_pack_then_encrypt(params_name):
+    """ctb_encrypt_gather (the packing read inside the encryption kernel) == ctb_pack_gather followed
+    by ctb_encrypt, ciphertext for ciphertext, at 32- and 64-bit limbs (same numpy draws)."""
+    from paper_2409_16675_b200 import he, linprot, packing
+    P = he.default_he_params(4096) if params_name == "p4096" else he.p8192_he_params()
+    ev = he.He(P)
+    keys = ev.keygen(2)
+    rng = np.random.default_rng(31)
+    x = rng.integers(-300, 300, size=(3, 9, 9))
+    w = rng.integers(-128, 128, size=(4, 3, 3, 3))
+    job = linprot.conv_job("e", x, w, packing.ConvShape(9, 9, 3, 1), P.plain_ring)
+    for side, plain in ((job.x_side, job.x_plain), (job.w_side, job.w_plain)):
+        a = ev.encrypt_many(side, keys, np.random.default_rng(8))
+        b = ev.encrypt_many(plain, keys, np.random.default_rng(8))
+        assert torch.equal(a.data, b.data)
+        gen_a, gen_b = torch.Generator(device="cuda"), torch.Generator(device="cuda")
+        gen_a.manual_seed(3)
+        gen_b.manual_seed(3)
+        assert torch.equal(ev.encrypt_many(side, keys, gen_a).data, ev.encrypt_many(plain, keys, gen_b).data)
+    fc = linprot.fc_job("f", rng.integers(-9, 9, size=50), rng.integers(-9, 9, size=(700, 50)), P.plain_ring)
+    a = ev.encrypt_many(fc.w_side, keys, np.random.default_rng(4))
+    assert torch.equal(a.data, ev.encrypt_many(fc.w_plain, keys, np.random.default_rng(4)).data)

@@ -17,16 +17,16 @@ P = default_he_params(4096)
 sess = W.Session.create(P)
 gen = torch.Generator(device="cuda")
 gen.manual_seed(1)
-(x, w, gy), jobs = W.cfg4_jobs(P, 32)
-batched = {k: W.concat_jobs(v, k) for k, v in jobs.items()}
-prepared = {k: W.offline(sess, job, gen) for k, (job, _) in batched.items()}
+x, w, gy = W.cfg4_tensors(32)
+builders = W.cfg4_builders(P, x, w, gy)
+prepared = {k: W.offline(sess, b(), gen) for k, b in builders.items()}
 
 
 def once():
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for k, (job, _) in batched.items():
-        W.online(sess, job, *prepared[k], gen)
+    for k, b in builders.items():
+        W.online(sess, b(), *prepared[k], gen)
     torch.cuda.synchronize()
     return 1e3 * (time.perf_counter() - t0)
 

@@ -14,18 +14,18 @@ P = default_he_params(4096)
 sess = W.Session.create(P)
 gen = torch.Generator(device="cuda")
 gen.manual_seed(1)
-(x, w, gy), jobs = W.cfg4_jobs(P, 32)
-batched = {k: W.concat_jobs(v, k) for k, v in jobs.items()}
+x, w, gy = W.cfg4_tensors(32)
+builders = W.cfg4_builders(P, x, w, gy)
 
 
 def once(prof=None):
-    prepared = {k: W.offline(sess, job, gen) for k, (job, _) in batched.items()}
+    prepared = {k: W.offline(sess, b(), gen) for k, b in builders.items()}
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     if prof:
         prof.__enter__()
-    for k, (job, _) in batched.items():
-        W.online(sess, job, *prepared[k], gen)
+    for k, b in builders.items():   # from the raw tensors: build, pack + mask, encrypt, server, decrypt + extract
+        W.online(sess, b(), *prepared[k], gen)
     torch.cuda.synchronize()
     if prof:
         prof.__exit__(None, None, None)

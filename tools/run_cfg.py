@@ -22,19 +22,17 @@ print(f"session {time.perf_counter()-t0:.2f}s", flush=True)
 gen = torch.Generator(device="cuda")
 gen.manual_seed(11)
 if which == "cfg4":
-    (x, w, gy), jobs = W.cfg4_jobs(P, images)
+    x, w, gy = W.cfg4_tensors(images)
+    builders = W.cfg4_builders(P, x, w, gy)
     for rep in range(2):
-        r = W.run_config(W.Session(sess.client, sess.server, sess.keys, sess.pks), jobs, gen)
+        r = W.run_config(sess, builders, gen)
         print(f"rep {rep}: offline {r['offline_ms']:.1f} ms ({r['ccmul']} CCMul), online {r['online_ms']:.1f} ms "
-              f"({r['sites']} sites)", flush=True)
-    t = P.t
-    fwd = W.signed(r["outputs"]["fwd"], t)
+              f"(core {r['online_core_ms']:.1f} ms, {r['sites']} sites)", flush=True)
+    fwd, gw, gx = (r["outputs"][k] for k in ("fwd", "gw", "gx"))
     ok_f = torch.equal(fwd, W.conv_reference_float(x, w, 1))
-    gw = W.signed(r["outputs"]["gw"], t)
     ref_gw = torch.stack([W.conv_reference_float(x[b][:, None], gy[b][:, None], 1).transpose(0, 1)
                           for b in range(images)])
     ok_gw = torch.equal(gw, ref_gw)
     wrot = torch.flip(w, dims=(2, 3)).transpose(0, 1).contiguous()
-    gx = W.signed(r["outputs"]["gx"], t)
     ok_gx = torch.equal(gx, W.conv_reference_float(gy, wrot, 1))
     print("fwd/gw/gx exact:", ok_f, ok_gw, ok_gx, tuple(fwd.shape), tuple(gw.shape), tuple(gx.shape))

@@ -12,6 +12,6 @@ P = default_he_params(4096)
 sess = W.Session.create(P)
 gen = torch.Generator(device="cuda")
 gen.manual_seed(1)
-(x, w, gy), jobs = W.cfg4_jobs(P, int(sys.argv[1]) if len(sys.argv) > 1 else 32)
-r = W.run_config(sess, jobs, gen)
+x, w, gy = W.cfg4_tensors(int(sys.argv[1]) if len(sys.argv) > 1 else 32)
+r = W.run_config(sess, W.cfg4_builders(P, x, w, gy), gen)
 print("offline", r["offline_ms"], "online", r["online_ms"])
