@@ -216,3 +216,33 @@ def test_encrypt_gather_equals_pack_then_encrypt(params_name):
     fc = linprot.fc_job("f", rng.integers(-9, 9, size=50), rng.integers(-9, 9, size=(700, 50)), P.plain_ring)
     a = ev.encrypt_many(fc.w_side, keys, np.random.default_rng(4))
     assert torch.equal(a.data, ev.encrypt_many(fc.w_plain, keys, np.random.default_rng(4)).data)
+
+
+def test_descriptor_bounds_are_enforced_per_element():
+    """Map rows beyond n_maps, sources beyond src_len and destinations beyond dst_len contribute
+    zero / are dropped instead of reading or writing out of bounds (ctb_pack_gather,
+    ctb_plain_scatter, ctb_decrypt_round_extract share the rule)."""
+    from paper_2409_16675_b200 import he, packing
+    P = he.default_he_params(4096)
+    ev = he.He(P)
+    ctx = ev.ctx
+    n = P.n
+    maps = torch.full((2, n), -1, dtype=torch.int32, device="cuda")
+    maps[0, :8] = torch.arange(8, dtype=torch.int32)
+    maps[1, :8] = torch.arange(8, dtype=torch.int32) + 4
+    src = torch.arange(1, 11, dtype=torch.int64, device="cuda") * -3      # 10 values, negative
+    kind = torch.tensor([0, 1, 5], dtype=torch.int32, device="cuda")      # kind 5: no such row
+    base = torch.tensor([0, 0, 0], dtype=torch.int64, device="cuda")
+    side = packing.Gather(src, maps, kind, base)
+    out = packing.gather(ctx, side).cpu().numpy()
+    t = P.t
+    assert [int(v) for v in out[0, :8]] == [(-3 * (i + 1)) % t for i in range(8)]
+    # row 1 reads src[4..11]: the last two are past src_len -> 0
+    assert [int(v) for v in out[1, :8]] == [(-3 * (i + 5)) % t for i in range(6)] + [0, 0]
+    assert not out[2].any() and not out[:, 8:].any()
+    # scatter: destinations past dst_len are dropped (rows 0 and 1 write disjoint ranges)
+    maps2 = maps.clone()
+    maps2[1, :8] = torch.arange(8, dtype=torch.int32) + 8
+    vals = torch.arange(3 * n, dtype=torch.int64, device="cuda").view(3, n) % t
+    res = packing.scatter(ctx, vals, packing.Scatter(maps2, kind, base, (10,))).cpu().numpy()
+    assert res.tolist() == list(range(8)) + [n, n + 1]
