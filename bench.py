@@ -357,10 +357,11 @@ def run_extras(torch, steps):
     # groups request (without it, sporadic allocator growth added up to ~100 ms to one family)
     W.run_cfg5(sess8, W.cfg5_tensors(4, seed=99), gen, group=4)
     T5 = W.cfg5_tensors(32)
-    r5 = W.run_cfg5(sess8, T5, gen, group=4)
+    r5 = W.run_cfg5(sess8, T5, gen, group=4)    # offline: a group's families concurrently on streams
+    wg = W.WEIGHT_GRADIENT_FAMILIES
+    r5w = W.run_cfg5(sess8, T5, gen, group=4, families=list(wg))   # the weight-gradient jobs alone
     ref5 = W.cfg5_reference_float(T5)
     ok5 = all(bool(torch.equal(v, ref5[k])) for k, v in r5["outputs"].items())
-    wg = W.WEIGHT_GRADIENT_FAMILIES
     K8 = int(sess8.server.ctx._lib.ctb_tensor_aux_size(sess8.server.ctx._h) or 11)
     L8, LT8, D8 = len(P8.cipher_ring.primes), len(P8.plain_ring.primes), P8.relin_digits
     on5 = sum(WC.online_job(8192, L8, LT8, *d) for d in r5["shapes"].values())
@@ -373,11 +374,12 @@ def run_extras(torch, steps):
         "cpu_baseline": _cpu_protocol(sec8, cores, wall8, r5["shapes"], "online", reps8, "online phase, batch 32"),
         "cpu_baseline_offline": _cpu_protocol(sec8, cores, wall8, r5["shapes"], "offline", reps8,
                                               "offline phase, batch 32"),
-        "offline_ms_weight_gradient_jobs": sum(r5["offline_ms"][k] for k in wg),
+        "offline_ms_weight_gradient_jobs": sum(r5w["offline_ms"].values()),
         "ccmul_weight_gradient_jobs": sum(r5["sites"][k] for k in wg),
         "sites_total": sum(r5["sites"].values()), "exact_vs_float64": ok5,
         "per_family_online_ms": {k: round(v, 2) for k, v in r5["online_ms"].items()},
-        "per_family_offline_ms": {k: round(v, 2) for k, v in r5["offline_ms"].items()},
+        "offline_concurrency": "each group's offline jobs run on one CUDA stream per family at once "
+                               "(workloads.run_cfg5 concurrent=True); the online jobs family by family",
         "workload": "batch 32: conv1 3->64 fwd+gw, conv2 64->64 s2 fwd+gx+gw (stride-1 + subsample / zero-upsampled gy),"
                     " FC 16384->10 fwd+gw (2 chunks of N) + gx; precompute protocol incl. offline CCMul for every job",
     }

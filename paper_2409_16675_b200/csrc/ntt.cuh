@@ -674,11 +674,21 @@ __device__ __forceinline__ void ntt_fwd_regs(T (&x)[NttShape<LOGN>::E], Exchange
     __trap();  // 64-bit limbs transform whole polynomials (never split)
   } else if constexpr (sizeof(T) == 8) {
     // 64-bit limbs: FP64 butterflies, inputs < 4p (< 2^52), outputs canonical [0, p) (the lazy
-    // schedule leaves |d| <= 4.5 p, which f64_to_canon reduces exactly)
+    // schedule leaves |d| <= 4.5 p, which f64_to_canon reduces exactly).  With at most 3 stages in
+    // the first pass the inputs need no centring: x - 2p in [-2p, 2p) (one DADD fused into the
+    // exponent splice) keeps the multiplied operand below 4p there (0.5 |Y| <= 2p < 2^51), and pass 1
+    // centres everything.
     const F64Prime P{(double)p, __drcp_rn((double)p)};
     double d[Sh::E];
+    if constexpr (Sh::FIRST_R <= 3 && Sh::NPASS > 1) {
+      const double off = __dadd_rn(4503599627370496.0, 2.0 * (double)p);   // 2^52 + 2p, exact
 #pragma unroll
-    for (int k = 0; k < Sh::E; ++k) d[k] = f64_center(f64_from_u64(x[k]), P);
+      for (int k = 0; k < Sh::E; ++k)
+        d[k] = __dadd_rn(__longlong_as_double((long long)((uint64_t)x[k] | 0x4330000000000000ull)), -off);
+    } else {
+#pragma unroll
+      for (int k = 0; k < Sh::E; ++k) d[k] = f64_center(f64_from_u64(x[k]), P);
+    }
     ntt_fwd_f64<T, LOGN, 0, SMEM, NBUF, GROUPS>(d, ex, tw, P);
 #pragma unroll
     for (int k = 0; k < Sh::E; ++k) x[k] = f64_to_canon(d[k], P);

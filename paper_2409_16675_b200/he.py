@@ -216,6 +216,8 @@ def _prepared(keys, name: str, ctx: RnsContext, build) -> torch.Tensor:
         npoly = src.numel() // (ctx.L * ctx.n)
         _lib.check(ctx._lib.ctb_prepare_operand(ctx._h, BASE_Q, _ptr(src), _ptr(hit), npoly, _stream()),
                    "ctb_prepare_operand")
+        # built once and then read from any stream (concurrent jobs): complete it before publishing
+        torch.cuda.current_stream().synchronize()
         cache[name] = hit
     return hit
 
@@ -240,7 +242,7 @@ class He:
         self.L = self.ctx.L
         self._delta_res = [params.delta % p for p in self.ctx.q_primes]
         self._zero_plain = None
-        self._draws = None
+        self._draws: dict = {}
 
     # -- helpers --------------------------------------------------------------
     def _t0(self) -> float:
@@ -400,10 +402,11 @@ class He:
         every consumer of the draws is queued before the next encryption overwrites them).  A fresh
         sub-megabyte allocation per call occasionally cost tens of ms in the caching allocator's
         small-block pool (cudaMalloc of a new segment) inside cfg5's online phase."""
-        buf = self._draws
+        key = torch.cuda.current_stream().cuda_stream   # one scratch per stream (concurrent jobs)
+        buf = self._draws.get(key)
         if buf is None or buf.numel() < nbytes:
             size = 1 << max(20, (nbytes - 1).bit_length())
-            buf = self._draws = torch.empty(size, dtype=torch.int8, device="cuda")
+            buf = self._draws[key] = torch.empty(size, dtype=torch.int8, device="cuda")
         return buf[:nbytes]
 
     def _s_prep(self, keys, power: int) -> torch.Tensor:
