@@ -63,7 +63,8 @@ int ctb_ctx_base_primes(const ctb_ctx_t* ctx, int base, uint64_t* out, uint32_t 
  * (ring.ntt_forward / ring.ntt_inverse, ring.py:549-569; the per-prime
  * transform of ring._NttPlan.forward/inverse, ring.py:186-217).  Output is
  * canonical; forward output is in the reference's bit-reversed order.
- * In-place allowed. */
+ * Inputs must be reduced residues (< p; 64-bit limbs accept up to 2p for the inverse and 4p for
+ * the forward transform).  In-place allowed. */
 int ctb_ntt_forward(const ctb_ctx_t* ctx, int base, const void* in, void* out, uint64_t n_polys,
                     void* stream);
 int ctb_ntt_inverse(const ctb_ctx_t* ctx, int base, const void* in, void* out, uint64_t n_polys,

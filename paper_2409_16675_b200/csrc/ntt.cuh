@@ -529,8 +529,11 @@ struct Strip {
 //               multiplied operand never exceeds 3.5 (|Y wp| <= 1.75 p < 2^51); all 16 values are
 //               centred once at the next pass boundary (3 ops per value per pass instead of 3 per
 //               butterfly per stage).
-//   inverse GS  X' = X + Y, Y' = mulmod(Y - X): X' is centred on every second stage (odd stages
-//               see inputs <= 1.5, even ones <= 1.5 + 1.5 = 3 for the difference, |.| wp <= 1.5 p).
+//   inverse GS  X' = X + Y, Y' = mulmod(Y - X): X' is centred on every second global stage, starting
+//               with the first, so the uncentred inputs may lie anywhere in [0, 2p) (every caller's
+//               are: canonical values, Montgomery products, sums kept below 2p): the differences reach
+//               at most 2p (first stage), then stay below 4p at the centring stages (|.| wp < 2p)
+//               while products stay below p; no input centring.
 // About 9.5 FP64 operations per butterfly instead of 11 with full reduction every stage.
 struct F64Prime {
   double p, pinv;
@@ -626,7 +629,7 @@ __device__ __forceinline__ void inv_pass_f64(double (&x)[NttShape<LOGN>::E], TwS
 #pragma unroll
     for (int i = R - 1; i >= 0; --i) {
       const int h = 1 << (R - i - 1);
-      const bool reduce = ((DONE + (R - 1 - i)) & 1) == 1;  // every second global stage
+      const bool reduce = ((DONE + (R - 1 - i)) & 1) == 0;  // every second global stage, from the first
 #pragma unroll
       for (int jb = 0; jb < (1 << i); ++jb) {
         double w, wp;
@@ -709,11 +712,12 @@ __device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchange
   if constexpr (sizeof(T) == 8 && K != Sh::NPASS - 1) {
     __trap();  // 64-bit limbs transform whole polynomials (never split)
   } else if constexpr (sizeof(T) == 8) {
-    // 64-bit limbs: FP64 butterflies, inputs < 4p, outputs canonical [0, p)
+    // 64-bit limbs: FP64 butterflies, inputs < 2p (taken as they are: the first stage centres),
+    // outputs canonical [0, p)
     const F64Prime P{(double)p, __drcp_rn((double)p)};
     double d[Sh::E];
 #pragma unroll
-    for (int k = 0; k < Sh::E; ++k) d[k] = f64_center(f64_from_u64(x[k]), P);
+    for (int k = 0; k < Sh::E; ++k) d[k] = f64_from_u64(x[k]);
     ntt_inv_f64<T, LOGN, Sh::NPASS - 1, SMEM, NBUF, GROUPS>(d, ex, tw, P);
 #pragma unroll
     for (int k = 0; k < Sh::E; ++k) x[k] = f64_to_canon(d[k], P);

@@ -222,11 +222,19 @@ def run_config(sess: Session, builders: dict, gen, concurrent: bool = True) -> d
     # online, encode/decode included
     _sync()
     t0 = time.perf_counter()
-    for k, build in builders.items():
-        job = build()
-        bundle, mp = prepared[k]
-        res["outputs"][k] = online(sess, job, bundle, mp, gen)
-        res["sites"] += len(job.shape)
+    with _Concurrent(len(builders), concurrent) as cc:
+        for i, (k, build) in enumerate(builders.items()):
+            # one family after the other, each on the stream its offline step used (its freed blocks
+            # are in that stream's allocator pool); the next waits for it
+            with cc.stream(i):
+                job = build()
+                bundle, mp = prepared[k]
+                res["outputs"][k] = online(sess, job, bundle, mp, gen)
+                done = torch.cuda.Event()
+                done.record()
+            if cc.enabled and i + 1 < len(cc.streams):
+                cc.streams[i + 1].wait_event(done)
+            res["sites"] += len(job.shape)
     _sync()
     res["online_ms"] = 1e3 * (time.perf_counter() - t0)
     # online core: pre-packed, pre-masked operands; no extraction (reuses the masks above: timing
@@ -333,7 +341,7 @@ def run_cfg5(sess: Session, T: dict, gen, group: int = 4, families=None, concurr
                         prepared[fam] = offline(sess, shape_jobs[fam], gen)
             _sync()
             res["offline_ms"]["all"] = res["offline_ms"].get("all", 0.0) + 1e3 * (time.perf_counter() - t0)
-        for fam in fams:
+        for i, fam in enumerate(fams):
             shape_job = shape_jobs[fam]
             _sync()
             t0 = time.perf_counter()
@@ -342,7 +350,10 @@ def run_cfg5(sess: Session, T: dict, gen, group: int = 4, families=None, concurr
                 _sync()
             t1 = time.perf_counter()
             bundle, mp = prepared.pop(fam)
-            out = online(sess, builders[fam](), bundle, mp, gen)
+            # (concurrent: on the family's own stream, one family at a time, so the online step
+            # reuses the blocks its offline step freed in that stream's allocator pool)
+            with _Concurrent(len(fams), concurrent) as cc, cc.stream(i):
+                out = online(sess, builders[fam](), bundle, mp, gen)
             _sync()
             t2 = time.perf_counter()
             if not concurrent:
