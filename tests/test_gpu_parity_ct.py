@@ -111,3 +111,44 @@ def test_p8192_fc_protocol_matches_restatement(p8192):
     x, w = np.array(c["x"]), np.array(c["w"])
     out, _ = _check(c, P, linprot.fc_job("fc", x, w, P.plain_ring))
     assert np.array_equal(out, w @ x)
+
+
+def _run_b(params, job, keygen_seed=3, online_seed=4):
+    from paper_2409_16675_b200 import channel, he, linprot
+    cli, srv = he.He(params, he.BACKEND_RLWE), he.He(params, he.BACKEND_RLWE)
+    keys = cli.keygen(keygen_seed)
+
+    def client(end):
+        linprot.setup_client(end, cli, keys)
+        return linprot.linear_b_client(end, cli, keys, np.random.default_rng(online_seed), job)
+
+    def server(end):
+        pks = linprot.setup_server(end, srv)
+        linprot.linear_b_server(end, srv, pks)
+
+    ce, se = channel.inproc_pair(capture=True)
+    res, _ = channel.run_pair(client, server, ce, se)
+    return res, ce.stats, srv
+
+
+@pytest.mark.parametrize("name", ["conv", "fc"])
+def test_protocol_b_transcripts_match_reference(name):
+    """CryptoTrain-B (direct per-site CCMul on the server, linprot.py:352-379): the device client +
+    server reproduce the reference transcripts byte for byte (tests/golden/make_golden_extra.py)."""
+    from paper_2409_16675_b200 import he, linprot, packing
+    g = json.loads((GOLD / "golden_extra.json").read_text())["protocol_b"][name]
+    plain = he.default_plain_params(512, 17, 2)
+    Ps = he.HeParams(he.default_cipher_params(512, plain.modulus), plain)
+    x, w = np.array(g["x"]), np.array(g["w"])
+    if name == "conv":
+        job = linprot.conv_job("bc", x, w, packing.ConvShape(8, 8, 3, 1), Ps.plain_ring)
+    else:
+        job = linprot.fc_job("bf", x, w, Ps.plain_ring)
+    res, stats, srv = _run_b(Ps, job)
+    tr = stats.transcript
+    assert len(tr["client"]) == g["c2s_len"] and len(tr["server"]) == g["s2c_len"]
+    assert hashlib.sha256(bytes(tr["client"])).hexdigest() == g["c2s"]
+    assert hashlib.sha256(bytes(tr["server"])).hexdigest() == g["s2c"]
+    signed = packing.to_signed_tensor(res.tensor, Ps.t).cpu().numpy().astype(np.int64)
+    assert digest(signed.astype(np.uint64)) == g["tensor"]
+    assert srv.meter.snapshot()["counts"] == g["server_counts"]
