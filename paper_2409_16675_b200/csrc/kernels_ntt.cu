@@ -235,7 +235,9 @@ struct StreamCfg {
                                (CTB_STREAM_G2_13 && sizeof(T) == 4 && LOGN == 13);
   static constexpr int GROUPS = (CTB_STREAM_GROUPS4 && sizeof(T) == 4 && LOGN == 12) ? 4
                                 : (CTB_STREAM_G2_13 && sizeof(T) == 4 && LOGN == 13) ? 2 : cpmul_groups<T, LOGN>();
-  static constexpr int CTAS_PER_SM = WIDE ? 1 : 2;
+  // (64-bit limbs: one 512-thread CTA per SM at ~108 registers, so the staging buffer fits beside
+  // the table and the image)
+  static constexpr int CTAS_PER_SM = WIDE || sizeof(T) == 8 ? 1 : 2;
   using Ex = Exchanger<T, LOGN, CPMUL_NBUF, GROUPS>;
   // eval-layout loads / stores through the exchange image (ntt.cuh eval_xpose_*)
   static constexpr bool XPOSE = CTB_EVAL_XPOSE && eval_xpose_ok<T, LOGN>(Ex::WORDS);
@@ -263,7 +265,11 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
   using C = StreamCfg<T, LOGN>;
   using Sh = NttShape<LOGN>;
   constexpr int GROUPS = C::GROUPS;
-  constexpr bool PF = C::PF_OK && OP != StreamOp::LiftPrepare && OP != StreamOp::LiftFwd;
+  // (64-bit limbs: not for the public inverse, whose bit-reversed reads from the staging buffer
+  // conflict -- measured +15% -- while its internal variant InvAdd reads the thread-major strip)
+  constexpr bool PF = C::PF_OK && OP != StreamOp::LiftPrepare && OP != StreamOp::LiftFwd &&
+                      !(sizeof(T) == 8 && OP == StreamOp::Inv);
+  constexpr bool EARLY = PF && sizeof(T) == 8;   // next-item load issued right after the staging read
   constexpr int TW_WORDS = SMEM_TW ? tw_words<T>(LOGN) : 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
@@ -301,6 +307,21 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
     const size_t off = ((size_t)b * L + limb) * (size_t)Sh::N;               // output item
     const size_t ioff = ((size_t)b * a.in_stride * L + limb) * (size_t)Sh::N;  // input item
     const size_t aoff = ((size_t)b * a.add_stride * L + limb) * (size_t)Sh::N;
+    auto issue_next = [&]() {
+      if constexpr (PF) {
+        if (leader) {
+          if (b + step < npoly) {
+            fence_proxy_async_smem();
+            bulk_load(stg, a.in + ((size_t)(b + step) * a.in_stride * L + limb) * Sh::N, Sh::N * sizeof(T), bar);
+          }
+          // the epilogue's per-item operands: start them towards L2 while this item transforms
+          if ((OP == StreamOp::InvAdd || OP == StreamOp::MulPrepared) && a.addend)
+            bulk_prefetch_l2(a.addend + aoff, Sh::N * sizeof(T));
+          if (OP == StreamOp::MulPrepared && a.b_stride)
+            bulk_prefetch_l2(a.bprep + ((size_t)b * a.b_stride * L + limb) * (size_t)Sh::N, Sh::N * sizeof(T));
+        }
+      }
+    };
     constexpr bool EVAL_IN = OP == StreamOp::Inv || OP == StreamOp::InvAdd;
     if constexpr (PF) {
       mbar_wait(bar, phase);
@@ -325,7 +346,13 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
         for (int k = 0; k < Sh::E; ++k) x[k] = stg[cb + coef_off<LOGN>(k)];
       }
       // the next item's staging load is issued after the transform's first exchange, whose
-      // barrier already orders every thread's staging read before it (see xform_fwd/xform_inv)
+      // barrier already orders every thread's staging read before it (see xform_fwd/xform_inv);
+      // 64-bit limbs transform whole polynomials, so they order the reads with one group barrier
+      // and issue the load right away (it then overlaps the whole transform, not just the store)
+      if constexpr (EARLY) {
+        group_sync<LOGN, GROUPS>();
+        issue_next();
+      }
     } else if constexpr (OP == StreamOp::LiftPrepare || OP == StreamOp::LiftFwd) {
       const uint64_t* src = a.plain + (size_t)b * Sh::N + cb;
       if (leader && b + step < npoly) bulk_prefetch_l2(a.plain + (size_t)(b + step) * Sh::N, Sh::N * 8);
@@ -356,21 +383,6 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) x[k] = a.in[ioff + cb + coef_off<LOGN>(k)];
     }
-    auto issue_next = [&]() {
-      if constexpr (PF) {
-        if (leader) {
-          if (b + step < npoly) {
-            fence_proxy_async_smem();
-            bulk_load(stg, a.in + ((size_t)(b + step) * a.in_stride * L + limb) * Sh::N, Sh::N * sizeof(T), bar);
-          }
-          // the epilogue's per-item operands: start them towards L2 while this item transforms
-          if ((OP == StreamOp::InvAdd || OP == StreamOp::MulPrepared) && a.addend)
-            bulk_prefetch_l2(a.addend + aoff, Sh::N * sizeof(T));
-          if (OP == StreamOp::MulPrepared && a.b_stride)
-            bulk_prefetch_l2(a.bprep + ((size_t)b * a.b_stride * L + limb) * (size_t)Sh::N, Sh::N * sizeof(T));
-        }
-      }
-    };
     // forward / inverse transform; with staging, split after the first exchange to issue the
     // next item's load there (PF implies 32-bit limbs and >= 3 passes)
     // (64-bit limbs transform whole polynomials on the FP64 path: issue after the transform)
@@ -383,7 +395,7 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
         ntt_fwd_regs<T, LOGN, 1, SMEM_TW, CPMUL_NBUF, GROUPS, STREAM_QE>(x, ex, tw, pr.p, pr.p2);
       } else {
         ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS, STREAM_QE>(x, ex, tw, pr.p, pr.p2);
-        issue_next();
+        if constexpr (!EARLY) issue_next();
       }
     };
     auto store_out = [&](const T (&v)[Sh::E]) {
@@ -411,7 +423,7 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
         }
       }
       ntt_inv_regs<T, LOGN, K, SMEM_TW, CPMUL_NBUF, GROUPS, STREAM_QE>(x, ex, tw, pr.p, pr.p2);
-      if (first_in_item) issue_next();
+      if (!EARLY && first_in_item) issue_next();
     };
     if constexpr (OP == StreamOp::Inv) {
       xform_inv(true);
