@@ -141,6 +141,74 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
   const TwSrc<T, SMEM_TW> tw{twp};
 
   T x[Sh::E];
+  if constexpr (sizeof(T) == 8) {
+    // 64-bit limbs: the whole CPMul stays in the FP64 domain -- the slotwise product is an FP64
+    // product of the centred forward outputs with the centred NTT(lift(pt)) N^-1 kept (as double
+    // bits) in the strip, so no conversions between the transforms and no 64-bit integer
+    // Montgomery products (which ran on the fma pipe while the FP64 pipe idled)
+    const F64Prime P{(double)pr.p, __drcp_rn((double)pr.p)};
+    const T nv = pr.ninv;
+    const double ninv_c = nv > pr.p / 2 ? -(double)(pr.p - nv) : (double)nv;   // centred N^-1
+    const double ninv_p = __dmul_rn(ninv_c, P.pinv);
+    double d[Sh::E];
+    auto load_d = [&](const T (&v)[Sh::E]) {   // canonical (< p) -> the forward transform's input
+      if constexpr (Sh::FIRST_R <= 3 && Sh::NPASS > 1) {
+        const double off = __dadd_rn(4503599627370496.0, 2.0 * P.p);
+#pragma unroll
+        for (int k = 0; k < Sh::E; ++k)
+          d[k] = __dadd_rn(__longlong_as_double((long long)((uint64_t)v[k] | 0x4330000000000000ull)), -off);
+      } else {
+#pragma unroll
+        for (int k = 0; k < Sh::E; ++k) d[k] = f64_center(f64_from_u64(v[k]), P);
+      }
+    };
+#pragma unroll 1
+    for (uint32_t b = slot * GROUPS + group; b < batch; b += nslots * GROUPS) {
+      {
+        const uint64_t* ppt = pt + (size_t)b * Sh::N + coef_base<LOGN>();
+#pragma unroll
+        for (int k = 0; k < Sh::E; ++k) {
+          const uint64_t v = __ldg(ppt + coef_off<LOGN>(k));
+          T r = csub(pr.reduce_plain(v, plain_fast), pr.p);  // v mod p
+          if (v > t_half) r = sub_mod(r, tmod, pr.p);         // centred lift: v - t
+          x[k] = r;
+        }
+        load_d(x);
+        ntt_fwd_f64<T, LOGN, 0, SMEM_TW, NB, GROUPS>(d, ex, tw, P);
+#pragma unroll
+        for (int k = 0; k < Sh::E; ++k) {   // y = centre(NTT(pt)) N^-1, |y| < p
+          const double yv = f64_mulmod(f64_center(d[k], P), ninv_c, ninv_p, P.p);
+          x[k] = (T)__double_as_longlong(yv);
+        }
+        ysm.store(x);
+      }
+#pragma unroll 1
+      for (int part = 0; part < 2; ++part) {
+        const size_t off = (((size_t)b * 2 + part) * L + limb) * (size_t)Sh::N + coef_base<LOGN>();
+#pragma unroll
+        for (int k = 0; k < Sh::E; ++k) x[k] = ct[off + coef_off<LOGN>(k)];
+        load_d(x);
+        ntt_fwd_f64<T, LOGN, 0, SMEM_TW, NB, GROUPS>(d, ex, tw, P);
+#pragma unroll
+        for (int c = 0; c < Strip<T, LOGN>::CHUNKS; ++c) {
+          T y[Strip<T, LOGN>::VEC];
+          ysm.load_chunk(c, y);
+#pragma unroll
+          for (int j = 0; j < Strip<T, LOGN>::VEC; ++j) {
+            const int k = c * Strip<T, LOGN>::VEC + j;
+            const double yv = __longlong_as_double((long long)y[j]);
+            // centred x (<= p/2) times |y| < p: |x y / p| < p / 2 and the product lies in (-p, p),
+            // an admissible input of the inverse transform (ntt.cuh: inputs below 2p)
+            d[k] = f64_mulmod(f64_center(d[k], P), yv, __dmul_rn(yv, P.pinv), P.p);
+          }
+        }
+        ntt_inv_f64<T, LOGN, Sh::NPASS - 1, SMEM_TW, NB, GROUPS>(d, ex, tw, P);
+#pragma unroll
+        for (int k = 0; k < Sh::E; ++k) out[off + coef_off<LOGN>(k)] = (T)f64_to_canon(d[k], P);
+      }
+    }
+    return;
+  }
 #pragma unroll 1
   for (uint32_t b = slot * GROUPS + group; b < batch; b += nslots * GROUPS) {
     {
