@@ -660,6 +660,11 @@ template <typename T, int LOGN>
 __host__ __device__ constexpr bool enc_pk_strip() {
   return CTB_ENC_PKSTRIP && !enc_pk_smem<T, LOGN>() && EvalVec<T, LOGN>::CONTIG && EvalVec<T, LOGN>::VEC * sizeof(T) == 16;
 }
+// 64-bit limbs: the encryption's products and transforms in the FP64 domain (key strips as doubles)
+template <typename T, int LOGN>
+__host__ __device__ constexpr bool enc_f64() {
+  return sizeof(T) == 8 && enc_pk_strip<T, LOGN>() && Strip<T, LOGN>::VEC == EvalVec<T, LOGN>::VEC;
+}
 
 template <typename T, int LOGN, bool SMEM_TW, bool GATHER = false>
 __global__ void __launch_bounds__(NttShape<LOGN>::THREADS * enc_groups<T, LOGN>(),
@@ -731,6 +736,92 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
       for (int k = 0; k < Sh::E; ++k) v[k] = __ldg(row + tid * Sh::E + k);
     }
   };
+  if constexpr (enc_f64<T, LOGN>()) {
+    // 64-bit limbs: NTT(u), the products with the public key and the inverse transforms stay in the
+    // FP64 domain (the key arrives as centred doubles NTT(pk) N^-1 in the thread-major strip layout,
+    // launch_encrypt); integer work only for the draws, Delta * lift(m) and the canonical store.
+    const F64Prime P{(double)pr.p, __drcp_rn((double)pr.p)};
+    using SV = Strip<T, LOGN>;
+#pragma unroll 1
+    for (uint32_t b = slot * GROUPS + group; b < batch; b += nslots * GROUPS) {
+      const int8_t* drow = draws + (size_t)b * 3 * Sh::N;
+      if (ntt_tid<LOGN>() == 0 && b + nslots * GROUPS < batch) {  // next item's inputs towards L2
+        const uint32_t nb = b + nslots * GROUPS;
+        if (!GATHER) bulk_prefetch_l2(m + (size_t)nb * Sh::N, (uint32_t)(Sh::N * 8));
+        bulk_prefetch_l2(draws + (size_t)nb * 3 * Sh::N, (uint32_t)(Sh::N * 3));
+      }
+      const int32_t* grow = nullptr;
+      int64_t gbase = 0;
+      if constexpr (GATHER) g.row(b, Sh::N, grow, gbase);
+      auto m_at = [&](int k) -> uint64_t {
+        if constexpr (GATHER) return g.value(grow, gbase, (uint32_t)(cb + coef_off<LOGN>(k)));
+        else return __ldg(m + (size_t)b * Sh::N + cb + coef_off<LOGN>(k));
+      };
+      double d[Sh::E];
+      {
+        int8_t u[Sh::E];
+        load_draws(drow, u);
+#pragma unroll
+        for (int k = 0; k < Sh::E; ++k) d[k] = (double)u[k];   // |u| <= 1: any transform input bound holds
+      }
+      ntt_fwd_f64<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS>(d, ex, tw, P);
+#pragma unroll
+      for (int k = 0; k < Sh::E; ++k) x[k] = (T)__double_as_longlong(f64_center(d[k], P));
+      usm.store(x);
+#pragma unroll 1
+      for (int pi = 0; pi < 2; ++pi) {
+        const int part = 1 - pi;   // part 0 last: its plaintext is read before the inverse transform
+        uint64_t mv[Sh::E];
+        if (part == 0) {
+#pragma unroll
+          for (int k = 0; k < Sh::E; ++k) mv[k] = m_at(k);
+        }
+        const T* kp = pkprep + ((size_t)part * L + limb) * Sh::N;
+#pragma unroll
+        for (int i = 0; i < SV::CHUNKS; ++i) {
+          T kv[SV::VEC], uu[SV::VEC];
+          unpack_chunk<T>(__ldg(reinterpret_cast<const uint4*>(kp) + i * Sh::THREADS + ntt_tid<LOGN>()), kv);
+          usm.load_chunk(i, uu);
+#pragma unroll
+          for (int c = 0; c < SV::VEC; ++c) {
+            const double kd = __longlong_as_double((long long)kv[c]);
+            d[i * SV::VEC + c] = f64_mulmod(__longlong_as_double((long long)uu[c]), kd, __dmul_rn(kd, P.pinv), P.p);
+          }
+        }
+        auto delta_m = [&](uint64_t v) -> T {  // Delta * lift(m) mod p
+          T l = csub(pr.reduce_u64_lazy(v), pr.p);
+          if (v > t_half) l = sub_mod(l, tmod, pr.p);
+          return csub(shoup_mul(l, delta, delta_q, pr.p), pr.p);
+        };
+        if (part == 0) {   // the NTT(u) strip is dead now: park Delta * lift(m) there
+#pragma unroll
+          for (int c = 0; c < SV::CHUNKS; ++c) {
+            T dm[SV::VEC];
+#pragma unroll
+            for (int j = 0; j < SV::VEC; ++j) dm[j] = delta_m(mv[c * SV::VEC + j]);
+            usm.store_chunk(c, dm);
+          }
+        }
+        int8_t e[Sh::E];  // issued before the inverse transform, consumed after it
+        load_draws(drow + (size_t)(1 + part) * Sh::N, e);
+        ntt_inv_f64<T, LOGN, Sh::NPASS - 1, SMEM_TW, CPMUL_NBUF, GROUPS>(d, ex, tw, P);   // inputs |.| < p
+        T* o = out + (((size_t)b * 2 + part) * L + limb) * Sh::N + cb;
+#pragma unroll
+        for (int c = 0; c < SV::CHUNKS; ++c) {
+          T dm[SV::VEC];
+          if (part == 0) usm.load_chunk(c, dm);
+#pragma unroll
+          for (int j = 0; j < SV::VEC; ++j) {
+            const int k = c * SV::VEC + j;
+            T v = add_mod((T)f64_to_canon(d[k], P), small(e[k]), pr.p);
+            if (part == 0) v = add_mod(v, dm[j], pr.p);
+            o[coef_off<LOGN>(k)] = v;
+          }
+        }
+      }
+    }
+    return;
+  }
   for (uint32_t b = slot * GROUPS + group; b < batch; b += nslots * GROUPS) {
     const int8_t* drow = draws + (size_t)b * 3 * Sh::N;
     if (ntt_tid<LOGN>() == 0 && b + nslots * GROUPS < batch) {  // next item's inputs towards L2
@@ -995,7 +1086,7 @@ static cudaError_t launch_mul_prepared(const Ctx* c, const Base* b, StreamArgs<T
       const size_t bytes = (size_t)b->size() * Sh::N * sizeof(T);
       cudaError_t e = c->pool ? cudaMallocFromPoolAsync(&tmp, bytes, c->pool, s) : cudaMallocAsync(&tmp, bytes, s);
       if (e != cudaSuccess) return e;
-      k_eval_to_strip<T, LOGN><<<(unsigned)b->size(), Sh::THREADS, 0, s>>>(a.bprep, (T*)tmp);
+      k_eval_to_strip<T, LOGN><<<(unsigned)b->size(), Sh::THREADS, 0, s>>>(a.bprep, (T*)tmp, nullptr, 1);
       if ((e = cudaGetLastError()) != cudaSuccess) { cudaFreeAsync(tmp, s); return e; }
       a.bprep = (const T*)tmp;
       a.bprep_strip = true;
@@ -1158,7 +1249,9 @@ static cudaError_t launch_encrypt(const Ctx* c, const Base* b, const uint64_t* m
     cudaError_t e = c->pool ? cudaMallocFromPoolAsync(&tmp, 2 * (size_t)L * Sh::N * sizeof(T), c->pool, s)
                             : cudaMallocAsync(&tmp, 2 * (size_t)L * Sh::N * sizeof(T), s);
     if (e != cudaSuccess) return e;
-    k_eval_to_strip<T, LOGN><<<(unsigned)(2 * L), Sh::THREADS, 0, s>>>((const T*)pkprep, (T*)tmp);
+    // (64-bit limbs: also out of the Montgomery domain into centred doubles for the FP64 products)
+    k_eval_to_strip<T, LOGN, enc_f64<T, LOGN>()><<<(unsigned)(2 * L), Sh::THREADS, 0, s>>>(
+        (const T*)pkprep, (T*)tmp, (const PrimeTab<T>*)b->d_tabs, L);
     if ((e = cudaGetLastError()) != cudaSuccess) { cudaFreeAsync(tmp, s); return e; }
     pk = tmp;
   }

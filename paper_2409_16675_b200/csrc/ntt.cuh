@@ -980,16 +980,33 @@ __device__ __forceinline__ void eval_xpose_apply(const T* src, T* img, F&& f) {
 // thread t at 16-byte index c * THREADS + t.  The eval layout gives thread t the block f(t)
 // (ntt.cuh eval_xpose_*), so direct eval-layout key loads put every lane of a warp in its own
 // 128-byte line; in this layout each warp load is 512 contiguous bytes.  One block per polynomial.
-template <typename T, int LOGN>
-__global__ void __launch_bounds__(NttShape<LOGN>::THREADS) k_eval_to_strip(const T* __restrict__ in, T* __restrict__ out) {
+// TO_F64 (64-bit limbs): the prepared operand (Montgomery domain, NTT * N^-1 * 2^64) leaves the
+// Montgomery domain and is stored as the bits of its centred double, the form the FP64 products take
+// (`tabs` / `L`: the primes, block b being limb b % L).
+template <typename T, int LOGN, bool TO_F64 = false>
+__global__ void __launch_bounds__(NttShape<LOGN>::THREADS) k_eval_to_strip(const T* __restrict__ in, T* __restrict__ out,
+                                                                          const PrimeTab<T>* __restrict__ tabs, int L) {
   using Sh = NttShape<LOGN>;
   using EV = EvalVec<T, LOGN>;
   const T* src = in + (size_t)blockIdx.x * Sh::N;
   uint4* dst = reinterpret_cast<uint4*>(out + (size_t)blockIdx.x * Sh::N);
+  T p = 0, pinv = 0;
+  if constexpr (TO_F64) {
+    p = tabs[blockIdx.x % L].p;
+    pinv = tabs[blockIdx.x % L].pinv;
+  }
 #pragma unroll
   for (int i = 0; i < EV::CHUNKS; ++i) {
     T v[EV::VEC];
     EV::load(src, i, v);
+    if constexpr (TO_F64) {
+#pragma unroll
+      for (int c = 0; c < EV::VEC; ++c) {
+        const T r = mont_mul(v[c], (T)1, p, pinv);   // x 2^-64: leaves the Montgomery domain, [0, p)
+        const double dv = r > p / 2 ? -(double)(p - r) : (double)r;
+        v[c] = (T)__double_as_longlong(dv);
+      }
+    }
     dst[i * Sh::THREADS + threadIdx.x] = pack_chunk<T>(v);
   }
 }

@@ -765,7 +765,7 @@ static cudaError_t launch_relin_accum(const Ctx* c, const void* ct3, int ct_part
     cudaError_t e = c->pool ? cudaMallocFromPoolAsync(&tmp, npoly * Sh::N * sizeof(T), c->pool, s)
                             : cudaMallocAsync(&tmp, npoly * Sh::N * sizeof(T), s);
     if (e != cudaSuccess) return e;
-    k_eval_to_strip<T, LOGN><<<(unsigned)npoly, Sh::THREADS, 0, s>>>((const T*)keyprep, (T*)tmp);
+    k_eval_to_strip<T, LOGN><<<(unsigned)npoly, Sh::THREADS, 0, s>>>((const T*)keyprep, (T*)tmp, nullptr, 1);
     if ((e = cudaGetLastError()) != cudaSuccess) { cudaFreeAsync(tmp, s); return e; }
     keys = tmp;
   }
