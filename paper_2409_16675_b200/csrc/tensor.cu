@@ -612,6 +612,12 @@ struct RelinCfg {
   static constexpr int MINB = (Sh::THREADS == 256 && sizeof(T) == 4) ? 3 : Sh::MINB;
 };
 
+// 64-bit limbs with key strips: relinearisation in the FP64 domain (keys as centred doubles)
+template <typename T, int LOGN, bool KSTRIP>
+__host__ __device__ constexpr bool relin_f64() {
+  return sizeof(T) == 8 && KSTRIP && !RelinCfg<T, LOGN>::PF;
+}
+
 template <typename T, int LOGN, bool SMEM_TW, bool KSTRIP = false>
 __global__ void __launch_bounds__(NttShape<LOGN>::THREADS, RelinCfg<T, LOGN>::MINB)
 k_relin_accum(const T* ct3, int ct_parts, const uint32_t* digits, const T* keyprep, T* out,
@@ -648,6 +654,57 @@ k_relin_accum(const T* ct3, int ct_parts, const uint32_t* digits, const T* keypr
   const TwSrc<T, SMEM_TW> tw{twp};
   const int cb = coef_base<LOGN>();
   using EV = EvalVec<T, LOGN>;
+  if constexpr (relin_f64<T, LOGN, KSTRIP>()) {
+    // 64-bit limbs: digit transforms, the key products and the sums in the FP64 domain (keys as
+    // centred doubles NTT(key) N^-1 in the thread-major strip, launch_relin_accum); the sums are
+    // re-centred every 4 digits (|acc| <= 4 x 0.6 p + p/2 stays exact and a valid product input)
+    const F64Prime P{(double)pr.p, __drcp_rn((double)pr.p)};
+    double a0[Sh::E], a1[Sh::E], dx[Sh::E];
+#pragma unroll 1
+    for (uint32_t b = slot; b < batch; b += nslots) {
+#pragma unroll
+      for (int j = 0; j < Sh::E; ++j) a0[j] = a1[j] = 0.0;
+#pragma unroll 1
+      for (int d = 0; d < D; ++d) {
+        const uint32_t* src = digits + ((size_t)b * D + d) * N + cb;
+#pragma unroll
+        for (int j = 0; j < Sh::E; ++j) dx[j] = (double)__ldg(src + coef_off<LOGN>(j));   // digit sums < 2^32
+        ntt_fwd_f64<T, LOGN, 0, SMEM_TW, 1, 1>(dx, ex, tw, P);
+        const uint4* kb = reinterpret_cast<const uint4*>(keyprep + (((size_t)d * 2 + 0) * L + limb) * N);
+        const uint4* ka = reinterpret_cast<const uint4*>(keyprep + (((size_t)d * 2 + 1) * L + limb) * N);
+#pragma unroll
+        for (int i = 0; i < EV::CHUNKS; ++i) {
+          T vb[EV::VEC], va[EV::VEC];
+          unpack_chunk<T>(__ldg(kb + i * Sh::THREADS + threadIdx.x), vb);
+          unpack_chunk<T>(__ldg(ka + i * Sh::THREADS + threadIdx.x), va);
+#pragma unroll
+          for (int c = 0; c < EV::VEC; ++c) {
+            const int j = i * EV::VEC + c;
+            const double xc = f64_center(dx[j], P);
+            const double kbd = __longlong_as_double((long long)vb[c]), kad = __longlong_as_double((long long)va[c]);
+            a0[j] = __dadd_rn(a0[j], f64_mulmod(xc, kbd, __dmul_rn(kbd, P.pinv), P.p));
+            a1[j] = __dadd_rn(a1[j], f64_mulmod(xc, kad, __dmul_rn(kad, P.pinv), P.p));
+          }
+        }
+        if ((d & 3) == 3) {
+#pragma unroll
+          for (int j = 0; j < Sh::E; ++j) a0[j] = f64_center(a0[j], P), a1[j] = f64_center(a1[j], P);
+        }
+      }
+#pragma unroll 1
+      for (int part = 0; part < 2; ++part) {
+#pragma unroll
+        for (int j = 0; j < Sh::E; ++j) dx[j] = f64_center(part == 0 ? a0[j] : a1[j], P);   // < p: inverse input
+        ntt_inv_f64<T, LOGN, Sh::NPASS - 1, SMEM_TW, 1, 1>(dx, ex, tw, P);
+        const size_t off = (((size_t)b * ct_parts + part) * L + limb) * N + cb;
+        const size_t oo = ((b * 2 + part) * L + limb) * N + cb;
+#pragma unroll
+        for (int j = 0; j < Sh::E; ++j)
+          out[oo + coef_off<LOGN>(j)] = add_mod((T)f64_to_canon(dx[j], P), ct3[off + coef_off<LOGN>(j)], pr.p);
+      }
+    }
+    return;
+  }
   T acc0[Sh::E], acc1[Sh::E], x[Sh::E];
 #pragma unroll 1
   for (uint32_t b = slot; b < batch; b += nslots) {
@@ -765,7 +822,8 @@ static cudaError_t launch_relin_accum(const Ctx* c, const void* ct3, int ct_part
     cudaError_t e = c->pool ? cudaMallocFromPoolAsync(&tmp, npoly * Sh::N * sizeof(T), c->pool, s)
                             : cudaMallocAsync(&tmp, npoly * Sh::N * sizeof(T), s);
     if (e != cudaSuccess) return e;
-    k_eval_to_strip<T, LOGN><<<(unsigned)npoly, Sh::THREADS, 0, s>>>((const T*)keyprep, (T*)tmp, nullptr, 1);
+    k_eval_to_strip<T, LOGN, relin_f64<T, LOGN, KS>()><<<(unsigned)npoly, Sh::THREADS, 0, s>>>(
+        (const T*)keyprep, (T*)tmp, (const PrimeTab<T>*)B.d_tabs, L);
     if ((e = cudaGetLastError()) != cudaSuccess) { cudaFreeAsync(tmp, s); return e; }
     keys = tmp;
   }
