@@ -165,14 +165,7 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
 #pragma unroll 1
     for (uint32_t b = slot * GROUPS + group; b < batch; b += nslots * GROUPS) {
       {
-        const uint64_t* ppt = pt + (size_t)b * Sh::N + coef_base<LOGN>();
-#pragma unroll
-        for (int k = 0; k < Sh::E; ++k) {
-          const uint64_t v = __ldg(ppt + coef_off<LOGN>(k));
-          T r = csub(pr.reduce_plain(v, plain_fast), pr.p);  // v mod p
-          if (v > t_half) r = sub_mod(r, tmod, pr.p);         // centred lift: v - t
-          x[k] = r;
-        }
+        lift_plain_regs<T, LOGN>(pt + (size_t)b * Sh::N + coef_base<LOGN>(), x, pr, tmod, t_half, plain_fast);
         load_d(x);
         ntt_fwd_f64<T, LOGN, 0, SMEM_TW, NB, GROUPS>(d, ex, tw, P);
 #pragma unroll
@@ -212,14 +205,7 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
 #pragma unroll 1
   for (uint32_t b = slot * GROUPS + group; b < batch; b += nslots * GROUPS) {
     {
-      const uint64_t* ppt = pt + (size_t)b * Sh::N + coef_base<LOGN>();
-#pragma unroll
-      for (int k = 0; k < Sh::E; ++k) {
-        const uint64_t v = __ldg(ppt + coef_off<LOGN>(k));
-        T r = csub(pr.reduce_plain(v, plain_fast), pr.p);  // v mod p
-        if (v > t_half) r = sub_mod(r, tmod, pr.p);         // centred lift: v - t
-        x[k] = r;
-      }
+      lift_plain_regs<T, LOGN>(pt + (size_t)b * Sh::N + coef_base<LOGN>(), x, pr, tmod, t_half, plain_fast);
       ntt_fwd_regs<T, LOGN, 0, SMEM_TW, NB, GROUPS>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) x[k] = shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p);
@@ -424,14 +410,7 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
     } else if constexpr (OP == StreamOp::LiftPrepare || OP == StreamOp::LiftFwd) {
       const uint64_t* src = a.plain + (size_t)b * Sh::N + cb;
       if (leader && b + step < npoly) bulk_prefetch_l2(a.plain + (size_t)(b + step) * Sh::N, Sh::N * 8);
-      const T tmod = tabs[limb].tmod;
-#pragma unroll
-      for (int k = 0; k < Sh::E; ++k) {
-        const uint64_t v = __ldg(src + coef_off<LOGN>(k));
-        T r = csub(pr.reduce_plain(v, a.plain_fast), pr.p);  // v mod p
-        if (v > a.t_half) r = sub_mod(r, tmod, pr.p);           // centred lift: v - t
-        x[k] = r;
-      }
+      lift_plain_regs<T, LOGN>(src, x, pr, tabs[limb].tmod, a.t_half, a.plain_fast);
     } else if constexpr (EVAL_IN) {
       constexpr bool SI = EvalVec<T, LOGN>::CONTIG && EvalVec<T, LOGN>::VEC * sizeof(T) == 16;
       if (SI && a.strip_in) {

@@ -1029,17 +1029,6 @@ struct PrimeRegs {
     if constexpr (sizeof(T) == 4) return reduce4(x, p);
     else return csub(shoup_mul<uint64_t>(x, 1ull, one_q, p), p);
   }
-  // Plain value v < 2^57 mod p into [0, 2p) with ONE Shoup product when p > 2^25
-  // (v = hi 2^25 + lo with lo < 2^25 < p); callers pass fast = (t < 2^57 and p > 2^25).
-  __device__ __forceinline__ T reduce_plain(uint64_t v, bool fast) const {
-    if constexpr (sizeof(T) == 4) {
-      if (fast) {
-        const uint32_t hi = (uint32_t)(v >> 25), lo = (uint32_t)v & ((1u << 25) - 1);
-        return csub(shoup_mul<uint32_t>(hi, c25, c25_q, p) + lo, p2);
-      }
-    }
-    return reduce_u64_lazy(v);
-  }
   // Any 32-bit value into [0, p).
   __device__ __forceinline__ T reduce_digit(uint32_t v) const {
     return csub(shoup_mul<T>((T)v, (T)1, one_q, p), p);
@@ -1056,5 +1045,37 @@ struct PrimeRegs {
     }
   }
 };
+
+// Centred lift of E plain values (he.py:325-327: v in [0, t) -> v - t when v > t/2, mod p) into
+// the registers of a forward transform.  `src` points at coef_base().  32-bit limbs with `fast`
+// (t < 2^57, p > 2^25): ONE Shoup product per value and no canonical reduction -- hi 2^25 + lo
+// + (p - t mod p when v > t/2) < 2p + 2^25 + p < 4p, an admissible forward input (the butterflies
+// take X in [0, 4p) and any 32-bit Y).  The branch on `fast` is hoisted out of the element loop:
+// as a per-element select ptxas predicated both reductions and issued the unused one too (10 of
+// 23 issue slots per value).  Otherwise canonical values in [0, p).
+template <typename T, int LOGN>
+__device__ __forceinline__ void lift_plain_regs(const uint64_t* __restrict__ src, T (&x)[NttShape<LOGN>::E],
+                                                const PrimeRegs<T>& pr, T tmod, uint64_t t_half, bool fast) {
+  using Sh = NttShape<LOGN>;
+  if constexpr (sizeof(T) == 4) {
+    if (fast) {
+      const T ptm = pr.p - tmod;
+#pragma unroll
+      for (int k = 0; k < Sh::E; ++k) {
+        const uint64_t v = __ldg(src + coef_off<LOGN>(k));
+        const uint32_t hi = (uint32_t)(v >> 25), lo = (uint32_t)v & ((1u << 25) - 1);
+        x[k] = shoup_mul<uint32_t>(hi, pr.c25, pr.c25_q, pr.p) + lo + (v > t_half ? ptm : (T)0);
+      }
+      return;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) {
+    const uint64_t v = __ldg(src + coef_off<LOGN>(k));
+    T r = csub(pr.reduce_u64_lazy(v), pr.p);             // v mod p
+    if (v > t_half) r = sub_mod(r, tmod, pr.p);           // centred lift: v - t
+    x[k] = r;
+  }
+}
 
 }  // namespace ctb

@@ -79,6 +79,48 @@ __global__ void k_imad(uint32_t* out, uint32_t w, uint32_t c, int iters) {
   for (int k = 0; k < CH; ++k) s ^= a[k];
   if (s == 12345) out[0] = s;
 }
+// ALU-pipe instructions of the butterfly: IADD3, VIADDMNMX (the fused conditional subtraction
+// min(x - 2p, x)), VIMNMX
+__global__ void k_iadd3(uint32_t* out, uint32_t b, uint32_t c, int iters) {
+  uint32_t a[CH];
+  for (int k = 0; k < CH; ++k) a[k] = threadIdx.x * 77 + k;
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int k = 0; k < CH; ++k) asm volatile("{.reg .u32 t; add.u32 t, %0, %1; add.u32 %0, t, %2;}" : "+r"(a[k]) : "r"(b), "r"(c));
+  uint32_t s = 0;
+  for (int k = 0; k < CH; ++k) s ^= a[k];
+  if (s == 12345) out[0] = s;
+}
+__global__ void k_csub(uint32_t* out, uint32_t b, int iters) {
+  uint32_t a[CH];
+  for (int k = 0; k < CH; ++k) a[k] = threadIdx.x * 77 + k;
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int k = 0; k < CH; ++k) a[k] = __viaddmin_u32(a[k], b, a[k]) ^ (uint32_t)i;
+  uint32_t s = 0;
+  for (int k = 0; k < CH; ++k) s ^= a[k];
+  if (s == 12345) out[0] = s;
+}
+__global__ void k_min(uint32_t* out, uint32_t b, int iters) {
+  uint32_t a[CH];
+  for (int k = 0; k < CH; ++k) a[k] = threadIdx.x * 77 + k;
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int k = 0; k < CH; ++k) a[k] = min(a[k], b) ^ (uint32_t)i;
+  uint32_t s = 0;
+  for (int k = 0; k < CH; ++k) s ^= a[k];
+  if (s == 12345) out[0] = s;
+}
+__global__ void k_xor(uint32_t* out, uint32_t b, int iters) {
+  uint32_t a[CH];
+  for (int k = 0; k < CH; ++k) a[k] = threadIdx.x * 77 + k;
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int k = 0; k < CH; ++k) a[k] = (a[k] & b) ^ (uint32_t)i;
+  uint32_t s = 0;
+  for (int k = 0; k < CH; ++k) s ^= a[k];
+  if (s == 12345) out[0] = s;
+}
 __global__ void k_imadhi(uint32_t* out, uint32_t wq, int iters) {
   uint32_t a[CH];
   for (int k = 0; k < CH; ++k) a[k] = threadIdx.x * 77 + k;
@@ -170,6 +212,10 @@ int main() {
   for (int rep = 0; rep < 2; ++rep) {
     time_it("imad", n, [](void* v) { Args* a = (Args*)v; k_imad<<<BLOCKS, THREADS>>>(a->u, a->w, a->p, a->iters); }, &A);
     time_it("imadhi", n, [](void* v) { Args* a = (Args*)v; k_imadhi<<<BLOCKS, THREADS>>>(a->u, a->wq, a->iters); }, &A);
+    time_it("iadd3", n, [](void* v) { Args* a = (Args*)v; k_iadd3<<<BLOCKS, THREADS>>>(a->u, a->w, a->p, a->iters); }, &A);
+    time_it("csub+xor", n, [](void* v) { Args* a = (Args*)v; k_csub<<<BLOCKS, THREADS>>>(a->u, 0u - 2 * a->p, a->iters); }, &A);
+    time_it("min+xor", n, [](void* v) { Args* a = (Args*)v; k_min<<<BLOCKS, THREADS>>>(a->u, a->p, a->iters); }, &A);
+    time_it("lop3", n, [](void* v) { Args* a = (Args*)v; k_xor<<<BLOCKS, THREADS>>>(a->u, a->p, a->iters); }, &A);
     time_it("dfma", n, [](void* v) { Args* a = (Args*)v; k_dfma<<<BLOCKS, THREADS>>>(a->d, 0.999, 1.0, a->iters); }, &A);
     time_it("shoup", n, [](void* v) { Args* a = (Args*)v; k_shoup<<<BLOCKS, THREADS>>>(a->u, a->p, a->w, a->wq, a->iters); }, &A);
     time_it("f64q", n, [](void* v) { Args* a = (Args*)v; k_f64q<<<BLOCKS, THREADS>>>(a->u, a->p, a->w, a->wp, a->kw, a->iters); }, &A);
