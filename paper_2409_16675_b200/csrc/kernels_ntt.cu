@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
 k_ring_mul(const T* a, uint64_t sa, const T* b, uint64_t sb, T* out,
            const PrimeTab<T>* __restrict__ tabs, int L) {
   using Sh = NttShape<LOGN>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   Exchanger<T, LOGN> ex{reinterpret_cast<T*>(smem_raw)};
   const int limb = blockIdx.x % L;
   const size_t poly = blockIdx.x / L;
@@ -120,7 +120,7 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
   using Ex = Exchanger<T, LOGN, NB, GROUPS>;
   constexpr int TW_WORDS = SMEM_TW ? tw_words<T>(LOGN) : 0;
   constexpr int GROUP_WORDS = Ex::WORDS + Sh::N;  // exchange image + NTT(pt) strip
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
   const int group = (int)(threadIdx.x / Sh::THREADS);
   T* gsm = tw_sm + TW_WORDS + group * GROUP_WORDS;
@@ -139,6 +139,7 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
     twp = tw_sm;
   }
   const TwSrc<T, SMEM_TW> tw{twp};
+  constexpr bool RELAX = vec_exchange<T, LOGN>() && WARP_EXCHANGE;
 
   T x[Sh::E];
   if constexpr (sizeof(T) == 8) {
@@ -206,17 +207,21 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
   for (uint32_t b = slot * GROUPS + group; b < batch; b += nslots * GROUPS) {
     {
       lift_plain_regs<T, LOGN>(pt + (size_t)b * Sh::N + coef_base<LOGN>(), x, pr, tmod, t_half, plain_fast);
-      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, NB, GROUPS>(x, ex, tw, pr.p, pr.p2);
+      // every transform of the loop runs with the relaxed exchange guard (ntt.cuh Exchanger): each
+      // follows one of the other direction, except part 0's forward transform right after this
+      // one -- the explicit group barrier below is that guard
+      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, NB, GROUPS, F64Q_NE, RELAX>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) x[k] = shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p);
       ysm.store(x);
+      if constexpr (RELAX) group_sync<LOGN, GROUPS>();
     }
 #pragma unroll 1
     for (int part = 0; part < 2; ++part) {
       const size_t off = (((size_t)b * 2 + part) * L + limb) * (size_t)Sh::N + coef_base<LOGN>();
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) x[k] = ct[off + coef_off<LOGN>(k)];
-      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, NB, GROUPS>(x, ex, tw, pr.p, pr.p2);
+      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, NB, GROUPS, F64Q_NE, RELAX>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
       for (int c = 0; c < Strip<T, LOGN>::CHUNKS; ++c) {
         T y[Strip<T, LOGN>::VEC];
@@ -227,7 +232,7 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
           x[k] = mont_mul(x[k], y[j], pr.p, pr.pinv);
         }
       }
-      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, NB, GROUPS>(x, ex, tw, pr.p, pr.p2);
+      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, NB, GROUPS, F64Q_NE, RELAX>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) out[off + coef_off<LOGN>(k)] = csub(x[k], pr.p);
     }
@@ -325,7 +330,7 @@ k_stream(const StreamArgs<T> a, const PrimeTab<T>* __restrict__ tabs, int L, uin
                       !(sizeof(T) == 8 && OP == StreamOp::Inv);
   constexpr bool EARLY = PF && sizeof(T) == 8;   // next-item load issued right after the staging read
   constexpr int TW_WORDS = SMEM_TW ? tw_words<T>(LOGN) : 0;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
   const int group = (int)(threadIdx.x / Sh::THREADS);
   T* gsm = tw_sm + TW_WORDS + group * C::GW;
@@ -664,7 +669,7 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
   constexpr bool ENC_XPOSE = !PKSM && !enc_pk_strip<T, LOGN>() && sizeof(T) == 4 && CTB_EVAL_XPOSE &&
                              EV::VEC == Strip<T, LOGN>::VEC && eval_xpose_ok<T, LOGN>(Ex::WORDS);
   static_assert(!PKSM || (EV::VEC == Strip<T, LOGN>::VEC && GROUPS >= 2), "key strips need contiguous eval chunks");
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
   const int group = (int)(threadIdx.x / Sh::THREADS);
   T* gsm = tw_sm + TW_WORDS + group * GROUP_WORDS;
@@ -933,7 +938,7 @@ __global__ void __launch_bounds__(NttShape<LOGN>::THREADS, NttShape<LOGN>::MINB)
 k_pp_mul(const uint64_t* a, const uint64_t* b, uint64_t* out, const PrimeTab<uint32_t>* __restrict__ tabs,
          int LT, uint32_t c_inv, uint32_t c_inv_q) {
   using Sh = NttShape<LOGN>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   Exchanger<uint32_t, LOGN> ex{reinterpret_cast<uint32_t*>(smem_raw)};
   const size_t off = (size_t)blockIdx.x * Sh::N;
   uint32_t r0[Sh::E];

@@ -82,9 +82,11 @@ __host__ __device__ constexpr int shape_q_entries(int logn) { return (shape_q_of
 // Words per prime in the twiddle table: (w, w') pairs (+ the FP64 quotient table) for 32-bit
 // limbs; one double w per entry for 64-bit limbs (the FP64 butterflies derive w/p as w * (1/p),
 // see the f64 section below).
+// (32-bit limbs: rounded up to 128 bytes, so the exchange images that follow a staged table keep
+// the 128-byte alignment the warp-local exchange's XORed addresses need)
 template <typename T>
 __host__ __device__ constexpr int tw_words(int logn) {
-  return sizeof(T) == 4 ? 2 * shape_tw_entries(logn) + 2 * shape_q_entries(logn) : shape_tw_entries(logn);
+  return sizeof(T) == 4 ? (2 * shape_tw_entries(logn) + 2 * shape_q_entries(logn) + 31) / 32 * 32 : shape_tw_entries(logn);
 }
 
 template <int LOGN>
@@ -159,6 +161,11 @@ __host__ __device__ constexpr int phys_map(int idx) {
 }
 template <typename T, int LOGN>
 __host__ __device__ constexpr bool vec_exchange() { return sizeof(T) == 4 && LOGN == 12; }
+// -DCTB_WARP_EXCHANGE=0 restores the group-wide map-2 exchange (A/B: tools/ab_variants.py)
+#ifndef CTB_WARP_EXCHANGE
+#define CTB_WARP_EXCHANGE 1
+#endif
+constexpr bool WARP_EXCHANGE = CTB_WARP_EXCHANGE;
 // map of the exchange between the passes starting at stages SA and SB
 template <typename T, int LOGN, int SA, int SB>
 __host__ __device__ constexpr int exchange_map() {
@@ -171,7 +178,8 @@ __host__ __device__ constexpr int exchange_vec() { return MAP == 1 && S == 0 ? 2
 
 template <typename T, int LOGN>
 struct SmemImage {
-  static constexpr int RAW = vec_exchange<T, LOGN>() ? (phys_map<T, LOGN, 2>((1 << LOGN) - 1) + 1)  // largest of maps 0-2
+  // vectorised exchanges: map 1 fills exactly N words and the warp-local exchange lives inside it
+  static constexpr int RAW = vec_exchange<T, LOGN>() ? (WARP_EXCHANGE ? (1 << LOGN) : phys_map<T, LOGN, 2>((1 << LOGN) - 1) + 1)
                                                      : phys<T, LOGN>((1 << LOGN) - 1) + 1;
   // rounded to 16 bytes: whatever follows an image (strips, staging) is vector-accessed
   static constexpr int WORDS = (RAW + 16 / (int)sizeof(T) - 1) / (16 / (int)sizeof(T)) * (16 / (int)sizeof(T));
@@ -181,6 +189,10 @@ struct SmemImage {
 // low six thread bits so its lanes avoid the bank of the middle passes.
 template <int LOGN, bool LAST>
 __host__ __device__ constexpr int pass_thread(int t) {
+  // N = 4096 rotates only the low five bits, so a warp's blocks in the last pass are the same 32
+  // blocks (index bits 9-11 = warp) it owns in the middle pass: the exchange between those two
+  // passes never leaves the warp (Exchanger::run_warp).  tools/swizzle_check.py covers both.
+  if constexpr (LAST && LOGN == 12 && WARP_EXCHANGE) return ((t & 15) << 1) | ((t >> 4) & 1) | (t & ~31);
   if constexpr (LAST && LOGN >= 10) return ((t & 31) << 1) | ((t >> 5) & 1) | (t & ~63);
   return t;
 }
@@ -230,6 +242,7 @@ __device__ __forceinline__ int tw_slot(int gg) {
 
 // Host helper: storage slot of group B in pass (s, r) (inverse of the above).
 __host__ __device__ constexpr int tw_group_slot(int logn, int s, int r, int B) {
+  if (s + r == logn && logn == 12 && WARP_EXCHANGE) return ((B >> 1) & 15) | ((B & 1) << 4) | (B & ~31);
   if (s + r == logn && logn >= 10) return ((B >> 1) & 31) | ((B & 1) << 5) | (B & ~63);
   return B;
 }
@@ -429,19 +442,100 @@ __device__ __forceinline__ void group_sync() {
 // Shared-memory exchange between two pass layouts.  NBUF = 2 double-buffers
 // (one barrier per exchange); NBUF = 1 halves the footprint for one more
 // resident CTA at the price of a second barrier (write-after-read guard).
+//
+// Vectorised case (32-bit words, N = 4096; one image whatever NBUF).  In the middle pass (stages
+// 4-7) warp w of the transform owns the index bits 9-11 = w, and with the five-bit last-pass
+// rotation (pass_thread) so it does in the last pass.  Map 1 keeps index bits 9-11 as address bits
+// 9-11, so:
+//   * the middle-pass side of the map-1 exchange touches only the warp's own 512-word block;
+//   * the exchange between the middle and the last pass is a 16 x 16 transposition inside each
+//     half-warp and runs INSIDE that block with __syncwarp only (run_warp): element (s = index bit
+//     8, m = bits 4-7, j = bits 0-3) sits at block word
+//         256 s + 32 (m & 7) + 16 (m3 ^ s) + 4 ((j >> 2) ^ ((m >> 1) & 3)) + (j & 3),
+//     conflict-free for the middle pass's scalar accesses (lanes (s, j): bank bits m3 ^ s,
+//     (j3 j2) ^ (m2 m1), j1 j0) and for the last pass's 128-bit accesses (a quarter warp varies
+//     m3 m2 m1 at fixed s, m0: 16-byte bank group (m3 ^ s, c ^ (m2 m1))).  The XORed address bits
+//     cost 7 LOP3 on the scalar side (8 bases, two stores each) and 3 on the vector side;
+//   * the first-pass side of map 1 is thread-stationary: the inverse's last exchange reads exactly
+//     the words the next forward transform's first exchange writes.
+// Group-wide barriers per transform: one write-after-read guard before its first exchange and one
+// read-after-write barrier in its map-1 exchange (instead of four).  RELAX drops the guard where
+// the caller knows the image's previous use: a forward transform right after an inverse one
+// (thread-stationary words: no synchronisation at all), an inverse right after a forward (the
+// warp's own block: __syncwarp).  Not after a transform of the same direction, nor after any other
+// use of the image (eval_xpose_*).
 template <typename T, int LOGN, int NBUF = 2, int GROUPS = 1>
 struct Exchanger {
   T* buf;      // NBUF * SmemImage::WORDS words
   int cur = 0;
-  static constexpr int WORDS = NBUF * SmemImage<T, LOGN>::WORDS;
-  template <int SA, int RA, int SB, int RB, typename U>
+  static constexpr bool WARPX = vec_exchange<T, LOGN>() && WARP_EXCHANGE;
+  static constexpr int WORDS = (WARPX ? 1 : NBUF) * SmemImage<T, LOGN>::WORDS;
+
+  // The warp-local exchange (see above).  FWD: middle pass -> last pass (scalar stores, 128-bit
+  // loads); otherwise last -> middle (128-bit stores, scalar loads).
+  template <bool FWD, bool RELAX, typename U>
+  __device__ __forceinline__ void run_warp(U (&x)[NttShape<LOGN>::E]) {
+    static_assert(vec_exchange<T, LOGN>() && NttShape<LOGN>::E == 16, "warp-local exchange: N = 4096, 32-bit words");
+    const int t = ntt_tid<LOGN>();
+    U* blk = reinterpret_cast<U*>(buf) + (t & ~31) * 16;                                   // 512 words per warp
+    // middle-pass lane (s = t4, j = t3..t0): word 272 s + j, then ^ 4 (m >> 1), + 32 (m & 7) per element m
+    const uint32_t mid = (uint32_t)__cvta_generic_to_shared(blk) + 4u * (272u * ((t >> 4) & 1) + (t & 15));
+    // last-pass lane (m0 = t4, s = t3, m3 m2 m1 = t2 t1 t0): row 256 s + 32 (m & 7) + 16 (m3 ^ s), chunk c ^ (m2 m1)
+    const int sl = (t >> 3) & 1;
+    const uint32_t row = (uint32_t)__cvta_generic_to_shared(blk) +
+                         4u * (256u * sl + 32u * (((t & 3) << 1) | ((t >> 4) & 1)) + 16u * (((t >> 2) & 1) ^ sl) + 4u * (t & 3));
+    if constexpr (FWD || RELAX) __syncwarp();
+    else group_sync<LOGN, GROUPS>();
+    if constexpr (FWD) {
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const uint32_t a = mid ^ (16u * v);
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(a + 128u * ((2 * v) & 7)), "r"((uint32_t)x[2 * v]) : "memory");
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(a + 128u * ((2 * v + 1) & 7)), "r"((uint32_t)x[2 * v + 1]) : "memory");
+      }
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t a0, a1, a2, a3;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "r"(row ^ (16u * c)) : "memory");
+        x[4 * c] = (U)a0; x[4 * c + 1] = (U)a1; x[4 * c + 2] = (U)a2; x[4 * c + 3] = (U)a3;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(row ^ (16u * c)), "r"((uint32_t)x[4 * c]),
+                     "r"((uint32_t)x[4 * c + 1]), "r"((uint32_t)x[4 * c + 2]), "r"((uint32_t)x[4 * c + 3]) : "memory");
+      __syncwarp();
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const uint32_t a = mid ^ (16u * v);
+        uint32_t lo, hi;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lo) : "r"(a + 128u * ((2 * v) & 7)) : "memory");
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hi) : "r"(a + 128u * ((2 * v + 1) & 7)) : "memory");
+        x[2 * v] = (U)lo; x[2 * v + 1] = (U)hi;
+      }
+    }
+  }
+
+  template <int SA, int RA, int SB, int RB, bool RELAX = false, typename U>
   __device__ __forceinline__ void run(U (&x)[NttShape<LOGN>::E]) {
     static_assert(sizeof(U) == sizeof(T), "exchange element width");
     using Sh = NttShape<LOGN>;
-    U* b = reinterpret_cast<U*>(buf + cur * SmemImage<T, LOGN>::WORDS);
-    if constexpr (NBUF == 2) cur ^= 1;
-    else group_sync<LOGN, GROUPS>();
     constexpr int MAP = exchange_map<T, LOGN, SA, SB>();
+    if constexpr (MAP == 2 && WARPX) {
+      run_warp<(SA < SB), RELAX>(x);
+      return;
+    }
+    U* b = reinterpret_cast<U*>(buf + (WARPX ? 0 : cur) * SmemImage<T, LOGN>::WORDS);
+    if constexpr (MAP == 1 && WARPX) {
+      // write-after-read guard: forward (first exchange of its transform) a group barrier unless
+      // RELAX; inverse (after the warp-local exchange, writing only the warp's own block) a warp one
+      if constexpr (SA > SB) __syncwarp();
+      else if constexpr (!RELAX) group_sync<LOGN, GROUPS>();
+    } else {
+      if constexpr (NBUF == 2) cur ^= 1;
+      else group_sync<LOGN, GROUPS>();
+    }
     constexpr int VA = exchange_vec<MAP, SA>(), VB = exchange_vec<MAP, SB>();
     U* wa = b + phys_map<T, LOGN, MAP>(pass_index<LOGN, SA, RA>(ntt_tid<LOGN>(), 0));
     U* wb = b + phys_map<T, LOGN, MAP>(pass_index<LOGN, SB, RB>(ntt_tid<LOGN>(), 0));
@@ -669,7 +763,8 @@ __device__ __forceinline__ void ntt_inv_f64(double (&x)[NttShape<LOGN>::E], Exch
   }
 }
 
-template <typename T, int LOGN, int K = 0, bool SMEM, int NBUF, int GROUPS, int QE = F64Q_NE>
+// RELAX (ntt_fwd_regs / ntt_inv_regs): the caller vouches for the image's previous use, see Exchanger.
+template <typename T, int LOGN, int K = 0, bool SMEM, int NBUF, int GROUPS, int QE = F64Q_NE, bool RELAX = false>
 __device__ __forceinline__ void ntt_fwd_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN, NBUF, GROUPS>& ex,
                                              TwSrc<T, SMEM> tw, T p, T p2) {
   using Sh = NttShape<LOGN>;
@@ -699,13 +794,14 @@ __device__ __forceinline__ void ntt_fwd_regs(T (&x)[NttShape<LOGN>::E], Exchange
     constexpr int S = Sh::pass_s(K), R = Sh::pass_r(K);
     fwd_pass<T, LOGN, K, SMEM, QE>(x, tw, p, p2);
     if constexpr (K + 1 < Sh::NPASS) {
-      ex.template run<S, R, Sh::pass_s(K + 1), Sh::pass_r(K + 1)>(x);
-      ntt_fwd_regs<T, LOGN, K + 1, SMEM, NBUF, GROUPS, QE>(x, ex, tw, p, p2);
+      ex.template run<S, R, Sh::pass_s(K + 1), Sh::pass_r(K + 1), RELAX>(x);
+      ntt_fwd_regs<T, LOGN, K + 1, SMEM, NBUF, GROUPS, QE, RELAX>(x, ex, tw, p, p2);
     }
   }
 }
 
-template <typename T, int LOGN, int K = NttShape<LOGN>::NPASS - 1, bool SMEM, int NBUF, int GROUPS, int QE = F64Q_NE>
+template <typename T, int LOGN, int K = NttShape<LOGN>::NPASS - 1, bool SMEM, int NBUF, int GROUPS, int QE = F64Q_NE,
+          bool RELAX = false>
 __device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN, NBUF, GROUPS>& ex,
                                              TwSrc<T, SMEM> tw, T p, T p2) {
   using Sh = NttShape<LOGN>;
@@ -725,8 +821,8 @@ __device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchange
     constexpr int S = Sh::pass_s(K), R = Sh::pass_r(K);
     inv_pass<T, LOGN, K, SMEM, QE>(x, tw, p, p2);
     if constexpr (K > 0) {
-      ex.template run<S, R, Sh::pass_s(K - 1), Sh::pass_r(K - 1)>(x);
-      ntt_inv_regs<T, LOGN, K - 1, SMEM, NBUF, GROUPS, QE>(x, ex, tw, p, p2);
+      ex.template run<S, R, Sh::pass_s(K - 1), Sh::pass_r(K - 1), RELAX>(x);
+      ntt_inv_regs<T, LOGN, K - 1, SMEM, NBUF, GROUPS, QE, RELAX>(x, ex, tw, p, p2);
     }
   }
 }

@@ -305,7 +305,7 @@ k_tensor_product(const uint32_t* A, const uint32_t* Bt, uint32_t* H, const Prime
   using T = uint32_t;
   constexpr int TW_WORDS = SMEM_TW ? tw_words<T>(LOGN) : 0;
   using Ex = Exchanger<T, LOGN, 1, 1>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
   Ex ex{tw_sm + TW_WORDS};
   T* strip = tw_sm + TW_WORDS + Ex::WORDS + threadIdx.x;  // 3 thread-private polys
@@ -627,7 +627,7 @@ k_relin_accum(const T* ct3, int ct_parts, const uint32_t* digits, const T* keypr
   constexpr bool PF = C::PF;
   constexpr int TW_WORDS = SMEM_TW ? tw_words<T>(LOGN) : 0;
   using Ex = typename C::Ex;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
   Ex ex{tw_sm + TW_WORDS};
   uint32_t* stg = reinterpret_cast<uint32_t*>(smem_raw + (SMEM_TW ? C::TW_BYTES : 0) + C::EX_BYTES);
@@ -898,7 +898,7 @@ k_site_product(const uint32_t* AX, const uint32_t* AW, const int32_t* __restrict
   constexpr int GROUPS = site_groups<LOGN>();
   constexpr int TW_WORDS = SMEM_TW ? tw_words<T>(LOGN) : 0;
   using Ex = Exchanger<T, LOGN, 1, GROUPS>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
   const int group = (int)(threadIdx.x / Sh::THREADS);
   T* gsm = tw_sm + TW_WORDS + group * site_group_words<LOGN, GROUPS>();

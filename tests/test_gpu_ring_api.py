@@ -102,7 +102,7 @@ def test_eval_addend_is_scaled_forward_ntt():
 def test_linear_addend_is_eval_addend_in_thread_major_layout():
     """ctb_linear_addend = ctb_eval_addend permuted into ctb_linear_online's internal layout: 16-byte
     chunk c of transform thread t at chunk c * (N/16) + t, where thread t holds the 16-word eval
-    block f(t) (f rotates the low 6 thread bits: ntt.cuh pass_thread)."""
+    block f(t) (at N = 4096 f rotates the low 5 thread bits: ntt.cuh pass_thread)."""
     import torch
     from paper_2409_16675_b200 import _lib
     from paper_2409_16675_b200.device import RnsContext, _ptr, _stream
@@ -116,7 +116,7 @@ def test_linear_addend_is_eval_addend_in_thread_major_layout():
     _lib.check(ctx._lib.ctb_linear_addend(ctx._h, 0, _ptr(x), _ptr(lin), 3, _stream()), "ctb_linear_addend")
     threads = P.n // 16
     t = torch.arange(threads)
-    f = (t & ~63) | ((t << 1) & 62) | ((t >> 5) & 1)
+    f = (t & ~31) | ((t << 1) & 30) | ((t >> 4) & 1)
     c = torch.arange(4)
     src = (4 * f[None, :] + c[:, None]).reshape(-1)           # eval chunk of strip chunk c*threads + t
     want = ev.view(3, ctx.L, P.n // 4, 4)[:, :, src.cuda()].reshape(3, ctx.L, P.n)

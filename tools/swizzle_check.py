@@ -16,6 +16,8 @@ def cfg(logn):
     return N, T, E, passes
 
 def sigma(logn, last, t):
+    if logn == 12 and last:   # five-bit rotation: the last exchange stays inside the warp
+        return ((t & 15) << 1) | ((t >> 4) & 1) | (t & ~31)
     if logn >= 10 and last:
         return ((t & 31) << 1) | ((t >> 5) & 1) | (t & ~63)
     return t
@@ -101,8 +103,57 @@ if __name__ == "__main__":
         return worst
 
     for m, w in MAPS.items():
+        if m == 2:
+            continue  # replaced by the warp-local exchange below (kept for reference)
         assert len({phys(i, w) for i in range(N)}) == N
-        sides = [(0, 2), (1, 1)] if m == 1 else [(1, 1), (2, 4)]
+        sides = [(0, 2), (1, 1)]
         degs = [vec_degree(w, p, v) for p, v in sides]
         assert degs == [1, 1], (m, degs)
         print(f"vector map {m}: sides (pass, words) {sides} conflict={degs} smem_words={phys(N - 1, w) + 1}")
+
+    # map 1 keeps index bits 9-11 as address bits 9-11: the middle pass touches only its warp's block
+    w1 = MAPS[1]
+    s1, r1 = passes[1]
+    for t in range(T):
+        for k in range(E):
+            assert phys(pass_idx(logn, N, T, E, s1, r1, False, t, k), w1) // 512 == t // 32
+    # and the first-pass side is thread-stationary (forward's writes == inverse's reads): same layout
+
+    # Warp-local exchange between the middle and the last pass (ntt.cuh Exchanger::run_warp): both
+    # sides must address every element identically, inside the warp's 512-word block, conflict-free.
+    def mid_addr(t, m):
+        mid = 272 * ((t >> 4) & 1) + (t & 15)
+        return (t & ~31) * 16 + ((mid ^ (4 * (m >> 1))) + 32 * (m & 7))
+
+    def last_addr(t, k):
+        sl = (t >> 3) & 1
+        row = 256 * sl + 32 * (((t & 3) << 1) | ((t >> 4) & 1)) + 16 * (((t >> 2) & 1) ^ sl) + 4 * (t & 3)
+        return (t & ~31) * 16 + (row ^ (4 * (k // 4))) + (k % 4)
+
+    s2, r2 = passes[2]
+    where = {}
+    for t in range(T):
+        for k in range(E):
+            a = mid_addr(t, k)
+            assert a // 512 == t // 32
+            idx = pass_idx(logn, N, T, E, s1, r1, False, t, k)
+            assert idx not in where
+            where[idx] = a
+    assert len(set(where.values())) == N
+    for t in range(T):
+        for k in range(E):
+            assert where[pass_idx(logn, N, T, E, s2, r2, True, t, k)] == last_addr(t, k), (t, k)
+    worst_s = worst_v = 1
+    for warp in range(T // 32):
+        for k in range(E):
+            worst_s = max(worst_s, degree([mid_addr(warp * 32 + l, k) for l in range(32)], 4))
+        for c in range(4):
+            for q in range(4):
+                banks = {}
+                for l in range(8 * q, 8 * q + 8):
+                    for i in range(4):
+                        a = last_addr(warp * 32 + l, 4 * c + i)
+                        banks.setdefault(a % 32, set()).add(a)
+                worst_v = max(worst_v, max(len(v) for v in banks.values()))
+    assert (worst_s, worst_v) == (1, 1), (worst_s, worst_v)
+    print(f"warp-local exchange (passes 1 <-> 2): both sides agree, inside the warp's block, conflict={[worst_s, worst_v]}")
