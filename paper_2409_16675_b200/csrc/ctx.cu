@@ -168,23 +168,23 @@ static int build_typed(Base& b, uint32_t logn, std::string& err, const uint64_t*
     pw[0] = 1;
     for (uint32_t i = 1; i < n; ++i) pw[i] = mulmod(pw[i - 1], psi, p);
     // pass k, group B, stage i, block jb -> psi^bitrev(2^(s+i) + B*2^i + jb) at pair
-    // tw_off(k) + e * 2^s + B with e = 2^i - 1 + jb (entry-major, see ntt.cuh TwSrc)
+    // shape_tw_pair(k, e, slot of B) with e = 2^i - 1 + jb (32-bit limbs; 64-bit limbs: tw_off(k) + e * 2^s + slot)
     for (int k = 0; k < shape_npass((int)logn); ++k) {
       const int s = shape_pass_s((int)logn, k), r = shape_pass_r((int)logn, k);
       for (int B = 0; B < (1 << s); ++B)
         for (int i = 0; i < r; ++i)
           for (int jb = 0; jb < (1 << i); ++jb) {
             const uint32_t mb = (1u << (s + i)) + ((uint32_t)B << i) + jb;
-            const size_t e = (size_t)shape_tw_off((int)logn, k) + ((size_t)((1u << i) - 1 + jb) << s) +
-                             tw_group_slot((int)logn, s, r, B);
+            const int ei = (1 << i) - 1 + jb, gslot = tw_group_slot((int)logn, s, r, B);
+            const size_t e = sizeof(T) == 4 ? (size_t)shape_tw_pair((int)logn, k, ei, gslot)
+                                            : (size_t)shape_tw_off((int)logn, k) + ((size_t)ei << s) + gslot;
             const uint64_t w = pw[bitrev(mb, logn)];
             if (sizeof(T) == 4) {
               f[2 * e] = (T)w;  f[2 * e + 1] = shoup_q<T>(w, p);
-              const int ei = (1 << i) - 1 + jb;
               if (ei < F64Q_NE) {  // FP64 quotient table (ntt.cuh F64Q_NE): w'/p = round(w 2^52 / p) 2^-52
                 const uint64_t num = (uint64_t)((((unsigned __int128)w << 52) + p / 2) / p);
                 const double wp = std::ldexp((double)num, -52);
-                const size_t qe = (size_t)shape_q_off((int)logn, k) + ((size_t)ei << s) + tw_group_slot((int)logn, s, r, B);
+                const size_t qe = (size_t)shape_q_index((int)logn, k, ei, gslot);
                 std::memcpy(reinterpret_cast<unsigned char*>(f + 2 * ent) + 8 * qe, &wp, 8);
               }
             } else {  // 64-bit limbs run the FP64 butterflies (ntt.cuh): w CENTRED, as a double

@@ -221,7 +221,10 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
       const size_t off = (((size_t)b * 2 + part) * L + limb) * (size_t)Sh::N + coef_base<LOGN>();
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) x[k] = ct[off + coef_off<LOGN>(k)];
-      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, NB, GROUPS, F64Q_NE, RELAX>(x, ex, tw, pr.p, pr.p2);
+      // canonical ciphertext residues in: the forward transform skips the conditional subtractions
+      // of its first stage (the inverse's inputs, Montgomery products of x < 4p and y < 2p, only
+      // lie below 2p)
+      ntt_fwd_regs<T, LOGN, 0, SMEM_TW, NB, GROUPS, F64Q_NE, RELAX, true>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
       for (int c = 0; c < Strip<T, LOGN>::CHUNKS; ++c) {
         T y[Strip<T, LOGN>::VEC];

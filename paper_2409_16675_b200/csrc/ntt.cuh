@@ -58,6 +58,13 @@ __host__ __device__ constexpr int shape_tw_off(int logn, int k) {
   return off;
 }
 __host__ __device__ constexpr int shape_tw_entries(int logn) { return shape_tw_off(logn, shape_npass(logn)); }
+// 32-bit limbs: (w, w') pair index of entry e (= 2^i - 1 + jb) of group slot `slot` in pass k.
+// Entries e and e + 1 with e odd (blocks jb, jb + 1 of one stage) are adjacent, so the passes read
+// two entries per 128-bit load, conflict-free for consecutive slots; entry 0 is the second half of
+// pair 0 (whose first half is unused).  64-bit limbs keep one word per entry at (e << s) + slot.
+__host__ __device__ constexpr int shape_tw_pair(int logn, int k, int e, int slot) {
+  return shape_tw_off(logn, k) + ((((e + 1) >> 1) << shape_pass_s(logn, k)) + slot) * 2 + ((e + 1) & 1);
+}
 // FP64-quotient butterflies (32-bit limbs).  The Shoup product a*w mod p costs IMAD.HI + 2 IMAD,
 // all on the fma-heavy pipe (IMAD.HI at half rate), which is what bounds the transforms.  For the
 // twiddle entries e < F64Q_NE of every pass (e = 2^i - 1 + jb: stage 0 and the first block of
@@ -76,6 +83,10 @@ __host__ __device__ constexpr int shape_q_off(int logn, int k) {
   int off = 0;
   for (int q = 0; q < k; ++q) off += F64Q_NE << shape_pass_s(logn, q);
   return off;
+}
+// index of the FP64 quotient of entry e (< F64Q_NE): slot-major, a slot's entries adjacent
+__host__ __device__ constexpr int shape_q_index(int logn, int k, int e, int slot) {
+  return shape_q_off(logn, k) + slot * F64Q_NE + e;
 }
 // doubles in the quotient table, rounded up to a 16-byte multiple
 __host__ __device__ constexpr int shape_q_entries(int logn) { return (shape_q_off(logn, shape_npass(logn)) + 1) & ~1; }
@@ -267,6 +278,15 @@ struct TwSrc {
       asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(at));
     return v;
   }
+  // two adjacent (w, w') entries with one 128-bit load (32-bit limbs)
+  __device__ __forceinline__ void load2(const T* at, T& w0, T& wq0, T& w1, T& wq1) const {
+    static_assert(sizeof(T) == 4, "paired twiddle entries: 32-bit limbs");
+    if constexpr (SMEM)
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(wq0), "=r"(w1), "=r"(wq1)
+                   : "r"((uint32_t)__cvta_generic_to_shared(at)));
+    else
+      asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(wq0), "=r"(w1), "=r"(wq1) : "l"(at));
+  }
   __device__ __forceinline__ void load(const T* at, T& w, T& wq) const {
     if constexpr (SMEM) {
       const uint32_t sa = (uint32_t)__cvta_generic_to_shared(at);
@@ -283,6 +303,20 @@ struct TwSrc {
   }
 };
 
+// ptxas turns two-input integer adds into IMAD.IADD (fma-heavy pipe, half rate on sm_100a -- the
+// pipe that bounds the transforms) when it judges the ALU pipe busier.  -DCTB_ALU_ADD=1 writes the
+// butterflies' two-input sums with a third operand the compiler cannot fold (a __constant__ zero),
+// which keeps them IADD3 on the ALU pipe (tools/probe/bfly_probe.cu: +8% on pure Shoup passes).
+#ifndef CTB_ALU_ADD
+#define CTB_ALU_ADD 0
+#endif
+__device__ __constant__ uint32_t g_opaque_zero = 0;
+template <typename T>
+__device__ __forceinline__ T add2(T a, T b) {
+  if constexpr (CTB_ALU_ADD && sizeof(T) == 4) return a + b + (T)g_opaque_zero;
+  else return a + b;
+}
+
 // Harvey CT butterfly.
 //  u32 (p < 2^30): X, Y in [0,4p) -> X+WY, X-WY in [0,4p).
 //  u64 (p < 2^50 in practice, < 2^57 required): no conditional subtraction --
@@ -290,7 +324,9 @@ struct TwSrc {
 //    stage, so canonical inputs stay below 53p after 13 stages (far below
 //    2^64); consumers are Shoup / Montgomery products (valid for any such
 //    input) or canon_fwd().
-template <typename T>
+// NOCS (32-bit limbs): the caller knows the conditional subtraction is a no-op (forward: X < 2p;
+// inverse: X + Y < 2p) -- the first stage of a transform whose inputs are canonical.
+template <typename T, bool NOCS = false>
 __device__ __forceinline__ void ct_bfly(T& X, T& Y, T w, T wq, T p, T p2) {
   if constexpr (sizeof(T) == 8) {
     const T t = shoup_mul_lazy4(Y, w, wq, p);
@@ -298,9 +334,9 @@ __device__ __forceinline__ void ct_bfly(T& X, T& Y, T w, T wq, T p, T p2) {
     X = x + t;
     Y = x + 2 * p2 - t;
   } else {
-    T x = csub(X, p2);
+    T x = NOCS ? X : csub(X, p2);
     T t = shoup_mul(Y, w, wq, p);
-    X = x + t;
+    X = add2(x, t);
     Y = x - t + p2;
   }
 }
@@ -309,7 +345,7 @@ __device__ __forceinline__ void ct_bfly(T& X, T& Y, T w, T wq, T p, T p2) {
 //  u32: X, Y in [0,2p) -> X+Y, (Y-X)W in [0,2p).
 //  u64: X, Y in [0,4p) -> same, in [0,4p) (approximate Shoup); ntt_inv_regs
 //       brings the outputs back below 2p after the last stage.
-template <typename T>
+template <typename T, bool NOCS = false>
 __device__ __forceinline__ void gs_bfly(T& X, T& Y, T w, T wq, T p, T p2) {
   if constexpr (sizeof(T) == 8) {
     const T p4 = 2 * p2;
@@ -318,7 +354,7 @@ __device__ __forceinline__ void gs_bfly(T& X, T& Y, T w, T wq, T p, T p2) {
     Y = shoup_mul_lazy4(v, w, wq, p);
     X = u;
   } else {
-    T u = csub(X + Y, p2);
+    T u = NOCS ? X + Y : csub(add2(X, Y), p2);
     T v = Y - X + p2;
     Y = shoup_mul(v, w, wq, p);
     X = u;
@@ -337,15 +373,20 @@ __device__ __forceinline__ uint32_t f64q_mul(uint32_t a, uint32_t w, double wp, 
   return r;  // a*w + p - q*p in (0, 2p)
 }
 __device__ __forceinline__ double f64q_k(double wp) { return __fma_rn(-4503599627370496.0, wp, 6755399441055744.0); }
-// the FP64 quotient of entry (pass K, e = 0, group slot); entry e is at [e << S0] from it
+// FP64 quotients of the group slot (pass K): entry e at [e] from it (ntt.cuh shape_q_index)
 template <typename T, int LOGN, int K>
 __device__ __forceinline__ const double* q_group(const T* tab, int slot) {
-  return reinterpret_cast<const double*>(tab + 2 * shape_tw_entries(LOGN)) + shape_q_off(LOGN, K) + slot;
+  return reinterpret_cast<const double*>(tab + 2 * shape_tw_entries(LOGN)) + shape_q_off(LOGN, K) + slot * F64Q_NE;
 }
 
-template <typename T, int LOGN, int K, bool SMEM, int QE = F64Q_NE>
+// CANON: the pass's inputs are below 2p (forward) / p (inverse), e.g. canonical residues from
+// memory: the first stage skips its conditional subtractions.
+// Twiddles are read two entries per 128-bit load (shape_tw_pair: the entries of blocks jb, jb + 1 of
+// a stage are adjacent); entry 0 alone.
+template <typename T, int LOGN, int K, bool SMEM, int QE = F64Q_NE, bool CANON = false>
 __device__ __forceinline__ void fwd_pass(T (&x)[NttShape<LOGN>::E], TwSrc<T, SMEM> tw, T p, T p2) {
   static_assert(QE <= F64Q_NE, "FP64 quotient entries beyond the table");
+  static_assert(sizeof(T) == 4, "integer butterflies: 32-bit limbs (64-bit limbs run the FP64 passes)");
   using Sh = NttShape<LOGN>;
   constexpr int S0 = Sh::pass_s(K), R = Sh::pass_r(K);
   constexpr int G = 1 << R;
@@ -353,41 +394,53 @@ __device__ __forceinline__ void fwd_pass(T (&x)[NttShape<LOGN>::E], TwSrc<T, SME
 #pragma unroll
   for (int gg = 0; gg < Sh::E / G; ++gg) {
     const int slot = tw_slot<LOGN, S0, R>(gg);
-    const T* tg = tw.tab + 2 * (Sh::tw_off(K) + slot);
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
+    const T* tg = tw.tab + 2 * Sh::tw_off(K) + 4 * slot;   // entry pair q at + 4 (q << S0) words
+    const double* qg = q_group<T, LOGN, K>(tw.tab, slot);
+    auto block = [&](int i, int jb, T w, T wq) {
       const int h = 1 << (R - i - 1);
+      const int e = (1 << i) - 1 + jb;
+      if (e < QE) {
+        const double wp = tw.loadq(qg + e);
+        const double kq = f64q_k(wp);
 #pragma unroll
-      for (int jb = 0; jb < (1 << i); ++jb) {
-        const int e = (1 << i) - 1 + jb;
-        T w, wq;
-        tw.load(tg + 2 * (e << S0), w, wq);
-        if (sizeof(T) == 4 && e < QE) {
-          const double wp = tw.loadq(q_group<T, LOGN, K>(tw.tab, slot) + (e << S0));
-          const double kq = f64q_k(wp);
-#pragma unroll
-          for (int jj = 0; jj < h; ++jj) {
-            const int a = gg * G + jb * 2 * h + jj;
-            const T xx = csub(x[a], p2);
-            const T t = (T)f64q_mul((uint32_t)x[a + h], (uint32_t)w, wp, kq, (uint32_t)p, (uint32_t)pn);
-            x[a] = xx + t;
-            x[a + h] = xx - t + p2;
-          }
-        } else {
-#pragma unroll
-          for (int jj = 0; jj < h; ++jj) {
-            const int a = gg * G + jb * 2 * h + jj;
-            ct_bfly(x[a], x[a + h], w, wq, p, p2);
-          }
+        for (int jj = 0; jj < h; ++jj) {
+          const int a = gg * G + jb * 2 * h + jj;
+          const T xx = (CANON && i == 0) ? x[a] : csub(x[a], p2);
+          const T t = (T)f64q_mul((uint32_t)x[a + h], (uint32_t)w, wp, kq, (uint32_t)p, (uint32_t)pn);
+          x[a] = add2(xx, t);
+          x[a + h] = xx - t + p2;
         }
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < h; ++jj) {
+          const int a = gg * G + jb * 2 * h + jj;
+          if (CANON && i == 0) ct_bfly<T, true>(x[a], x[a + h], w, wq, p, p2);
+          else ct_bfly(x[a], x[a + h], w, wq, p, p2);
+        }
+      }
+    };
+    {
+      T w, wq;
+      tw.load(tg + 2, w, wq);  // entry 0: second half of pair 0
+      block(0, 0, w, wq);
+    }
+#pragma unroll
+    for (int i = 1; i < R; ++i) {
+#pragma unroll
+      for (int jb = 0; jb < (1 << i); jb += 2) {
+        T w0, wq0, w1, wq1;
+        tw.load2(tg + 4 * ((((1 << i) + jb) >> 1) << S0), w0, wq0, w1, wq1);
+        block(i, jb, w0, wq0);
+        block(i, jb + 1, w1, wq1);
       }
     }
   }
 }
 
-template <typename T, int LOGN, int K, bool SMEM, int QE = F64Q_NE>
+template <typename T, int LOGN, int K, bool SMEM, int QE = F64Q_NE, bool CANON = false>
 __device__ __forceinline__ void inv_pass(T (&x)[NttShape<LOGN>::E], TwSrc<T, SMEM> tw, T p, T p2) {
   static_assert(QE <= F64Q_NE, "FP64 quotient entries beyond the table");
+  static_assert(sizeof(T) == 4, "integer butterflies: 32-bit limbs (64-bit limbs run the FP64 passes)");
   using Sh = NttShape<LOGN>;
   constexpr int S0 = Sh::pass_s(K), R = Sh::pass_r(K);
   constexpr int G = 1 << R;
@@ -395,33 +448,46 @@ __device__ __forceinline__ void inv_pass(T (&x)[NttShape<LOGN>::E], TwSrc<T, SME
 #pragma unroll
   for (int gg = 0; gg < Sh::E / G; ++gg) {
     const int slot = (1 << S0) - 1 - tw_slot<LOGN, S0, R>(gg);  // mirrored group
-    const T* tg = tw.tab + 2 * (Sh::tw_off(K) + slot);
-#pragma unroll
-    for (int i = R - 1; i >= 0; --i) {
+    const T* tg = tw.tab + 2 * Sh::tw_off(K) + 4 * slot;
+    const double* qg = q_group<T, LOGN, K>(tw.tab, slot);
+    // block jb of stage i with the mirrored entry e = 2^i - 1 + (2^i - 1 - jb)
+    auto block = [&](int i, int jb, T w, T wq) {
       const int h = 1 << (R - i - 1);
+      const int e = (1 << i) - 1 + ((1 << i) - 1 - jb);
+      if (e < QE) {
+        const double wp = tw.loadq(qg + e);
+        const double kq = f64q_k(wp);
 #pragma unroll
-      for (int jb = 0; jb < (1 << i); ++jb) {
-        const int e = (1 << i) - 1 + ((1 << i) - 1 - jb);  // mirrored block
-        T w, wq;
-        tw.load(tg + 2 * (e << S0), w, wq);
-        if (sizeof(T) == 4 && e < QE) {
-          const double wp = tw.loadq(q_group<T, LOGN, K>(tw.tab, slot) + (e << S0));
-          const double kq = f64q_k(wp);
+        for (int jj = 0; jj < h; ++jj) {
+          const int a = gg * G + jb * 2 * h + jj;
+          const T X = x[a], Y = x[a + h];
+          x[a] = (CANON && i == R - 1) ? X + Y : csub(add2(X, Y), p2);
+          x[a + h] = (T)f64q_mul((uint32_t)(Y - X + p2), (uint32_t)w, wp, kq, (uint32_t)p, (uint32_t)pn);
+        }
+      } else {
 #pragma unroll
-          for (int jj = 0; jj < h; ++jj) {
-            const int a = gg * G + jb * 2 * h + jj;
-            const T X = x[a], Y = x[a + h];
-            x[a] = csub(X + Y, p2);
-            x[a + h] = (T)f64q_mul((uint32_t)(Y - X + p2), (uint32_t)w, wp, kq, (uint32_t)p, (uint32_t)pn);
-          }
-        } else {
-#pragma unroll
-          for (int jj = 0; jj < h; ++jj) {
-            const int a = gg * G + jb * 2 * h + jj;
-            gs_bfly(x[a], x[a + h], w, wq, p, p2);
-          }
+        for (int jj = 0; jj < h; ++jj) {
+          const int a = gg * G + jb * 2 * h + jj;
+          if (CANON && i == R - 1) gs_bfly<T, true>(x[a], x[a + h], w, wq, p, p2);
+          else gs_bfly(x[a], x[a + h], w, wq, p, p2);
         }
       }
+    };
+#pragma unroll
+    for (int i = R - 1; i >= 1; --i) {
+#pragma unroll
+      for (int jb = 0; jb < (1 << i); jb += 2) {
+        // blocks jb, jb + 1 use entries e, e - 1 with e + 1 = 2^(i+1) - 1 - jb: halves 1 and 0 of one pair
+        T w0, wq0, w1, wq1;
+        tw.load2(tg + 4 * ((((1 << (i + 1)) - 1 - jb) >> 1) << S0), w0, wq0, w1, wq1);
+        block(i, jb, w1, wq1);
+        block(i, jb + 1, w0, wq0);
+      }
+    }
+    {
+      T w, wq;
+      tw.load(tg + 2, w, wq);
+      block(0, 0, w, wq);
     }
   }
 }
@@ -764,7 +830,9 @@ __device__ __forceinline__ void ntt_inv_f64(double (&x)[NttShape<LOGN>::E], Exch
 }
 
 // RELAX (ntt_fwd_regs / ntt_inv_regs): the caller vouches for the image's previous use, see Exchanger.
-template <typename T, int LOGN, int K = 0, bool SMEM, int NBUF, int GROUPS, int QE = F64Q_NE, bool RELAX = false>
+// CANON: inputs below 2p (forward) / p (inverse), see fwd_pass; applies to the transform's first pass.
+template <typename T, int LOGN, int K = 0, bool SMEM, int NBUF, int GROUPS, int QE = F64Q_NE, bool RELAX = false,
+          bool CANON = false>
 __device__ __forceinline__ void ntt_fwd_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN, NBUF, GROUPS>& ex,
                                              TwSrc<T, SMEM> tw, T p, T p2) {
   using Sh = NttShape<LOGN>;
@@ -792,16 +860,16 @@ __device__ __forceinline__ void ntt_fwd_regs(T (&x)[NttShape<LOGN>::E], Exchange
     for (int k = 0; k < Sh::E; ++k) x[k] = f64_to_canon(d[k], P);
   } else {
     constexpr int S = Sh::pass_s(K), R = Sh::pass_r(K);
-    fwd_pass<T, LOGN, K, SMEM, QE>(x, tw, p, p2);
+    fwd_pass<T, LOGN, K, SMEM, QE, CANON>(x, tw, p, p2);
     if constexpr (K + 1 < Sh::NPASS) {
       ex.template run<S, R, Sh::pass_s(K + 1), Sh::pass_r(K + 1), RELAX>(x);
-      ntt_fwd_regs<T, LOGN, K + 1, SMEM, NBUF, GROUPS, QE, RELAX>(x, ex, tw, p, p2);
+      ntt_fwd_regs<T, LOGN, K + 1, SMEM, NBUF, GROUPS, QE, RELAX, false>(x, ex, tw, p, p2);
     }
   }
 }
 
 template <typename T, int LOGN, int K = NttShape<LOGN>::NPASS - 1, bool SMEM, int NBUF, int GROUPS, int QE = F64Q_NE,
-          bool RELAX = false>
+          bool RELAX = false, bool CANON = false>
 __device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchanger<T, LOGN, NBUF, GROUPS>& ex,
                                              TwSrc<T, SMEM> tw, T p, T p2) {
   using Sh = NttShape<LOGN>;
@@ -819,10 +887,10 @@ __device__ __forceinline__ void ntt_inv_regs(T (&x)[NttShape<LOGN>::E], Exchange
     for (int k = 0; k < Sh::E; ++k) x[k] = f64_to_canon(d[k], P);
   } else {
     constexpr int S = Sh::pass_s(K), R = Sh::pass_r(K);
-    inv_pass<T, LOGN, K, SMEM, QE>(x, tw, p, p2);
+    inv_pass<T, LOGN, K, SMEM, QE, CANON>(x, tw, p, p2);
     if constexpr (K > 0) {
       ex.template run<S, R, Sh::pass_s(K - 1), Sh::pass_r(K - 1), RELAX>(x);
-      ntt_inv_regs<T, LOGN, K - 1, SMEM, NBUF, GROUPS, QE, RELAX>(x, ex, tw, p, p2);
+      ntt_inv_regs<T, LOGN, K - 1, SMEM, NBUF, GROUPS, QE, RELAX, false>(x, ex, tw, p, p2);
     }
   }
 }

@@ -185,8 +185,8 @@ __global__ void k_check_f64q(const uint32_t* tw, int words, const uint64_t* prim
   const int s = shape_pass_s(logn, k), r = shape_pass_r(logn, k);
   const int e = idx >> s, slot = idx & ((1 << s) - 1);
   if (e >= (1 << r) - 1) return;  // no such stage/block in a short pass: entry unused
-  const uint32_t w = f[2 * (shape_tw_off(logn, k) + (e << s) + slot)];
-  const double wp = qt[shape_q_off(logn, k) + (e << s) + slot];
+  const uint32_t w = f[2 * shape_tw_pair(logn, k, e, slot)];
+  const double wp = qt[shape_q_index(logn, k, e, slot)];
   const double kq = f64q_k(wp);
   const uint32_t pn = 0u - p;
   unsigned long long nbad = 0;
