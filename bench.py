@@ -152,9 +152,11 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------- ours
-def probe_modmul_peak(torch, lib, word: int, f64q_of_8=None):
+def probe_modmul_peak(torch, lib, word: int, f64q_of_8=None, splice=False, bfly_ctx=None):
     """Register-resident modmul/s: Shoup at `word` bytes, or (f64q_of_8 given) the 30-bit mix of
-    Shoup and FP64-quotient products (ctb_probe_modmul_mix)."""
+    Shoup and FP64-quotient products (ctb_probe_modmul_mix; splice: the round-1 form of the
+    quotient), or (bfly_ctx given) complete butterflies/s of k_cpmul's own register pass
+    (ctb_probe_bfly_pass)."""
     import ctypes
     sink = torch.zeros(1, dtype=torch.int64, device="cuda")
     stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -162,8 +164,12 @@ def probe_modmul_peak(torch, lib, word: int, f64q_of_8=None):
     iters = 4000 if word == 4 else 1000
 
     def launch():
-        if f64q_of_8 is None:
+        if bfly_ctx is not None:
+            rc = lib.ctb_probe_bfly_pass(bfly_ctx._h, iters // 2, ctypes.c_void_p(sink.data_ptr()), ctypes.byref(n), stream)
+        elif f64q_of_8 is None:
             rc = lib.ctb_probe_modmul(word, iters, ctypes.c_void_p(sink.data_ptr()), ctypes.byref(n), stream)
+        elif splice:
+            rc = lib.ctb_probe_modmul_mix_splice(f64q_of_8, iters, ctypes.c_void_p(sink.data_ptr()), ctypes.byref(n), stream)
         else:
             rc = lib.ctb_probe_modmul_mix(f64q_of_8, iters, ctypes.c_void_p(sink.data_ptr()), ctypes.byref(n), stream)
         assert rc == 0, "modmul probe failed"
@@ -494,9 +500,13 @@ def run_ours(args):
     # modmul/s of k_cpmul's own butterfly product mix (3/8 FP64-quotient, 5/8 Shoup), register
     # resident; the pure forms are reported beside it
     lib = _lib.load()
-    modmul_peak = probe_modmul_peak(torch, lib, 4, f64q_of_8=3)
+    mix_conv = probe_modmul_peak(torch, lib, 4, f64q_of_8=3)
+    mix_splice = probe_modmul_peak(torch, lib, 4, f64q_of_8=3, splice=True)
+    modmul_peak = max(mix_conv, mix_splice)    # the faster form of the mix is the denominator
     peak_shoup = probe_modmul_peak(torch, lib, 4)
-    peak_f64q = probe_modmul_peak(torch, lib, 4, f64q_of_8=8)
+    peak_f64q = probe_modmul_peak(torch, lib, 4, f64q_of_8=8, splice=True)
+    peak_f64q_conv = probe_modmul_peak(torch, lib, 4, f64q_of_8=8)
+    bfly_peak = probe_modmul_peak(torch, lib, 4, bfly_ctx=ctx)
     avg_launch_s = statistics.mean(step_ms) * 1e-3
     modmuls_per = L * (5 * (N // 2) * (N.bit_length() - 1) + 2 * N)   # 3 fwd + 2 inv NTTs + 2 pointwise
     bytes_per = 16 * L * N + 8 * N                                     # read c (u32) + pt (u64), write out
@@ -528,11 +538,21 @@ def run_ours(args):
                 "traffic": _ncu_traffic("k_cpmul<u32,12>", B),
                 "kernel": "k_cpmul<uint32_t,12>",
                 "algorithmic_per_cpmul": {"modmuls": modmuls_per, "bytes": bytes_per},
-                "peak_source": {"int": "measured now: ctb_probe_modmul_mix(3) -- k_cpmul's butterfly product mix "
-                                       "(3/8 FP64-quotient, 5/8 Shoup), u32, register-resident",
+                "peak_source": {"int": "measured now: k_cpmul's butterfly product mix (3/8 FP64-quotient, 5/8 Shoup), "
+                                       "u32, register-resident -- the faster of ctb_probe_modmul_mix(3) (quotient "
+                                       "operand converted on the XU pipe, as the kernel runs it) and "
+                                       "ctb_probe_modmul_mix_splice(3) (exponent splice, the round-1 form)",
                                 "hbm": hbm_src},
-                "int_probes_gmodmul_s": {"mix_3_of_8": modmul_peak / 1e9, "shoup": peak_shoup / 1e9,
-                                         "f64_quotient": peak_f64q / 1e9},
+                "int_probes_gmodmul_s": {"mix_3_of_8": mix_conv / 1e9, "mix_3_of_8_splice": mix_splice / 1e9,
+                                         "shoup": peak_shoup / 1e9, "f64_quotient_splice": peak_f64q / 1e9,
+                                         "f64_quotient": peak_f64q_conv / 1e9},
+                # the modmul probes leave out the butterflies' additions (ALU pipe), which co-limit the
+                # transforms: k_cpmul's own radix-16 register pass, no exchanges / global traffic
+                "butterfly_pass_probe": {"gbfly_s": bfly_peak / 1e9, "frac": achieved_mm / bfly_peak,
+                                         "source": "measured now: ctb_probe_bfly_pass (complete Harvey butterflies of "
+                                                   "the N=4096 middle pass, twiddles from shared memory, one "
+                                                   "1024-thread CTA per SM); achieved counts the slotwise products "
+                                                   "as butterflies"},
                 "hbm": {"achieved_gbs": achieved_bw, "peak_gbs": hbm_peak, "frac": achieved_bw / hbm_peak},
                 "t_min_ms": 1e3 * max(t_int, t_hbm), "t_measured_ms": 1e3 * avg_launch_s,
             },

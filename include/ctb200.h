@@ -305,6 +305,17 @@ int ctb_probe_modmul(int word_bytes, uint64_t iters, void* sink, uint64_t* modmu
  * the 8 chains take the FP64-pipe quotient (3 = the share k_cpmul uses), the rest are Shoup
  * products.  Same launch shape and contract as ctb_probe_modmul; bench.py divides by it. */
 int ctb_probe_modmul_mix(int f64q_of_8, uint64_t iters, void* sink, uint64_t* modmuls, void* stream);
+/* The same mix with the quotient's operand assembled by the exponent splice (the round-1 form;
+ * ctb_probe_modmul_mix converts it with I2F.F64.U32 like the kernels do now). */
+int ctb_probe_modmul_mix_splice(int f64q_of_8, uint64_t iters, void* sink, uint64_t* modmuls, void* stream);
+
+/* Instrumentation: one radix-16 register pass of the 32-bit forward transform at N = 4096 exactly as
+ * ctb_cpmul runs it (32 complete Harvey butterflies per thread: conditional subtraction, product,
+ * sum, difference; twiddles from shared memory), repeated register-resident with no exchanges and no
+ * global traffic, one 1024-thread CTA per SM; *bflys receives the butterflies performed.  The
+ * ceiling of a transform's own arithmetic (the modmul probes leave out the ALU-pipe additions).
+ * Needs a context with N = 4096 and 32-bit cipher limbs. */
+int ctb_probe_bfly_pass(const ctb_ctx_t* ctx, uint64_t iters, void* sink, uint64_t* bflys, void* stream);
 
 /* Instrumentation: the 50-bit product of the FP64 butterflies (64-bit limbs: exact integers in
  * doubles, 6 FP64 operations per product, ntt.cuh f64_mulmod).  Same launch shape and contract as

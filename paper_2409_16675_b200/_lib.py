@@ -87,6 +87,8 @@ SIGNATURES: dict[str, tuple] = {
     "ctb_slot_sum": (_int, [_c_void_p, _int, _c_void_p, _u32, _c_void_p, _c_void_p, _u32, _c_void_p, _c_void_p]),
     "ctb_probe_modmul": (_int, [_int, _u64, _c_void_p, ctypes.POINTER(_u64), _c_void_p]),
     "ctb_probe_modmul_mix": (_int, [_int, _u64, _c_void_p, ctypes.POINTER(_u64), _c_void_p]),
+    "ctb_probe_modmul_mix_splice": (_int, [_int, _u64, _c_void_p, ctypes.POINTER(_u64), _c_void_p]),
+    "ctb_probe_bfly_pass": (_int, [_c_void_p, _u64, _c_void_p, ctypes.POINTER(_u64), _c_void_p]),
     "ctb_probe_modmul_f64": (_int, [_u64, _c_void_p, ctypes.POINTER(_u64), _c_void_p]),
     "ctb_probe_bfly_f64": (_int, [_u64, _c_void_p, ctypes.POINTER(_u64), _c_void_p]),
     "ctb_check_f64q": (_int, [_c_void_p, _int, _u64, _u64, ctypes.POINTER(_u64), _c_void_p]),

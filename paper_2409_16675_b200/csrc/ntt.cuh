@@ -278,9 +278,18 @@ struct TwSrc {
       asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(at));
     return v;
   }
-  // two adjacent (w, w') entries with one 128-bit load (32-bit limbs)
+  // two adjacent (w, w') entries with one 128-bit load (32-bit limbs); -DCTB_TW_LOAD2=0 reads them
+  // with two 64-bit loads (A/B)
+#ifndef CTB_TW_LOAD2
+#define CTB_TW_LOAD2 1
+#endif
   __device__ __forceinline__ void load2(const T* at, T& w0, T& wq0, T& w1, T& wq1) const {
     static_assert(sizeof(T) == 4, "paired twiddle entries: 32-bit limbs");
+    if constexpr (!CTB_TW_LOAD2) {
+      load(at, w0, wq0);
+      load(at + 2, w1, wq1);
+      return;
+    }
     if constexpr (SMEM)
       asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(wq0), "=r"(w1), "=r"(wq1)
                    : "r"((uint32_t)__cvta_generic_to_shared(at)));
@@ -364,8 +373,20 @@ __device__ __forceinline__ void gs_bfly(T& X, T& Y, T w, T wq, T p, T p2) {
 // FP64-quotient product (see F64Q_NE): a < 2^32, w < p < 2^30, wp = w'/p, kq = 1.5 2^52 - 2^52 wp
 // (exact).  fma((2^52 + a), wp, kq) = 1.5 2^52 + a wp exactly before its one rounding, to the
 // nearest integer (ulp 1 there): the low word is rint(a wp) in {floor, ceil}(a w / p).
+// CONV converts a with I2F.F64.U32 (XU pipe, otherwise idle; no register pair to assemble, no kq)
+// instead of the exponent splice: fma(a, wp, 1.5 2^52), same quotient.  Entries e in
+// [CTB_F64Q_CONV_LO, CTB_F64Q_CONV_HI) convert, the others splice (A/B: tools/ab_variants.py;
+// all-convert measured 1.197 vs all-splice 1.220 ms per 4096 CPMul).
+#ifndef CTB_F64Q_CONV_LO
+#define CTB_F64Q_CONV_LO 0
+#endif
+#ifndef CTB_F64Q_CONV_HI
+#define CTB_F64Q_CONV_HI 16
+#endif
+template <bool CONV = true>
 __device__ __forceinline__ uint32_t f64q_mul(uint32_t a, uint32_t w, double wp, double kq, uint32_t p, uint32_t pn) {
-  const double qd = __fma_rn(__hiloint2double(0x43300000, (int)a), wp, kq);
+  const double qd = CONV ? __fma_rn(__uint2double_rn(a), wp, 6755399441055744.0)
+                         : __fma_rn(__hiloint2double(0x43300000, (int)a), wp, kq);
   const uint32_t q = (uint32_t)__double2loint(qd);
   uint32_t t, r;
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(a), "r"(w), "r"(p));
@@ -406,7 +427,9 @@ __device__ __forceinline__ void fwd_pass(T (&x)[NttShape<LOGN>::E], TwSrc<T, SME
         for (int jj = 0; jj < h; ++jj) {
           const int a = gg * G + jb * 2 * h + jj;
           const T xx = (CANON && i == 0) ? x[a] : csub(x[a], p2);
-          const T t = (T)f64q_mul((uint32_t)x[a + h], (uint32_t)w, wp, kq, (uint32_t)p, (uint32_t)pn);
+          const T t = (e >= CTB_F64Q_CONV_LO && e < CTB_F64Q_CONV_HI)
+                          ? (T)f64q_mul<true>((uint32_t)x[a + h], (uint32_t)w, wp, kq, (uint32_t)p, (uint32_t)pn)
+                          : (T)f64q_mul<false>((uint32_t)x[a + h], (uint32_t)w, wp, kq, (uint32_t)p, (uint32_t)pn);
           x[a] = add2(xx, t);
           x[a + h] = xx - t + p2;
         }
@@ -462,7 +485,9 @@ __device__ __forceinline__ void inv_pass(T (&x)[NttShape<LOGN>::E], TwSrc<T, SME
           const int a = gg * G + jb * 2 * h + jj;
           const T X = x[a], Y = x[a + h];
           x[a] = (CANON && i == R - 1) ? X + Y : csub(add2(X, Y), p2);
-          x[a + h] = (T)f64q_mul((uint32_t)(Y - X + p2), (uint32_t)w, wp, kq, (uint32_t)p, (uint32_t)pn);
+          x[a + h] = (e >= CTB_F64Q_CONV_LO && e < CTB_F64Q_CONV_HI)
+                         ? (T)f64q_mul<true>((uint32_t)(Y - X + p2), (uint32_t)w, wp, kq, (uint32_t)p, (uint32_t)pn)
+                         : (T)f64q_mul<false>((uint32_t)(Y - X + p2), (uint32_t)w, wp, kq, (uint32_t)p, (uint32_t)pn);
         }
       } else {
 #pragma unroll

@@ -29,7 +29,9 @@ __global__ void __launch_bounds__(256) k_probe_shoup(T* sink, uint64_t iters, T 
 // The 32-bit butterfly mix of k_cpmul: NF of the 8 chains take their quotient from the FP64 pipe
 // (ntt.cuh f64q_mul), the rest are Shoup products -- k_cpmul runs 12 of the 32 butterflies of a
 // radix-16 pass (37.5% = 3/8) on the FP64 quotient.
-template <int NF>
+// CONV: the quotient's operand converted with I2F.F64.U32 (as the kernels run it) or assembled by
+// the exponent splice (the round-1 form).
+template <int NF, bool CONV>
 __global__ void __launch_bounds__(256) k_probe_mix(uint32_t* sink, uint64_t iters, uint32_t p, uint32_t w, uint32_t wq,
                                                    double wp) {
   uint32_t a[CHAINS];
@@ -39,7 +41,7 @@ __global__ void __launch_bounds__(256) k_probe_mix(uint32_t* sink, uint64_t iter
   const uint32_t pn = 0u - p;
   for (uint64_t i = 0; i < iters; ++i) {
 #pragma unroll
-    for (int j = 0; j < CHAINS; ++j) a[j] = j < NF ? f64q_mul(a[j], w, wp, kq, p, pn) : shoup_mul(a[j], w, wq, p);
+    for (int j = 0; j < CHAINS; ++j) a[j] = j < NF ? f64q_mul<CONV>(a[j], w, wp, kq, p, pn) : shoup_mul(a[j], w, wq, p);
   }
   uint32_t acc = 0;
 #pragma unroll
@@ -118,7 +120,50 @@ extern "C" int ctb_probe_modmul_f64(uint64_t iters, void* sink, uint64_t* modmul
   return cuda_status(cudaGetLastError(), "ctb_probe_modmul_f64");
 }
 
-extern "C" int ctb_probe_modmul_mix(int f64q_of_8, uint64_t iters, void* sink, uint64_t* modmuls, void* stream) {
+// One radix-16 register pass of the 32-bit forward transform at N = 4096 exactly as k_cpmul runs it
+// (ntt.cuh fwd_pass of the middle pass: 32 Harvey butterflies per thread -- conditional subtraction,
+// product, sum, difference -- twiddles from the prime's table staged in shared memory, FP64 quotients
+// on the first two entries), repeated register-resident: no exchanges, no global traffic, one
+// 1024-thread CTA per SM like k_cpmul.  The ceiling of a transform's own arithmetic: the modmul
+// probes above leave out the butterflies' ALU-pipe additions, which co-limit the kernels.
+template <int LOGN>
+__global__ void __launch_bounds__(1024, 1) k_probe_bfly_pass(uint32_t* sink, uint64_t iters,
+                                                             const PrimeTab<uint32_t>* __restrict__ tabs) {
+  using Sh = NttShape<LOGN>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint32_t* tw_sm = reinterpret_cast<uint32_t*>(smem_raw);
+  PrimeRegs<uint32_t> pr(tabs);
+  stage_twiddles(pr.fwd, tw_sm, tw_words<uint32_t>(LOGN), 1024);
+  __syncthreads();
+  const TwSrc<uint32_t, true> tw{tw_sm};
+  uint32_t x[Sh::E];
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) x[k] = (threadIdx.x * 2654435761u + k * 40503u + blockIdx.x) % pr.p;
+  for (uint64_t i = 0; i < iters; ++i) fwd_pass<uint32_t, LOGN, 1, true>(x, tw, pr.p, pr.p2);
+  uint32_t acc = 0;
+#pragma unroll
+  for (int k = 0; k < Sh::E; ++k) acc ^= x[k];
+  if (acc == 0x5eedu) sink[0] = acc;
+}
+
+extern "C" int ctb_probe_bfly_pass(const ctb_ctx_t* ctx, uint64_t iters, void* sink, uint64_t* bflys, void* stream) {
+  if (!ctx) { set_error("ctb_probe_bfly_pass: null context"); return ERR_ARG; }
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  const Base& b = c->base[BASE_Q];
+  if (c->logn != 12 || b.word != 4) { set_error("ctb_probe_bfly_pass: needs N = 4096 and 32-bit cipher limbs"); return ERR_ARG; }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = (size_t)tw_words<uint32_t>(12) * 4;
+  auto kern = k_probe_bfly_pass<12>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_status(e, "ctb_probe_bfly_pass");
+  kern<<<(unsigned)sms, 1024, smem, (cudaStream_t)stream>>>((uint32_t*)sink, iters, (const PrimeTab<uint32_t>*)b.d_tabs);
+  if (bflys) *bflys = (uint64_t)sms * 1024 * 32 * iters;
+  return cuda_status(cudaGetLastError(), "ctb_probe_bfly_pass");
+}
+
+static int probe_mix(int f64q_of_8, bool conv, uint64_t iters, void* sink, uint64_t* modmuls, void* stream) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -128,16 +173,24 @@ extern "C" int ctb_probe_modmul_mix(int f64q_of_8, uint64_t iters, void* sink, u
   const uint32_t wq = (uint32_t)(((uint64_t)w << 32) / p);
   const double wp = std::ldexp((double)(uint64_t)((((unsigned __int128)w << 52) + p / 2) / p), -52);
   uint32_t* o = (uint32_t*)sink;
-  switch (f64q_of_8) {
-    case 0: k_probe_mix<0><<<grid, block, 0, s>>>(o, iters, p, w, wq, wp); break;
-    case 3: k_probe_mix<3><<<grid, block, 0, s>>>(o, iters, p, w, wq, wp); break;
-    case 8: k_probe_mix<8><<<grid, block, 0, s>>>(o, iters, p, w, wq, wp); break;
+  switch (f64q_of_8 + (conv ? 16 : 0)) {
+    case 0: case 16: k_probe_mix<0, false><<<grid, block, 0, s>>>(o, iters, p, w, wq, wp); break;
+    case 3: k_probe_mix<3, false><<<grid, block, 0, s>>>(o, iters, p, w, wq, wp); break;
+    case 8: k_probe_mix<8, false><<<grid, block, 0, s>>>(o, iters, p, w, wq, wp); break;
+    case 19: k_probe_mix<3, true><<<grid, block, 0, s>>>(o, iters, p, w, wq, wp); break;
+    case 24: k_probe_mix<8, true><<<grid, block, 0, s>>>(o, iters, p, w, wq, wp); break;
     default:
       set_error("ctb_probe_modmul_mix: f64q_of_8 must be 0, 3 or 8");
       return ERR_ARG;
   }
   if (modmuls) *modmuls = (uint64_t)grid * block * CHAINS * iters;
   return cuda_status(cudaGetLastError(), "ctb_probe_modmul_mix");
+}
+extern "C" int ctb_probe_modmul_mix(int f64q_of_8, uint64_t iters, void* sink, uint64_t* modmuls, void* stream) {
+  return probe_mix(f64q_of_8, true, iters, sink, modmuls, stream);
+}
+extern "C" int ctb_probe_modmul_mix_splice(int f64q_of_8, uint64_t iters, void* sink, uint64_t* modmuls, void* stream) {
+  return probe_mix(f64q_of_8, false, iters, sink, modmuls, stream);
 }
 
 extern "C" int ctb_probe_modmul(int word_bytes, uint64_t iters, void* sink, uint64_t* modmuls,
@@ -201,7 +254,8 @@ __global__ void k_check_f64q(const uint32_t* tw, int words, const uint64_t* prim
       z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
       a = (uint32_t)(z ^ (z >> 31));
     }
-    const uint32_t res = f64q_mul(a, w, wp, kq, p, pn);
+    const uint32_t res = f64q_mul<true>(a, w, wp, kq, p, pn), res2 = f64q_mul<false>(a, w, wp, kq, p, pn);
+    if (res2 != res) ++nbad;   // both quotient forms agree
     if (res >= 2 * p || res % p != (uint32_t)((uint64_t)a * w % p)) ++nbad;
   }
   if (nbad) atomicAdd(bad, nbad);
