@@ -657,7 +657,7 @@ template <typename T, int LOGN, bool SMEM_TW, bool GATHER = false>
 __global__ void __launch_bounds__(NttShape<LOGN>::THREADS * enc_groups<T, LOGN>(),
                                   enc_groups<T, LOGN>() == 4 ? 1 : (enc_groups<T, LOGN>() == 2 ? 2 : NttShape<LOGN>::MINB))
 k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, const T* __restrict__ pkprep, T* out,
-          const PrimeTab<T>* __restrict__ tabs, int L, uint64_t t_half, uint32_t batch,
+          const PrimeTab<T>* __restrict__ tabs, int L, uint64_t t_half, uint32_t batch, bool plain_fast,
           const __grid_constant__ PlainGather g) {
   using Sh = NttShape<LOGN>;
   constexpr int GROUPS = enc_groups<T, LOGN>();
@@ -672,6 +672,9 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
   constexpr bool ENC_XPOSE = !PKSM && !enc_pk_strip<T, LOGN>() && sizeof(T) == 4 && CTB_EVAL_XPOSE &&
                              EV::VEC == Strip<T, LOGN>::VEC && eval_xpose_ok<T, LOGN>(Ex::WORDS);
   static_assert(!PKSM || (EV::VEC == Strip<T, LOGN>::VEC && GROUPS >= 2), "key strips need contiguous eval chunks");
+  // relaxed exchange guards / first-stage shortcuts of the 32-bit transforms (see the item loop)
+  constexpr bool RELAX = vec_exchange<T, LOGN>() && WARP_EXCHANGE && !ENC_XPOSE;
+  constexpr bool KEY_CANON = sizeof(T) == 4;   // prepared key words are canonical (ctb_prepare_operand)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
   const int group = (int)(threadIdx.x / Sh::THREADS);
@@ -832,7 +835,12 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
 #pragma unroll
       for (int k = 0; k < Sh::E; ++k) x[k] = small(u[k]);
     }
-    ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+    // canonical draws in, and the slotwise products below are canonical too (x < 4p times a
+    // canonical prepared key word: Montgomery output in [0, p)): every transform skips the
+    // conditional subtractions of its first stage.  RELAX (ntt.cuh Exchanger): the forward transform
+    // follows the previous item's inverse, part pi = 0's inverse follows it; only the second
+    // inverse follows a transform of its own direction and gets the explicit guard barrier.
+    ntt_fwd_regs<T, LOGN, 0, SMEM_TW, CPMUL_NBUF, GROUPS, F64Q_NE, RELAX, true>(x, ex, tw, pr.p, pr.p2);
     usm.store(x);
     // MSTRIP: part 1 first; part 0's plaintext reads are issued before its slotwise product and
     // Delta * lift(m) is parked in the NTT(u) strip (dead after that product) across the inverse
@@ -881,6 +889,14 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
         if (v > t_half) l = sub_mod(l, tmod, pr.p);
         return csub(shoup_mul(l, delta, delta_q, pr.p), pr.p);
       };
+      // 32-bit limbs, t < 2^57, p > 2^25 (lift_plain_regs): the lift lazily below 4p with one Shoup
+      // product -- the product by Delta takes any 32-bit operand
+      auto delta_m_fast = [&](uint64_t v) -> T {
+        const uint32_t hi = (uint32_t)(v >> 25), lo = (uint32_t)v & ((1u << 25) - 1);
+        const T l = (T)(shoup_mul<uint32_t>(hi, (uint32_t)pr.c25, (uint32_t)pr.c25_q, (uint32_t)pr.p) + lo +
+                        (v > t_half ? (uint32_t)(pr.p - tmod) : 0u));
+        return csub(shoup_mul(l, delta, delta_q, pr.p), pr.p);
+      };
       if (MSTRIP && part == 0) {
         Strip<T, LOGN> dsm = usm;
 #pragma unroll
@@ -893,8 +909,16 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
       }
       int8_t e[Sh::E];  // issued before the inverse transform, consumed after it
       load_draws(drow + (size_t)(1 + part) * Sh::N, e);
-      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, CPMUL_NBUF, GROUPS>(x, ex, tw, pr.p, pr.p2);
+      if (RELAX && pi == 1) group_sync<LOGN, GROUPS>();
+      ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, CPMUL_NBUF, GROUPS, F64Q_NE, RELAX, KEY_CANON>(x, ex, tw, pr.p, pr.p2);
       T* o = out + (((size_t)b * 2 + part) * L + limb) * Sh::N + cb;
+      if (sizeof(T) == 4 && !MSTRIP && part == 0 && plain_fast) {
+#pragma unroll
+        for (int k = 0; k < Sh::E; ++k) {
+          T v = add_mod(csub(x[k], pr.p), small(e[k]), pr.p);
+          o[coef_off<LOGN>(k)] = add_mod(v, delta_m_fast(m_at(k)), pr.p);
+        }
+      } else {
 #pragma unroll
       for (int c = 0; c < Strip<T, LOGN>::CHUNKS; ++c) {
         T d[Strip<T, LOGN>::VEC];
@@ -906,6 +930,7 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
           if (part == 0) v = add_mod(v, MSTRIP ? d[j] : delta_m(m_at(k)), pr.p);
           o[coef_off<LOGN>(k)] = v;
         }
+      }
       }
     }
   }
@@ -1246,7 +1271,7 @@ static cudaError_t launch_encrypt(const Ctx* c, const Base* b, const uint64_t* m
   const uint64_t max_grid = (batch + GROUPS - 1) / GROUPS * (uint64_t)L;
   grid = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(grid / L * L, (uint64_t)L), max_grid);
   cudaError_t e = launch_kernel_grid(kern, grid, threads, smem, s, m, draws, (const T*)pk, (T*)out,
-                                     (const PrimeTab<T>*)b->d_tabs, L, c->t_half, (uint32_t)batch, g);
+                                     (const PrimeTab<T>*)b->d_tabs, L, c->t_half, (uint32_t)batch, c->plain_fast, g);
   if (tmp) {
     const cudaError_t f = cudaFreeAsync(tmp, s);
     if (e == cudaSuccess) e = f;
