@@ -97,6 +97,14 @@ __host__ __device__ constexpr int cpmul_groups() { return sizeof(T) == 4 && (LOG
 #ifndef CTB_CPMUL_NBUF
 #define CTB_CPMUL_NBUF 1
 #endif
+// next item prefetched towards L2 (cp.async.bulk.prefetch.L2) by one thread per group
+#ifndef CTB_CPMUL_PF_L2
+#define CTB_CPMUL_PF_L2 1
+#endif
+// read-once / write-once data with streaming cache hints (ld.global.cs / st.global.cs)
+#ifndef CTB_CPMUL_STREAM_HINTS
+#define CTB_CPMUL_STREAM_HINTS 1
+#endif
 template <typename T, int LOGN>
 __host__ __device__ constexpr int cpmul_kernel_groups() {
   return (sizeof(T) == 4 && LOGN == 12) ? CTB_CPMUL_GROUPS : cpmul_groups<T, LOGN>();
@@ -165,6 +173,14 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
     };
 #pragma unroll 1
     for (uint32_t b = slot * GROUPS + group; b < batch; b += nslots * GROUPS) {
+      if constexpr (CTB_CPMUL_PF_L2) {   // the next item towards L2 (see the 32-bit loop below)
+        if (ntt_tid<LOGN>() == 0 && b + nslots * GROUPS < batch) {
+          const uint32_t nb = b + nslots * GROUPS;
+          bulk_prefetch_l2(pt + (size_t)nb * Sh::N, (uint32_t)(Sh::N * 8));
+          bulk_prefetch_l2(ct + (((size_t)nb * 2) * L + limb) * (size_t)Sh::N, (uint32_t)(Sh::N * sizeof(T)));
+          bulk_prefetch_l2(ct + (((size_t)nb * 2 + 1) * L + limb) * (size_t)Sh::N, (uint32_t)(Sh::N * sizeof(T)));
+        }
+      }
       {
         lift_plain_regs<T, LOGN>(pt + (size_t)b * Sh::N + coef_base<LOGN>(), x, pr, tmod, t_half, plain_fast);
         load_d(x);
@@ -205,6 +221,16 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
   }
 #pragma unroll 1
   for (uint32_t b = slot * GROUPS + group; b < batch; b += nslots * GROUPS) {
+    if constexpr (CTB_CPMUL_PF_L2) {
+      // the group's next item towards L2 while this one transforms (its loads then pay the L2, not
+      // the HBM latency): this limb's two ciphertext parts and the plaintext
+      if (ntt_tid<LOGN>() == 0 && b + nslots * GROUPS < batch) {
+        const uint32_t nb = b + nslots * GROUPS;
+        bulk_prefetch_l2(pt + (size_t)nb * Sh::N, (uint32_t)(Sh::N * 8));
+        bulk_prefetch_l2(ct + (((size_t)nb * 2) * L + limb) * (size_t)Sh::N, (uint32_t)(Sh::N * sizeof(T)));
+        bulk_prefetch_l2(ct + (((size_t)nb * 2 + 1) * L + limb) * (size_t)Sh::N, (uint32_t)(Sh::N * sizeof(T)));
+      }
+    }
     {
       lift_plain_regs<T, LOGN>(pt + (size_t)b * Sh::N + coef_base<LOGN>(), x, pr, tmod, t_half, plain_fast);
       // every transform of the loop runs with the relaxed exchange guard (ntt.cuh Exchanger): each
@@ -220,7 +246,7 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
     for (int part = 0; part < 2; ++part) {
       const size_t off = (((size_t)b * 2 + part) * L + limb) * (size_t)Sh::N + coef_base<LOGN>();
 #pragma unroll
-      for (int k = 0; k < Sh::E; ++k) x[k] = ct[off + coef_off<LOGN>(k)];
+      for (int k = 0; k < Sh::E; ++k) x[k] = CTB_CPMUL_STREAM_HINTS ? __ldcs(ct + off + coef_off<LOGN>(k)) : ct[off + coef_off<LOGN>(k)];
       // canonical ciphertext residues in: the forward transform skips the conditional subtractions
       // of its first stage (the inverse's inputs, Montgomery products of x < 4p and y < 2p, only
       // lie below 2p)
@@ -237,7 +263,10 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
       }
       ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, NB, GROUPS, F64Q_NE, RELAX>(x, ex, tw, pr.p, pr.p2);
 #pragma unroll
-      for (int k = 0; k < Sh::E; ++k) out[off + coef_off<LOGN>(k)] = csub(x[k], pr.p);
+      for (int k = 0; k < Sh::E; ++k) {
+        if constexpr (CTB_CPMUL_STREAM_HINTS) __stcs(out + off + coef_off<LOGN>(k), csub(x[k], pr.p));
+        else out[off + coef_off<LOGN>(k)] = csub(x[k], pr.p);
+      }
     }
   }
 }
