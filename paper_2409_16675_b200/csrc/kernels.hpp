@@ -29,7 +29,7 @@ template <typename T, int LOGN, int EXTRA_POLYS = 0, typename... KArgs, typename
 inline cudaError_t launch_ntt_kernel(void (*kern)(KArgs...), size_t nblocks, cudaStream_t s,
                                      Args... args) {
   using Sh = NttShape<LOGN>;
-  const size_t smem = (2 * (size_t)SmemImage<T, LOGN>::WORDS + (size_t)EXTRA_POLYS * Sh::N) * sizeof(T);
+  const size_t smem = ((size_t)Exchanger<T, LOGN>::WORDS + (size_t)EXTRA_POLYS * Sh::N) * sizeof(T);   // default NBUF = 2
   if (!smem_attr_done((const void*)kern)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
