@@ -79,8 +79,15 @@ extern "C" int ctb_ctx_create(ctb_ctx_t** out, uint32_t n, const uint64_t* q_pri
                       n_t ? delta.data() : nullptr);
   if (rc) { delete c; set_error("cipher base: " + err); return rc == -2 ? ERR_CUDA : ERR_ARG; }
   {
-    bool fast = c->t && c->t < (1ull << 57) && c->base[BASE_Q].word == 4;
-    for (uint32_t i = 0; i < n_q; ++i) fast = fast && q_primes[i] > (1ull << 25);
+    // 32-bit limbs: t < 2^57 and every cipher prime > 2^25 (one Shoup product per lifted value);
+    // 64-bit limbs: t <= every cipher prime (a plain value is its own residue: no product at all)
+    bool fast = c->t != 0;
+    if (c->base[BASE_Q].word == 4) {
+      fast = fast && c->t < (1ull << 57);
+      for (uint32_t i = 0; i < n_q; ++i) fast = fast && q_primes[i] > (1ull << 25);
+    } else {
+      for (uint32_t i = 0; i < n_q; ++i) fast = fast && c->t <= q_primes[i];
+    }
     c->plain_fast = fast;
   }
   rc = build_rns_consts(c, err);

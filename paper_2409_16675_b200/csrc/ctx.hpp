@@ -33,7 +33,8 @@ struct Ctx {
   Base base[BASE_COUNT];
   uint64_t t = 0, t_half = 0;   // plain modulus (0 when the context has no plain ring)
   uint32_t crt_inv = 0, crt_inv_q = 0;  // (t0^-1 mod t1) and Shoup quotient, 2-prime plain CRT
-  bool plain_fast = false;      // t < 2^57 and every cipher prime > 2^25 (lift_plain_regs, ntt.cuh)
+  bool plain_fast = false;      // cheap plaintext lift (lift_plain_regs, ntt.cuh): u32 limbs t < 2^57 and every
+                                // cipher prime > 2^25; u64 limbs t <= every cipher prime
   uint32_t relin_base_bits = 16;
   uint32_t wave_chunk = 296;    // items per limb-major chunk (= 2 x SM count, set at creation)
   RnsConsts* rns = nullptr;

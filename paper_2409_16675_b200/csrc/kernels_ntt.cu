@@ -812,13 +812,27 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
           if (v > t_half) l = sub_mod(l, tmod, pr.p);
           return csub(shoup_mul(l, delta, delta_q, pr.p), pr.p);
         };
+        auto delta_m_small = [&](uint64_t v) -> T {  // t <= p: m is its own residue (lift_plain_regs)
+          const T l = (T)(v > t_half ? v + (uint64_t)(pr.p - tmod) : v);
+          return csub(shoup_mul(l, delta, delta_q, pr.p), pr.p);
+        };
         if (part == 0) {   // the NTT(u) strip is dead now: park Delta * lift(m) there
+          if (plain_fast) {
+#pragma unroll
+            for (int c = 0; c < SV::CHUNKS; ++c) {
+              T dm[SV::VEC];
+#pragma unroll
+              for (int j = 0; j < SV::VEC; ++j) dm[j] = delta_m_small(mv[c * SV::VEC + j]);
+              usm.store_chunk(c, dm);
+            }
+          } else {
 #pragma unroll
           for (int c = 0; c < SV::CHUNKS; ++c) {
             T dm[SV::VEC];
 #pragma unroll
             for (int j = 0; j < SV::VEC; ++j) dm[j] = delta_m(mv[c * SV::VEC + j]);
             usm.store_chunk(c, dm);
+          }
           }
         }
         int8_t e[Sh::E];  // issued before the inverse transform, consumed after it

@@ -1241,7 +1241,8 @@ struct PrimeRegs {
 // + (p - t mod p when v > t/2) < 2p + 2^25 + p < 4p, an admissible forward input (the butterflies
 // take X in [0, 4p) and any 32-bit Y).  The branch on `fast` is hoisted out of the element loop:
 // as a per-element select ptxas predicated both reductions and issued the unused one too (10 of
-// 23 issue slots per value).  Otherwise canonical values in [0, p).
+// 23 issue slots per value).  64-bit limbs with `fast` (t <= p): the value is its own residue.
+// Otherwise canonical values in [0, p) through the general 64-bit reduction.
 template <typename T, int LOGN>
 __device__ __forceinline__ void lift_plain_regs(const uint64_t* __restrict__ src, T (&x)[NttShape<LOGN>::E],
                                                 const PrimeRegs<T>& pr, T tmod, uint64_t t_half, bool fast) {
@@ -1254,6 +1255,16 @@ __device__ __forceinline__ void lift_plain_regs(const uint64_t* __restrict__ src
         const uint64_t v = __ldg(src + coef_off<LOGN>(k));
         const uint32_t hi = (uint32_t)(v >> 25), lo = (uint32_t)v & ((1u << 25) - 1);
         x[k] = shoup_mul<uint32_t>(hi, pr.c25, pr.c25_q, pr.p) + lo + (v > t_half ? ptm : (T)0);
+      }
+      return;
+    }
+  } else {
+    if (fast) {   // 64-bit limbs, t <= p: v is its own residue and t mod p = t -- no product
+      const T ptm = pr.p - tmod;
+#pragma unroll
+      for (int k = 0; k < Sh::E; ++k) {
+        const uint64_t v = __ldg(src + coef_off<LOGN>(k));
+        x[k] = (T)(v > t_half ? v + ptm : v);              // canonical
       }
       return;
     }
