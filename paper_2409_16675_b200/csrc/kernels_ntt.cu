@@ -98,6 +98,9 @@ __host__ __device__ constexpr int cpmul_groups() { return sizeof(T) == 4 && (LOG
 #define CTB_CPMUL_NBUF 1
 #endif
 // next item prefetched towards L2 (cp.async.bulk.prefetch.L2) by one thread per group
+#ifndef CTB_CPMUL_F64_POINTWISE
+#define CTB_CPMUL_F64_POINTWISE 1
+#endif
 #ifndef CTB_CPMUL_PF_L2
 #define CTB_CPMUL_PF_L2 1
 #endif
@@ -148,6 +151,10 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
   }
   const TwSrc<T, SMEM_TW> tw{twp};
   constexpr bool RELAX = vec_exchange<T, LOGN>() && WARP_EXCHANGE;
+  // slotwise products (and the N^-1 scaling) with FP64-pipe quotients (ntt.cuh f64_pointwise)
+  constexpr bool F64PW = CTB_CPMUL_F64_POINTWISE && sizeof(T) == 4;
+  const double pinv_d = __drcp_rn((double)pr.p), ninv_d = (double)pr.ninv;
+  const uint32_t pn32 = 0u - (uint32_t)pr.p;
 
   T x[Sh::E];
   if constexpr (sizeof(T) == 8) {
@@ -237,8 +244,14 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
       // follows one of the other direction, except part 0's forward transform right after this
       // one -- the explicit group barrier below is that guard
       ntt_fwd_regs<T, LOGN, 0, SMEM_TW, NB, GROUPS, F64Q_NE, RELAX>(x, ex, tw, pr.p, pr.p2);
+      if constexpr (F64PW) {   // y = NTT(pt) N^-1 (no Montgomery factor: the slotwise products are FP64-quotient)
 #pragma unroll
-      for (int k = 0; k < Sh::E; ++k) x[k] = shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p);
+        for (int k = 0; k < Sh::E; ++k)
+          x[k] = (T)f64_pointwise((uint32_t)x[k], (uint32_t)pr.ninv, ninv_d, pinv_d, (uint32_t)pr.p, pn32);
+      } else {
+#pragma unroll
+        for (int k = 0; k < Sh::E; ++k) x[k] = shoup_mul(x[k], pr.ninvr, pr.ninvr_q, pr.p);
+      }
       ysm.store(x);
       if constexpr (RELAX) group_sync<LOGN, GROUPS>();
     }
@@ -258,7 +271,10 @@ k_cpmul(const T* ct, const uint64_t* __restrict__ pt, T* out, const PrimeTab<T>*
 #pragma unroll
         for (int j = 0; j < Strip<T, LOGN>::VEC; ++j) {
           const int k = c * Strip<T, LOGN>::VEC + j;
-          x[k] = mont_mul(x[k], y[j], pr.p, pr.pinv);
+          if constexpr (F64PW)
+            x[k] = (T)f64_pointwise((uint32_t)x[k], (uint32_t)y[j], __uint2double_rn((uint32_t)y[j]), pinv_d, (uint32_t)pr.p, pn32);
+          else
+            x[k] = mont_mul(x[k], y[j], pr.p, pr.pinv);
         }
       }
       ntt_inv_regs<T, LOGN, Sh::NPASS - 1, SMEM_TW, NB, GROUPS, F64Q_NE, RELAX>(x, ex, tw, pr.p, pr.p2);

@@ -393,6 +393,19 @@ __device__ __forceinline__ uint32_t f64q_mul(uint32_t a, uint32_t w, double wp, 
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(q), "r"(pn), "r"(t));
   return r;  // a*w + p - q*p in (0, 2p)
 }
+// Product of two DATA operands on the FP64 pipe (32-bit limbs): x < 2^32, y < 2^32, p < 2^30.
+// q = rint(fl(x y) fl(1/p)) by the magic-constant FMA: |q - x y / p| <= 1/2 + 2^-19 (both roundings
+// are relative 2^-53 on a quotient below 2^34), only its low word matters, and x y + p - q p in
+// (0.49 p, 1.51 p) takes 2 IMAD -- 4 fma-heavy cycles instead of the Montgomery product's 12 (two
+// IMAD.HI), the conversions on the XU pipe.  No Montgomery factor: the result is x y mod p.
+__device__ __forceinline__ uint32_t f64_pointwise(uint32_t x, uint32_t y, double yd, double pinv, uint32_t p, uint32_t pn) {
+  const double qd = __fma_rn(__dmul_rn(__uint2double_rn(x), yd), pinv, 6755399441055744.0);
+  const uint32_t q = (uint32_t)__double2loint(qd);
+  uint32_t t, r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(x), "r"(y), "r"(p));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(q), "r"(pn), "r"(t));
+  return r;
+}
 __device__ __forceinline__ double f64q_k(double wp) { return __fma_rn(-4503599627370496.0, wp, 6755399441055744.0); }
 // FP64 quotients of the group slot (pass K): entry e at [e] from it (ntt.cuh shape_q_index)
 template <typename T, int LOGN, int K>
