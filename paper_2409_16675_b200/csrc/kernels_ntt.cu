@@ -98,6 +98,9 @@ __host__ __device__ constexpr int cpmul_groups() { return sizeof(T) == 4 && (LOG
 #define CTB_CPMUL_NBUF 1
 #endif
 // next item prefetched towards L2 (cp.async.bulk.prefetch.L2) by one thread per group
+#ifndef CTB_ENC_F64_POINTWISE
+#define CTB_ENC_F64_POINTWISE 1
+#endif
 #ifndef CTB_CPMUL_F64_POINTWISE
 #define CTB_CPMUL_F64_POINTWISE 1
 #endif
@@ -719,7 +722,12 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
   static_assert(!PKSM || (EV::VEC == Strip<T, LOGN>::VEC && GROUPS >= 2), "key strips need contiguous eval chunks");
   // relaxed exchange guards / first-stage shortcuts of the 32-bit transforms (see the item loop)
   constexpr bool RELAX = vec_exchange<T, LOGN>() && WARP_EXCHANGE && !ENC_XPOSE;
-  constexpr bool KEY_CANON = sizeof(T) == 4;   // prepared key words are canonical (ctb_prepare_operand)
+  // slotwise products with FP64-pipe quotients (ntt.cuh f64_pointwise) when the key is staged in
+  // shared memory (converted out of the Montgomery domain once per CTA)
+  constexpr bool F64PW = CTB_ENC_F64_POINTWISE && sizeof(T) == 4 && PKSM;
+  // Montgomery products with canonical prepared key words (ctb_prepare_operand) are canonical;
+  // the FP64-quotient products lie in (0.49 p, 1.51 p): no first-stage shortcut for the inverse
+  constexpr bool KEY_CANON = sizeof(T) == 4 && !F64PW;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* tw_sm = reinterpret_cast<T*>(smem_raw);
   const int group = (int)(threadIdx.x / Sh::THREADS);
@@ -742,6 +750,10 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
       for (int i = 0; i < EV::CHUNKS; ++i) {
         T v[EV::VEC];
         EV::load(kp, i, v);
+        if constexpr (F64PW) {   // out of the Montgomery domain: the FP64-quotient products carry no 2^-W
+#pragma unroll
+          for (int c = 0; c < EV::VEC; ++c) v[c] = mont_mul(v[c], (T)1, pr.p, pr.pinv);
+        }
         ks.store_chunk(i, v);
       }
     }
@@ -752,6 +764,7 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
     twp = tw_sm;
   }
   const TwSrc<T, SMEM_TW> tw{twp};
+  const double pinv_d = __drcp_rn((double)pr.p);
   auto small = [&](int8_t v) -> T {  // |v| <= 127 < p: canonical residue
     return v < 0 ? pr.p - (T)(-(int)v) : (T)v;
   };
@@ -935,7 +948,13 @@ k_encrypt(const uint64_t* __restrict__ m, const int8_t* __restrict__ draws, cons
           T uu[EV::VEC];
           usm.load_chunk(i, uu);
 #pragma unroll
-          for (int c = 0; c < EV::VEC; ++c) x[i * EV::VEC + c] = mont_mul(uu[c], v[c], pr.p, pr.pinv);
+          for (int c = 0; c < EV::VEC; ++c) {
+            if constexpr (F64PW)
+              x[i * EV::VEC + c] = (T)f64_pointwise((uint32_t)uu[c], (uint32_t)v[c], __uint2double_rn((uint32_t)v[c]), pinv_d,
+                                                    (uint32_t)pr.p, 0u - (uint32_t)pr.p);
+            else
+              x[i * EV::VEC + c] = mont_mul(uu[c], v[c], pr.p, pr.pinv);
+          }
         } else {
           T uu[Strip<T, LOGN>::VEC];
           usm.load_chunk(i / Strip<T, LOGN>::VEC, uu);
