@@ -398,6 +398,15 @@ __device__ __forceinline__ uint32_t f64q_mul(uint32_t a, uint32_t w, double wp, 
 // are relative 2^-53 on a quotient below 2^34), only its low word matters, and x y + p - q p in
 // (0.49 p, 1.51 p) takes 2 IMAD -- 4 fma-heavy cycles instead of the Montgomery product's 12 (two
 // IMAD.HI), the conversions on the XU pipe.  No Montgomery factor: the result is x y mod p.
+__device__ __forceinline__ uint32_t f64_pointwise2(uint32_t x, uint32_t y, double xd, double yd, double pinv, uint32_t p,
+                                                   uint32_t pn) {   // both operands already converted
+  const double qd = __fma_rn(__dmul_rn(xd, yd), pinv, 6755399441055744.0);
+  const uint32_t q = (uint32_t)__double2loint(qd);
+  uint32_t t, r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(x), "r"(y), "r"(p));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(q), "r"(pn), "r"(t));
+  return r;
+}
 __device__ __forceinline__ uint32_t f64_pointwise(uint32_t x, uint32_t y, double yd, double pinv, uint32_t p, uint32_t pn) {
   const double qd = __fma_rn(__dmul_rn(__uint2double_rn(x), yd), pinv, 6755399441055744.0);
   const uint32_t q = (uint32_t)__double2loint(qd);
@@ -1182,9 +1191,10 @@ __device__ __forceinline__ void eval_xpose_apply(const T* src, T* img, F&& f) {
 // thread t at 16-byte index c * THREADS + t.  The eval layout gives thread t the block f(t)
 // (ntt.cuh eval_xpose_*), so direct eval-layout key loads put every lane of a warp in its own
 // 128-byte line; in this layout each warp load is 512 contiguous bytes.  One block per polynomial.
-// TO_F64 (64-bit limbs): the prepared operand (Montgomery domain, NTT * N^-1 * 2^64) leaves the
-// Montgomery domain and is stored as the bits of its centred double, the form the FP64 products take
-// (`tabs` / `L`: the primes, block b being limb b % L).
+// TO_F64: the prepared operand (Montgomery domain, NTT * N^-1 * 2^W) leaves the Montgomery domain;
+// 64-bit limbs store the bits of its centred double, the form the FP64 products take, 32-bit limbs
+// the canonical word for the FP64-quotient products (`tabs` / `L`: the primes, block b being limb
+// b % L).
 template <typename T, int LOGN, bool TO_F64 = false>
 __global__ void __launch_bounds__(NttShape<LOGN>::THREADS) k_eval_to_strip(const T* __restrict__ in, T* __restrict__ out,
                                                                           const PrimeTab<T>* __restrict__ tabs, int L) {
@@ -1204,9 +1214,13 @@ __global__ void __launch_bounds__(NttShape<LOGN>::THREADS) k_eval_to_strip(const
     if constexpr (TO_F64) {
 #pragma unroll
       for (int c = 0; c < EV::VEC; ++c) {
-        const T r = mont_mul(v[c], (T)1, p, pinv);   // x 2^-64: leaves the Montgomery domain, [0, p)
-        const double dv = r > p / 2 ? -(double)(p - r) : (double)r;
-        v[c] = (T)__double_as_longlong(dv);
+        const T r = mont_mul(v[c], (T)1, p, pinv);   // x 2^-W: leaves the Montgomery domain, [0, p)
+        if constexpr (sizeof(T) == 8) {
+          const double dv = r > p / 2 ? -(double)(p - r) : (double)r;
+          v[c] = (T)__double_as_longlong(dv);
+        } else {
+          v[c] = r;   // 32-bit limbs: the canonical word (FP64-quotient products convert it on use)
+        }
       }
     }
     dst[i * Sh::THREADS + threadIdx.x] = pack_chunk<T>(v);

@@ -594,6 +594,13 @@ __global__ void __launch_bounds__(256) k_relin_digits(const TQ* ct3, uint32_t* d
 #ifndef CTB_RELIN_XPOSE
 #define CTB_RELIN_XPOSE 0
 #endif
+// 32-bit limbs: key products with FP64-pipe quotients (ntt.cuh f64_pointwise), keys converted out
+// of the Montgomery domain with the thread-major layout
+#ifndef CTB_RELIN_F64_POINTWISE
+#define CTB_RELIN_F64_POINTWISE 1
+#endif
+template <typename T, bool KSTRIP>
+__host__ __device__ constexpr bool RELIN_F64PW() { return CTB_RELIN_F64_POINTWISE && sizeof(T) == 4 && KSTRIP && !CTB_RELIN_XPOSE; }
 // L2 prefetch of the next digit polynomial while the current one transforms
 #ifndef CTB_RELIN_L2PF
 #define CTB_RELIN_L2PF 1
@@ -706,6 +713,8 @@ k_relin_accum(const T* ct3, int ct_parts, const uint32_t* digits, const T* keypr
     return;
   }
   T acc0[Sh::E], acc1[Sh::E], x[Sh::E];
+  const double pinv_d = __drcp_rn((double)pr.p);
+  const uint32_t pn32 = 0u - (uint32_t)pr.p;
 #pragma unroll 1
   for (uint32_t b = slot; b < batch; b += nslots) {
 #pragma unroll
@@ -780,8 +789,14 @@ k_relin_accum(const T* ct3, int ct_parts, const uint32_t* digits, const T* keypr
 #pragma unroll
         for (int c = 0; c < EV::VEC; ++c) {
           const int j = i * EV::VEC + c;
+          if constexpr (RELIN_F64PW<T, KSTRIP>()) {   // keys out of the Montgomery domain (k_eval_to_strip)
+            const double xd = __uint2double_rn((uint32_t)x[j]);
+            acc0[j] = csub(acc0[j] + (T)f64_pointwise2((uint32_t)x[j], (uint32_t)vb[c], xd, __uint2double_rn((uint32_t)vb[c]), pinv_d, (uint32_t)pr.p, pn32), pr.p2);
+            acc1[j] = csub(acc1[j] + (T)f64_pointwise2((uint32_t)x[j], (uint32_t)va[c], xd, __uint2double_rn((uint32_t)va[c]), pinv_d, (uint32_t)pr.p, pn32), pr.p2);
+          } else {
           acc0[j] = csub(acc0[j] + mont_mul(x[j], vb[c], pr.p, pr.pinv), pr.p2);
           acc1[j] = csub(acc1[j] + mont_mul(x[j], va[c], pr.p, pr.pinv), pr.p2);
+          }
         }
       }
     }
@@ -822,7 +837,7 @@ static cudaError_t launch_relin_accum(const Ctx* c, const void* ct3, int ct_part
     cudaError_t e = c->pool ? cudaMallocFromPoolAsync(&tmp, npoly * Sh::N * sizeof(T), c->pool, s)
                             : cudaMallocAsync(&tmp, npoly * Sh::N * sizeof(T), s);
     if (e != cudaSuccess) return e;
-    k_eval_to_strip<T, LOGN, relin_f64<T, LOGN, KS>()><<<(unsigned)npoly, Sh::THREADS, 0, s>>>(
+    k_eval_to_strip<T, LOGN, relin_f64<T, LOGN, KS>() || RELIN_F64PW<T, KS>()><<<(unsigned)npoly, Sh::THREADS, 0, s>>>(
         (const T*)keyprep, (T*)tmp, (const PrimeTab<T>*)B.d_tabs, L);
     if ((e = cudaGetLastError()) != cudaSuccess) { cudaFreeAsync(tmp, s); return e; }
     keys = tmp;
