@@ -35,8 +35,13 @@ namespace ctb {
 #ifndef CTB_LIN_BLOCKS_PER_SM
 #define CTB_LIN_BLOCKS_PER_SM 4
 #endif
+// resident blocks the registers are capped for (the gather lives on memory-level parallelism: 32-bit
+// limbs 4 blocks of 64 registers instead of 3 of 70, 636 -> 605 us per cfg4 job; 5 blocks spill)
+#ifndef CTB_LIN_MINB
+#define CTB_LIN_MINB 4
+#endif
 template <typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? CTB_LIN_MINB : 1)
 k_lin_accum(const T* __restrict__ X, const T* __restrict__ W, const T* __restrict__ MXp, const T* __restrict__ MWp,
             const int32_t* __restrict__ slot_ptr, const int32_t* __restrict__ site_x,
             const int32_t* __restrict__ site_w, const T* __restrict__ init, T* __restrict__ acc,
